@@ -1,0 +1,167 @@
+/*
+ * tsb200.h -- C ABI of the B200-native shared-loading data plane
+ * (TensorSocket, arXiv 2409.18749; reference = /root/reference/pkg).
+ *
+ * Plain pointers, sizes and integer status codes only: no torch types.  Every
+ * device operation is asynchronous on a caller-supplied cudaStream_t passed
+ * as `void *stream` (NULL = legacy default stream).  Status: 0 = ok, < 0 =
+ * error; tsb_last_error() returns a thread-local message.  The Python facade
+ * (paper_2409_18749_b200/_lib.py) maps codes to the reference's exception
+ * classes (payload.py:48-61).
+ *
+ * Which reference interface each entry point replaces is cited per function
+ * (paths relative to /root/reference/pkg).
+ */
+#ifndef TSB200_H
+#define TSB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSB_OK 0
+#define TSB_ERR_INVALID -1   /* ValueError            (payload.py:181-193)   */
+#define TSB_ERR_CUDA -2      /* ResourceError         (payload.py:60-61)     */
+#define TSB_ERR_STALE -3     /* StaleHandleError      (payload.py:52-53)     */
+#define TSB_ERR_CORRUPT -4   /* CorruptSegmentError   (payload.py:56-57)     */
+#define TSB_ERR_UNSUPPORTED -5
+
+#define TSB_IPC_HANDLE_BYTES 64
+
+/* collate output kinds (NCHW); PASSTHROUGH keeps the sample bytes as-is */
+#define TSB_OUT_U8 0
+#define TSB_OUT_F32 1
+#define TSB_OUT_BF16 2
+
+/* ---- library / errors ---------------------------------------------------- */
+const char *tsb_last_error(void);
+int tsb_version(void);
+int tsb_device_count(int *n);
+int tsb_set_device(int dev);
+int tsb_get_device(int *dev);
+int tsb_device_info(int dev, int *sm_count, int *cc_major, int *cc_minor, size_t *hbm_bytes);
+
+/* ---- memory & streams (plumbing; no torch) -------------------------------- */
+int tsb_malloc(void **p, size_t bytes);                 /* device HBM */
+int tsb_free(void *p);
+int tsb_host_alloc(void **p, size_t bytes);             /* pinned + device-mapped */
+int tsb_host_free(void *p);
+int tsb_host_register(void *p, size_t bytes);           /* pin + map caller memory */
+int tsb_host_unregister(void *p);
+int tsb_host_device_ptr(void *host, void **dev);        /* device alias of pinned host */
+int tsb_memcpy_async(void *dst, const void *src, size_t bytes, void *stream); /* cudaMemcpyDefault */
+int tsb_memset_async(void *dst, int value, size_t bytes, void *stream);
+int tsb_stream_create(void **stream);
+int tsb_stream_destroy(void *stream);
+int tsb_stream_sync(void *stream);
+int tsb_device_sync(void);
+int tsb_event_create(void **ev);
+int tsb_event_destroy(void *ev);
+int tsb_event_record(void *ev, void *stream);
+int tsb_event_sync(void *ev);
+int tsb_event_elapsed_ms(void *start, void *end, float *ms);
+int tsb_stream_wait_event(void *stream, void *ev);
+int tsb_enable_peer(int dev, int peer);                 /* cudaDeviceEnablePeerAccess */
+int tsb_can_access_peer(int dev, int peer, int *can);
+
+/* ---- RNG + shuffle (host native; reference kernels.py / pipeline.py) ---- */
+/* kernels.py:40-45 */
+uint64_t tsb_mix64(uint64_t x);
+/* kernels.py:48-53 */
+uint64_t tsb_derive_key(uint64_t seed, uint64_t epoch, uint64_t index);
+/* kernels.py:170-178 (sequential Fisher-Yates; once per epoch) */
+int tsb_permutation(int64_t n, uint64_t key, int64_t *out);
+/* pipeline.py:113-123 */
+int tsb_epoch_order(int64_t n, uint64_t shuffle_seed, uint64_t epoch, int reshuffle, int64_t *out);
+
+/* ---- batch production kernels (replace pipeline.py:158-213 prepare_batch) */
+/* Synthetic source (pipeline.py:183-189, kernels.py:112-121): sample s of the
+ * batch = SplitMix64 stream keyed derive_key(seed, epoch, indices[s]).
+ * d_indices: device int64[b]. */
+int tsb_fill_synthetic(void *out, const int64_t *d_indices, int64_t b, uint64_t seed,
+                       uint64_t epoch, int64_t sample_bytes, void *stream);
+/* Store materialisation (pipeline.py:139-155 write_directory_dataset):
+ * sample i = stream keyed derive_key(seed, 0, first + i). */
+int tsb_make_store(void *out, uint64_t seed, int64_t first, int64_t count, int64_t sample_bytes,
+                   void *stream);
+/* Directory/store source collate (pipeline.py:190-210): out = concat of
+ * src[indices[s]] for s < b.  src may be HBM or pinned host (device-mapped). */
+int tsb_gather(const void *src, const int64_t *d_indices, int64_t b, int64_t sample_bytes,
+               void *out, void *stream);
+/* NEW (no reference; SURVEY.md §8a A6'): per-sample crop/flip params from
+ * the reference RNG stream.  d_params: device int32[b][3] = (oy, ox, flip). */
+int tsb_aug_params(uint64_t aug_seed, uint64_t epoch, const int64_t *d_indices, int64_t b,
+                   int pad, int flip, int32_t *d_params, void *stream);
+/* NEW fused collate/augment: uint8 HWC samples (HBM or pinned host) ->
+ * pad/crop/flip -> normalise -> NCHW u8/f32/bf16 written into `out` (a ring
+ * slot).  scale/bias: host float[c] (NULL = identity).  d_params: optional
+ * device table from tsb_aug_params (NULL = derive in-kernel). */
+int tsb_collate_augment(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
+                        int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
+                        const float *scale, const float *bias, int out_kind,
+                        const int32_t *d_params, void *out, void *stream);
+
+/* ---- integrity (wire.py:170-172 checksum; payload.py:218,362-364) ------- */
+/* CRC-32/IEEE of n device bytes into *d_out (device uint32).  Needs a
+ * device workspace of tsb_crc32_workspace_bytes() bytes. */
+size_t tsb_crc32_workspace_bytes(void);
+int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, void *stream);
+
+/* ---- device batch ring (replaces payload.py:165-370 create/map/release
+ *      and the producer ledger's release gate, producer.py:169-252) ------- */
+typedef struct tsb_ring tsb_ring;
+/* One HBM allocation: `slots` payload slots of slot_bytes + a control block
+ * (ready word per slot, release cursor per consumer). */
+int tsb_ring_create(int dev, int slots, size_t slot_bytes, int max_consumers, tsb_ring **out);
+/* CUDA-IPC export for same-GPU consumer processes (64-byte handle). */
+int tsb_ring_export(tsb_ring *r, void *handle_out);
+int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_consumers,
+                    tsb_ring **out);
+int tsb_ring_destroy(tsb_ring *r);
+int tsb_ring_slot_ptr(tsb_ring *r, int slot, void **out);
+int tsb_ring_base_ptr(tsb_ring *r, void **out);
+int tsb_ring_geometry(tsb_ring *r, int *slots, size_t *slot_bytes, int *max_consumers);
+/* Producer: ready[slot] = seq after all prior work on `stream` (release). */
+int tsb_ring_publish(tsb_ring *r, int slot, uint64_t seq, void *stream);
+/* Consumer: `stream` waits until ready[slot] >= seq (acquire). */
+int tsb_ring_wait_ready(tsb_ring *r, int slot, uint64_t seq, void *stream);
+/* Consumer release (device-counted ack): cursor[consumer] = seq after all
+ * prior work on `stream` (bs/consumer.py:330 Ack + release_view). */
+int tsb_ring_ack(tsb_ring *r, int consumer, uint64_t seq, void *stream);
+/* Producer gate before reusing a slot: `stream` waits until every consumer
+ * in live[0..n_live) has cursor >= seq (producer.py:230-238 flow gate). */
+int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, void *stream);
+/* Host: cursor[consumer] = UINT64_MAX so no device wait can wedge on an
+ * evicted consumer (producer.py:255-269 evict_stale). */
+int tsb_ring_evict(tsb_ring *r, int consumer);
+/* Host: reset a consumer cursor (admission, producer.py:629-642). */
+int tsb_ring_set_cursor(tsb_ring *r, int consumer, uint64_t value);
+int tsb_ring_read_cursor(tsb_ring *r, int consumer, uint64_t *out);
+int tsb_ring_read_ready(tsb_ring *r, int slot, uint64_t *out);
+/* 1 = stream mem-ops (cuStreamWaitValue64), 0 = spin kernels. */
+int tsb_ring_sync_mode(void);
+
+/* ---- fan-out + rebatch (NEW) -------------------------- */
+/* Copy `bytes` from src into each of dsts[0..n_dst) (device or peer
+ * pointers; P2P stores over NVLink/NVSwitch).  dsts: HOST array of n_dst
+ * (<= 8) device pointers, passed to the kernel by value. */
+int tsb_fanout(const void *src, void *const *dsts, int n_dst, size_t bytes, void *stream);
+/* Fused: collate/augment written straight into n_dst (<= 8) destinations
+ * (host array of device/peer pointers) -- collate + fan-out in one pass. */
+int tsb_collate_augment_fanout(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
+                               int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
+                               const float *scale, const float *bias, int out_kind,
+                               void *const *dsts, int n_dst, void *stream);
+/* Rebatch gather: copy `count` samples starting at ring sample position
+ * `first` (sample-granular ring of ring_samples samples of sample_bytes,
+ * wrapping) into out. */
+int tsb_rebatch_gather(const void *ring_base, int64_t ring_samples, int64_t sample_bytes,
+                       int64_t first, int64_t count, void *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSB200_H */

@@ -1,0 +1,98 @@
+// Shared helpers for the tsb200 C-ABI library (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/tsb200.h"
+
+namespace tsb {
+
+void set_error(const char *fmt, ...);
+
+#define TSB_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            ::tsb::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                             cudaGetErrorString(e_));                               \
+            return TSB_ERR_CUDA;                                                    \
+        }                                                                           \
+    } while (0)
+
+#define TSB_CHECK(cond, ...)                                                        \
+    do {                                                                            \
+        if (!(cond)) {                                                              \
+            ::tsb::set_error(__VA_ARGS__);                                          \
+            return TSB_ERR_INVALID;                                                 \
+        }                                                                           \
+    } while (0)
+
+#define TSB_LAUNCH_CHECK()                                                          \
+    do {                                                                            \
+        cudaError_t e_ = cudaGetLastError();                                        \
+        if (e_ != cudaSuccess) {                                                    \
+            ::tsb::set_error("%s:%d launch: %s", __FILE__, __LINE__,                \
+                             cudaGetErrorString(e_));                               \
+            return TSB_ERR_CUDA;                                                    \
+        }                                                                           \
+    } while (0)
+
+constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ULL;
+constexpr uint64_t MIX2 = 0x94D049BB133111EBULL;
+constexpr uint64_t SHUFFLE_DOMAIN = 0x53485546ULL;  // pipeline.py:25
+constexpr uint64_t AUG_DOMAIN = 0x41554731ULL;      // "AUG1" (SURVEY.md §8a A6')
+
+// kernels.py:40-45 SplitMix64 finalizer (u64 wrap-around)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * MIX1;
+    z = (z ^ (z >> 27)) * MIX2;
+    return z ^ (z >> 31);
+}
+
+// kernels.py:48-53
+__host__ __device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t epoch,
+                                                        uint64_t index) {
+    uint64_t h = mix64(seed + GAMMA);
+    h = mix64((h ^ epoch) + GAMMA);
+    h = mix64((h ^ index) + GAMMA);
+    return h;
+}
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
+// 128-bit streaming global accesses (guide G13/G14)
+__device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_cs_v4(void *p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_v4(void *p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+}  // namespace tsb

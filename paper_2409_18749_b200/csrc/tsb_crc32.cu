@@ -1,0 +1,209 @@
+// Device CRC-32/IEEE (zlib-compatible: reflected 0xEDB88320, init/xorout ~0).
+//
+// Replaces wire.py:170-172 `checksum` as called per batch by create_segment
+// (payload.py:218) and map_segment(verify_checksum) (payload.py:362-364).
+//
+// Parallel form of the sequential CRC via linearity over GF(2):
+//   raw(A||B) = x^(8|B|) * raw(A)  xor  raw(B)          (raw = zero-init CRC)
+//   crc(M)    = raw(M) xor x^(8|M|) * 0xFFFFFFFF xor 0xFFFFFFFF
+// and raw(0^z || M) = raw(M), so the message is front-padded (virtually) to a
+// whole number of 2 KB units.  Each warp owns one unit: every lane runs the
+// byte-table CRC over its 64 B (table replicated 32x in shared memory so lane
+// l always hits bank l -- conflict-free), a 5-level shuffle tree combines the
+// 32 lane CRCs, the unit CRC is shifted by the bytes that follow it, and the
+// shifted values are XOR-reduced (XOR is associative/commutative) with one
+// atomicXor per warp.  Multiplication by a constant x^k mod P uses 4-bit
+// tables (8 nibbles x 16 entries).  HBM-bound: one read of the data.
+#include <mutex>
+
+#include "tsb_common.cuh"
+
+using namespace tsb;
+
+namespace {
+
+constexpr uint32_t POLY = 0xEDB88320u;
+constexpr int UNIT = 2048;        // bytes per warp unit
+constexpr int LANE_BYTES = 64;    // bytes per lane
+constexpr int TREE_LEVELS = 5;    // 32 lanes
+constexpr int SHIFT_BITS = 32;    // unit-shift tables: 2048 * 2^k, k < 32
+constexpr int NT = 8 * 16;        // u32 per nibble table
+constexpr int CRC_THREADS = 256;
+
+__device__ uint32_t g_byte_tab[256];
+__device__ uint32_t g_tree_tab[TREE_LEVELS * NT];
+__device__ uint32_t g_shift_tab[SHIFT_BITS * NT];
+
+uint32_t h_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ POLY : b >> 1;
+    }
+    return p;
+}
+uint32_t h_x8n(uint64_t n) {  // x^(8n) mod P, reflected
+    uint32_t p = 1u << 31, sq = 1u << 30;
+    for (int i = 0; i < 3; ++i) sq = h_multmodp(sq, sq);
+    while (n) {
+        if (n & 1) p = h_multmodp(sq, p);
+        n >>= 1;
+        sq = h_multmodp(sq, sq);
+    }
+    return p;
+}
+void h_nibble_table(uint32_t k, uint32_t *t) {
+    for (int j = 0; j < 8; ++j)
+        for (uint32_t q = 0; q < 16; ++q) t[j * 16 + q] = h_multmodp(k, q << (4 * j));
+}
+
+std::mutex g_mu;
+bool g_ready[64] = {false};
+
+int ensure_tables() {
+    int dev = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 64 && g_ready[dev]) return TSB_OK;
+    static uint32_t bt[256], tt[TREE_LEVELS * NT], st[SHIFT_BITS * NT];
+    for (uint32_t i = 0; i < 256; ++i) {
+        uint32_t r = i;
+        for (int k = 0; k < 8; ++k) r = (r >> 1) ^ (POLY & (0u - (r & 1u)));
+        bt[i] = r;
+    }
+    for (int k = 0; k < TREE_LEVELS; ++k) h_nibble_table(h_x8n((uint64_t)LANE_BYTES << k), tt + k * NT);
+    for (int k = 0; k < SHIFT_BITS; ++k) h_nibble_table(h_x8n((uint64_t)UNIT << k), st + k * NT);
+    TSB_CUDA(cudaMemcpyToSymbol(g_byte_tab, bt, sizeof(bt)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_tree_tab, tt, sizeof(tt)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_shift_tab, st, sizeof(st)));
+    if (dev < 64) g_ready[dev] = true;
+    return TSB_OK;
+}
+
+__device__ __forceinline__ uint32_t mul_nib(uint32_t v, const uint32_t *t) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r ^= t[j * 16 + ((v >> (4 * j)) & 15u)];
+    return r;
+}
+
+struct CrcSmem {
+    uint32_t rep[256 * 32];  // rep[i*32 + lane] = byte_tab[i]
+    uint32_t tree[TREE_LEVELS * NT];
+    uint32_t shift[SHIFT_BITS * NT];
+};
+
+__global__ void crc_init_kernel(uint32_t *out, uint32_t c) { *out = c; }
+
+__global__ void __launch_bounds__(CRC_THREADS)
+    crc_kernel(const uint8_t *__restrict__ data, uint64_t n, uint64_t z, uint64_t n_units,
+               int vec, uint32_t *out) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    CrcSmem &sm = *reinterpret_cast<CrcSmem *>(smem_raw);
+    for (int i = threadIdx.x; i < 256 * 32; i += CRC_THREADS) sm.rep[i] = g_byte_tab[i >> 5];
+    for (int i = threadIdx.x; i < TREE_LEVELS * NT; i += CRC_THREADS) sm.tree[i] = g_tree_tab[i];
+    for (int i = threadIdx.x; i < SHIFT_BITS * NT; i += CRC_THREADS) sm.shift[i] = g_shift_tab[i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * CRC_THREADS + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * CRC_THREADS) >> 5;
+    const uint32_t *rep = sm.rep + lane;
+    uint32_t acc = 0;
+
+    for (uint64_t u = warp; u < n_units; u += nwarps) {
+        // virtual byte position of this lane's chunk (front-padded by z zeros)
+        const int64_t vpos = (int64_t)(u * UNIT + (uint64_t)lane * LANE_BYTES) - (int64_t)z;
+        uint32_t c = 0;
+        if (vec && vpos >= 0) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(data + vpos);
+            uint4 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q[k] = ld_nc_v4(p + k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t wv[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        c = rep[((c ^ (wv[j] >> (8 * b))) & 0xFFu) << 5] ^ (c >> 8);
+                }
+            }
+        } else {
+            for (int k = 0; k < LANE_BYTES; ++k) {
+                const int64_t p = vpos + k;
+                const uint32_t byte = (p >= 0 && (uint64_t)p < n) ? data[p] : 0u;
+                c = rep[((c ^ byte) & 0xFFu) << 5] ^ (c >> 8);
+            }
+        }
+        // combine the 32 lane CRCs (each covers 64 B) in address order
+#pragma unroll
+        for (int k = 0; k < TREE_LEVELS; ++k) {
+            const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, c, 1 << k);
+            if (lane & (1 << k))
+                c = mul_nib(other, sm.tree + k * NT) ^ c;  // other is the left half
+            else
+                c = mul_nib(c, sm.tree + k * NT) ^ other;
+        }
+        // shift by the whole units that follow this one
+        uint64_t q = n_units - 1 - u;
+        if (lane == 0) {
+            int k = 0;
+            while (q) {
+                if (q & 1) c = mul_nib(c, sm.shift + k * NT);
+                q >>= 1;
+                ++k;
+            }
+            acc ^= c;
+        }
+    }
+    if (lane == 0 && acc) atomicXor(out, acc);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t tsb_crc32_workspace_bytes(void) { return 0; }
+
+int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, void *stream) {
+    (void)d_workspace;
+    TSB_CHECK(d_out, "null output");
+    TSB_CHECK(data || n == 0, "null data");
+    int rc = ensure_tables();
+    if (rc) return rc;
+    auto s = as_stream(stream);
+    // init term: x^(8n) * 0xFFFFFFFF xor 0xFFFFFFFF (n = 0 -> 0)
+    const uint32_t init = h_multmodp(h_x8n(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+    crc_init_kernel<<<1, 1, 0, s>>>(d_out, init);
+    TSB_LAUNCH_CHECK();
+    if (n == 0) return TSB_OK;
+    const uint64_t z = (UNIT - n % UNIT) % UNIT;
+    const uint64_t n_units = (n + z) / UNIT;
+    TSB_CHECK(n_units < (1ull << SHIFT_BITS), "buffer too large for CRC shift tables");
+    const int vec = ((((uintptr_t)data) - z) & 15) == 0;
+    const size_t smem = sizeof(CrcSmem);
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        TSB_CUDA(cudaFuncSetAttribute(crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr_set[dev] = true;
+    }
+    const uint64_t warps_per_block = CRC_THREADS / 32;
+    uint64_t blocks = (n_units + warps_per_block - 1) / warps_per_block;
+    const uint64_t cap = (uint64_t)sm_count() * 4;  // persistent: ~4 CTAs per SM
+    if (blocks > cap) blocks = cap;
+    crc_kernel<<<(unsigned)blocks, CRC_THREADS, smem, s>>>(static_cast<const uint8_t *>(data), n, z,
+                                                           n_units, vec, d_out);
+    TSB_LAUNCH_CHECK();
+    return TSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// Fan-out (one slot -> N destination slots, local or peer GPUs over
+// NVLink/NVSwitch with P2P stores) and the per-consumer rebatch gather.
+//
+// NEW subsystems (no reference code): the reference's
+// "broadcast" is every consumer mapping the same shm name
+// (bs/consumer.py:319-321); across GPUs the bytes must move.  Each source
+// 16-byte vector is loaded once and stored to every destination, so the
+// producer reads HBM once and its egress is (N-1) x bytes on NVLink.
+#include "tsb_common.cuh"
+
+using namespace tsb;
+
+namespace {
+
+constexpr int FO_THREADS = 512;
+constexpr int FO_MAX = 8;
+struct DstList {
+    void *p[FO_MAX];
+    int n;
+};
+
+__global__ void __launch_bounds__(FO_THREADS)
+    fanout_v16_kernel(const uint4 *__restrict__ src, DstList d, uint64_t n16) {
+    const uint64_t stride = (uint64_t)gridDim.x * FO_THREADS;
+    uint64_t i = (uint64_t)blockIdx.x * FO_THREADS + threadIdx.x;
+    constexpr int U = 4;
+    for (; i + (U - 1) * stride < n16; i += U * stride) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_nc_v4(src + i + u * stride);
+#pragma unroll
+        for (int k = 0; k < FO_MAX; ++k) {
+            if (k < d.n) {
+                uint4 *o = static_cast<uint4 *>(d.p[k]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) st_v4(o + i + u * stride, v[u]);
+            }
+        }
+    }
+    for (; i < n16; i += stride) {
+        uint4 v = ld_nc_v4(src + i);
+#pragma unroll
+        for (int k = 0; k < FO_MAX; ++k)
+            if (k < d.n) st_v4(static_cast<uint4 *>(d.p[k]) + i, v);
+    }
+}
+
+__global__ void fanout_tail_kernel(const uint8_t *__restrict__ src, DstList d, uint64_t from,
+                                   uint64_t n) {
+    for (uint64_t i = from + threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < FO_MAX; ++k)
+            if (k < d.n) static_cast<uint8_t *>(d.p[k])[i] = src[i];
+}
+
+// Rebatch: out[j] = ring[(first + j) mod ring_samples], whole samples.
+constexpr int RB_THREADS = 256;
+constexpr int64_t RB_BYTES_PER_CTA = 64 * 1024;
+
+__global__ void __launch_bounds__(RB_THREADS)
+    rebatch_kernel(const uint8_t *__restrict__ ring, int64_t ring_samples, int64_t sb,
+                   int64_t first, uint8_t *__restrict__ out, int vec) {
+    const int64_t j = blockIdx.y;
+    const int64_t pos = (first + j) % ring_samples;
+    const uint8_t *in = ring + pos * sb;
+    uint8_t *o = out + j * sb;
+    const int64_t b0 = (int64_t)blockIdx.x * RB_BYTES_PER_CTA;
+    const int64_t b1 = min(b0 + RB_BYTES_PER_CTA, sb);
+    if (vec) {
+        for (int64_t k = b0 + 16 * threadIdx.x; k < b1; k += 16 * RB_THREADS)
+            st_v4(o + k, ld_nc_v4(in + k));
+    } else {
+        for (int64_t k = b0 + threadIdx.x; k < b1; k += RB_THREADS) o[k] = in[k];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsb_fanout(const void *src, void *const *dsts, int n_dst, size_t bytes, void *stream) {
+    TSB_CHECK(src && dsts && n_dst >= 1 && n_dst <= FO_MAX, "n_dst must be 1..%d", FO_MAX);
+    DstList d{};
+    d.n = n_dst;
+    bool aligned = ((uintptr_t)src & 15) == 0;
+    for (int i = 0; i < n_dst; ++i) {
+        TSB_CHECK(dsts[i], "null destination %d", i);
+        d.p[i] = dsts[i];
+        aligned = aligned && (((uintptr_t)dsts[i] & 15) == 0);
+    }
+    if (!bytes) return TSB_OK;
+    auto s = as_stream(stream);
+    uint64_t n16 = aligned ? bytes / 16 : 0;
+    if (n16) {
+        uint64_t blocks = (n16 + FO_THREADS * 4 - 1) / (FO_THREADS * 4);
+        const uint64_t cap = (uint64_t)sm_count() * 4;
+        if (blocks > cap) blocks = cap;
+        fanout_v16_kernel<<<(unsigned)blocks, FO_THREADS, 0, s>>>(
+            static_cast<const uint4 *>(src), d, n16);
+        TSB_LAUNCH_CHECK();
+    }
+    if (n16 * 16 < bytes) {
+        fanout_tail_kernel<<<1, 256, 0, s>>>(static_cast<const uint8_t *>(src), d, n16 * 16, bytes);
+        TSB_LAUNCH_CHECK();
+    }
+    return TSB_OK;
+}
+
+int tsb_rebatch_gather(const void *ring_base, int64_t ring_samples, int64_t sample_bytes,
+                       int64_t first, int64_t count, void *out, void *stream) {
+    TSB_CHECK(ring_base && out, "null pointer");
+    TSB_CHECK(ring_samples > 0 && sample_bytes > 0 && first >= 0 && count >= 0 &&
+                  count <= 65535,
+              "bad rebatch geometry");
+    if (!count) return TSB_OK;
+    const int vec = (sample_bytes % 16 == 0) && (((uintptr_t)ring_base & 15) == 0) &&
+                    (((uintptr_t)out & 15) == 0);
+    dim3 grid((unsigned)((sample_bytes + RB_BYTES_PER_CTA - 1) / RB_BYTES_PER_CTA), (unsigned)count);
+    rebatch_kernel<<<grid, RB_THREADS, 0, as_stream(stream)>>>(
+        static_cast<const uint8_t *>(ring_base), ring_samples, sample_bytes, first % ring_samples,
+        static_cast<uint8_t *>(out), vec);
+    TSB_LAUNCH_CHECK();
+    return TSB_OK;
+}
+
+}  // extern "C"

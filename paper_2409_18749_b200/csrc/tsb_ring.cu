@@ -1,0 +1,318 @@
+// Device batch ring: HBM slots + device-resident ready words and per-consumer
+// release cursors ("acks counted on the device").
+//
+// Replaces the reference transport seam (payload.py:165-370: one POSIX shm
+// segment per batch, unlinked on release) and the data-path half of the
+// producer ledger (producer.py:169-252: release when every admitted consumer
+// acked; announce gate while fewer than buffer_depth are pending).
+//
+//   producer stream:  wait_free(slot's previous seq) -> collate -> publish(seq)
+//   consumer stream:  wait_ready(seq) -> <use the zero-copy view> -> ack(seq)
+//
+// Synchronisation is entirely on device streams: CUDA stream memory
+// operations (cuStreamWaitValue64 / cuStreamWriteValue64, executed by the
+// GPU front end without occupying SMs -- they also work across processes
+// on the same GPU, where kernels are time-sliced) with spin kernels as the
+// device-side alternative.  Host threads only enqueue; eviction writes a
+// +inf cursor so no wait can wedge on a dead consumer (producer.py:255-269).
+#include <cuda.h>
+#include <stdlib.h>
+
+#include <mutex>
+
+#include "tsb_common.cuh"
+
+using namespace tsb;
+
+struct tsb_ring {
+    int dev;
+    int slots;
+    size_t slot_bytes;
+    size_t slot_stride;
+    int max_consumers;
+    uint8_t *base;
+    uint64_t *ready;   // [slots]
+    uint64_t *cursor;  // [max_consumers]
+    size_t total;
+    bool imported;
+    cudaStream_t host_stream;  // private non-blocking stream for host pokes
+};
+
+namespace {
+
+typedef CUresult (*PFN_wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_devattr)(int *, CUdevice_attribute, CUdevice);
+
+PFN_wait64 g_wait64 = nullptr;
+PFN_write64 g_write64 = nullptr;
+int g_mode = -1;  // 1 memops, 0 kernels
+std::mutex g_mu;
+
+int resolve_mode() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_mode >= 0) return g_mode;
+    g_mode = 0;
+    const char *env = getenv("TSB_SYNC");
+    if (env && env[0] == 'k') return g_mode;  // TSB_SYNC=kernel forces spin kernels
+    cudaDriverEntryPointQueryResult q1, q2, q3;
+    void *w = nullptr, *wr = nullptr, *da = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWriteValue64", &wr, cudaEnableDefault, &q2) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuDeviceGetAttribute", &da, cudaEnableDefault, &q3) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess ||
+        q3 != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return g_mode;
+    }
+    int dev = 0, ok = 0;
+    cudaGetDevice(&dev);
+    if (reinterpret_cast<PFN_devattr>(da)(&ok, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS,
+                                          (CUdevice)dev) != CUDA_SUCCESS)
+        ok = 0;
+    if (ok) {
+        g_wait64 = reinterpret_cast<PFN_wait64>(w);
+        g_write64 = reinterpret_cast<PFN_write64>(wr);
+        g_mode = 1;
+    }
+    return g_mode;
+}
+
+// ---- spin-kernel path ------------------------------------------------------
+constexpr int MAX_WAIT = 64;
+struct WaitSet {
+    const uint64_t *addr[MAX_WAIT];
+    int n;
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void signal_kernel(uint64_t *addr, uint64_t value) {
+    __threadfence_system();
+    st_release_sys(addr, value);
+}
+
+__global__ void wait_kernel(WaitSet set, uint64_t value) {
+    const int i = threadIdx.x;
+    if (i < set.n) {
+        while (ld_acquire_sys(set.addr[i]) < value) __nanosleep(128);
+    }
+    __syncthreads();
+    __threadfence_system();
+}
+
+int dev_write(tsb_ring *r, uint64_t *addr, uint64_t v, void *stream) {
+    if (resolve_mode() == 1) {
+        CUresult e = g_write64((CUstream)stream, (CUdeviceptr)addr, v, 0);
+        if (e != CUDA_SUCCESS) {
+            set_error("cuStreamWriteValue64 failed (%d)", (int)e);
+            return TSB_ERR_CUDA;
+        }
+        return TSB_OK;
+    }
+    (void)r;
+    signal_kernel<<<1, 1, 0, as_stream(stream)>>>(addr, v);
+    TSB_LAUNCH_CHECK();
+    return TSB_OK;
+}
+
+int dev_wait(const uint64_t *const *addrs, int n, uint64_t v, void *stream) {
+    if (n <= 0) return TSB_OK;
+    if (resolve_mode() == 1) {
+        for (int i = 0; i < n; ++i) {
+            CUresult e = g_wait64((CUstream)stream, (CUdeviceptr)addrs[i], v,
+                                  CU_STREAM_WAIT_VALUE_GEQ);
+            if (e != CUDA_SUCCESS) {
+                set_error("cuStreamWaitValue64 failed (%d)", (int)e);
+                return TSB_ERR_CUDA;
+            }
+        }
+        return TSB_OK;
+    }
+    for (int i0 = 0; i0 < n; i0 += MAX_WAIT) {
+        WaitSet set{};
+        set.n = n - i0 < MAX_WAIT ? n - i0 : MAX_WAIT;
+        for (int i = 0; i < set.n; ++i) set.addr[i] = addrs[i0 + i];
+        wait_kernel<<<1, 64, 0, as_stream(stream)>>>(set, v);
+        TSB_LAUNCH_CHECK();
+    }
+    return TSB_OK;
+}
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+void layout(tsb_ring *r) {
+    r->slot_stride = round_up(r->slot_bytes ? r->slot_bytes : 16, 256);
+    const size_t payload = r->slot_stride * (size_t)r->slots;
+    const size_t ctl = round_up(sizeof(uint64_t) * (size_t)(r->slots + r->max_consumers), 256);
+    r->total = payload + ctl;
+}
+
+void bind(tsb_ring *r) {
+    const size_t payload = r->slot_stride * (size_t)r->slots;
+    r->ready = reinterpret_cast<uint64_t *>(r->base + payload);
+    r->cursor = r->ready + r->slots;
+}
+
+int host_write(tsb_ring *r, uint64_t *addr, uint64_t v) {
+    TSB_CUDA(cudaMemcpyAsync(addr, &v, sizeof(v), cudaMemcpyHostToDevice, r->host_stream));
+    TSB_CUDA(cudaStreamSynchronize(r->host_stream));
+    return TSB_OK;
+}
+int host_read(tsb_ring *r, const uint64_t *addr, uint64_t *out) {
+    TSB_CUDA(cudaMemcpyAsync(out, addr, sizeof(*out), cudaMemcpyDeviceToHost, r->host_stream));
+    TSB_CUDA(cudaStreamSynchronize(r->host_stream));
+    return TSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsb_ring_sync_mode(void) { return resolve_mode(); }
+
+int tsb_ring_create(int dev, int slots, size_t slot_bytes, int max_consumers, tsb_ring **out) {
+    TSB_CHECK(out, "null out");
+    TSB_CHECK(slots >= 1 && max_consumers >= 1 && max_consumers <= 4096,
+              "bad ring geometry slots=%d consumers=%d", slots, max_consumers);
+    TSB_CUDA(cudaSetDevice(dev));
+    tsb_ring *r = new tsb_ring{};
+    r->dev = dev;
+    r->slots = slots;
+    r->slot_bytes = slot_bytes;
+    r->max_consumers = max_consumers;
+    layout(r);
+    cudaError_t e = cudaMalloc(&r->base, r->total);
+    if (e != cudaSuccess) {
+        delete r;
+        set_error("ring allocation of %zu bytes failed: %s", r->total, cudaGetErrorString(e));
+        return TSB_ERR_CUDA;
+    }
+    bind(r);
+    TSB_CUDA(cudaStreamCreateWithFlags(&r->host_stream, cudaStreamNonBlocking));
+    TSB_CUDA(cudaMemsetAsync(r->ready, 0, sizeof(uint64_t) * (r->slots + r->max_consumers),
+                             r->host_stream));
+    TSB_CUDA(cudaStreamSynchronize(r->host_stream));
+    resolve_mode();
+    *out = r;
+    return TSB_OK;
+}
+
+int tsb_ring_export(tsb_ring *r, void *handle_out) {
+    TSB_CHECK(r && handle_out, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == TSB_IPC_HANDLE_BYTES, "ipc handle size");
+    cudaIpcMemHandle_t h;
+    TSB_CUDA(cudaIpcGetMemHandle(&h, r->base));
+    memcpy(handle_out, &h, sizeof(h));
+    return TSB_OK;
+}
+
+int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_consumers,
+                    tsb_ring **out) {
+    TSB_CHECK(handle && out, "null argument");
+    tsb_ring *r = new tsb_ring{};
+    TSB_CUDA(cudaGetDevice(&r->dev));
+    r->slots = slots;
+    r->slot_bytes = slot_bytes;
+    r->max_consumers = max_consumers;
+    layout(r);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        delete r;
+        cudaGetLastError();
+        set_error("cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        return TSB_ERR_STALE;
+    }
+    r->base = static_cast<uint8_t *>(p);
+    r->imported = true;
+    bind(r);
+    TSB_CUDA(cudaStreamCreateWithFlags(&r->host_stream, cudaStreamNonBlocking));
+    resolve_mode();
+    *out = r;
+    return TSB_OK;
+}
+
+int tsb_ring_destroy(tsb_ring *r) {
+    if (!r) return TSB_OK;
+    int rc = TSB_OK;
+    if (r->host_stream) cudaStreamDestroy(r->host_stream);
+    cudaError_t e = r->imported ? cudaIpcCloseMemHandle(r->base) : cudaFree(r->base);
+    if (e != cudaSuccess) {
+        set_error("ring release: %s", cudaGetErrorString(e));
+        rc = TSB_ERR_CUDA;
+    }
+    delete r;
+    return rc;
+}
+
+int tsb_ring_slot_ptr(tsb_ring *r, int slot, void **out) {
+    TSB_CHECK(r && out, "null argument");
+    TSB_CHECK(slot >= 0 && slot < r->slots, "slot %d out of range", slot);
+    *out = r->base + r->slot_stride * (size_t)slot;
+    return TSB_OK;
+}
+int tsb_ring_base_ptr(tsb_ring *r, void **out) {
+    TSB_CHECK(r && out, "null argument");
+    *out = r->base;
+    return TSB_OK;
+}
+int tsb_ring_geometry(tsb_ring *r, int *slots, size_t *slot_bytes, int *max_consumers) {
+    TSB_CHECK(r, "null ring");
+    if (slots) *slots = r->slots;
+    if (slot_bytes) *slot_bytes = r->slot_stride;
+    if (max_consumers) *max_consumers = r->max_consumers;
+    return TSB_OK;
+}
+
+int tsb_ring_publish(tsb_ring *r, int slot, uint64_t seq, void *stream) {
+    TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
+    return dev_write(r, r->ready + slot, seq, stream);
+}
+int tsb_ring_wait_ready(tsb_ring *r, int slot, uint64_t seq, void *stream) {
+    TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
+    const uint64_t *a = r->ready + slot;
+    return dev_wait(&a, 1, seq, stream);
+}
+int tsb_ring_ack(tsb_ring *r, int consumer, uint64_t seq, void *stream) {
+    TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
+    return dev_write(r, r->cursor + consumer, seq, stream);
+}
+int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, void *stream) {
+    TSB_CHECK(r && (live || n_live == 0), "null argument");
+    if (n_live <= 0 || seq == 0) return TSB_OK;
+    const uint64_t *addrs[4096];
+    TSB_CHECK(n_live <= 4096, "too many consumers");
+    for (int i = 0; i < n_live; ++i) {
+        TSB_CHECK(live[i] >= 0 && live[i] < r->max_consumers, "bad consumer %d", live[i]);
+        addrs[i] = r->cursor + live[i];
+    }
+    return dev_wait(addrs, n_live, seq, stream);
+}
+int tsb_ring_evict(tsb_ring *r, int consumer) {
+    TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
+    return host_write(r, r->cursor + consumer, ~0ull);
+}
+int tsb_ring_set_cursor(tsb_ring *r, int consumer, uint64_t value) {
+    TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
+    return host_write(r, r->cursor + consumer, value);
+}
+int tsb_ring_read_cursor(tsb_ring *r, int consumer, uint64_t *out) {
+    TSB_CHECK(r && out && consumer >= 0 && consumer < r->max_consumers, "bad consumer");
+    return host_read(r, r->cursor + consumer, out);
+}
+int tsb_ring_read_ready(tsb_ring *r, int slot, uint64_t *out) {
+    TSB_CHECK(r && out && slot >= 0 && slot < r->slots, "bad slot");
+    return host_read(r, r->ready + slot, out);
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+"""DeviceRing: the HBM batch ring that replaces the reference's per-batch
+POSIX shm segments (payload.py:165-370) and its ack-gated release
+(producer.py:169-252).
+
+A ring is one device allocation holding ``slots`` payload slots plus a
+control block of device words:
+
+* ``ready[slot]``   -- global sequence number (1-based) of the batch the slot
+  currently holds, written by the producer's stream after the batch is
+  complete (release semantics);
+* ``cursor[k]``     -- highest sequence consumer k has *released*; written by
+  the consumer's stream once its work on that batch is done.
+
+Batch with sequence q (q = epoch*epoch_len + index + 1) lives in slot
+(q-1) % slots.  The producer may overwrite a slot for q only once every live
+consumer released q - slots (device wait on the cursors), so a ring of S
+slots bounds drift to S batches with no host round trip on the data path.
+Eviction writes cursor = 2**64-1 so no device wait can wedge
+(producer.py:255-269).
+
+Zero-copy views: same process -> the pointer; other processes on the same
+GPU -> CUDA-IPC import of the whole allocation (handle shipped once, inside
+the Announce's segment name).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _lib
+from ._lib import IPC_HANDLE_BYTES, call, load
+
+SENTINEL = (1 << 64) - 1
+
+_TORCH_TYPESTR = {
+    "uint8": "|u1", "int8": "|i1", "int16": "<i2", "int32": "<i4", "int64": "<i8",
+    "float32": "<f4", "float64": "<f8", "float16": "<f2", "bfloat16": "<i2",
+}
+
+
+class _CAI:
+    """__cuda_array_interface__ holder; keeps the owning ring alive."""
+
+    def __init__(self, ptr: int, shape, typestr: str, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {
+            "shape": tuple(int(s) for s in shape), "typestr": typestr,
+            "data": (int(ptr), False), "version": 3, "strides": None, "stream": None,
+        }
+
+
+def tensor_view(ptr: int, shape, dtype, owner=None):
+    """Zero-copy torch CUDA tensor over device memory at ``ptr``."""
+    import torch
+
+    name = str(dtype).replace("torch.", "")
+    typestr = _TORCH_TYPESTR[name]
+    t = torch.as_tensor(_CAI(ptr, shape, typestr, owner), device="cuda")
+    if name == "bfloat16":
+        t = t.view(torch.bfloat16)
+    return t
+
+
+class DeviceRing:
+    def __init__(self, slots: int, slot_bytes: int, max_consumers: int = 64,
+                 device: int | None = None):
+        L = load()
+        if device is None:
+            dev = ctypes.c_int(0)
+            call("tsb_get_device", ctypes.byref(dev))
+            device = dev.value
+        h = ctypes.c_void_p()
+        call("tsb_ring_create", device, slots, slot_bytes, max_consumers, ctypes.byref(h))
+        self._init(h, slots, slot_bytes, max_consumers, device, imported=False)
+        self._L = L
+
+    def _init(self, h, slots, slot_bytes, max_consumers, device, imported):
+        self._h = h
+        self.slots = slots
+        self.slot_bytes = slot_bytes
+        self.max_consumers = max_consumers
+        self.device = device
+        self.imported = imported
+        self.pid = os.getpid()
+        geo_slots, stride, mc = ctypes.c_int(), ctypes.c_size_t(), ctypes.c_int()
+        call("tsb_ring_geometry", h, ctypes.byref(geo_slots), ctypes.byref(stride),
+             ctypes.byref(mc))
+        self.slot_stride = stride.value
+        base = ctypes.c_void_p()
+        call("tsb_ring_base_ptr", h, ctypes.byref(base))
+        self.base = base.value
+
+    @classmethod
+    def import_handle(cls, handle: bytes, slots: int, slot_bytes: int, max_consumers: int):
+        """Open a ring exported by another process on this GPU (CUDA IPC)."""
+        if len(handle) != IPC_HANDLE_BYTES:
+            raise ValueError("IPC handle must be 64 bytes")
+        load()
+        buf = ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES)
+        h = ctypes.c_void_p()
+        call("tsb_ring_import", buf, slots, slot_bytes, max_consumers, ctypes.byref(h))
+        self = cls.__new__(cls)
+        dev = ctypes.c_int(0)
+        call("tsb_get_device", ctypes.byref(dev))
+        self._init(h, slots, slot_bytes, max_consumers, dev.value, imported=True)
+        return self
+
+    # -- identity -----------------------------------------------------------
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        call("tsb_ring_export", self._h, buf)
+        return buf.raw
+
+    def slot_ptr(self, slot: int) -> int:
+        if not 0 <= slot < self.slots:
+            raise IndexError(slot)
+        return self.base + self.slot_stride * slot
+
+    def slot_of(self, seq: int) -> int:
+        return (seq - 1) % self.slots
+
+    def view(self, slot: int, shape, dtype, byte_offset: int = 0):
+        return tensor_view(self.slot_ptr(slot) + byte_offset, shape, dtype, owner=self)
+
+    # -- device sync words ----------------------------------------------------
+    def publish(self, slot: int, seq: int, stream=None) -> None:
+        call("tsb_ring_publish", self._h, slot, seq, _stream(stream))
+
+    def wait_ready(self, slot: int, seq: int, stream=None) -> None:
+        call("tsb_ring_wait_ready", self._h, slot, seq, _stream(stream))
+
+    def ack(self, consumer: int, seq: int, stream=None) -> None:
+        call("tsb_ring_ack", self._h, consumer, seq, _stream(stream))
+
+    def wait_free(self, live, seq: int, stream=None) -> None:
+        live = list(live)
+        arr = (ctypes.c_int * max(1, len(live)))(*live)
+        call("tsb_ring_wait_free", self._h, arr, len(live), seq, _stream(stream))
+
+    def evict(self, consumer: int) -> None:
+        call("tsb_ring_evict", self._h, consumer)
+
+    def set_cursor(self, consumer: int, value: int) -> None:
+        call("tsb_ring_set_cursor", self._h, consumer, value)
+
+    def read_cursor(self, consumer: int) -> int:
+        v = ctypes.c_uint64()
+        call("tsb_ring_read_cursor", self._h, consumer, ctypes.byref(v))
+        return v.value
+
+    def read_ready(self, slot: int) -> int:
+        v = ctypes.c_uint64()
+        call("tsb_ring_read_ready", self._h, slot, ctypes.byref(v))
+        return v.value
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h and os.getpid() == self.pid:
+            call("tsb_ring_destroy", h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sync_mode() -> str:
+    return "memops" if load().tsb_ring_sync_mode() == 1 else "kernels"
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+
+        return _lib.stream_handle(torch.cuda.current_stream().cuda_stream)
+    return _lib.stream_handle(stream)
