@@ -5,6 +5,10 @@
 // augment of SURVEY.md §8a A6'.  All of them are HBM-bound byte movers
 // (no contraction -> no tensor cores): 128-bit coalesced accesses, source rows
 // staged through shared memory, grids of thousands of CTAs.
+#include <stdlib.h>
+
+#include <utility>
+
 #include "tsb_common.cuh"
 
 using namespace tsb;
@@ -109,15 +113,32 @@ __global__ void aug_params_kernel(uint64_t aug_mixed, uint64_t epoch,
 // ---------------------------------------------------------------------------
 // Fused collate/augment: uint8 HWC -> pad/crop/flip -> normalise -> NCHW.
 //
-// CTA = (sample, block of ROWS output rows).  The crop shifts whole rows, so
-// the source rows of a row block are one contiguous byte range: it is
-// staged into shared memory with 16-byte loads (coalesced, read once), then
-// every thread emits 16-byte stores of VEC consecutive x of one channel row
-// -- NCHW channel planes are written as fully coalesced streams.
-// Normalisation is fl(fl(u*scale)+bias) (no FMA), bit-exact with the oracle.
+// Persistent CTAs (grid = SMs x resident CTAs) walk work items = (sample,
+// block of R output rows), round-robin.  The crop shifts whole rows, so an
+// item's source rows are contiguous in the sample: one elected thread
+// streams them into a shared-memory stage with TMA 1D bulk copies
+// (cp.async.bulk, one per row, completion on an mbarrier) NSTAGE-1 items
+// ahead of the CTA's compute.  Shared rows carry a permanent zero border of
+// `pad` pixels on both sides, and out-of-range source rows point at a zero
+// row, so the inner loop has no bounds checks.
+//
+// Each thread owns fixed (row, group of P consecutive output pixels) slots:
+// it reads the P*C source bytes of its pixels as 32-bit words (funnel-shift
+// realigned; the misalignment depends only on the item's crop offset, so
+// it is CTA-uniform), extracts each byte straight into the float 2^23+u with
+// one PRMT against 0x4B000000 (exact), and writes one 16-byte store per
+// channel plane (NCHW planes are written as coalesced streams).
+// Normalisation is fl(fl(u*scale)+bias) (__fmul_rn/__fadd_rn: no FMA),
+// bit-exact with the oracle; bf16 packs with the hardware RNE
+// cvt.rn.bf16x2.f32.  Crop/flip params for all of the CTA's items are derived
+// in parallel by warp 0 in the prologue (or read from a param table).
+// Sources TMA cannot address (pinned host memory, unaligned rows) use the
+// same loop with cooperative 16-byte LDG staging instead.
 constexpr int CA_THREADS = 256;
-constexpr int CA_ROWS = 8;
 constexpr int MAX_DST = 8;
+constexpr int MAX_STAGES = 16;
+constexpr int MAX_SLOTS = 64;      // slots per thread per item
+constexpr int META_CAP = 64;       // items whose params are cached per CTA
 
 struct Norm {
     float scale[4];
@@ -127,136 +148,345 @@ struct Dsts {
     void *p[MAX_DST];
     int n;
 };
+struct CaGeom {
+    int h, w, b;
+    int pad;
+    int log2r, R;      // rows per item (power of two)
+    int nrb;           // row blocks per sample
+    int items;         // b * nrb
+    int rs;            // shared row stride (bytes)
+    int io;            // interior offset in a shared row (16B aligned)
+    int rdoff;         // io - pad*c: smem col of source pixel sx = rdoff + (sx + pad)*c
+    int row_bytes;     // w*c
+    int groups;        // w / P
+    int slots;         // R * groups
+    int nstage;        // pipeline depth (shared-memory stages)
+    int use_tma;
+    int vec_ldg;       // 16B LDG staging allowed
+    int64_t plane;     // h*w
+    int64_t sample_bytes;
+};
+struct ItemPar {
+    int s, oy, ox, fl;
+    int64_t src_off;  // byte offset of the sample in the store (idx[s] * sample_bytes)
+};
 
 template <int OUT_KIND>
 struct OutTraits;
 template <>
 struct OutTraits<TSB_OUT_U8> {
-    static constexpr int VEC = 16;
+    static constexpr int P = 16;
     static constexpr int ELEM = 1;
 };
 template <>
 struct OutTraits<TSB_OUT_F32> {
-    static constexpr int VEC = 4;
+    static constexpr int P = 4;
     static constexpr int ELEM = 4;
 };
 template <>
 struct OutTraits<TSB_OUT_BF16> {
-    static constexpr int VEC = 8;
+    static constexpr int P = 8;
     static constexpr int ELEM = 2;
 };
 
-__device__ __forceinline__ uint32_t bf16_rne_bits(float f) {
-    uint32_t u = __float_as_uint(f);
-    // inputs are finite (u8 * finite scale + finite bias); RNE on the top half
-    u += 0x7FFFu + ((u >> 16) & 1u);
-    return u >> 16;
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t r;  // RNE for finite values, identical to the oracle's integer RNE
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
 }
 
-template <int OUT_KIND>
-__global__ void __launch_bounds__(CA_THREADS)
-    collate_augment_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
-                           int h, int w, int c, int pad, int flip_en, uint64_t aug_mixed,
-                           uint64_t epoch, Norm norm, const int32_t *__restrict__ params,
-                           Dsts dsts, int vec_src) {
-    using T = OutTraits<OUT_KIND>;
-    extern __shared__ __align__(16) uint8_t rows[];
-    __shared__ int s_par[3];
-
-    const int s = blockIdx.y;
-    const int y0 = blockIdx.x * CA_ROWS;
-    const int nrows = min(CA_ROWS, h - y0);
-    const int row_bytes = w * c;
-    const int64_t sample_bytes = (int64_t)h * row_bytes;
-
-    if (threadIdx.x == 0) {
-        int oy, ox, fl;
-        if (params) {
-            oy = params[3 * s];
-            ox = params[3 * s + 1];
-            fl = params[3 * s + 2];
-        } else {
-            derive_aug(aug_mixed, epoch, idx[s], pad, flip_en, oy, ox, fl);
-        }
-        s_par[0] = oy;
-        s_par[1] = ox;
-        s_par[2] = fl;
+__device__ __forceinline__ ItemPar item_par(const CaGeom &g, int item,
+                                            const int64_t *__restrict__ idx,
+                                            const int32_t *__restrict__ params,
+                                            uint64_t aug_mixed, uint64_t epoch, int flip_en) {
+    ItemPar p;
+    p.s = item / g.nrb;
+    p.src_off = idx[p.s] * g.sample_bytes;
+    if (params) {
+        p.oy = params[3 * p.s];
+        p.ox = params[3 * p.s + 1];
+        p.fl = params[3 * p.s + 2];
+    } else {
+        derive_aug(aug_mixed, epoch, idx[p.s], g.pad, flip_en, p.oy, p.ox, p.fl);
     }
-    __syncthreads();
-    const int oy = s_par[0], ox = s_par[1], fl = s_par[2];
+    return p;
+}
 
-    // contiguous source row range for this row block
-    const int sy_first = y0 + oy - pad;  // source row of output row y0
-    const int lo = max(sy_first, 0);
-    const int hi = min(sy_first + nrows, h);  // exclusive
-    const uint8_t *sample = src + idx[s] * sample_bytes;
-    if (hi > lo) {
-        const uint8_t *g = sample + (int64_t)lo * row_bytes;
-        uint8_t *sm = rows + (lo - sy_first) * row_bytes;
-        const int nbytes = (hi - lo) * row_bytes;
-        if (vec_src) {
-            const int n16 = nbytes >> 4;
-            for (int v = threadIdx.x; v < n16; v += CA_THREADS)
-                reinterpret_cast<uint4 *>(sm)[v] = ld_nc_v4(g + 16 * v);
+// byte k (compile-time) of the realigned word window -> float(u) exactly
+template <int K>
+__device__ __forceinline__ float byte_to_float(const uint32_t *wv) {
+    constexpr uint32_t sel = (K & 3) | (4u << 4) | (5u << 8) | (7u << 12);
+    const uint32_t bits = __byte_perm(wv[K >> 2], 0x4B000000u, sel);
+    return __uint_as_float(bits) - 8388608.0f;  // (2^23 + u) - 2^23, exact
+}
+template <int K>
+__device__ __forceinline__ uint32_t byte_at(const uint32_t *wv) {
+    return (wv[K >> 2] >> (8 * (K & 3))) & 0xFFu;
+}
+
+template <int OUT_KIND, int C, bool FLIP, int Q>
+struct Emit {
+    // element (pixel q, channel ch) -> window byte index
+    static constexpr int kidx(int q, int ch) {
+        return (FLIP ? (OutTraits<OUT_KIND>::P - 1 - q) : q) * C + ch;
+    }
+};
+
+template <int OUT_KIND, int C, bool FLIP, int CH, int... Qs>
+__device__ __forceinline__ uint4 make_vec(const uint32_t *wv, float sc, float bi,
+                                         std::integer_sequence<int, Qs...>) {
+    constexpr int P = OutTraits<OUT_KIND>::P;
+    if constexpr (OUT_KIND == TSB_OUT_U8) {
+        uint32_t b[P] = {byte_at<Emit<OUT_KIND, C, FLIP, 0>::kidx(Qs, CH)>(wv)...};
+        return make_uint4(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24),
+                          b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24),
+                          b[8] | (b[9] << 8) | (b[10] << 16) | (b[11] << 24),
+                          b[12] | (b[13] << 8) | (b[14] << 16) | (b[15] << 24));
+    } else {
+        float f[P] = {__fadd_rn(
+            __fmul_rn(byte_to_float<Emit<OUT_KIND, C, FLIP, 0>::kidx(Qs, CH)>(wv), sc), bi)...};
+        if constexpr (OUT_KIND == TSB_OUT_F32) {
+            return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                              __float_as_uint(f[3]));
         } else {
-            for (int v = threadIdx.x; v < nbytes; v += CA_THREADS) sm[v] = g[v];
+            return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                              pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
         }
     }
-    __syncthreads();
+}
 
-    const int xg_per_row = w / T::VEC;
-    const int items = c * nrows * xg_per_row;
-    const int64_t plane = (int64_t)h * w;
-    for (int it = threadIdx.x; it < items; it += CA_THREADS) {
-        const int xg = it % xg_per_row;
-        const int rc = it / xg_per_row;
-        const int r = rc % nrows;
-        const int ch = rc / nrows;
-        const int sy = sy_first + r;
-        const bool row_ok = (sy >= 0) && (sy < h);
-        const uint8_t *srow = rows + r * row_bytes + ch;
-        const int x0 = xg * T::VEC;
-        uint8_t u[T::VEC];
-#pragma unroll
-        for (int k = 0; k < T::VEC; ++k) {
-            const int x = x0 + k;
-            const int sx = (fl ? (w - 1 - x) : x) + ox - pad;
-            u[k] = (row_ok && sx >= 0 && sx < w) ? srow[sx * c] : (uint8_t)0;
-        }
-        uint4 v;
-        if constexpr (OUT_KIND == TSB_OUT_U8) {
-            uint32_t wv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                wv[q] = (uint32_t)u[4 * q] | ((uint32_t)u[4 * q + 1] << 8) |
-                        ((uint32_t)u[4 * q + 2] << 16) | ((uint32_t)u[4 * q + 3] << 24);
-            v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        } else {
-            // static indexing only (dynamic param-array indexing spills to local)
-            float sc = norm.scale[0], bi = norm.bias[0];
-            if (ch == 1) { sc = norm.scale[1]; bi = norm.bias[1]; }
-            else if (ch == 2) { sc = norm.scale[2]; bi = norm.bias[2]; }
-            else if (ch == 3) { sc = norm.scale[3]; bi = norm.bias[3]; }
-            float f[T::VEC];
-#pragma unroll
-            for (int k = 0; k < T::VEC; ++k) f[k] = __fadd_rn(__fmul_rn((float)u[k], sc), bi);
-            if constexpr (OUT_KIND == TSB_OUT_F32) {
-                v = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
-                               __float_as_uint(f[2]), __float_as_uint(f[3]));
-            } else {
-                uint32_t wv[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    wv[q] = bf16_rne_bits(f[2 * q]) | (bf16_rne_bits(f[2 * q + 1]) << 16);
-                v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-            }
-        }
-        const int64_t off =
-            (((int64_t)s * c + ch) * plane + (int64_t)(y0 + r) * w + x0) * T::ELEM;
+template <int OUT_KIND, int C, bool MULTI, bool FLIP, int CH>
+__device__ __forceinline__ void emit_channel(const uint32_t *wv, const Norm &norm, const Dsts &dsts,
+                                             int64_t off, int64_t plane_bytes) {
+    constexpr int P = OutTraits<OUT_KIND>::P;
+    const uint4 v = make_vec<OUT_KIND, C, FLIP, CH>(wv, norm.scale[CH], norm.bias[CH],
+                                                    std::make_integer_sequence<int, P>{});
+    const int64_t o = off + CH * plane_bytes;
+    if constexpr (!MULTI) {
+        st_v4(static_cast<uint8_t *>(dsts.p[0]) + o, v);
+    } else {
 #pragma unroll
         for (int d = 0; d < MAX_DST; ++d)
-            if (d < dsts.n) st_v4(static_cast<uint8_t *>(dsts.p[d]) + off, v);
+            if (d < dsts.n) st_v4(static_cast<uint8_t *>(dsts.p[d]) + o, v);
     }
+}
+
+template <int OUT_KIND, int C, bool MULTI, bool FLIP, int... CHs>
+__device__ __forceinline__ void emit_pixels(const uint32_t *smem_words, uint32_t ws_off,
+                                            const Norm &norm, const Dsts &dsts, int64_t off,
+                                            int64_t plane_bytes,
+                                            std::integer_sequence<int, CHs...>) {
+    constexpr int P = OutTraits<OUT_KIND>::P;
+    constexpr int NB = P * C;               // window bytes
+    constexpr int NW = (NB + 3) / 4 + 1;    // words incl. misalignment
+    // ws_off: shared byte offset of the window's lowest-address byte
+    const uint32_t *wp = smem_words + (ws_off >> 2);
+    const int shift = 8 * (int)(ws_off & 3);
+    uint32_t raw[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) raw[i] = wp[i];
+    uint32_t wv[NW - 1];
+#pragma unroll
+    for (int i = 0; i < NW - 1; ++i) wv[i] = __funnelshift_r(raw[i], raw[i + 1], shift);
+    (emit_channel<OUT_KIND, C, MULTI, FLIP, CHs>(wv, norm, dsts, off, plane_bytes), ...);
+}
+
+template <int OUT_KIND, int C, bool MULTI>
+__global__ void __launch_bounds__(CA_THREADS + 32)
+    collate_augment_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
+                           CaGeom g, int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
+                           const int32_t *__restrict__ params, Dsts dsts) {
+    using T = OutTraits<OUT_KIND>;
+    constexpr int P = T::P;
+    constexpr int NCW = CA_THREADS / 32;  // consumer warps; warp NCW is the producer
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int stage_bytes = g.R * g.rs;
+    const uint32_t *smem_words = reinterpret_cast<const uint32_t *>(smem);
+    uint8_t *zero_row = smem + g.nstage * stage_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(zero_row + g.rs);
+    uint64_t *empty = full + g.nstage;
+    ItemPar *par = reinterpret_cast<ItemPar *>(empty + g.nstage);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nk = (g.items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+    // zero all stages + the zero row once: borders are never overwritten
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(smem);
+        const int n16 = (g.nstage * stage_bytes + g.rs) >> 4;
+        for (int i = tid; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    // crop/flip params + source offsets of this CTA's items, derived in parallel
+    for (int k = tid; k < min(nk, META_CAP); k += blockDim.x)
+        par[k] = item_par(g, blockIdx.x + k * gridDim.x, idx, params, aug_mixed, epoch, flip_en);
+    if (tid == 0) {
+        for (int i = 0; i < g.nstage; ++i) {
+            mbar_init(&full[i], g.use_tma ? 1 : 32);
+            mbar_init(&empty[i], NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto get_par = [&](int k) -> ItemPar {
+        return k < META_CAP ? par[k]
+                            : item_par(g, blockIdx.x + k * gridDim.x, idx, params, aug_mixed,
+                                       epoch, flip_en);
+    };
+
+    if (warp == NCW) {
+        // ---------------- producer warp: stage source rows -----------------
+        for (int k = 0; k < nk; ++k) {
+            const int st = k % g.nstage;
+            if (k >= g.nstage) mbar_wait(&empty[st], ((k / g.nstage) - 1) & 1);
+            const int item = blockIdx.x + k * gridDim.x;
+            const ItemPar p = get_par(k);
+            const int y0 = (item - p.s * g.nrb) << g.log2r;
+            const int nrows = min(g.R, g.h - y0);
+            const int sy_first = y0 + p.oy - g.pad;
+            const int lo = max(sy_first, 0), hi = min(sy_first + nrows, g.h);
+            const uint8_t *sample = src + p.src_off;
+            uint8_t *dst = smem + st * stage_bytes + g.io;
+            if (g.use_tma) {
+                if (lane == 0) {
+                    fence_proxy_async();
+                    mbar_arrive_expect_tx(&full[st],
+                                          (uint32_t)max(0, hi - lo) * (uint32_t)g.row_bytes);
+                    for (int r = lo; r < hi; ++r)
+                        tma_load_1d(dst + (r - sy_first) * g.rs, sample + (int64_t)r * g.row_bytes,
+                                    (uint32_t)g.row_bytes, &full[st]);
+                }
+            } else {
+                if (g.vec_ldg) {
+                    const int per_row = g.row_bytes >> 4;
+                    const int n16 = max(0, hi - lo) * per_row;
+                    for (int v = lane; v < n16; v += 32) {
+                        const int r = v / per_row, q = v - r * per_row;
+                        const uint4 val =
+                            ld_nc_v4(sample + (int64_t)(lo + r) * g.row_bytes + 16 * q);
+                        uint32_t *d = reinterpret_cast<uint32_t *>(dst + (lo + r - sy_first) * g.rs +
+                                                                   16 * q);
+                        d[0] = val.x;  // io may only be 4B aligned
+                        d[1] = val.y;
+                        d[2] = val.z;
+                        d[3] = val.w;
+                    }
+                } else {
+                    const int n = max(0, hi - lo) * g.row_bytes;
+                    for (int v = lane; v < n; v += 32) {
+                        const int r = v / g.row_bytes, q = v - r * g.row_bytes;
+                        dst[(lo + r - sy_first) * g.rs + q] =
+                            sample[(int64_t)(lo + r) * g.row_bytes + q];
+                    }
+                }
+                mbar_arrive(&full[st]);  // release: this lane's staging stores
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps: emit normalised NCHW ------------------
+    const int64_t plane_bytes = g.plane * T::ELEM;
+    // first slot of this thread; further slots every CA_THREADS (no divisions in the loop)
+    const int r_first = tid / g.groups;
+    const int x_first = (tid - r_first * g.groups) * P;
+    const int dr = CA_THREADS / g.groups;
+    const int dx = (CA_THREADS - dr * g.groups) * P;
+    for (int k = 0; k < nk; ++k) {
+        const int st = k % g.nstage;
+        const int item = blockIdx.x + k * gridDim.x;
+        const ItemPar p = get_par(k);
+        const int y0 = (item - p.s * g.nrb) << g.log2r;
+        const int nrows = min(g.R, g.h - y0);
+        const int sy_first = y0 + p.oy - g.pad;
+        const int lo = max(sy_first, 0), hi = min(sy_first + nrows, g.h);
+        const int64_t out_item = ((int64_t)p.s * C * g.plane + (int64_t)y0 * g.w) * T::ELEM;
+        mbar_wait(&full[st], (k / g.nstage) & 1);
+        int r = r_first, x0 = x_first;
+#pragma unroll 1
+        for (int sl = tid; sl < g.slots; sl += CA_THREADS) {
+            if (r < nrows) {
+                const int sy = sy_first + r;
+                const uint32_t row_off = (sy >= lo && sy < hi)
+                                             ? (uint32_t)(st * stage_bytes + r * g.rs)
+                                             : (uint32_t)(g.nstage * stage_bytes);
+                const int64_t off = out_item + ((int64_t)r * g.w + x0) * T::ELEM;
+                if (!p.fl) {
+                    const uint32_t ws = row_off + g.rdoff + (x0 + p.ox) * C;
+                    emit_pixels<OUT_KIND, C, MULTI, false>(smem_words, ws, norm, dsts, off,
+                                                           plane_bytes,
+                                                           std::make_integer_sequence<int, C>{});
+                } else {
+                    const uint32_t ws = row_off + g.rdoff + (g.w - P - x0 + p.ox) * C;
+                    emit_pixels<OUT_KIND, C, MULTI, true>(smem_words, ws, norm, dsts, off,
+                                                          plane_bytes,
+                                                          std::make_integer_sequence<int, C>{});
+                }
+            }
+            r += dr;
+            x0 += dx;
+            if (x0 >= g.w) {
+                x0 -= g.w;
+                r += 1;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
+    }
+}
+
+template <int K, int C, bool MULTI>
+int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
+              uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
+              size_t smem, cudaStream_t s) {
+    auto kern = collate_augment_kernel<K, C, MULTI>;
+    static int occ_cache[64] = {0};
+    static size_t smem_cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) dev = 63;
+    if (smem_cache[dev] != smem) {
+        TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CA_THREADS + 32, smem));
+        occ_cache[dev] = occ > 0 ? occ : 1;
+        smem_cache[dev] = smem;
+    }
+    const int slots = sm_count() * occ_cache[dev];
+    const int grid = g.items < slots ? g.items : slots;
+    kern<<<grid, CA_THREADS + 32, smem, s>>>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts);
+    TSB_LAUNCH_CHECK();
+    return TSB_OK;
+}
+
+template <int K, int C>
+int launch_ca_m(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
+                uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
+                size_t smem, cudaStream_t s) {
+    if (dsts.n == 1)
+        return launch_ca<K, C, false>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+    return launch_ca<K, C, true>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+}
+
+template <int K>
+int launch_ca_c(int c, const uint8_t *src, const int64_t *idx, CaGeom g, int flip,
+                uint64_t aug_mixed, uint64_t epoch, const Norm &norm, const int32_t *params,
+                const Dsts &dsts, size_t smem, cudaStream_t s) {
+    switch (c) {
+        case 1: return launch_ca_m<K, 1>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+        case 2: return launch_ca_m<K, 2>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+        case 3: return launch_ca_m<K, 3>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+        default: return launch_ca_m<K, 4>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+    }
+}
+
+int is_device_memory(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return a.type == cudaMemoryTypeDevice;
 }
 
 int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, int w, int c,
@@ -266,47 +496,72 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     TSB_CHECK(src && d_indices, "null src/indices");
     TSB_CHECK(b >= 0 && h > 0 && w > 0 && c > 0 && c <= 4, "bad shape b=%lld h=%d w=%d c=%d",
               (long long)b, h, w, c);
-    TSB_CHECK(pad >= 0 && pad <= 1 << 20, "bad pad %d", pad);
+    TSB_CHECK(pad >= 0 && pad <= 4096, "bad pad %d", pad);
     TSB_CHECK(out_kind >= TSB_OUT_U8 && out_kind <= TSB_OUT_BF16, "bad out_kind %d", out_kind);
-    TSB_CHECK(b <= 65535, "batch %lld exceeds grid.y limit", (long long)b);
     if (b == 0) return TSB_OK;
     const int vec = out_kind == TSB_OUT_U8 ? 16 : out_kind == TSB_OUT_F32 ? 4 : 8;
-    const int elem = out_kind == TSB_OUT_U8 ? 1 : out_kind == TSB_OUT_F32 ? 4 : 2;
     TSB_CHECK(w % vec == 0, "width %d must be a multiple of %d for this output kind", w, vec);
     for (int d = 0; d < dsts.n; ++d)
         TSB_CHECK(((uintptr_t)dsts.p[d] & 15) == 0, "output must be 16-byte aligned");
-    (void)elem;
     Norm norm;
     for (int i = 0; i < 4; ++i) {
         norm.scale[i] = (scale && i < c) ? scale[i] : 1.0f;
         norm.bias[i] = (bias && i < c) ? bias[i] : 0.0f;
     }
-    const int row_bytes = w * c;
-    const int vec_src = ((row_bytes & 15) == 0) && (((uintptr_t)src & 15) == 0);
-    const size_t smem = (size_t)CA_ROWS * row_bytes;
+    CaGeom g{};
+    g.h = h;
+    g.w = w;
+    g.b = (int)b;
+    g.pad = pad;
+    g.row_bytes = w * c;
+    g.sample_bytes = (int64_t)h * w * c;
+    g.plane = (int64_t)h * w;
+    // interior 16B aligned for TMA; >= 4 spare bytes each side for the word window
+    g.io = (pad * c + 4 + 15) & ~15;
+    g.rdoff = g.io - pad * c;
+    g.rs = (g.io + w * c + pad * c + 8 + 15) & ~15;
+    g.groups = w / vec;
+    const bool aligned_rows = (g.row_bytes % 16 == 0) && (((uintptr_t)src & 15) == 0) &&
+                              (g.sample_bytes % 16 == 0);
+    g.use_tma = aligned_rows && is_device_memory(src);
+    if (const char *e = getenv("TSB_CA_NOTMA")) g.use_tma = g.use_tma && !atoi(e);
+    g.vec_ldg = aligned_rows && (g.io % 4 == 0);
+    // rows per item (measured on B200, B=256 224x224x3): enough output per item to
+    // amortise the per-item pipeline handoff -- f32 R=4 (10.7 KB out), bf16/u8 R=16.
+    int R = out_kind == TSB_OUT_F32 ? 4 : 16;
+    while (R > 1 && (int64_t)R > h) R >>= 1;
+    while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R >>= 1;
+    int nstage = 4;
+    if (const char *e = getenv("TSB_CA_R")) R = atoi(e);          // tuning knobs
+    if (const char *e = getenv("TSB_CA_STAGES")) nstage = atoi(e);
+    TSB_CHECK(R >= 1 && R <= 64 && (R & (R - 1)) == 0, "rows per item must be a power of 2 <= 64");
+    TSB_CHECK(nstage >= 2 && nstage <= MAX_STAGES, "stages must be 2..%d", MAX_STAGES);
+    if (R > h) R = 1;
+    TSB_CHECK(R * g.groups <= MAX_SLOTS * CA_THREADS, "image width %d too large", w);
+    while (nstage > 2 && (size_t)(nstage * R + 1) * g.rs + 2048 > 64 * 1024) --nstage;
+    while (R > 1 && (size_t)(nstage * R + 1) * g.rs + 2048 > 200 * 1024) R >>= 1;
+    g.R = R;
+    g.nstage = nstage;
+    g.log2r = 0;
+    while ((1 << g.log2r) < R) ++g.log2r;
+    g.nrb = (h + R - 1) / R;
+    TSB_CHECK(b * (int64_t)g.nrb < (1ll << 31), "too many work items");
+    g.items = (int)(b * g.nrb);
+    g.slots = R * g.groups;
+    const size_t smem = (size_t)(nstage * R + 1) * g.rs + 2 * nstage * sizeof(uint64_t) +
+                        META_CAP * sizeof(ItemPar);
     TSB_CHECK(smem <= 200 * 1024, "row too wide for shared staging (%zu B)", smem);
     const uint64_t aug_mixed = mix64(aug_seed ^ AUG_DOMAIN);
-    dim3 grid((h + CA_ROWS - 1) / CA_ROWS, (unsigned)b);
+    const auto *s8 = static_cast<const uint8_t *>(src);
     auto s = as_stream(stream);
-#define TSB_LAUNCH_CA(K)                                                                   \
-    do {                                                                                   \
-        if (smem > 48 * 1024)                                                              \
-            TSB_CUDA(cudaFuncSetAttribute(collate_augment_kernel<K>,                       \
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                          (int)smem));                                     \
-        collate_augment_kernel<K><<<grid, CA_THREADS, smem, s>>>(                          \
-            static_cast<const uint8_t *>(src), d_indices, h, w, c, pad, flip, aug_mixed,   \
-            epoch, norm, d_params, dsts, vec_src);                                         \
-    } while (0)
     if (out_kind == TSB_OUT_U8)
-        TSB_LAUNCH_CA(TSB_OUT_U8);
-    else if (out_kind == TSB_OUT_F32)
-        TSB_LAUNCH_CA(TSB_OUT_F32);
-    else
-        TSB_LAUNCH_CA(TSB_OUT_BF16);
-#undef TSB_LAUNCH_CA
-    TSB_LAUNCH_CHECK();
-    return TSB_OK;
+        return launch_ca_c<TSB_OUT_U8>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
+                                       dsts, smem, s);
+    if (out_kind == TSB_OUT_F32)
+        return launch_ca_c<TSB_OUT_F32>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
+                                        dsts, smem, s);
+    return launch_ca_c<TSB_OUT_BF16>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
+                                     dsts, smem, s);
 }
 
 }  // namespace
