@@ -1,0 +1,262 @@
+"""Device batch production: dataset model + the fused collate/augment loader.
+
+Mirrors the reference dataset model (bs/pipeline.py:32-123):
+
+* ``SyntheticSource(seed, sample_shape, dtype)`` -- sample bytes are the
+  SplitMix64 stream keyed ``derive_key(seed, epoch, idx)``, generated
+  straight into the ring slot by ``tsb_fill_synthetic`` (pipeline.py:183-189).
+* ``StoreSource`` -- DirectorySource semantics (pipeline.py:45-54,190-210):
+  a fixed sample store (sample i never changes across epochs) resident in
+  HBM or in pinned host memory (the kernel reads host memory directly over
+  PCIe).  ``StoreSource.synthetic(...)`` materialises the store of
+  ``write_directory_dataset`` (pipeline.py:139-155) with ``tsb_make_store``.
+* ``DatasetSpec`` -- samples_per_epoch, batch_size, shuffle seed, drop-last
+  ``epoch_len = N // B`` (pipeline.py:57-97); the per-epoch order is the
+  reference Fisher-Yates permutation (host C++, uploaded once per epoch).
+* ``AugmentSpec`` -- NEW (no reference): RandomCrop(pad)+HFlip+Normalize with
+  params from the reference RNG (SURVEY.md §8a A6'), output NCHW
+  float32/bfloat16/uint8.
+
+``CollateLoader`` is what a ``TensorProducer`` wraps for the B200 path: it
+writes each batch (input, then int64 sample indices as the target) directly
+into a ring slot with one kernel launch + one tiny D2D copy.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import dataplane as dp
+from .wire import DType
+
+
+@dataclass(frozen=True)
+class SyntheticSource:
+    seed: int = 0
+    sample_shape: tuple = (256,)
+    dtype: DType = DType.U8
+
+    @property
+    def sample_nbytes(self) -> int:
+        return int(np.prod(self.sample_shape)) * DType(self.dtype).size
+
+
+class StoreSource:
+    """Fixed sample store (DirectorySource semantics) in HBM or pinned host memory."""
+
+    def __init__(self, samples, sample_shape, dtype: DType = DType.U8):
+        import torch
+
+        self.samples = samples  # flat uint8 tensor: N * sample_nbytes
+        self.sample_shape = tuple(sample_shape)
+        self.dtype = DType(dtype)
+        if samples.dtype != torch.uint8 or samples.dim() != 1:
+            raise TypeError("store must be a flat uint8 tensor")
+        if not samples.is_cuda and not samples.is_pinned():
+            raise ValueError("store must live in HBM (cuda) or pinned host memory")
+        self.num_samples = samples.numel() // self.sample_nbytes
+
+    @property
+    def sample_nbytes(self) -> int:
+        return int(np.prod(self.sample_shape)) * self.dtype.size
+
+    @property
+    def location(self) -> str:
+        return "hbm" if self.samples.is_cuda else "pinned"
+
+    @classmethod
+    def synthetic(cls, seed: int, num_samples: int, sample_shape, dtype: DType = DType.U8,
+                  location: str = "hbm"):
+        """Store whose file i = fill(derive_key(seed, 0, i)) (pipeline.py:139-155)."""
+        import torch
+
+        sb = int(np.prod(sample_shape)) * DType(dtype).size
+        if sb % 8:
+            raise ValueError("sample size must be a multiple of 8 bytes")
+        dev = torch.empty(num_samples * sb, dtype=torch.uint8, device="cuda")
+        dp.make_store(dev, seed, num_samples, sb)
+        if location == "hbm":
+            return cls(dev, sample_shape, dtype)
+        host = torch.empty(num_samples * sb, dtype=torch.uint8).pin_memory()
+        host.copy_(dev)
+        del dev
+        return cls(host, sample_shape, dtype)
+
+
+@dataclass(frozen=True)
+class DatasetSpec:
+    source: object
+    samples_per_epoch: int
+    batch_size: int
+    shuffle_seed: int = 0
+    reshuffle_each_epoch: bool = True
+
+    def __post_init__(self):
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.samples_per_epoch < self.batch_size:
+            raise ValueError("samples_per_epoch must be >= batch_size")
+        if isinstance(self.source, SyntheticSource) and self.source.sample_nbytes % 8:
+            raise ValueError("synthetic sample size must be a multiple of 8 bytes "
+                             f"(got {self.source.sample_nbytes})")
+        if isinstance(self.source, StoreSource) and \
+                self.samples_per_epoch > self.source.num_samples:
+            raise ValueError("samples_per_epoch exceeds the store")
+
+    @property
+    def epoch_len(self) -> int:
+        return self.samples_per_epoch // self.batch_size
+
+
+@dataclass(frozen=True)
+class AugmentSpec:
+    pad: int = 16
+    flip: bool = True
+    mean: tuple = dp.IMAGENET_MEAN
+    std: tuple = dp.IMAGENET_STD
+    out_dtype: str = "float32"      # float32 | bfloat16 | uint8 (crop/flip only)
+    seed: int = 0
+    normalize: bool = True
+
+    @property
+    def out_kind(self) -> int:
+        return {"float32": dp.OUT_F32, "bfloat16": dp.OUT_BF16, "uint8": dp.OUT_U8}[self.out_dtype]
+
+    @property
+    def wire_dtype(self) -> DType:
+        return {"float32": DType.F32, "bfloat16": DType.BF16, "uint8": DType.U8}[self.out_dtype]
+
+
+@dataclass
+class _EpochOrder:
+    epoch: int = -1
+    host: np.ndarray | None = None
+    dev: object = None
+
+
+class CollateLoader:
+    """Device data loader: ``len()`` batches per epoch; each batch is produced
+    straight into caller memory (a ring slot) by sm_100a kernels.
+
+    Layout of a produced batch (the reference pair encoding, sl/abi.py:27-31):
+    ``input`` bytes followed by ``target`` = int64 sample indices [B].
+    input = (B, *sample_shape) raw samples, or (B, C, H, W) with an AugmentSpec
+    (sample_shape must be (H, W, C) uint8).
+    """
+
+    def __init__(self, dataset: DatasetSpec, augment: AugmentSpec | None = None,
+                 with_target: bool = True, device: int | None = None):
+        import torch
+
+        self.dataset = dataset
+        self.augment = augment
+        self.with_target = with_target
+        self.device = torch.cuda.current_device() if device is None else device
+        self._order = _EpochOrder()
+        self.epoch = 0  # the epoch __iter__ produces next
+        src = dataset.source
+        if augment is not None:
+            if DType(src.dtype) != DType.U8 or len(src.sample_shape) != 3:
+                raise ValueError("augment needs uint8 HWC samples")
+            if isinstance(src, SyntheticSource):
+                raise ValueError("augment reads from a StoreSource")
+            self._scale, self._bias = (dp.norm_consts(augment.mean, augment.std)
+                                       if augment.normalize and augment.out_kind != dp.OUT_U8
+                                       else (None, None))
+
+    # -- geometry ----------------------------------------------------------
+    def __len__(self) -> int:
+        return self.dataset.epoch_len
+
+    @property
+    def input_shape(self) -> tuple:
+        src, b = self.dataset.source, self.dataset.batch_size
+        if self.augment is None:
+            return (b, *src.sample_shape)
+        h, w, c = src.sample_shape
+        return (b, c, h, w)
+
+    @property
+    def input_dtype(self) -> DType:
+        return self.augment.wire_dtype if self.augment else DType(self.dataset.source.dtype)
+
+    @property
+    def input_nbytes(self) -> int:
+        return int(np.prod(self.input_shape)) * self.input_dtype.size
+
+    @property
+    def target_shape(self) -> tuple:
+        return (self.dataset.batch_size,) if self.with_target else (0,)
+
+    @property
+    def target_dtype(self) -> DType:
+        return DType.I64
+
+    @property
+    def batch_nbytes(self) -> int:
+        return self.input_nbytes + (8 * self.dataset.batch_size if self.with_target else 0)
+
+    @property
+    def h2d_bytes_per_batch(self) -> int:
+        """Bytes that cross PCIe per batch (pinned-host store ingest)."""
+        src = self.dataset.source
+        if isinstance(src, StoreSource) and src.location == "pinned":
+            return self.dataset.batch_size * src.sample_nbytes
+        return 0
+
+    # -- epoch order -----------------------------------------------------------
+    def order(self, epoch: int):
+        """(host int64 order, device int64 order) of an epoch (pipeline.py:113-123)."""
+        import torch
+
+        if self._order.epoch != epoch:
+            d = self.dataset
+            host = dp.epoch_order(d.samples_per_epoch, d.shuffle_seed, epoch,
+                                  d.reshuffle_each_epoch)
+            dev = torch.from_numpy(host).to(f"cuda:{self.device}", non_blocking=False)
+            self._order = _EpochOrder(epoch, host, dev)
+        return self._order.host, self._order.dev
+
+    def indices(self, epoch: int, batch_index: int) -> np.ndarray:
+        host, _ = self.order(epoch)
+        b = self.dataset.batch_size
+        return host[batch_index * b:(batch_index + 1) * b]
+
+    # -- production ----------------------------------------------------------
+    def produce_into(self, out_ptr: int, epoch: int, batch_index: int, stream=None) -> None:
+        """Write batch (epoch, batch_index) at device address out_ptr (ring slot)."""
+        if batch_index >= len(self):
+            raise ValueError(f"batch_index {batch_index} >= epoch_len {len(self)}")
+        _, dorder = self.order(epoch)
+        d = self.dataset
+        b = d.batch_size
+        didx = dorder[batch_index * b:(batch_index + 1) * b]
+        src = d.source
+        if isinstance(src, SyntheticSource):
+            dp.fill_synthetic(out_ptr, didx, b, src.seed, epoch, src.sample_nbytes, stream)
+        elif self.augment is None:
+            dp.gather(src.samples, didx, b, src.sample_nbytes, out_ptr, stream)
+        else:
+            a = self.augment
+            h, w, c = src.sample_shape
+            dp.collate_augment(src.samples, didx, b, h, w, c, a.pad, a.flip, a.seed, epoch,
+                               a.out_kind, out_ptr, scale=self._scale, bias=self._bias,
+                               stream=stream)
+        if self.with_target:
+            dp.memcpy_async(out_ptr + self.input_nbytes, didx, 8 * b, stream)
+
+    def __iter__(self):
+        """Standalone (non-shared) iteration: fresh device tensors per batch."""
+        import torch
+
+        epoch = self.epoch
+        self.epoch += 1
+        for i in range(len(self)):
+            buf = torch.empty(self.batch_nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+            self.produce_into(buf.data_ptr(), epoch, i)
+            inp = buf[:self.input_nbytes].view(getattr(torch, self.input_dtype.torch_name))
+            inp = inp.view(self.input_shape)
+            tgt = buf[self.input_nbytes:].view(torch.int64) if self.with_target else None
+            yield inp, tgt

@@ -108,8 +108,25 @@ __global__ void wait_kernel(WaitSet set, uint64_t value) {
     __threadfence_system();
 }
 
+// Driver-API stream memops need a current context on the calling thread;
+// runtime calls create it lazily, so bind the ring's device first.
+int bind_ctx(int dev) {
+    static thread_local int bound_dev = -1;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) {
+        TSB_CUDA(cudaSetDevice(dev));
+        bound_dev = -1;
+    }
+    if (bound_dev != dev) {
+        TSB_CUDA(cudaFree(nullptr));  // no-op that makes the primary context current
+        bound_dev = dev;
+    }
+    return TSB_OK;
+}
+
 int dev_write(tsb_ring *r, uint64_t *addr, uint64_t v, void *stream) {
     if (resolve_mode() == 1) {
+        if (int rc = bind_ctx(r->dev)) return rc;
         CUresult e = g_write64((CUstream)stream, (CUdeviceptr)addr, v, 0);
         if (e != CUDA_SUCCESS) {
             set_error("cuStreamWriteValue64 failed (%d)", (int)e);
@@ -123,9 +140,10 @@ int dev_write(tsb_ring *r, uint64_t *addr, uint64_t v, void *stream) {
     return TSB_OK;
 }
 
-int dev_wait(const uint64_t *const *addrs, int n, uint64_t v, void *stream) {
+int dev_wait(tsb_ring *r, const uint64_t *const *addrs, int n, uint64_t v, void *stream) {
     if (n <= 0) return TSB_OK;
     if (resolve_mode() == 1) {
+        if (int rc = bind_ctx(r->dev)) return rc;
         for (int i = 0; i < n; ++i) {
             CUresult e = g_wait64((CUstream)stream, (CUdeviceptr)addrs[i], v,
                                   CU_STREAM_WAIT_VALUE_GEQ);
@@ -281,7 +299,7 @@ int tsb_ring_publish(tsb_ring *r, int slot, uint64_t seq, void *stream) {
 int tsb_ring_wait_ready(tsb_ring *r, int slot, uint64_t seq, void *stream) {
     TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
     const uint64_t *a = r->ready + slot;
-    return dev_wait(&a, 1, seq, stream);
+    return dev_wait(r, &a, 1, seq, stream);
 }
 int tsb_ring_ack(tsb_ring *r, int consumer, uint64_t seq, void *stream) {
     TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
@@ -296,7 +314,7 @@ int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, v
         TSB_CHECK(live[i] >= 0 && live[i] < r->max_consumers, "bad consumer %d", live[i]);
         addrs[i] = r->cursor + live[i];
     }
-    return dev_wait(addrs, n_live, seq, stream);
+    return dev_wait(r, addrs, n_live, seq, stream);
 }
 int tsb_ring_evict(tsb_ring *r, int consumer) {
     TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);

@@ -158,3 +158,8 @@ __all__ = [
     "epoch_order", "norm_consts", "fill_synthetic", "make_store", "gather", "aug_params",
     "collate_augment", "collate_augment_fanout", "crc32", "fanout", "rebatch_gather",
 ]
+
+
+def memcpy_async(dst, src, nbytes: int, stream=None) -> None:
+    """cudaMemcpyAsync(Default) on the given stream (device/pinned pointers or tensors)."""
+    call("tsb_memcpy_async", ptr(dst), ptr(src), nbytes, current_stream(stream))
