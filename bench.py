@@ -1,0 +1,471 @@
+"""Benchmark of the shared-loading hot path on B200 (prints ONE JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU)
+
+Workload (BASELINE.json configs[1], "C2"): 1 producer + 4 consumers on one
+B200 via CUDA IPC zero copy, ResNet-50-shaped batches of 256: a
+DirectorySource-equivalent store of 16,384 uint8 224x224x3 samples
+(SplitMix64, the reference RNG), the reference epoch shuffle, then the fused
+collate/augment (RandomCrop pad 16 + HFlip with params from the reference RNG,
+ImageNet normalise) to float32 NCHW written into the device ring; consumers in
+other processes map the ring over CUDA IPC and release slots with
+device-counted acks.  A step = one batch of 256 produced and delivered to all
+4 consumers.  N > 1: one independent producer + 4 consumers per GPU (weak
+scaling; the units -- batches -- are sharded across ranks, no data-path
+collective).
+
+value: delivered samples/s summed over all consumers (the reference's
+aggregate metric, bs/harness.py:574 + bs/cli.py:220-236), inputs resident in
+HBM, native producer loop, device-timed (CUDA events), max over ranks.
+e2e:   the same metric through the public API (TensorProducer(CollateLoader)
++ SharedLoader consumer processes), samples read from a PINNED HOST store by
+the kernel over PCIe every step; each consumer reads back one element per
+batch (.item(), the "step result"); consumer-side fetch timestamps with the
+reference formula.
+--impl reference: the CPU oracle port (oracle/, C + OpenMP, the reference
+path restated: shuffle + collate(+augment) + CRC per batch) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W, C = 224, 224, 3
+SAMPLE_BYTES = H * W * C           # 150,528 B u8 HWC
+B = 256
+N_SAMPLES = 16384                  # samples_per_epoch
+N_CONSUMERS = 4
+RING_SLOTS = 8
+PAD = 16
+OUT_BYTES = C * H * W * 4          # f32 NCHW per sample
+ALG_BYTES_PER_SAMPLE = SAMPLE_BYTES + OUT_BYTES  # 752,640 B read + write (collate)
+METRIC = "delivered samples/sec (all consumers)"
+WORKLOAD = ("C2: 1 producer + 4 same-GPU consumers via CUDA IPC zero copy, 224x224x3 u8 store "
+            "-> ResNet-50-shaped f32 NCHW (crop pad16 + hflip from the reference RNG + ImageNet "
+            "normalise), batch 256")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- helpers ---
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.rows = []
+        self._p = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self._p = None
+
+    def _read(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self._p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self._p.terminate()
+        try:
+            self._p.wait(2)
+        except subprocess.TimeoutExpired:
+            self._p.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the collate kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("collate_f32_b256_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------- consumer workers ---
+def device_consumer(dev, handle, slots, slot_bytes, max_consumers, cursor, warmup, steps, q):
+    """Minimal consumer process: maps the ring over CUDA IPC, waits for each
+    batch and releases it (device-counted ack); device-timed."""
+    import torch
+
+    torch.cuda.set_device(dev)
+    from paper_2409_18749_b200 import dataplane as dp
+    from paper_2409_18749_b200.ring import DeviceRing, consume_range
+
+    ring = DeviceRing.import_handle(handle, slots, slot_bytes, max_consumers)
+    s = torch.cuda.Stream()
+    e0, e1 = dp.DeviceEvent(), dp.DeviceEvent()
+    q.put(("ready", cursor))
+    consume_range(ring, cursor, 1, warmup, stream=s)
+    consume_range(ring, cursor, warmup + 1, steps, events=[e0, e1], stream=s)
+    s.synchronize()
+    q.put(("done", cursor, e0.elapsed_ms(e1)))
+    ring.close()
+
+
+def api_consumer(dev, bcast, agg, cid, warmup, steps, q):
+    """e2e consumer through the public API: SharedLoader over CUDA IPC; reads
+    one element per batch back to the host (the step result)."""
+    import torch
+
+    torch.cuda.set_device(dev)
+    from paper_2409_18749_b200 import SharedLoader
+
+    loader = SharedLoader(bcast, agg, consumer_id=cid)
+    times, n = [], 0
+    q.put(("ready", cid))
+    for _epoch in range(1 << 20):
+        for inp, tgt in loader:
+            _ = float(inp.view(-1)[0].item())  # D2H of the step result (4 B)
+            n += 1
+            if n > warmup:
+                times.append(time.monotonic())
+            if n >= warmup + steps:
+                break
+        if n >= warmup + steps or loader.finished:
+            break
+    loader.close()
+    rate = (len(times) - 1) / (times[-1] - times[0]) * B if len(times) > 1 else 0.0
+    q.put(("done", cid, rate, n))
+
+
+# --------------------------------------------------------------- ours ------
+def run_ours(args):
+    import multiprocessing as mp
+
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = local
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec, StoreSource,
+                                       TensorProducer)
+    from paper_2409_18749_b200 import dataplane as dp
+    from paper_2409_18749_b200.ring import DeviceRing, produce_range, sync_mode
+
+    K, Wm = args.steps, args.warmup
+    ctx = mp.get_context("spawn")
+
+    # ---- device-resident run (value) ----
+    store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="hbm")
+    ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
+    loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
+    ring = DeviceRing(RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, device=dev)
+    handle = ring.export()
+    q = ctx.Queue()
+    procs = [ctx.Process(target=device_consumer,
+                         args=(dev, handle, RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, k, Wm, K, q))
+             for k in range(N_CONSUMERS)]
+    for p in procs:
+        p.start()
+    for _ in procs:
+        assert q.get(timeout=300)[0] == "ready"
+    stream = torch.cuda.Stream()
+    live = list(range(N_CONSUMERS))
+    L = len(loader)
+
+    def produce(seq0, n, events=None):
+        """Enqueue n batches starting at global seq0 (1-based), across epochs."""
+        done = 0
+        while done < n:
+            q0 = seq0 + done
+            epoch, bi = divmod(q0 - 1, L)
+            m = min(n - done, L - bi)
+            a = loader.produce_args(epoch)
+            evs = None if events is None else events[2 * done:2 * (done + m)]
+            produce_range(ring, a, q0, bi, m, live, events=evs, stream=stream)
+            done += m
+
+    produce(1, Wm)
+    stream.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    kev = [dp.DeviceEvent() for _ in range(2 * K)]
+    t0, t1 = dp.DeviceEvent(), dp.DeviceEvent()
+    clocks = Clocks(dev)
+    clocks.start()
+    t0.record(stream)
+    produce(Wm + 1, K, events=kev)
+    t1.record(stream)
+    stream.synchronize()
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_ms(t1)
+    cons_ms = {}
+    for _ in procs:
+        msg = q.get(timeout=300)
+        cons_ms[msg[1]] = msg[2]
+    for p in procs:
+        p.join(60)
+    launch_ms = [kev[2 * i].elapsed_ms(kev[2 * i + 1]) for i in range(K)]
+    avg_launch_ms = sum(launch_ms) / K
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    else:
+        ms_max = ms
+    value = world * N_CONSUMERS * B * K / (ms_max / 1e3)
+    consumer_rates = {k: (K - 1) * B / (v / 1e3) for k, v in cons_ms.items() if v > 0}
+    ring.close()
+    del store, loader
+
+    # ---- e2e through the public API (pinned host store, PCIe ingest) ----
+    e2e = run_e2e(args, ctx, dev, rank, world)
+
+    peak, peak_src = measured_hbm_peak()
+    achieved = B * ALG_BYTES_PER_SAMPLE / (avg_launch_ms / 1e3) / 1e9
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
+        "steps": K, "warmup": Wm, "ms_per_step": round(ms_max / K, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: SplitMix64 DirectorySource-equivalent store (reference RNG), "
+                "reference Fisher-Yates epoch order",
+        "config": {"workload": WORKLOAD, "global_batch": B * world, "batch_per_gpu": B,
+                   "consumers_per_gpu": N_CONSUMERS, "samples_per_epoch": N_SAMPLES,
+                   "ring_slots": RING_SLOTS, "sample": "224x224x3 u8 -> 3x224x224 f32",
+                   "store": "HBM-resident (value) / pinned host (e2e)",
+                   "l2": "inputs larger than L2: 2.47 GB store, 1.2 GB ring of 8 slots",
+                   "parallelism": f"weak: {world} independent producer(s), 4 IPC consumers each",
+                   "sync": sync_mode()},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(), "kernel": "collate_augment_kernel<f32,C=3>",
+                     "alg_bytes_per_launch": B * ALG_BYTES_PER_SAMPLE,
+                     "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src},
+        "e2e": e2e,
+        "gpu_launches": K,
+        "clocks": clk,
+        "extra": {"producer_ms": round(ms, 3),
+                  "consumer_rates_samples_s": {str(k): round(v, 1) for k, v in consumer_rates.items()},
+                  "produced_samples_per_s": round(world * B * K / (ms_max / 1e3), 1),
+                  "collate_launch_ms_min": round(min(launch_ms), 5),
+                  "collate_launch_ms_max": round(max(launch_ms), 5)},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def run_e2e(args, ctx, dev, rank, world):
+    import torch
+
+    from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec, StoreSource,
+                                       TensorProducer)
+
+    K, Wm = args.steps, args.warmup
+    tmp = f"/tmp/tsb-bench-{os.getpid()}"
+    os.makedirs(tmp, exist_ok=True)
+    bcast, agg = f"unix:{tmp}/b.sock", f"unix:{tmp}/a.sock"
+    store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="pinned")
+    ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
+    loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
+    producer = TensorProducer(loader, bcast, agg, min_consumers=N_CONSUMERS, ring_slots=RING_SLOTS,
+                              heartbeat_timeout_s=60.0)
+    q = ctx.Queue()
+    procs = [ctx.Process(target=api_consumer, args=(dev, bcast, agg, 1000 + k, Wm, K, q))
+             for k in range(N_CONSUMERS)]
+    for p in procs:
+        p.start()
+    total = Wm + K
+    t_start = time.monotonic()
+    produced = 0
+    while produced < total:
+        for _ in producer:
+            produced += 1
+            if produced >= total:
+                break
+    producer.join(drain_timeout_s=60)
+    rates = {}
+    for _ in procs:
+        msg = q.get(timeout=300)
+        while msg[0] != "done":
+            msg = q.get(timeout=300)
+        rates[msg[1]] = msg[2]
+    for p in procs:
+        p.join(60)
+    producer.close()
+    wall = time.monotonic() - t_start
+    value = sum(rates.values())
+    if world > 1:
+        t = torch.tensor([value], device="cuda")
+        torch.distributed.all_reduce(t)
+        value = float(t.item())
+    return {"value": round(value, 1), "unit": "samples/s",
+            "h2d_bytes_per_step": B * SAMPLE_BYTES,
+            "d2h_bytes_per_step": 4 * N_CONSUMERS,
+            "path": "TensorProducer(CollateLoader(pinned-host StoreSource)) -> 4 SharedLoader "
+                    "processes (CUDA IPC); kernel reads samples over PCIe; consumers .item() "
+                    "one element per batch",
+            "per_consumer": {str(k): round(v, 1) for k, v in rates.items()},
+            "wall_s": round(wall, 2), "batches_produced": produced}
+
+
+# -------------------------------------------------------------- CPU port ----
+def cpu_reference_step(o, store, order, bi, nthreads, out, scale, bias):
+    """One batch of the reference CPU path, restated (oracle/): collate +
+    augment (f32 NCHW) on all threads, then the segment CRC (payload.py:218)."""
+    idx = order[bi * B:(bi + 1) * B]
+    o.collate_augment(store, idx, H, W, C, PAD, True, 0, 0, o.OUT_F32, scale, bias,
+                      nthreads=nthreads, out=out)
+    return o.crc32(out)
+
+
+def cpu_baseline(seconds: float = 15.0):
+    from oracle import oracle as o
+
+    nthreads = os.cpu_count() or 1
+    n_store = 2048
+    store = o.make_store(0, n_store, SAMPLE_BYTES, nthreads=nthreads)
+    order = o.epoch_order(n_store, 0, 0)
+    scale, bias = o.norm_consts()
+    import numpy as np
+
+    out = np.empty((B, C, H, W), dtype=np.float32)
+    cpu_reference_step(o, store, order, 0, nthreads, out, scale, bias)  # warm
+    t0 = time.monotonic()
+    n = 0
+    while True:
+        cpu_reference_step(o, store, order, n % (n_store // B), nthreads, out, scale, bias)
+        n += 1
+        if time.monotonic() - t0 >= seconds or n >= 200:
+            break
+    dt = time.monotonic() - t0
+    produced = n * B / dt
+    return {"value": round(produced * N_CONSUMERS, 1), "unit": "samples/s", "cores": nthreads,
+            "kind": "port",
+            "sample": f"{n} batches x {B} samples ({dt:.1f} s): oracle C/OpenMP collate+augment "
+                      f"f32 NCHW + CRC-32 per batch, {nthreads} threads; delivered = "
+                      f"{N_CONSUMERS} zero-copy consumers x produced",
+            "produced_samples_per_s": round(produced, 1), "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as o
+
+    import numpy as np
+
+    nthreads = os.cpu_count() or 1
+    n_store = 2048
+    store = o.make_store(0, n_store, SAMPLE_BYTES, nthreads=nthreads)
+    order = o.epoch_order(n_store, 0, 0)
+    scale, bias = o.norm_consts()
+    out = np.empty((B, C, H, W), dtype=np.float32)
+    for i in range(args.warmup):
+        cpu_reference_step(o, store, order, i % (n_store // B), nthreads, out, scale, bias)
+    t0 = time.monotonic()
+    for i in range(args.steps):
+        cpu_reference_step(o, store, order, i % (n_store // B), nthreads, out, scale, bias)
+    dt = time.monotonic() - t0
+    value = N_CONSUMERS * B * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (same store/order/augment as ours)",
+        "config": {"workload": WORKLOAD, "global_batch": B, "samples_per_epoch": n_store},
+        "cpu_baseline": {"value": round(value, 1), "unit": "samples/s", "cores": nthreads,
+                         "kind": "port",
+                         "sample": f"{args.steps} batches x {B}: oracle C/OpenMP collate+augment "
+                                   f"+ CRC-32, {N_CONSUMERS} zero-copy consumers",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": round(value, 1), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

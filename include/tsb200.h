@@ -161,6 +161,37 @@ int tsb_collate_augment_fanout(const void *src, const int64_t *d_indices, int64_
 int tsb_rebatch_gather(const void *ring_base, int64_t ring_samples, int64_t sample_bytes,
                        int64_t first, int64_t count, void *out, void *stream);
 
+/* ---- native producer/consumer loops (replace the per-batch host work of
+ *      Producer._try_announce, producer.py:506-534, and
+ *      ConsumerSession.next_batch, consumer.py:286-338) ------------------- */
+#define TSB_SRC_AUGMENT 0   /* store -> fused collate/augment            */
+#define TSB_SRC_GATHER 1    /* store -> passthrough gather (DirectorySource) */
+#define TSB_SRC_SYNTHETIC 2 /* SplitMix64 generator (SyntheticSource)    */
+typedef struct {
+    int mode;                /* TSB_SRC_*                                     */
+    const void *src;         /* store base: HBM or pinned host (NULL synthetic) */
+    const int64_t *d_order;  /* device int64 epoch order (pipeline.py:113-123) */
+    int64_t batch_size;
+    int64_t sample_bytes;    /* raw sample bytes                              */
+    int h, w, c, pad, flip, out_kind;
+    uint64_t seed;           /* augment seed / synthetic source seed         */
+    uint64_t epoch;
+    float scale[4], bias[4]; /* normalisation (identity: 1, 0)               */
+    int with_target;         /* append int64 sample indices after the input  */
+    int64_t input_bytes;     /* bytes of the input part of a slot            */
+    uint32_t *d_crc;         /* optional device uint32[slots]: batch CRC-32   */
+} tsb_produce_args;
+/* Enqueue batches batch0..batch0+n-1 of one epoch (global seq seq0..) on
+ * `stream`: per batch wait_free(live, q - slots) -> produce into slot ->
+ * [crc] -> publish(slot, q).  ev: NULL or 2n events recorded around each
+ * batch's production kernel (for per-launch timing). */
+int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int64_t batch0,
+                      int n, const int *live, int n_live, void **ev, void *stream);
+/* Consumer: per batch q in seq0..seq0+n-1: wait_ready -> ack (a consumer
+ * that maps and releases, bs/cli.py:252-258).  ev: NULL or 2 events recorded
+ * after the first and after the last ready wait. */
+int tsb_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, void **ev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

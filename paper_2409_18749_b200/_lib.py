@@ -95,6 +95,25 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_rebatch_gather": (i32, [vp, i64, i64, i64, i64, vp, vp]),
 }
 
+class ProduceArgs(ctypes.Structure):
+    """Mirror of tsb_produce_args (include/tsb200.h)."""
+    _fields_ = [
+        ("mode", ctypes.c_int), ("src", ctypes.c_void_p), ("d_order", ctypes.c_void_p),
+        ("batch_size", ctypes.c_int64), ("sample_bytes", ctypes.c_int64),
+        ("h", ctypes.c_int), ("w", ctypes.c_int), ("c", ctypes.c_int), ("pad", ctypes.c_int),
+        ("flip", ctypes.c_int), ("out_kind", ctypes.c_int), ("seed", ctypes.c_uint64),
+        ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
+        ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
+        ("d_crc", ctypes.c_void_p),
+    ]
+
+
+SRC_AUGMENT, SRC_GATHER, SRC_SYNTHETIC = 0, 1, 2
+
+SIGNATURES["tsb_produce_range"] = (i32, [vp, ctypes.POINTER(ProduceArgs), u64, i64, i32,
+                                         ctypes.POINTER(i32), i32, pp, vp])
+SIGNATURES["tsb_consume_range"] = (i32, [vp, i32, u64, i32, pp, vp])
+
 _lib = None
 _lock = threading.Lock()
 

@@ -247,6 +247,37 @@ class CollateLoader:
         if self.with_target:
             dp.memcpy_async(out_ptr + self.input_nbytes, didx, 8 * b, stream)
 
+    def produce_args(self, epoch: int, with_crc=None):
+        """tsb_produce_args for the native range producer (ring.produce_range)."""
+        from . import _lib
+
+        _, dorder = self.order(epoch)
+        d, src = self.dataset, self.dataset.source
+        a = _lib.ProduceArgs()
+        a.d_order = dorder.data_ptr()
+        a.batch_size = d.batch_size
+        a.sample_bytes = src.sample_nbytes
+        a.epoch = epoch
+        a.with_target = int(self.with_target)
+        a.input_bytes = self.input_nbytes
+        a.d_crc = 0 if with_crc is None else with_crc.data_ptr()
+        for i in range(4):
+            a.scale[i], a.bias[i] = 1.0, 0.0
+        if isinstance(src, SyntheticSource):
+            a.mode, a.seed = _lib.SRC_SYNTHETIC, src.seed
+        elif self.augment is None:
+            a.mode, a.src = _lib.SRC_GATHER, src.samples.data_ptr()
+        else:
+            aug = self.augment
+            h, w, c = src.sample_shape
+            a.mode, a.src = _lib.SRC_AUGMENT, src.samples.data_ptr()
+            a.h, a.w, a.c, a.pad, a.flip, a.out_kind = h, w, c, aug.pad, int(aug.flip), aug.out_kind
+            a.seed = aug.seed
+            if self._scale is not None:
+                for i in range(c):
+                    a.scale[i], a.bias[i] = float(self._scale[i]), float(self._bias[i])
+        return a
+
     def __iter__(self):
         """Standalone (non-shared) iteration: fresh device tensors per batch."""
         import torch

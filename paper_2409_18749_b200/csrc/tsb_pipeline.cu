@@ -1,0 +1,75 @@
+// Native producer/consumer loops over the device ring: one host call enqueues
+// a whole range of batches (memops + kernels), so the per-batch host cost is
+// a few driver calls instead of a Python round trip.
+#include "tsb_common.cuh"
+
+using namespace tsb;
+
+extern "C" {
+
+int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int64_t batch0,
+                      int n, const int *live, int n_live, void **ev, void *stream) {
+    TSB_CHECK(r && a && a->d_order, "null argument");
+    TSB_CHECK(seq0 >= 1 && n >= 0 && batch0 >= 0, "bad range");
+    int slots = 0;
+    size_t stride = 0;
+    if (int rc = tsb_ring_geometry(r, &slots, &stride, nullptr)) return rc;
+    const int64_t b = a->batch_size;
+    const size_t nbytes = (size_t)a->input_bytes + (a->with_target ? 8 * (size_t)b : 0);
+    TSB_CHECK(nbytes <= stride, "batch (%zu B) exceeds the ring slot (%zu B)", nbytes, stride);
+    auto s = as_stream(stream);
+    for (int i = 0; i < n; ++i) {
+        const uint64_t q = seq0 + (uint64_t)i;
+        const int slot = (int)((q - 1) % (uint64_t)slots);
+        const int64_t bi = batch0 + i;
+        const int64_t *idx = a->d_order + bi * b;
+        void *out = nullptr;
+        if (int rc = tsb_ring_slot_ptr(r, slot, &out)) return rc;
+        if (q > (uint64_t)slots)
+            if (int rc = tsb_ring_wait_free(r, live, n_live, q - (uint64_t)slots, stream)) return rc;
+        if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i]), s));
+        int rc = TSB_OK;
+        switch (a->mode) {
+            case TSB_SRC_AUGMENT:
+                rc = tsb_collate_augment(a->src, idx, b, a->h, a->w, a->c, a->pad, a->flip,
+                                         a->seed, a->epoch, a->scale, a->bias, a->out_kind,
+                                         nullptr, out, stream);
+                break;
+            case TSB_SRC_GATHER:
+                rc = tsb_gather(a->src, idx, b, a->sample_bytes, out, stream);
+                break;
+            case TSB_SRC_SYNTHETIC:
+                rc = tsb_fill_synthetic(out, idx, b, a->seed, a->epoch, a->sample_bytes, stream);
+                break;
+            default:
+                TSB_CHECK(false, "bad produce mode %d", a->mode);
+        }
+        if (rc) return rc;
+        if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
+        if (a->with_target)
+            TSB_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(out) + a->input_bytes, idx, 8 * b,
+                                     cudaMemcpyDeviceToDevice, s));
+        if (a->d_crc)
+            if (int rc2 = tsb_crc32(out, nbytes, a->d_crc + slot, nullptr, stream)) return rc2;
+        if (int rc3 = tsb_ring_publish(r, slot, q, stream)) return rc3;
+    }
+    return TSB_OK;
+}
+
+int tsb_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, void **ev, void *stream) {
+    TSB_CHECK(r && seq0 >= 1 && n >= 0, "bad argument");
+    int slots = 0;
+    if (int rc = tsb_ring_geometry(r, &slots, nullptr, nullptr)) return rc;
+    auto s = as_stream(stream);
+    for (int i = 0; i < n; ++i) {
+        const uint64_t q = seq0 + (uint64_t)i;
+        const int slot = (int)((q - 1) % (uint64_t)slots);
+        if (int rc = tsb_ring_wait_ready(r, slot, q, stream)) return rc;
+        if (ev && i == 0) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[0]), s));
+        if (ev && i == n - 1) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[1]), s));
+        if (int rc = tsb_ring_ack(r, consumer, q, stream)) return rc;
+    }
+    return TSB_OK;
+}
+
+}  // extern "C"

@@ -163,3 +163,34 @@ __all__ = [
 def memcpy_async(dst, src, nbytes: int, stream=None) -> None:
     """cudaMemcpyAsync(Default) on the given stream (device/pinned pointers or tensors)."""
     call("tsb_memcpy_async", ptr(dst), ptr(src), nbytes, current_stream(stream))
+
+
+class DeviceEvent:
+    """Raw CUDA event owned by libtsb200 (timing on any stream, incl. inside
+    native range calls)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        call("tsb_event_create", ctypes.byref(h))
+        self.handle = h.value
+
+    @property
+    def cuda_event(self) -> int:
+        return self.handle
+
+    def record(self, stream=None) -> None:
+        call("tsb_event_record", self.handle, current_stream(stream))
+
+    def synchronize(self) -> None:
+        call("tsb_event_sync", self.handle)
+
+    def elapsed_ms(self, end: "DeviceEvent") -> float:
+        ms = ctypes.c_float()
+        call("tsb_event_elapsed_ms", self.handle, end.handle, ctypes.byref(ms))
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            load().tsb_event_destroy(self.handle)
+        except Exception:
+            pass

@@ -176,3 +176,25 @@ def _stream(stream):
 
         return _lib.stream_handle(torch.cuda.current_stream().cuda_stream)
     return _lib.stream_handle(stream)
+
+
+def _ev_array(events):
+    if events is None:
+        return None
+    return (ctypes.c_void_p * len(events))(*[int(e.cuda_event) if hasattr(e, "cuda_event")
+                                              else int(e) for e in events])
+
+
+def produce_range(ring: DeviceRing, args, seq0: int, batch0: int, n: int, live, events=None,
+                  stream=None) -> None:
+    """Native producer loop: n batches of one epoch into the ring (tsb_produce_range)."""
+    live = list(live)
+    arr = (ctypes.c_int * max(1, len(live)))(*live)
+    call("tsb_produce_range", ring._h, ctypes.byref(args), seq0, batch0, n, arr, len(live),
+         _ev_array(events), _stream(stream))
+
+
+def consume_range(ring: DeviceRing, consumer: int, seq0: int, n: int, events=None,
+                  stream=None) -> None:
+    """Native consumer loop: wait_ready -> ack for n batches (tsb_consume_range)."""
+    call("tsb_consume_range", ring._h, consumer, seq0, n, _ev_array(events), _stream(stream))
