@@ -30,6 +30,8 @@ extern "C" {
 #define TSB_ERR_UNSUPPORTED -5
 
 #define TSB_IPC_HANDLE_BYTES 64
+/* cursor value of an evicted consumer / dropped retention (2^62) */
+#define TSB_CURSOR_EVICTED 0x4000000000000000ULL
 
 /* collate output kinds (NCHW); PASSTHROUGH keeps the sample bytes as-is */
 #define TSB_OUT_U8 0
@@ -132,10 +134,11 @@ int tsb_ring_wait_ready(tsb_ring *r, int slot, uint64_t seq, void *stream);
  * prior work on `stream` (bs/consumer.py:330 Ack + release_view). */
 int tsb_ring_ack(tsb_ring *r, int consumer, uint64_t seq, void *stream);
 /* Producer gate before reusing a slot: `stream` waits until every consumer
- * in live[0..n_live) has cursor >= seq (producer.py:230-238 flow gate). */
+ * in live[0..n_live) has cursor >= seq (producer.py:230-238 flow gate).
+ * seq == 0 is a no-op. */
 int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, void *stream);
-/* Host: cursor[consumer] = UINT64_MAX so no device wait can wedge on an
- * evicted consumer (producer.py:255-269 evict_stale). */
+/* Host: cursor[consumer] = TSB_CURSOR_EVICTED so no device wait can wedge on
+ * an evicted consumer (producer.py:255-269 evict_stale). */
 int tsb_ring_evict(tsb_ring *r, int consumer);
 /* Host: reset a consumer cursor (admission, producer.py:629-642). */
 int tsb_ring_set_cursor(tsb_ring *r, int consumer, uint64_t value);
@@ -143,6 +146,15 @@ int tsb_ring_read_cursor(tsb_ring *r, int consumer, uint64_t *out);
 int tsb_ring_read_ready(tsb_ring *r, int slot, uint64_t *out);
 /* 1 = stream mem-ops (cuStreamWaitValue64), 0 = spin kernels. */
 int tsb_ring_sync_mode(void);
+/* Host-shared control block: the ready/cursor words move into caller host
+ * memory (e.g. a POSIX shm segment every process maps), registered as
+ * device-mapped; device memops then target host memory and host-side
+ * readers/writers (evict, consumers that only map + ack) never touch a
+ * GPU channel -- no cross-process GPU context switch per batch. */
+size_t tsb_ring_control_bytes(int slots, int max_consumers);
+int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int init);
+/* Host consumer: spin until ready[slot] >= seq (timeout_us < 0 = forever). */
+int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeout_us);
 
 /* ---- fan-out + rebatch (NEW) -------------------------- */
 /* Copy `bytes` from src into each of dsts[0..n_dst) (device or peer
@@ -180,6 +192,8 @@ typedef struct {
     int with_target;         /* append int64 sample indices after the input  */
     int64_t input_bytes;     /* bytes of the input part of a slot            */
     uint32_t *d_crc;         /* optional device uint32[slots]: batch CRC-32   */
+    int wait_stride;         /* gate slot reuse every k batches (<=1: every batch);
+                                effective ring depth = slots - k + 1 */
 } tsb_produce_args;
 /* Enqueue batches batch0..batch0+n-1 of one epoch (global seq seq0..) on
  * `stream`: per batch wait_free(live, q - slots) -> produce into slot ->

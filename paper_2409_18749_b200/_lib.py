@@ -89,6 +89,9 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_ring_read_cursor": (i32, [vp, i32, ctypes.POINTER(u64)]),
     "tsb_ring_read_ready": (i32, [vp, i32, ctypes.POINTER(u64)]),
     "tsb_ring_sync_mode": (i32, []),
+    "tsb_ring_control_bytes": (sz, [i32, i32]),
+    "tsb_ring_attach_host_control": (i32, [vp, vp, sz, i32]),
+    "tsb_ring_host_wait_ready": (i32, [vp, i32, u64, i64]),
     "tsb_fanout": (i32, [vp, pp, i32, sz, vp]),
     "tsb_collate_augment_fanout": (i32, [vp, vp, i64, i32, i32, i32, i32, i32, u64, u64, fp, fp,
                                          i32, pp, i32, vp]),
@@ -104,7 +107,7 @@ class ProduceArgs(ctypes.Structure):
         ("flip", ctypes.c_int), ("out_kind", ctypes.c_int), ("seed", ctypes.c_uint64),
         ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
         ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
-        ("d_crc", ctypes.c_void_p),
+        ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int),
     ]
 
 

@@ -166,6 +166,17 @@ struct CaGeom {
     int64_t plane;     // h*w
     int64_t sample_bytes;
 };
+// Fused epilogue: write the int64 sample indices (the batch "target") after
+// the input, and publish the ring slot from the last CTA to finish (grid
+// completion counter; release at system scope), replacing a memcpy launch and
+// a stream memop per batch.
+struct Epi {
+    int64_t *tgt;            // nullptr = no target copy
+    uint64_t *ready;         // nullptr = no publish
+    uint64_t seq;
+    unsigned int *counter;   // device completion counter (reset by the last CTA)
+};
+
 struct ItemPar {
     int s, oy, ox, fl;
     int64_t src_off;  // byte offset of the sample in the store (idx[s] * sample_bytes)
@@ -295,7 +306,7 @@ template <int OUT_KIND, int C, bool MULTI>
 __global__ void __launch_bounds__(CA_THREADS + 32)
     collate_augment_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
                            CaGeom g, int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
-                           const int32_t *__restrict__ params, Dsts dsts) {
+                           const int32_t *__restrict__ params, Dsts dsts, Epi ep) {
     using T = OutTraits<OUT_KIND>;
     constexpr int P = T::P;
     constexpr int NCW = CA_THREADS / 32;  // consumer warps; warp NCW is the producer
@@ -386,6 +397,8 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     }
 
     // ---------------- consumer warps: emit normalised NCHW ------------------
+    if (ep.tgt && blockIdx.x == 0)
+        for (int i = tid; i < g.b; i += CA_THREADS) ep.tgt[i] = idx[i];
     const int64_t plane_bytes = g.plane * T::ELEM;
     // first slot of this thread; further slots every CA_THREADS (no divisions in the loop)
     const int r_first = tid / g.groups;
@@ -433,12 +446,25 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
     }
+    if (ep.ready) {
+        __threadfence();                                       // this thread's stores
+        asm volatile("bar.sync 1, %0;" ::"n"(CA_THREADS) : "memory");  // consumer warps only
+        if (tid == 0) {
+            const unsigned int prev = atomicAdd(ep.counter, 1u);
+            if (prev == gridDim.x - 1) {  // last CTA: every store of the batch is visible
+                *ep.counter = 0u;
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready), "l"(ep.seq)
+                             : "memory");
+            }
+        }
+    }
 }
 
 template <int K, int C, bool MULTI>
 int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
               uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
-              size_t smem, cudaStream_t s) {
+              size_t smem, cudaStream_t s, const Epi &ep) {
     auto kern = collate_augment_kernel<K, C, MULTI>;
     static int occ_cache[64] = {0};
     static size_t smem_cache[64] = {0};
@@ -454,7 +480,8 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
     }
     const int slots = sm_count() * occ_cache[dev];
     const int grid = g.items < slots ? g.items : slots;
-    kern<<<grid, CA_THREADS + 32, smem, s>>>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts);
+    kern<<<grid, CA_THREADS + 32, smem, s>>>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
+                                             ep);
     TSB_LAUNCH_CHECK();
     return TSB_OK;
 }
@@ -462,21 +489,23 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
 template <int K, int C>
 int launch_ca_m(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
                 uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
-                size_t smem, cudaStream_t s) {
+                size_t smem, cudaStream_t s, const Epi &ep) {
     if (dsts.n == 1)
-        return launch_ca<K, C, false>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
-    return launch_ca<K, C, true>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+        return launch_ca<K, C, false>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem,
+                                      s, ep);
+    return launch_ca<K, C, true>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s,
+                                 ep);
 }
 
 template <int K>
 int launch_ca_c(int c, const uint8_t *src, const int64_t *idx, CaGeom g, int flip,
                 uint64_t aug_mixed, uint64_t epoch, const Norm &norm, const int32_t *params,
-                const Dsts &dsts, size_t smem, cudaStream_t s) {
+                const Dsts &dsts, size_t smem, cudaStream_t s, const Epi &ep) {
     switch (c) {
-        case 1: return launch_ca_m<K, 1>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
-        case 2: return launch_ca_m<K, 2>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
-        case 3: return launch_ca_m<K, 3>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
-        default: return launch_ca_m<K, 4>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s);
+        case 1: return launch_ca_m<K, 1>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s, ep);
+        case 2: return launch_ca_m<K, 2>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s, ep);
+        case 3: return launch_ca_m<K, 3>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s, ep);
+        default: return launch_ca_m<K, 4>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, smem, s, ep);
     }
 }
 
@@ -492,7 +521,7 @@ int is_device_memory(const void *p) {
 int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, int w, int c,
                    int pad, int flip, uint64_t aug_seed, uint64_t epoch, const float *scale,
                    const float *bias, int out_kind, const int32_t *d_params, const Dsts &dsts,
-                   void *stream) {
+                   void *stream, const Epi &ep = Epi{}) {
     TSB_CHECK(src && d_indices, "null src/indices");
     TSB_CHECK(b >= 0 && h > 0 && w > 0 && c > 0 && c <= 4, "bad shape b=%lld h=%d w=%d c=%d",
               (long long)b, h, w, c);
@@ -556,15 +585,31 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     auto s = as_stream(stream);
     if (out_kind == TSB_OUT_U8)
         return launch_ca_c<TSB_OUT_U8>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
-                                       dsts, smem, s);
+                                       dsts, smem, s, ep);
     if (out_kind == TSB_OUT_F32)
         return launch_ca_c<TSB_OUT_F32>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
-                                        dsts, smem, s);
+                                        dsts, smem, s, ep);
     return launch_ca_c<TSB_OUT_BF16>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
-                                     dsts, smem, s);
+                                     dsts, smem, s, ep);
 }
 
 }  // namespace
+
+namespace tsb {
+// collate/augment with the fused epilogue (target copy + slot publish)
+int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
+                            int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
+                            const float *scale, const float *bias, int out_kind, void *out,
+                            int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
+                            void *stream) {
+    Dsts d{};
+    d.p[0] = out;
+    d.n = 1;
+    Epi ep{tgt, ready, seq, counter};
+    return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
+                          out_kind, nullptr, d, stream, ep);
+}
+}  // namespace tsb
 
 extern "C" {
 

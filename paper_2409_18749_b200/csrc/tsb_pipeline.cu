@@ -5,6 +5,15 @@
 
 using namespace tsb;
 
+namespace tsb {
+int ring_publish_ptrs(tsb_ring *r, int slot, uint64_t **ready, unsigned int **counter);
+int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
+                            int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
+                            const float *scale, const float *bias, int out_kind, void *out,
+                            int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
+                            void *stream);
+}  // namespace tsb
+
 extern "C" {
 
 int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int64_t batch0,
@@ -17,6 +26,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     const int64_t b = a->batch_size;
     const size_t nbytes = (size_t)a->input_bytes + (a->with_target ? 8 * (size_t)b : 0);
     TSB_CHECK(nbytes <= stride, "batch (%zu B) exceeds the ring slot (%zu B)", nbytes, stride);
+    TSB_CHECK(a->wait_stride <= slots, "wait_stride %d exceeds the ring depth %d", a->wait_stride,
+              slots);
     auto s = as_stream(stream);
     for (int i = 0; i < n; ++i) {
         const uint64_t q = seq0 + (uint64_t)i;
@@ -25,12 +36,37 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         const int64_t *idx = a->d_order + bi * b;
         void *out = nullptr;
         if (int rc = tsb_ring_slot_ptr(r, slot, &out)) return rc;
-        if (q > (uint64_t)slots)
-            if (int rc = tsb_ring_wait_free(r, live, n_live, q - (uint64_t)slots, stream)) return rc;
+        // reuse gate, amortised over blocks of `stride` batches: one wait on every
+        // live cursor covers the slots of the whole block (each device wait on a
+        // host-shared word costs a PCIe round trip)
+        const uint64_t stride = a->wait_stride > 1 ? (uint64_t)a->wait_stride : 1;
+        if (i == 0 || (q - 1) % stride == 0) {
+            uint64_t block_end = q + (stride - 1 - (q - 1) % stride);
+            const uint64_t last = seq0 + (uint64_t)n - 1;
+            if (block_end > last) block_end = last;
+            if (block_end > (uint64_t)slots)
+                if (int rc = tsb_ring_wait_free(r, live, n_live, block_end - (uint64_t)slots, stream))
+                    return rc;
+        }
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i]), s));
         int rc = TSB_OK;
+        bool published = false;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
+                if (!a->d_crc) {  // fused epilogue: target copy + publish from the kernel
+                    uint64_t *ready = nullptr;
+                    unsigned int *counter = nullptr;
+                    if ((rc = ring_publish_ptrs(r, slot, &ready, &counter))) return rc;
+                    int64_t *tgt = a->with_target
+                                       ? reinterpret_cast<int64_t *>(static_cast<uint8_t *>(out) +
+                                                                     a->input_bytes)
+                                       : nullptr;
+                    rc = collate_augment_publish(a->src, idx, b, a->h, a->w, a->c, a->pad,
+                                                 a->flip, a->seed, a->epoch, a->scale, a->bias,
+                                                 a->out_kind, out, tgt, ready, q, counter, stream);
+                    published = true;
+                    break;
+                }
                 rc = tsb_collate_augment(a->src, idx, b, a->h, a->w, a->c, a->pad, a->flip,
                                          a->seed, a->epoch, a->scale, a->bias, a->out_kind,
                                          nullptr, out, stream);
@@ -46,6 +82,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         }
         if (rc) return rc;
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
+        if (published) continue;
         if (a->with_target)
             TSB_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(out) + a->input_bytes, idx, 8 * b,
                                      cudaMemcpyDeviceToDevice, s));

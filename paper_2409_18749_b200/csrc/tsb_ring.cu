@@ -17,6 +17,7 @@
 // +inf cursor so no wait can wedge on a dead consumer (producer.py:255-269).
 #include <cuda.h>
 #include <stdlib.h>
+#include <time.h>
 
 #include <mutex>
 
@@ -31,8 +32,10 @@ struct tsb_ring {
     size_t slot_stride;
     int max_consumers;
     uint8_t *base;
-    uint64_t *ready;   // [slots]
-    uint64_t *cursor;  // [max_consumers]
+    uint64_t *ready;   // [slots]          device-visible address (memops)
+    uint64_t *cursor;  // [max_consumers]  device-visible address (memops)
+    uint64_t *h_ctl;   // host view of a host-shared control block (or null)
+    unsigned int *counters;  // [slots] device completion counters (fused publish)
     size_t total;
     bool imported;
     cudaStream_t host_stream;  // private non-blocking stream for host pokes
@@ -166,31 +169,57 @@ int dev_wait(tsb_ring *r, const uint64_t *const *addrs, int n, uint64_t v, void 
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+size_t ctl_words_bytes(const tsb_ring *r) {
+    return round_up(sizeof(uint64_t) * (size_t)(r->slots + r->max_consumers), 256);
+}
+
 void layout(tsb_ring *r) {
     r->slot_stride = round_up(r->slot_bytes ? r->slot_bytes : 16, 256);
     const size_t payload = r->slot_stride * (size_t)r->slots;
-    const size_t ctl = round_up(sizeof(uint64_t) * (size_t)(r->slots + r->max_consumers), 256);
-    r->total = payload + ctl;
+    r->total = payload + ctl_words_bytes(r) + round_up(sizeof(unsigned int) * r->slots, 256);
 }
 
 void bind(tsb_ring *r) {
     const size_t payload = r->slot_stride * (size_t)r->slots;
     r->ready = reinterpret_cast<uint64_t *>(r->base + payload);
     r->cursor = r->ready + r->slots;
+    r->counters = reinterpret_cast<unsigned int *>(r->base + payload + ctl_words_bytes(r));
 }
 
+// host view of a control word (host-shared control block), or null
+uint64_t *host_word(tsb_ring *r, const uint64_t *dev_addr) {
+    if (!r->h_ctl) return nullptr;
+    return r->h_ctl + (dev_addr - r->ready);
+}
 int host_write(tsb_ring *r, uint64_t *addr, uint64_t v) {
+    if (uint64_t *h = host_word(r, addr)) {
+        __atomic_store_n(h, v, __ATOMIC_RELEASE);
+        return TSB_OK;
+    }
     TSB_CUDA(cudaMemcpyAsync(addr, &v, sizeof(v), cudaMemcpyHostToDevice, r->host_stream));
     TSB_CUDA(cudaStreamSynchronize(r->host_stream));
     return TSB_OK;
 }
 int host_read(tsb_ring *r, const uint64_t *addr, uint64_t *out) {
+    if (uint64_t *h = host_word(r, addr)) {
+        *out = __atomic_load_n(h, __ATOMIC_ACQUIRE);
+        return TSB_OK;
+    }
     TSB_CUDA(cudaMemcpyAsync(out, addr, sizeof(*out), cudaMemcpyDeviceToHost, r->host_stream));
     TSB_CUDA(cudaStreamSynchronize(r->host_stream));
     return TSB_OK;
 }
 
 }  // namespace
+
+namespace tsb {
+int ring_publish_ptrs(tsb_ring *r, int slot, uint64_t **ready, unsigned int **counter) {
+    TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
+    *ready = r->ready + slot;
+    *counter = r->counters + slot;
+    return TSB_OK;
+}
+}  // namespace tsb
 
 extern "C" {
 
@@ -215,7 +244,7 @@ int tsb_ring_create(int dev, int slots, size_t slot_bytes, int max_consumers, ts
     }
     bind(r);
     TSB_CUDA(cudaStreamCreateWithFlags(&r->host_stream, cudaStreamNonBlocking));
-    TSB_CUDA(cudaMemsetAsync(r->ready, 0, sizeof(uint64_t) * (r->slots + r->max_consumers),
+    TSB_CUDA(cudaMemsetAsync(r->ready, 0, r->total - r->slot_stride * (size_t)r->slots,
                              r->host_stream));
     TSB_CUDA(cudaStreamSynchronize(r->host_stream));
     resolve_mode();
@@ -260,9 +289,54 @@ int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_co
     return TSB_OK;
 }
 
+size_t tsb_ring_control_bytes(int slots, int max_consumers) {
+    return round_up(sizeof(uint64_t) * (size_t)(slots + max_consumers), 4096);
+}
+
+int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int init) {
+    TSB_CHECK(r && host_ctl, "null argument");
+    TSB_CHECK(!r->h_ctl, "ring already has a host control block");
+    const size_t need = sizeof(uint64_t) * (size_t)(r->slots + r->max_consumers);
+    TSB_CHECK(bytes >= need && ((uintptr_t)host_ctl & 7) == 0,
+              "host control block too small or misaligned (%zu < %zu)", bytes, need);
+    if (init) memset(host_ctl, 0, need);
+    TSB_CUDA(cudaSetDevice(r->dev));
+    TSB_CUDA(cudaHostRegister(host_ctl, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    void *dptr = nullptr;
+    TSB_CUDA(cudaHostGetDevicePointer(&dptr, host_ctl, 0));
+    r->h_ctl = static_cast<uint64_t *>(host_ctl);
+    r->ready = static_cast<uint64_t *>(dptr);
+    r->cursor = r->ready + r->slots;
+    return TSB_OK;
+}
+
+int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeout_us) {
+    TSB_CHECK(r && r->h_ctl && slot >= 0 && slot < r->slots, "needs a host control block");
+    uint64_t *h = r->h_ctl + slot;
+    int64_t spins = 0;
+    struct timespec t0, t;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    while (__atomic_load_n(h, __ATOMIC_ACQUIRE) < seq) {
+        if (++spins > 256) {
+            clock_gettime(CLOCK_MONOTONIC, &t);
+            const int64_t us = (t.tv_sec - t0.tv_sec) * 1000000 + (t.tv_nsec - t0.tv_nsec) / 1000;
+            if (timeout_us >= 0 && us > timeout_us) {
+                set_error("timed out waiting for slot %d seq %llu", slot, (unsigned long long)seq);
+                return TSB_ERR_STALE;
+            }
+            if (spins > 4096) {
+                struct timespec ns = {0, 2000};
+                nanosleep(&ns, nullptr);
+            }
+        }
+    }
+    return TSB_OK;
+}
+
 int tsb_ring_destroy(tsb_ring *r) {
     if (!r) return TSB_OK;
     int rc = TSB_OK;
+    if (r->h_ctl) cudaHostUnregister(r->h_ctl);
     if (r->host_stream) cudaStreamDestroy(r->host_stream);
     cudaError_t e = r->imported ? cudaIpcCloseMemHandle(r->base) : cudaFree(r->base);
     if (e != cudaSuccess) {
@@ -318,7 +392,9 @@ int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, v
 }
 int tsb_ring_evict(tsb_ring *r, int consumer) {
     TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
-    return host_write(r, r->cursor + consumer, ~0ull);
+    // "+inf" for every wait: far ahead of any sequence, yet positive under the
+    // wrap-around GEQ of cuStreamWaitValue64 ((int64_t)(*addr - v) >= 0)
+    return host_write(r, r->cursor + consumer, TSB_CURSOR_EVICTED);
 }
 int tsb_ring_set_cursor(tsb_ring *r, int consumer, uint64_t value) {
     TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);

@@ -22,7 +22,9 @@ Differences behind the same API (B200 data plane):
   name carries the slot and its 80-byte segment header (segment.py).
 
 Keyword-only extensions: ``ring_slots`` (device ring depth; bounds drift),
-``min_consumers`` (start barrier, bs/producer.py:73-76 -- the facade's
+``control`` ("host": ring control words in a host-shared, device-mapped
+shm block -- evictions and map-and-ack consumers never touch a GPU channel;
+"device": words in HBM), ``min_consumers`` (start barrier, bs/producer.py:73-76 -- the facade's
 missing barrier is the start race noted in SURVEY.md §4), ``checksum``
 (device CRC-32 of every batch into Announce.checksum), ``rubberband_fraction``
 (late-join replay window, bs/producer.py:119-135; 0 = facade behaviour),
@@ -61,7 +63,7 @@ class TensorProducer:
                  pause_poll_s: float = 0.05, *, ring_slots: int | None = None,
                  min_consumers: int = 1, checksum: bool = False,
                  rubberband_fraction: float = 0.0, max_consumers: int = 64,
-                 device: int | None = None):
+                 device: int | None = None, control: str = "host"):
         import torch
 
         if not hasattr(data_loader, "__len__"):
@@ -81,6 +83,7 @@ class TensorProducer:
         self._fraction = rubberband_fraction
         self._max_consumers = max_consumers
         self._ring_slots = ring_slots
+        self._control = control
         self.device = torch.cuda.current_device() if device is None else device
         self._epoch = 0
         self._announced_in_epoch = 0
@@ -122,7 +125,8 @@ class TensorProducer:
             if slots <= window:
                 raise ValueError(f"ring_slots={slots} must exceed the rubberband window {window}")
             # cursor index max_consumers is the producer's retention cursor
-            self._ring = DeviceRing(slots, nbytes, self._max_consumers + 1, device=self.device)
+            self._ring = DeviceRing(slots, nbytes, self._max_consumers + 1, device=self.device,
+                                    control=self._control)
             self._stream = torch.cuda.Stream(device=self.device)
             self._events = [torch.cuda.Event() for _ in range(slots)]
             self._crc = torch.zeros(slots, dtype=torch.int32, device=f"cuda:{self.device}")
@@ -130,7 +134,7 @@ class TensorProducer:
             _RINGS[self.ring_id] = self._ring
             self._descriptor = sg.RingDescriptor(
                 self.ring_id, os.getpid(), self.device, slots, nbytes, self._max_consumers + 1,
-                self._ring.export())
+                self._ring.export(), self._ring.control_name)
         self._lock.notify_all()
 
     @property

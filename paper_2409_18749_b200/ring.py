@@ -15,7 +15,7 @@ Batch with sequence q (q = epoch*epoch_len + index + 1) lives in slot
 (q-1) % slots.  The producer may overwrite a slot for q only once every live
 consumer released q - slots (device wait on the cursors), so a ring of S
 slots bounds drift to S batches with no host round trip on the data path.
-Eviction writes cursor = 2**64-1 so no device wait can wedge
+Eviction writes cursor = 2**62 (TSB_CURSOR_EVICTED) so no device wait can wedge
 (producer.py:255-269).
 
 Zero-copy views: same process -> the pointer; other processes on the same
@@ -26,12 +26,13 @@ the Announce's segment name).
 from __future__ import annotations
 
 import ctypes
+import mmap
 import os
 
 from . import _lib
 from ._lib import IPC_HANDLE_BYTES, call, load
 
-SENTINEL = (1 << 64) - 1
+SENTINEL = 1 << 62  # TSB_CURSOR_EVICTED: positive under the memop wrap-around GEQ
 
 _TORCH_TYPESTR = {
     "uint8": "|u1", "int8": "|i1", "int16": "<i2", "int32": "<i4", "int64": "<i8",
@@ -62,9 +63,35 @@ def tensor_view(ptr: int, shape, dtype, owner=None):
     return t
 
 
+class _HostControl:
+    """POSIX shm segment holding the ring's control words (/dev/shm/<name>)."""
+
+    def __init__(self, name: str, nbytes: int, create: bool):
+        self.name = name
+        self.path = f"/dev/shm/{name}"
+        flags = os.O_RDWR | (os.O_CREAT | os.O_EXCL if create else 0)
+        fd = os.open(self.path, flags, 0o600)
+        try:
+            if create:
+                os.ftruncate(fd, nbytes)
+            self.mm = mmap.mmap(fd, nbytes)
+        finally:
+            os.close(fd)
+        self._buf = (ctypes.c_char * nbytes).from_buffer(self.mm)
+        self.addr = ctypes.addressof(self._buf)
+        self.nbytes = nbytes
+        self.owner = create
+
+    def unlink(self):
+        try:
+            os.unlink(self.path)
+        except FileNotFoundError:
+            pass
+
+
 class DeviceRing:
     def __init__(self, slots: int, slot_bytes: int, max_consumers: int = 64,
-                 device: int | None = None):
+                 device: int | None = None, control: str = "device"):
         L = load()
         if device is None:
             dev = ctypes.c_int(0)
@@ -74,6 +101,17 @@ class DeviceRing:
         call("tsb_ring_create", device, slots, slot_bytes, max_consumers, ctypes.byref(h))
         self._init(h, slots, slot_bytes, max_consumers, device, imported=False)
         self._L = L
+        self.ctl = None
+        if control == "host":
+            nb = L.tsb_ring_control_bytes(slots, max_consumers)
+            self.ctl = _HostControl(f"tsbc-{os.getpid()}-{id(self) & 0xFFFFFF:x}", nb, True)
+            call("tsb_ring_attach_host_control", self._h, self.ctl.addr, nb, 1)
+        elif control != "device":
+            raise ValueError("control must be 'device' or 'host'")
+
+    @property
+    def control_name(self) -> str:
+        return self.ctl.name if self.ctl is not None else "-"
 
     def _init(self, h, slots, slot_bytes, max_consumers, device, imported):
         self._h = h
@@ -92,11 +130,13 @@ class DeviceRing:
         self.base = base.value
 
     @classmethod
-    def import_handle(cls, handle: bytes, slots: int, slot_bytes: int, max_consumers: int):
-        """Open a ring exported by another process on this GPU (CUDA IPC)."""
+    def import_handle(cls, handle: bytes, slots: int, slot_bytes: int, max_consumers: int,
+                      control_name: str = "-"):
+        """Open a ring exported by another process on this GPU (CUDA IPC); with a
+        host control block, map the same shm segment."""
         if len(handle) != IPC_HANDLE_BYTES:
             raise ValueError("IPC handle must be 64 bytes")
-        load()
+        L = load()
         buf = ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES)
         h = ctypes.c_void_p()
         call("tsb_ring_import", buf, slots, slot_bytes, max_consumers, ctypes.byref(h))
@@ -104,6 +144,11 @@ class DeviceRing:
         dev = ctypes.c_int(0)
         call("tsb_get_device", ctypes.byref(dev))
         self._init(h, slots, slot_bytes, max_consumers, dev.value, imported=True)
+        self.ctl = None
+        if control_name and control_name != "-":
+            nb = L.tsb_ring_control_bytes(slots, max_consumers)
+            self.ctl = _HostControl(control_name, nb, False)
+            call("tsb_ring_attach_host_control", self._h, self.ctl.addr, nb, 0)
         return self
 
     # -- identity -----------------------------------------------------------
@@ -134,6 +179,8 @@ class DeviceRing:
         call("tsb_ring_ack", self._h, consumer, seq, _stream(stream))
 
     def wait_free(self, live, seq: int, stream=None) -> None:
+        if seq <= 0:
+            return
         live = list(live)
         arr = (ctypes.c_int * max(1, len(live)))(*live)
         call("tsb_ring_wait_free", self._h, arr, len(live), seq, _stream(stream))
@@ -154,10 +201,23 @@ class DeviceRing:
         call("tsb_ring_read_ready", self._h, slot, ctypes.byref(v))
         return v.value
 
+    # -- host-side consumer ops (host control block) ---------------------------
+    def host_wait_ready(self, slot: int, seq: int, timeout_s: float = -1.0) -> None:
+        """Spin on the host until the slot holds seq (no GPU channel involved)."""
+        call("tsb_ring_host_wait_ready", self._h, slot, seq,
+             -1 if timeout_s < 0 else int(timeout_s * 1e6))
+
+    def host_ack(self, consumer: int, seq: int) -> None:
+        """Release up to seq from the host (consumer finished with the batch)."""
+        call("tsb_ring_set_cursor", self._h, consumer, seq)
+
     def close(self) -> None:
         h, self._h = getattr(self, "_h", None), None
         if h and os.getpid() == self.pid:
             call("tsb_ring_destroy", h)
+        ctl = getattr(self, "ctl", None)
+        if ctl is not None and ctl.owner and os.getpid() == self.pid:
+            ctl.unlink()
 
     def __del__(self):
         try:

@@ -135,10 +135,11 @@ class RingDescriptor:
     slot_bytes: int
     max_consumers: int
     ipc_handle: bytes
+    control: str = "-"  # host-shared control block (shm name) or "-" (device words)
 
     def name(self) -> str:
         n = (f"tsbr:{self.ring_id:x}:{self.pid}:{self.device}:{self.slots}:{self.slot_bytes}:"
-             f"{self.max_consumers}:{_b64(self.ipc_handle)}")
+             f"{self.max_consumers}:{self.control}:{_b64(self.ipc_handle)}")
         assert len(n) <= 255
         return n
 
@@ -146,6 +147,6 @@ class RingDescriptor:
     def parse(cls, name: str) -> "RingDescriptor | None":
         if not name.startswith("tsbr:"):
             return None
-        _, rid, pid, dev, slots, sb, mc, h = name.split(":", 7)
+        _, rid, pid, dev, slots, sb, mc, ctl, h = name.split(":", 8)
         return cls(int(rid, 16), int(pid), int(dev), int(slots), int(sb), int(mc),
-                   base64.b64decode(h))
+                   base64.b64decode(h), ctl)

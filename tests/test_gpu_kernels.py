@@ -232,7 +232,7 @@ def test_ring_device_sync_in_process():
     assert ring.read_cursor(0) == 12 and ring.read_cursor(1) == 12
     assert ring.read_ready(ring.slot_of(12)) == 12
     ring.evict(1)
-    assert ring.read_cursor(1) == (1 << 64) - 1
+    assert ring.read_cursor(1) == 1 << 62
     print("sync mode:", sync_mode())
     ring.close()
 

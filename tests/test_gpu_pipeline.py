@@ -1,0 +1,109 @@
+"""Native producer/consumer loops (tsb_produce_range / tsb_consume_range) over
+the device ring, incl. the collate kernel's fused epilogue (target copy +
+slot publish from the last CTA) and the host-shared control block."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec,  # noqa: E402
+                                   StoreSource, SyntheticSource)
+from paper_2409_18749_b200.ring import DeviceRing, consume_range, produce_range  # noqa: E402
+from paper_2409_18749_b200.wire import DType  # noqa: E402
+
+
+def _snapshots(ld, ring, n, epoch=0, stride=1):
+    """Produce n batches through the native loop; one in-process consumer
+    stream snapshots each slot between wait_ready and ack."""
+    ps, cs = torch.cuda.Stream(), torch.cuda.Stream()
+    ring.set_cursor(0, epoch * len(ld))  # admitted at the epoch start (producer.py semantics)
+    args = ld.produce_args(epoch)
+    args.wait_stride = stride
+    produce_range(ring, args, epoch * len(ld) + 1, 0, n, [0], stream=ps)
+    snaps = []
+    for i in range(n):
+        q = epoch * len(ld) + 1 + i
+        slot = ring.slot_of(q)
+        with torch.cuda.stream(cs):
+            ring.wait_ready(slot, q, cs)
+            snaps.append(ring.view(slot, (ld.batch_nbytes,), torch.uint8).clone())
+            ring.ack(0, q, cs)
+    torch.cuda.synchronize()
+    return [s.cpu().numpy() for s in snaps]
+
+
+@pytest.mark.parametrize("control,stride", [("device", 1), ("host", 1), ("host", 2)])
+@pytest.mark.parametrize("out_dtype,kind", [("float32", 1), ("bfloat16", 2), ("uint8", 0)])
+def test_produce_range_augment_fused_publish(oracle, control, stride, out_dtype, kind):
+    h, w, c, B, N = 32, 64, 3, 8, 96
+    store = StoreSource.synthetic(3, N, (h, w, c))
+    ld = CollateLoader(DatasetSpec(store, N, B, shuffle_seed=5),
+                       AugmentSpec(pad=4, flip=True, out_dtype=out_dtype, seed=9))
+    ring = DeviceRing(3, ld.batch_nbytes, 1, control=control)
+    snaps = _snapshots(ld, ring, 10, epoch=1, stride=stride)
+    store_h = oracle.make_store(3, N, h * w * c)
+    order = oracle.epoch_order(N, 5, 1)
+    scale, bias = oracle.norm_consts()
+    for i, snap in enumerate(snaps):
+        idx = order[i * B:(i + 1) * B]
+        want = oracle.collate_augment(store_h, idx, h, w, c, 4, True, 9, 1, kind,
+                                      scale if kind else None, bias if kind else None)
+        assert snap[:ld.input_nbytes].tobytes() == want.tobytes()
+        np.testing.assert_array_equal(snap[ld.input_nbytes:].view(np.int64), idx)
+    assert ring.read_ready(ring.slot_of(len(ld) + 10)) == len(ld) + 10
+    ring.close()
+
+
+@pytest.mark.parametrize("mode", ["gather", "synthetic"])
+def test_produce_range_passthrough(golden, mode):
+    case = golden["prepare_batch"][0]  # 224x224x3 u8 B=64 N=1024 epoch 0
+    if mode == "synthetic":
+        src = SyntheticSource(0, (224, 224, 3), DType.U8)
+    else:  # epoch 0 store == synthetic epoch 0 (DirectorySource semantics)
+        src = StoreSource.synthetic(0, 1024, (224, 224, 3))
+    ld = CollateLoader(DatasetSpec(src, 1024, 64, shuffle_seed=0))
+    ring = DeviceRing(2, ld.batch_nbytes, 1, control="host")
+    snaps = _snapshots(ld, ring, 4)
+    import zlib
+
+    assert zlib.crc32(snaps[0][:ld.input_nbytes].tobytes()) == case["crc32"]
+    assert zlib.crc32(snaps[3][:ld.input_nbytes].tobytes()) == golden["prepare_batch"][1]["crc32"]
+    np.testing.assert_array_equal(snaps[0][ld.input_nbytes:].view(np.int64), case["indices"])
+    ring.close()
+
+
+def test_host_consumer_ops_and_eviction():
+    ring = DeviceRing(2, 1 << 16, 2, control="host")
+    s = torch.cuda.Stream()
+    ring.publish(1, 7, s)
+    s.synchronize()
+    ring.host_wait_ready(1, 7, timeout_s=5)
+    with pytest.raises(Exception):
+        ring.host_wait_ready(0, 1, timeout_s=0.01)
+    ring.host_ack(0, 5)
+    assert ring.read_cursor(0) == 5
+    # a device wait on an evicted consumer must not wedge the stream
+    ring.wait_free([0, 1], 9, s)
+    ring.evict(1)
+    ring.host_ack(0, 9)
+    s.synchronize()
+    ring.close()
+
+
+def test_consume_range_events():
+    from paper_2409_18749_b200 import dataplane as dp
+
+    ring = DeviceRing(4, 4096, 1)
+    ps, cs = torch.cuda.Stream(), torch.cuda.Stream()
+    e0, e1 = dp.DeviceEvent(), dp.DeviceEvent()
+    consume_range(ring, 0, 1, 8, events=[e0, e1], stream=cs)
+    for q in range(1, 9):
+        ring.wait_free([0], q - 4, ps)
+        ring.publish(ring.slot_of(q), q, ps)
+    cs.synchronize()
+    assert ring.read_cursor(0) == 8 and e0.elapsed_ms(e1) >= 0
+    ring.close()
