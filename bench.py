@@ -67,14 +67,49 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+    """SM clock + throttle-reason sampling during the timed region
+    (B200_PROFILING.md clocks line).  NVML in a thread at 5 ms (the timed
+    region can be a few hundred ms); nvidia-smi -lms 100 as the fallback."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, dev: int):
         self.dev = dev
         self.rows = []
         self._p = None
+        self._nv = None
+        self._stop = threading.Event()
 
     def start(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self._max = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self._t.start()
+            return
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            self._nv = None
+        self._start_smi()
+
+    def _poll_nvml(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((sm, [n for n, a in self.REASONS if rs & getattr(nv, a)]))
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.005)
+
+    def _start_smi(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -94,6 +129,15 @@ class Clocks:
                 self.rows.append(parts)
 
     def stop(self):
+        if self._nv is not None:
+            self._stop.set()
+            self._t.join(1)
+            if not self.rows:
+                return {"sm_mhz": None, "sm_max_mhz": self._max, "reasons": ["no samples"]}
+            return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                    "sm_max_mhz": float(self._max),
+                    "reasons": sorted({n for r in self.rows for n in r[1]}),
+                    "samples": len(self.rows), "source": "nvml"}
         if self._p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)

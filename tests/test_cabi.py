@@ -67,3 +67,18 @@ def test_sm100a_cubin_in_library():
     out = subprocess.run([cuobjdump, "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_product_never_imports_the_oracle():
+    """The oracle is test infrastructure: no module of the product package may
+    import, load or execute anything under oracle/ (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2409_18749_b200")
+    offenders = []
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                if re.search(r"^\s*(from|import)\s+oracle\b|ts_oracle|libts_oracle|"
+                             r"import_module\(\s*['\"]oracle", src, flags=re.M):
+                    offenders.append(f)
+    assert not offenders, offenders
