@@ -192,9 +192,17 @@ typedef struct {
     int with_target;         /* append int64 sample indices after the input  */
     int64_t input_bytes;     /* bytes of the input part of a slot            */
     uint32_t *d_crc;         /* optional device uint32[slots]: batch CRC-32   */
-    int wait_stride;         /* gate slot reuse every k batches (<=1: every batch);
-                                effective ring depth = slots - k + 1 */
+    int wait_stride;         /* device gate: wait on the cursors every k batches
+                                (<=1: every batch); effective depth slots - k + 1 */
+    int gate;                /* TSB_GATE_DEVICE: the stream waits on the cursors
+                                (the calling thread never blocks).  TSB_GATE_HOST
+                                (rings with a host control block): the calling
+                                thread blocks until the slot is free, the stream
+                                carries only kernels and consecutive fused batches
+                                chain with programmatic dependent launch */
 } tsb_produce_args;
+#define TSB_GATE_DEVICE 0
+#define TSB_GATE_HOST 1
 /* Enqueue batches batch0..batch0+n-1 of one epoch (global seq seq0..) on
  * `stream`: per batch wait_free(live, q - slots) -> produce into slot ->
  * [crc] -> publish(slot, q).  ev: NULL or 2n events recorded around each

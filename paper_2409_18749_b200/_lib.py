@@ -107,8 +107,11 @@ class ProduceArgs(ctypes.Structure):
         ("flip", ctypes.c_int), ("out_kind", ctypes.c_int), ("seed", ctypes.c_uint64),
         ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
         ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
-        ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int),
+        ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int), ("gate", ctypes.c_int),
     ]
+
+
+GATE_DEVICE, GATE_HOST = 0, 1
 
 
 SRC_AUGMENT, SRC_GATHER, SRC_SYNTHETIC = 0, 1, 2

@@ -175,7 +175,12 @@ struct Epi {
     uint64_t *ready;         // nullptr = no publish
     uint64_t seq;
     unsigned int *counter;   // device completion counter (reset by the last CTA)
+    int pdl;                 // launch as a programmatic dependent of the previous batch
 };
+
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 struct ItemPar {
     int s, oy, ox, fl;
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
                 mbar_arrive(&full[st]);  // release: this lane's staging stores
             }
         }
+        pdl_launch_dependents();
         return;
     }
 
@@ -446,6 +452,11 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
     }
+    // the next batch's CTAs may take this SM's slots as soon as they free up:
+    // its prologue and first loads overlap this batch's tail.  It writes a
+    // different ring slot, and its gate was checked on the host, so it never
+    // needs this grid's results (no griddepcontrol.wait anywhere).
+    pdl_launch_dependents();
     if (ep.ready) {
         __threadfence();                                       // this thread's stores
         asm volatile("bar.sync 1, %0;" ::"n"(CA_THREADS) : "memory");  // consumer warps only
@@ -480,6 +491,21 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
     }
     const int slots = sm_count() * occ_cache[dev];
     const int grid = g.items < slots ? g.items : slots;
+    if (ep.pdl) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(CA_THREADS + 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, src, idx, g, flip, aug_mixed, epoch, norm, params,
+                                    dsts, ep));
+        return TSB_OK;
+    }
     kern<<<grid, CA_THREADS + 32, smem, s>>>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
                                              ep);
     TSB_LAUNCH_CHECK();
@@ -510,12 +536,19 @@ int launch_ca_c(int c, const uint8_t *src, const int64_t *idx, CaGeom g, int fli
 }
 
 int is_device_memory(const void *p) {
+    // one-entry cache: a producer launches over the same store every batch
+    static thread_local const void *last_p = nullptr;
+    static thread_local int last_v = 0;
+    if (p == last_p) return last_v;
     cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    int v = 0;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess)
         cudaGetLastError();
-        return 0;
-    }
-    return a.type == cudaMemoryTypeDevice;
+    else
+        v = a.type == cudaMemoryTypeDevice;
+    last_p = p;
+    last_v = v;
+    return v;
 }
 
 int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, int w, int c,
@@ -601,11 +634,11 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
-                            void *stream) {
+                            int pdl, void *stream) {
     Dsts d{};
     d.p[0] = out;
     d.n = 1;
-    Epi ep{tgt, ready, seq, counter};
+    Epi ep{tgt, ready, seq, counter, pdl};
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
                           out_kind, nullptr, d, stream, ep);
 }

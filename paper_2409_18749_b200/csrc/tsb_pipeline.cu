@@ -1,17 +1,21 @@
 // Native producer/consumer loops over the device ring: one host call enqueues
 // a whole range of batches (memops + kernels), so the per-batch host cost is
 // a few driver calls instead of a Python round trip.
+#include <stdlib.h>
+
 #include "tsb_common.cuh"
 
 using namespace tsb;
 
 namespace tsb {
 int ring_publish_ptrs(tsb_ring *r, int slot, uint64_t **ready, unsigned int **counter);
+bool ring_has_host_control(const tsb_ring *r);
+int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need);
 int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
                             int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
-                            void *stream);
+                            int pdl, void *stream);
 }  // namespace tsb
 
 extern "C" {
@@ -29,6 +33,16 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     TSB_CHECK(a->wait_stride <= slots, "wait_stride %d exceeds the ring depth %d", a->wait_stride,
               slots);
     auto s = as_stream(stream);
+    // Host-shared control words: gate on the host (no device wait in the
+    // stream), and chain consecutive fused batches with programmatic dependent
+    // launch.  The first batch of a range keeps full stream ordering (the
+    // previous op on the stream may be anything).
+    TSB_CHECK(a->gate == TSB_GATE_DEVICE || ring_has_host_control(r),
+              "TSB_GATE_HOST needs a ring with a host control block");
+    const bool host_gate = a->gate == TSB_GATE_HOST;
+    static const bool no_pdl = getenv("TSB_NO_PDL") && atoi(getenv("TSB_NO_PDL"));      // A/B knobs
+    static const bool no_fused = getenv("TSB_NO_FUSED") && atoi(getenv("TSB_NO_FUSED"));
+    bool prev_fused = false;
     for (int i = 0; i < n; ++i) {
         const uint64_t q = seq0 + (uint64_t)i;
         const int slot = (int)((q - 1) % (uint64_t)slots);
@@ -40,7 +54,10 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         // live cursor covers the slots of the whole block (each device wait on a
         // host-shared word costs a PCIe round trip)
         const uint64_t stride = a->wait_stride > 1 ? (uint64_t)a->wait_stride : 1;
-        if (i == 0 || (q - 1) % stride == 0) {
+        if (host_gate) {
+            if (q > (uint64_t)slots)
+                if (int rc = ring_host_gate(r, live, n_live, q - (uint64_t)slots)) return rc;
+        } else if (i == 0 || (q - 1) % stride == 0) {
             uint64_t block_end = q + (stride - 1 - (q - 1) % stride);
             const uint64_t last = seq0 + (uint64_t)n - 1;
             if (block_end > last) block_end = last;
@@ -53,7 +70,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         bool published = false;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
-                if (!a->d_crc) {  // fused epilogue: target copy + publish from the kernel
+                if (!a->d_crc && !no_fused) {  // fused epilogue: target copy + publish from the kernel
                     uint64_t *ready = nullptr;
                     unsigned int *counter = nullptr;
                     if ((rc = ring_publish_ptrs(r, slot, &ready, &counter))) return rc;
@@ -61,9 +78,11 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                        ? reinterpret_cast<int64_t *>(static_cast<uint8_t *>(out) +
                                                                      a->input_bytes)
                                        : nullptr;
+                    const int pdl = prev_fused && host_gate && !ev && !no_pdl;
                     rc = collate_augment_publish(a->src, idx, b, a->h, a->w, a->c, a->pad,
                                                  a->flip, a->seed, a->epoch, a->scale, a->bias,
-                                                 a->out_kind, out, tgt, ready, q, counter, stream);
+                                                 a->out_kind, out, tgt, ready, q, counter, pdl,
+                                                 stream);
                     published = true;
                     break;
                 }
@@ -81,6 +100,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                 TSB_CHECK(false, "bad produce mode %d", a->mode);
         }
         if (rc) return rc;
+        prev_fused = published;
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
         if (published) continue;
         if (a->with_target)

@@ -219,6 +219,35 @@ int ring_publish_ptrs(tsb_ring *r, int slot, uint64_t **ready, unsigned int **co
     *counter = r->counters + slot;
     return TSB_OK;
 }
+
+bool ring_has_host_control(const tsb_ring *r) { return r && r->h_ctl; }
+
+// Host-side flow gate for rings whose control words live in host-shared
+// memory: block the enqueuing thread until every live cursor has released
+// `need` (wrap-around GEQ, as cuStreamWaitValue64; the eviction sentinel
+// passes).  The producer's stream then carries only kernels, so consecutive
+// batches chain with programmatic dependent launch instead of stalling the
+// GPU front end on a PCIe poll per cursor.  Same rule as the device wait
+// (producer.py:230-238 flow gate): the host never runs more than `slots`
+// batches ahead of the slowest live consumer.
+int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need) {
+    TSB_CHECK(r && r->h_ctl, "host gate needs a host control block");
+    if (n_live <= 0 || need == 0) return TSB_OK;
+    for (int i = 0; i < n_live; ++i) {
+        TSB_CHECK(live[i] >= 0 && live[i] < r->max_consumers, "bad consumer %d", live[i]);
+        const uint64_t *h = r->h_ctl + r->slots + live[i];
+        int64_t spins = 0;
+        while ((int64_t)(__atomic_load_n(h, __ATOMIC_ACQUIRE) - need) < 0) {
+            if (++spins < 2048) {
+                __builtin_ia32_pause();
+            } else {
+                struct timespec ns = {0, 5000};
+                nanosleep(&ns, nullptr);
+            }
+        }
+    }
+    return TSB_OK;
+}
 }  // namespace tsb
 
 extern "C" {

@@ -107,3 +107,74 @@ def test_consume_range_events():
     cs.synchronize()
     assert ring.read_cursor(0) == 8 and e0.elapsed_ms(e1) >= 0
     ring.close()
+
+
+@pytest.mark.parametrize("out_dtype,kind", [("float32", 1), ("bfloat16", 2)])
+def test_host_gate_pdl_chain_with_concurrent_consumer(oracle, out_dtype, kind):
+    """TSB_GATE_HOST: the producer thread blocks on the host-shared cursors and
+    the stream carries only PDL-chained fused kernels.  A host consumer thread
+    (map-and-ack, bs/cli.py:252-258) checks every batch against the oracle
+    before releasing it -- a slot overwritten early would show up as a mismatch
+    -- and its ack is what lets the producer run ahead."""
+    import threading
+
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    h, w, c, B, N, S, n = 32, 64, 3, 8, 96, 3, 24
+    store = StoreSource.synthetic(4, N, (h, w, c))
+    ld = CollateLoader(DatasetSpec(store, N, B, shuffle_seed=2),
+                       AugmentSpec(pad=4, flip=True, out_dtype=out_dtype, seed=1))
+    ring = DeviceRing(S, ld.batch_nbytes, 2, control="host")
+    ring.set_cursor(0, 0)
+    ring.evict(1)  # a dead consumer slot must not block the host gate
+    store_h = oracle.make_store(4, N, h * w * c)
+    scale, bias = oracle.norm_consts()
+    L = len(ld)
+    errors = []
+
+    def consumer():
+        try:
+            for q in range(1, n + 1):
+                epoch, bi = divmod(q - 1, L)
+                slot = ring.slot_of(q)
+                ring.host_wait_ready(slot, q, timeout_s=60)
+                got = ring.view(slot, (ld.batch_nbytes,), torch.uint8).cpu().numpy()
+                idx = oracle.epoch_order(N, 2, epoch)[bi * B:(bi + 1) * B]
+                want = oracle.collate_augment(store_h, idx, h, w, c, 4, True, 1, epoch, kind,
+                                              scale, bias)
+                if got[:ld.input_nbytes].tobytes() != want.tobytes():
+                    errors.append(q)
+                ring.host_ack(0, q)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+            ring.evict(0)
+
+    t = threading.Thread(target=consumer)
+    t.start()
+    ps = torch.cuda.Stream()
+    q = 1
+    while q <= n:
+        epoch, bi = divmod(q - 1, L)
+        m = min(n - q + 1, L - bi)
+        a = ld.produce_args(epoch)
+        a.gate = GATE_HOST
+        produce_range(ring, a, q, bi, m, [0, 1], stream=ps)
+        q += m
+    ps.synchronize()
+    t.join(120)
+    assert not t.is_alive() and not errors, errors
+    assert ring.read_cursor(0) == n
+    ring.close()
+
+
+def test_host_gate_needs_host_control():
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    store = StoreSource.synthetic(0, 16, (8, 16, 3))
+    ld = CollateLoader(DatasetSpec(store, 16, 4), AugmentSpec(pad=2, out_dtype="float32"))
+    ring = DeviceRing(2, ld.batch_nbytes, 1, control="device")
+    a = ld.produce_args(0)
+    a.gate = GATE_HOST
+    with pytest.raises(ValueError, match="host control"):
+        produce_range(ring, a, 1, 0, 1, [0])
+    ring.close()

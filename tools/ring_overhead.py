@@ -62,6 +62,7 @@ def run(mode, ncons, control="device"):
     live = list(range(ncons)) if mode != "none" else []
     a = ld.produce_args(0)
     a.wait_stride = STRIDE
+    a.gate = int(os.environ.get("GATE", 0)) if control == "host" else 0
     produce_range(ring, a, 1, 0, Wm, live, stream=s)
     s.synchronize()
     e0, e1 = dp.DeviceEvent(), dp.DeviceEvent()
