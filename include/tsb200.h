@@ -30,6 +30,9 @@ extern "C" {
 #define TSB_ERR_UNSUPPORTED -5
 
 #define TSB_IPC_HANDLE_BYTES 64
+/* max writers per ring (sharded ingest) and max fan-out destinations */
+#define TSB_MAX_WRITERS 8
+#define TSB_MAX_DST 8
 /* cursor value of an evicted consumer / dropped retention (2^62) */
 #define TSB_CURSOR_EVICTED 0x4000000000000000ULL
 
@@ -122,13 +125,22 @@ int tsb_ring_create(int dev, int slots, size_t slot_bytes, int max_consumers, ts
 int tsb_ring_export(tsb_ring *r, void *handle_out);
 int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_consumers,
                     tsb_ring **out);
+/* Rings with `writers` > 1 (sharded ingest): slot s is complete when each of
+ * the writers published it (one ready word per writer and slot). */
+int tsb_ring_create_ex(int dev, int slots, size_t slot_bytes, int max_consumers, int writers,
+                       tsb_ring **out);
+int tsb_ring_import_ex(const void *handle, int slots, size_t slot_bytes, int max_consumers,
+                       int writers, tsb_ring **out);
+int tsb_ring_writers(tsb_ring *r, int *writers);
 int tsb_ring_destroy(tsb_ring *r);
 int tsb_ring_slot_ptr(tsb_ring *r, int slot, void **out);
 int tsb_ring_base_ptr(tsb_ring *r, void **out);
 int tsb_ring_geometry(tsb_ring *r, int *slots, size_t *slot_bytes, int *max_consumers);
 /* Producer: ready[slot] = seq after all prior work on `stream` (release). */
 int tsb_ring_publish(tsb_ring *r, int slot, uint64_t seq, void *stream);
-/* Consumer: `stream` waits until ready[slot] >= seq (acquire). */
+/* Writer `writer`'s shard of the slot is complete (sharded ingest). */
+int tsb_ring_publish_shard(tsb_ring *r, int slot, int writer, uint64_t seq, void *stream);
+/* Consumer: `stream` waits until ready[slot] >= seq for every writer (acquire). */
 int tsb_ring_wait_ready(tsb_ring *r, int slot, uint64_t seq, void *stream);
 /* Consumer release (device-counted ack): cursor[consumer] = seq after all
  * prior work on `stream` (bs/consumer.py:330 Ack + release_view). */
@@ -152,6 +164,7 @@ int tsb_ring_sync_mode(void);
  * readers/writers (evict, consumers that only map + ack) never touch a
  * GPU channel -- no cross-process GPU context switch per batch. */
 size_t tsb_ring_control_bytes(int slots, int max_consumers);
+size_t tsb_ring_control_bytes_ex(int slots, int max_consumers, int writers);
 int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int init);
 /* Host consumer: spin until ready[slot] >= seq (timeout_us < 0 = forever). */
 int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeout_us);
@@ -213,6 +226,25 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
  * that maps and releases, bs/cli.py:252-258).  ev: NULL or 2 events recorded
  * after the first and after the last ready wait. */
 int tsb_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, void **ev, void *stream);
+
+/* Sharded ingest + fused fan-out (NEW, the data "broadcast"
+ * of bs/consumer.py:319-321 across GPUs).  Writer `shard` of `n_shards`
+ * produces rows [shard*B/n_shards, (shard+1)*B/n_shards) of every batch and
+ * stores them straight into the same slot of each of rings[0..n_rings)
+ * (<= TSB_MAX_DST): its own device's ring and peer rings opened over CUDA
+ * IPC, i.e. P2P stores over NVLink/NVSwitch -- the all-gather is fused into
+ * the producing kernel.  The kernel's last CTA publishes ready[slot][shard]
+ * in every ring.  rings[local] lives on the launching device (its completion
+ * counters are used).  live = the concatenated live-cursor lists of the
+ * rings, n_live[i] entries for ring i; the gate is on the host, so every
+ * ring needs a host control block.  Each ring must have n_shards writers.
+ * n_shards == 1 with several rings is the single-producer star.  Modes:
+ * TSB_SRC_AUGMENT (fused collate/augment), TSB_SRC_GATHER, TSB_SRC_SYNTHETIC
+ * (sample_bytes a multiple of 16 for the last two).  Consecutive batches
+ * are chained with programmatic dependent launch. */
+int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_produce_args *a,
+                      int shard, int n_shards, uint64_t seq0, int64_t batch0, int n,
+                      const int *live, const int *n_live, void *stream);
 
 #ifdef __cplusplus
 }

@@ -92,6 +92,11 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_ring_control_bytes": (sz, [i32, i32]),
     "tsb_ring_attach_host_control": (i32, [vp, vp, sz, i32]),
     "tsb_ring_host_wait_ready": (i32, [vp, i32, u64, i64]),
+    "tsb_ring_create_ex": (i32, [i32, i32, sz, i32, i32, pp]),
+    "tsb_ring_import_ex": (i32, [vp, i32, sz, i32, i32, pp]),
+    "tsb_ring_writers": (i32, [vp, ctypes.POINTER(i32)]),
+    "tsb_ring_publish_shard": (i32, [vp, i32, i32, u64, vp]),
+    "tsb_ring_control_bytes_ex": (sz, [i32, i32, i32]),
     "tsb_fanout": (i32, [vp, pp, i32, sz, vp]),
     "tsb_collate_augment_fanout": (i32, [vp, vp, i64, i32, i32, i32, i32, i32, u64, u64, fp, fp,
                                          i32, pp, i32, vp]),
@@ -119,6 +124,8 @@ SRC_AUGMENT, SRC_GATHER, SRC_SYNTHETIC = 0, 1, 2
 SIGNATURES["tsb_produce_range"] = (i32, [vp, ctypes.POINTER(ProduceArgs), u64, i64, i32,
                                          ctypes.POINTER(i32), i32, pp, vp])
 SIGNATURES["tsb_consume_range"] = (i32, [vp, i32, u64, i32, pp, vp])
+SIGNATURES["tsb_produce_group"] = (i32, [pp, i32, i32, ctypes.POINTER(ProduceArgs), i32, i32, u64,
+                                         i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp])
 
 _lib = None
 _lock = threading.Lock()

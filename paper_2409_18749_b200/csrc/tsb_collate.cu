@@ -169,17 +169,54 @@ struct CaGeom {
 // Fused epilogue: write the int64 sample indices (the batch "target") after
 // the input, and publish the ring slot from the last CTA to finish (grid
 // completion counter; release at system scope), replacing a memcpy launch and
-// a stream memop per batch.
+// a stream memop per batch.  With several destinations (fan-out to peer
+// rings) every destination gets the target and its ready word.
 struct Epi {
-    int64_t *tgt;            // nullptr = no target copy
-    uint64_t *ready;         // nullptr = no publish
+    int64_t *tgt[MAX_DST];   // per destination: target region (nullptr = none)
+    uint64_t *ready[MAX_DST];  // per destination: this writer's ready word (nullptr = none)
+    int n;                   // destinations with a tgt/ready entry
     uint64_t seq;
-    unsigned int *counter;   // device completion counter (reset by the last CTA)
+    unsigned int *counter;   // device completion counter (reset by the last CTA); nullptr = no publish
     int pdl;                 // launch as a programmatic dependent of the previous batch
+    int sys_fence;           // destinations on other devices: order stores at system scope
 };
 
 __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ void write_targets(const Epi &ep, const int64_t *__restrict__ idx, int b,
+                                              int tid, int nthreads) {
+    for (int d = 0; d < ep.n; ++d)
+        if (ep.tgt[d])
+            for (int i = tid; i < b; i += nthreads) ep.tgt[d][i] = idx[i];
+}
+
+// Last CTA to finish publishes the slot: every thread orders its stores
+// (gpu scope, or system scope when peers are among the destinations), the
+// CTA's `nthreads` participating threads meet on named barrier 1, one thread
+// bumps the completion counter and the last CTA release-stores each
+// destination's ready word at system scope (host-shared control words and
+// peer devices both observe it).
+__device__ __forceinline__ void publish_epilogue(const Epi &ep, int tid, int nthreads) {
+    if (!ep.counter) return;
+    if (ep.sys_fence)
+        __threadfence_system();
+    else
+        __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+    if (tid == 0) {
+        const unsigned int prev = atomicAdd(ep.counter, 1u);
+        if (prev == gridDim.x - 1) {  // last CTA: every store of the batch is visible
+            *ep.counter = 0u;
+            __threadfence_system();
+            for (int d = 0; d < ep.n; ++d)
+                if (ep.ready[d])
+                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready[d]),
+                                 "l"(ep.seq)
+                                 : "memory");
+        }
+    }
 }
 
 struct ItemPar {
@@ -403,8 +440,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     }
 
     // ---------------- consumer warps: emit normalised NCHW ------------------
-    if (ep.tgt && blockIdx.x == 0)
-        for (int i = tid; i < g.b; i += CA_THREADS) ep.tgt[i] = idx[i];
+    if (blockIdx.x == 0) write_targets(ep, idx, g.b, tid, CA_THREADS);
     const int64_t plane_bytes = g.plane * T::ELEM;
     // first slot of this thread; further slots every CA_THREADS (no divisions in the loop)
     const int r_first = tid / g.groups;
@@ -457,19 +493,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     // different ring slot, and its gate was checked on the host, so it never
     // needs this grid's results (no griddepcontrol.wait anywhere).
     pdl_launch_dependents();
-    if (ep.ready) {
-        __threadfence();                                       // this thread's stores
-        asm volatile("bar.sync 1, %0;" ::"n"(CA_THREADS) : "memory");  // consumer warps only
-        if (tid == 0) {
-            const unsigned int prev = atomicAdd(ep.counter, 1u);
-            if (prev == gridDim.x - 1) {  // last CTA: every store of the batch is visible
-                *ep.counter = 0u;
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready), "l"(ep.seq)
-                             : "memory");
-            }
-        }
-    }
+    publish_epilogue(ep, tid, CA_THREADS);
 }
 
 template <int K, int C, bool MULTI>
@@ -626,6 +650,83 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
                                      dsts, smem, s, ep);
 }
 
+// ---------------------------------------------------------------------------
+// Passthrough fan-out (gather from a store, or the SplitMix64 synthetic
+// source) with the fused epilogue: every 16-byte vector of the shard is
+// loaded (or generated) once and stored to each destination slot -- the
+// local ring and peer rings over NVLink.  Work items = (sample, 16 KB chunk),
+// strided over a persistent grid; 4 independent 16 B loads per thread.
+constexpr int PT_THREADS = 256;
+constexpr int PT_CHUNK = 16384;
+
+template <bool SYNTH, bool MULTI>
+__global__ void __launch_bounds__(PT_THREADS)
+    passthrough_multi_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
+                             int64_t sb, int b, uint64_t seed, uint64_t epoch, Dsts dsts, Epi ep) {
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0) write_targets(ep, idx, b, tid, PT_THREADS);
+    const int chunks = (int)((sb + PT_CHUNK - 1) / PT_CHUNK);
+    const int items = b * chunks;
+    const int64_t nvec = sb >> 4;
+    constexpr int U = PT_CHUNK / 16 / PT_THREADS;  // 4
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int s = it / chunks, c = it - s * chunks;
+        const int64_t v0 = (int64_t)c * (PT_CHUNK / 16);
+        const int64_t v1 = min(v0 + PT_CHUNK / 16, nvec);
+        const uint64_t key = SYNTH ? derive_key(seed, epoch, (uint64_t)idx[s]) : 0;
+        const uint8_t *in = SYNTH ? nullptr : src + idx[s] * sb;
+        const int64_t out_off = (int64_t)s * sb;
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = v0 + tid + u * PT_THREADS;
+            if (k < v1) {
+                if constexpr (SYNTH) {
+                    const uint64_t a = mix64(key + (uint64_t)(2 * k + 1) * GAMMA);
+                    const uint64_t bb = mix64(key + (uint64_t)(2 * k + 2) * GAMMA);
+                    v[u] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)bb,
+                                      (uint32_t)(bb >> 32));
+                } else {
+                    v[u] = ld_nc_v4(in + 16 * k);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = v0 + tid + u * PT_THREADS;
+            if (k < v1) {
+                if constexpr (!MULTI) {
+                    st_v4(static_cast<uint8_t *>(dsts.p[0]) + out_off + 16 * k, v[u]);
+                } else {
+#pragma unroll
+                    for (int d = 0; d < MAX_DST; ++d)
+                        if (d < dsts.n)
+                            st_v4(static_cast<uint8_t *>(dsts.p[d]) + out_off + 16 * k, v[u]);
+                }
+            }
+        }
+    }
+    pdl_launch_dependents();
+    publish_epilogue(ep, tid, PT_THREADS);
+}
+
+template <typename Kern, typename... Args>
+int launch_maybe_pdl(Kern kern, int grid, int block, size_t smem, cudaStream_t s, bool pdl,
+                     Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+    return TSB_OK;
+}
+
 }  // namespace
 
 namespace tsb {
@@ -638,9 +739,71 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     Dsts d{};
     d.p[0] = out;
     d.n = 1;
-    Epi ep{tgt, ready, seq, counter, pdl};
+    Epi ep{};
+    ep.tgt[0] = tgt;
+    ep.ready[0] = ready;
+    ep.n = 1;
+    ep.seq = seq;
+    ep.counter = counter;
+    ep.pdl = pdl;
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
                           out_kind, nullptr, d, stream, ep);
+}
+
+// One batch shard into n destinations (fan-out), fused target copy + publish:
+// outs[d] = the shard's input base in destination d, tgts[d] its target base,
+// readys[d] this writer's ready word in destination d's ring.
+int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int h, int w, int c,
+                  int pad, int flip, uint64_t seed, uint64_t epoch, const float *scale,
+                  const float *bias, int out_kind, int64_t sample_bytes, void *const *outs,
+                  int64_t *const *tgts, uint64_t *const *readys, int n, unsigned int *counter,
+                  uint64_t seq, int pdl, int sys_fence, void *stream) {
+    TSB_CHECK(n >= 1 && n <= MAX_DST, "destinations must be 1..%d", MAX_DST);
+    Dsts d{};
+    Epi ep{};
+    for (int i = 0; i < n; ++i) {
+        TSB_CHECK(outs[i], "null destination %d", i);
+        d.p[i] = outs[i];
+        ep.tgt[i] = tgts ? tgts[i] : nullptr;
+        ep.ready[i] = readys ? readys[i] : nullptr;
+    }
+    d.n = ep.n = n;
+    ep.seq = seq;
+    ep.counter = counter;
+    ep.pdl = pdl;
+    ep.sys_fence = sys_fence;
+    if (mode == TSB_SRC_AUGMENT)
+        return launch_collate(src, idx, b, h, w, c, pad, flip, seed, epoch, scale, bias, out_kind,
+                              nullptr, d, stream, ep);
+    TSB_CHECK(mode == TSB_SRC_GATHER || mode == TSB_SRC_SYNTHETIC, "bad produce mode %d", mode);
+    TSB_CHECK(sample_bytes > 0 && sample_bytes % 16 == 0,
+              "fan-out passthrough needs sample_bytes %% 16 == 0 (got %lld)",
+              (long long)sample_bytes);
+    TSB_CHECK(b >= 0 && b < (1 << 24), "bad batch %lld", (long long)b);
+    for (int i = 0; i < n; ++i)
+        TSB_CHECK(((uintptr_t)outs[i] & 15) == 0, "destination %d must be 16-byte aligned", i);
+    const bool synth = mode == TSB_SRC_SYNTHETIC;
+    TSB_CHECK(synth || (src && ((uintptr_t)src & 15) == 0), "store must be 16-byte aligned");
+    const int64_t chunks = (sample_bytes + PT_CHUNK - 1) / PT_CHUNK;
+    int64_t items = b * chunks;
+    TSB_CHECK(items < (1ll << 31), "too many work items");
+    const int64_t cap = (int64_t)sm_count() * 8;
+    const int grid = (int)(items < 1 ? 1 : (items < cap ? items : cap));
+    auto s = as_stream(stream);
+    const auto *s8 = static_cast<const uint8_t *>(src);
+    const int bb = (int)b;
+    if (synth) {
+        if (n == 1)
+            return launch_maybe_pdl(passthrough_multi_kernel<true, false>, grid, PT_THREADS, 0, s,
+                                    pdl, s8, idx, sample_bytes, bb, seed, epoch, d, ep);
+        return launch_maybe_pdl(passthrough_multi_kernel<true, true>, grid, PT_THREADS, 0, s, pdl,
+                                s8, idx, sample_bytes, bb, seed, epoch, d, ep);
+    }
+    if (n == 1)
+        return launch_maybe_pdl(passthrough_multi_kernel<false, false>, grid, PT_THREADS, 0, s, pdl,
+                                s8, idx, sample_bytes, bb, seed, epoch, d, ep);
+    return launch_maybe_pdl(passthrough_multi_kernel<false, true>, grid, PT_THREADS, 0, s, pdl, s8,
+                            idx, sample_bytes, bb, seed, epoch, d, ep);
 }
 }  // namespace tsb
 

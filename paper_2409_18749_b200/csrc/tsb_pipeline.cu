@@ -8,7 +8,14 @@
 using namespace tsb;
 
 namespace tsb {
-int ring_publish_ptrs(tsb_ring *r, int slot, uint64_t **ready, unsigned int **counter);
+int ring_publish_ptrs(tsb_ring *r, int slot, int writer, uint64_t **ready, unsigned int **counter);
+int ring_writers(const tsb_ring *r);
+int ring_phys_device(const tsb_ring *r);
+int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int h, int w, int c,
+                  int pad, int flip, uint64_t seed, uint64_t epoch, const float *scale,
+                  const float *bias, int out_kind, int64_t sample_bytes, void *const *outs,
+                  int64_t *const *tgts, uint64_t *const *readys, int n, unsigned int *counter,
+                  uint64_t seq, int pdl, int sys_fence, void *stream);
 bool ring_has_host_control(const tsb_ring *r);
 int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need);
 int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
@@ -70,10 +77,10 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         bool published = false;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
-                if (!a->d_crc && !no_fused) {  // fused epilogue: target copy + publish from the kernel
+                if (!a->d_crc && !no_fused && ring_writers(r) == 1) {  // fused epilogue: target copy + publish from the kernel
                     uint64_t *ready = nullptr;
                     unsigned int *counter = nullptr;
-                    if ((rc = ring_publish_ptrs(r, slot, &ready, &counter))) return rc;
+                    if ((rc = ring_publish_ptrs(r, slot, 0, &ready, &counter))) return rc;
                     int64_t *tgt = a->with_target
                                        ? reinterpret_cast<int64_t *>(static_cast<uint8_t *>(out) +
                                                                      a->input_bytes)
@@ -126,6 +133,81 @@ int tsb_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, void **ev
         if (ev && i == n - 1) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[1]), s));
         if (int rc = tsb_ring_ack(r, consumer, q, stream)) return rc;
     }
+    return TSB_OK;
+}
+
+int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_produce_args *a,
+                      int shard, int n_shards, uint64_t seq0, int64_t batch0, int n,
+                      const int *live, const int *n_live, void *stream) {
+    TSB_CHECK(rings && a && a->d_order && n_live, "null argument");
+    TSB_CHECK(n_rings >= 1 && n_rings <= TSB_MAX_DST, "rings must be 1..%d", TSB_MAX_DST);
+    TSB_CHECK(local >= 0 && local < n_rings, "bad local ring %d", local);
+    TSB_CHECK(n_shards >= 1 && shard >= 0 && shard < n_shards, "bad shard %d/%d", shard, n_shards);
+    TSB_CHECK(seq0 >= 1 && n >= 0 && batch0 >= 0, "bad range");
+    TSB_CHECK(!a->d_crc, "per-batch CRC is not fused into the fan-out path");
+    const int64_t b = a->batch_size;
+    TSB_CHECK(b >= n_shards, "batch %lld smaller than the %d shards", (long long)b, n_shards);
+    const size_t nbytes = (size_t)a->input_bytes + (a->with_target ? 8 * (size_t)b : 0);
+    int slots = 0;
+    size_t stride = 0;
+    if (int rc = tsb_ring_geometry(rings[0], &slots, &stride, nullptr)) return rc;
+    const int dev = ring_phys_device(rings[local]);
+    int sys_fence = 0, n_live_total = 0;
+    for (int k = 0; k < n_rings; ++k) {
+        int sk = 0;
+        size_t st = 0;
+        TSB_CHECK(rings[k], "null ring %d", k);
+        if (int rc = tsb_ring_geometry(rings[k], &sk, &st, nullptr)) return rc;
+        TSB_CHECK(sk == slots && st >= nbytes, "ring %d: %d slots of %zu B (need %d of %zu B)", k,
+                  sk, st, slots, nbytes);
+        TSB_CHECK(ring_writers(rings[k]) == n_shards, "ring %d has %d writers, not %d shards", k,
+                  ring_writers(rings[k]), n_shards);
+        TSB_CHECK(ring_has_host_control(rings[k]), "ring %d needs a host control block", k);
+        TSB_CHECK(n_live[k] >= 0, "bad live count");
+        if (ring_phys_device(rings[k]) != dev) sys_fence = 1;
+        n_live_total += n_live[k];
+    }
+    TSB_CHECK(live || n_live_total == 0, "null live list");
+    // shard rows and their byte offsets inside a slot
+    const int64_t s0 = shard * b / n_shards, s1 = (shard + 1) * b / n_shards, bs = s1 - s0;
+    const int64_t out_sample = a->input_bytes / b;
+    TSB_CHECK(out_sample * b == a->input_bytes, "input_bytes is not a whole number of samples");
+    auto s = as_stream(stream);
+    for (int i = 0; i < n; ++i) {
+        const uint64_t q = seq0 + (uint64_t)i;
+        const int slot = (int)((q - 1) % (uint64_t)slots);
+        // host flow gate: every ring's live consumers released the slot's previous batch
+        if (q > (uint64_t)slots) {
+            int off = 0;
+            for (int k = 0; k < n_rings; ++k) {
+                if (int rc = ring_host_gate(rings[k], live + off, n_live[k], q - (uint64_t)slots))
+                    return rc;
+                off += n_live[k];
+            }
+        }
+        void *outs[TSB_MAX_DST];
+        int64_t *tgts[TSB_MAX_DST];
+        uint64_t *readys[TSB_MAX_DST];
+        unsigned int *counter = nullptr;
+        for (int k = 0; k < n_rings; ++k) {
+            void *base = nullptr;
+            if (int rc = tsb_ring_slot_ptr(rings[k], slot, &base)) return rc;
+            uint8_t *b8 = static_cast<uint8_t *>(base);
+            outs[k] = b8 + s0 * out_sample;
+            tgts[k] = a->with_target ? reinterpret_cast<int64_t *>(b8 + a->input_bytes) + s0
+                                     : nullptr;
+            if (int rc = ring_publish_ptrs(rings[k], slot, shard, &readys[k],
+                                           k == local ? &counter : nullptr))
+                return rc;
+        }
+        const int64_t *idx = a->d_order + (batch0 + i) * b + s0;
+        if (int rc = produce_multi(a->mode, a->src, idx, bs, a->h, a->w, a->c, a->pad, a->flip,
+                                   a->seed, a->epoch, a->scale, a->bias, a->out_kind,
+                                   a->sample_bytes, outs, tgts, readys, n_rings, counter, q,
+                                   i > 0, sys_fence, stream))
+            return rc;
+    }
+    (void)s;
     return TSB_OK;
 }
 

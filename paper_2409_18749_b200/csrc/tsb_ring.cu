@@ -31,8 +31,10 @@ struct tsb_ring {
     size_t slot_bytes;
     size_t slot_stride;
     int max_consumers;
+    int writers;       // ready words per slot (sharded ingest: one per writer)
+    int phys_dev;      // device whose HBM holds the ring (!= dev for a peer import)
     uint8_t *base;
-    uint64_t *ready;   // [slots]          device-visible address (memops)
+    uint64_t *ready;   // [slots][writers] device-visible address (memops)
     uint64_t *cursor;  // [max_consumers]  device-visible address (memops)
     uint64_t *h_ctl;   // host view of a host-shared control block (or null)
     unsigned int *counters;  // [slots] device completion counters (fused publish)
@@ -169,9 +171,10 @@ int dev_wait(tsb_ring *r, const uint64_t *const *addrs, int n, uint64_t v, void 
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-size_t ctl_words_bytes(const tsb_ring *r) {
-    return round_up(sizeof(uint64_t) * (size_t)(r->slots + r->max_consumers), 256);
+size_t ctl_words(const tsb_ring *r) {
+    return (size_t)r->slots * (size_t)r->writers + (size_t)r->max_consumers;
 }
+size_t ctl_words_bytes(const tsb_ring *r) { return round_up(sizeof(uint64_t) * ctl_words(r), 256); }
 
 void layout(tsb_ring *r) {
     r->slot_stride = round_up(r->slot_bytes ? r->slot_bytes : 16, 256);
@@ -182,8 +185,12 @@ void layout(tsb_ring *r) {
 void bind(tsb_ring *r) {
     const size_t payload = r->slot_stride * (size_t)r->slots;
     r->ready = reinterpret_cast<uint64_t *>(r->base + payload);
-    r->cursor = r->ready + r->slots;
+    r->cursor = r->ready + (size_t)r->slots * r->writers;
     r->counters = reinterpret_cast<unsigned int *>(r->base + payload + ctl_words_bytes(r));
+}
+
+uint64_t *ready_word(tsb_ring *r, int slot, int writer) {
+    return r->ready + (size_t)slot * r->writers + writer;
 }
 
 // host view of a control word (host-shared control block), or null
@@ -213,12 +220,16 @@ int host_read(tsb_ring *r, const uint64_t *addr, uint64_t *out) {
 }  // namespace
 
 namespace tsb {
-int ring_publish_ptrs(tsb_ring *r, int slot, uint64_t **ready, unsigned int **counter) {
+int ring_publish_ptrs(tsb_ring *r, int slot, int writer, uint64_t **ready,
+                      unsigned int **counter) {
     TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
-    *ready = r->ready + slot;
-    *counter = r->counters + slot;
+    TSB_CHECK(writer >= 0 && writer < r->writers, "bad writer %d", writer);
+    *ready = ready_word(r, slot, writer);
+    if (counter) *counter = r->counters + slot;
     return TSB_OK;
 }
+int ring_writers(const tsb_ring *r) { return r->writers; }
+int ring_phys_device(const tsb_ring *r) { return r->phys_dev; }
 
 bool ring_has_host_control(const tsb_ring *r) { return r && r->h_ctl; }
 
@@ -235,7 +246,7 @@ int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need) {
     if (n_live <= 0 || need == 0) return TSB_OK;
     for (int i = 0; i < n_live; ++i) {
         TSB_CHECK(live[i] >= 0 && live[i] < r->max_consumers, "bad consumer %d", live[i]);
-        const uint64_t *h = r->h_ctl + r->slots + live[i];
+        const uint64_t *h = r->h_ctl + (size_t)r->slots * r->writers + live[i];
         int64_t spins = 0;
         while ((int64_t)(__atomic_load_n(h, __ATOMIC_ACQUIRE) - need) < 0) {
             if (++spins < 2048) {
@@ -255,15 +266,23 @@ extern "C" {
 int tsb_ring_sync_mode(void) { return resolve_mode(); }
 
 int tsb_ring_create(int dev, int slots, size_t slot_bytes, int max_consumers, tsb_ring **out) {
+    return tsb_ring_create_ex(dev, slots, slot_bytes, max_consumers, 1, out);
+}
+
+int tsb_ring_create_ex(int dev, int slots, size_t slot_bytes, int max_consumers, int writers,
+                       tsb_ring **out) {
     TSB_CHECK(out, "null out");
     TSB_CHECK(slots >= 1 && max_consumers >= 1 && max_consumers <= 4096,
               "bad ring geometry slots=%d consumers=%d", slots, max_consumers);
+    TSB_CHECK(writers >= 1 && writers <= TSB_MAX_WRITERS, "writers must be 1..%d", TSB_MAX_WRITERS);
     TSB_CUDA(cudaSetDevice(dev));
     tsb_ring *r = new tsb_ring{};
     r->dev = dev;
     r->slots = slots;
     r->slot_bytes = slot_bytes;
     r->max_consumers = max_consumers;
+    r->writers = writers;
+    r->phys_dev = dev;
     layout(r);
     cudaError_t e = cudaMalloc(&r->base, r->total);
     if (e != cudaSuccess) {
@@ -292,12 +311,19 @@ int tsb_ring_export(tsb_ring *r, void *handle_out) {
 
 int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_consumers,
                     tsb_ring **out) {
+    return tsb_ring_import_ex(handle, slots, slot_bytes, max_consumers, 1, out);
+}
+
+int tsb_ring_import_ex(const void *handle, int slots, size_t slot_bytes, int max_consumers,
+                       int writers, tsb_ring **out) {
     TSB_CHECK(handle && out, "null argument");
+    TSB_CHECK(writers >= 1 && writers <= TSB_MAX_WRITERS, "writers must be 1..%d", TSB_MAX_WRITERS);
     tsb_ring *r = new tsb_ring{};
     TSB_CUDA(cudaGetDevice(&r->dev));
     r->slots = slots;
     r->slot_bytes = slot_bytes;
     r->max_consumers = max_consumers;
+    r->writers = writers;
     layout(r);
     cudaIpcMemHandle_t h;
     memcpy(&h, handle, sizeof(h));
@@ -311,6 +337,12 @@ int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_co
     }
     r->base = static_cast<uint8_t *>(p);
     r->imported = true;
+    r->phys_dev = r->dev;
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, p) == cudaSuccess)
+        r->phys_dev = pa.device;
+    else
+        cudaGetLastError();
     bind(r);
     TSB_CUDA(cudaStreamCreateWithFlags(&r->host_stream, cudaStreamNonBlocking));
     resolve_mode();
@@ -319,13 +351,17 @@ int tsb_ring_import(const void *handle, int slots, size_t slot_bytes, int max_co
 }
 
 size_t tsb_ring_control_bytes(int slots, int max_consumers) {
-    return round_up(sizeof(uint64_t) * (size_t)(slots + max_consumers), 4096);
+    return tsb_ring_control_bytes_ex(slots, max_consumers, 1);
+}
+size_t tsb_ring_control_bytes_ex(int slots, int max_consumers, int writers) {
+    return round_up(sizeof(uint64_t) * ((size_t)slots * (size_t)writers + (size_t)max_consumers),
+                    4096);
 }
 
 int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int init) {
     TSB_CHECK(r && host_ctl, "null argument");
     TSB_CHECK(!r->h_ctl, "ring already has a host control block");
-    const size_t need = sizeof(uint64_t) * (size_t)(r->slots + r->max_consumers);
+    const size_t need = sizeof(uint64_t) * ctl_words(r);
     TSB_CHECK(bytes >= need && ((uintptr_t)host_ctl & 7) == 0,
               "host control block too small or misaligned (%zu < %zu)", bytes, need);
     if (init) memset(host_ctl, 0, need);
@@ -335,16 +371,17 @@ int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int 
     TSB_CUDA(cudaHostGetDevicePointer(&dptr, host_ctl, 0));
     r->h_ctl = static_cast<uint64_t *>(host_ctl);
     r->ready = static_cast<uint64_t *>(dptr);
-    r->cursor = r->ready + r->slots;
+    r->cursor = r->ready + (size_t)r->slots * r->writers;
     return TSB_OK;
 }
 
 int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeout_us) {
     TSB_CHECK(r && r->h_ctl && slot >= 0 && slot < r->slots, "needs a host control block");
-    uint64_t *h = r->h_ctl + slot;
     int64_t spins = 0;
     struct timespec t0, t;
     clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int w = 0; w < r->writers; ++w) {
+    uint64_t *h = r->h_ctl + (size_t)slot * r->writers + w;
     while (__atomic_load_n(h, __ATOMIC_ACQUIRE) < seq) {
         if (++spins > 256) {
             clock_gettime(CLOCK_MONOTONIC, &t);
@@ -358,6 +395,7 @@ int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeou
                 nanosleep(&ns, nullptr);
             }
         }
+    }
     }
     return TSB_OK;
 }
@@ -387,6 +425,11 @@ int tsb_ring_base_ptr(tsb_ring *r, void **out) {
     *out = r->base;
     return TSB_OK;
 }
+int tsb_ring_writers(tsb_ring *r, int *writers) {
+    TSB_CHECK(r && writers, "null argument");
+    *writers = r->writers;
+    return TSB_OK;
+}
 int tsb_ring_geometry(tsb_ring *r, int *slots, size_t *slot_bytes, int *max_consumers) {
     TSB_CHECK(r, "null ring");
     if (slots) *slots = r->slots;
@@ -397,12 +440,20 @@ int tsb_ring_geometry(tsb_ring *r, int *slots, size_t *slot_bytes, int *max_cons
 
 int tsb_ring_publish(tsb_ring *r, int slot, uint64_t seq, void *stream) {
     TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
-    return dev_write(r, r->ready + slot, seq, stream);
+    for (int w = 0; w < r->writers; ++w)
+        if (int rc = dev_write(r, ready_word(r, slot, w), seq, stream)) return rc;
+    return TSB_OK;
+}
+int tsb_ring_publish_shard(tsb_ring *r, int slot, int writer, uint64_t seq, void *stream) {
+    TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
+    TSB_CHECK(writer >= 0 && writer < r->writers, "bad writer %d", writer);
+    return dev_write(r, ready_word(r, slot, writer), seq, stream);
 }
 int tsb_ring_wait_ready(tsb_ring *r, int slot, uint64_t seq, void *stream) {
     TSB_CHECK(r && slot >= 0 && slot < r->slots, "bad slot");
-    const uint64_t *a = r->ready + slot;
-    return dev_wait(r, &a, 1, seq, stream);
+    const uint64_t *a[TSB_MAX_WRITERS];
+    for (int w = 0; w < r->writers; ++w) a[w] = ready_word(r, slot, w);
+    return dev_wait(r, a, r->writers, seq, stream);
 }
 int tsb_ring_ack(tsb_ring *r, int consumer, uint64_t seq, void *stream) {
     TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
@@ -435,7 +486,14 @@ int tsb_ring_read_cursor(tsb_ring *r, int consumer, uint64_t *out) {
 }
 int tsb_ring_read_ready(tsb_ring *r, int slot, uint64_t *out) {
     TSB_CHECK(r && out && slot >= 0 && slot < r->slots, "bad slot");
-    return host_read(r, r->ready + slot, out);
+    uint64_t lo = ~0ull;
+    for (int w = 0; w < r->writers; ++w) {  // complete when every writer's shard landed
+        uint64_t v = 0;
+        if (int rc = host_read(r, ready_word(r, slot, w), &v)) return rc;
+        if (v < lo) lo = v;
+    }
+    *out = lo;
+    return TSB_OK;
 }
 
 }  // extern "C"

@@ -90,20 +90,25 @@ class _HostControl:
 
 
 class DeviceRing:
+    """``writers`` > 1: a ring of a sharded-ingest group -- slot s is complete
+    once each of the writers published its shard (one ready word each)."""
+
     def __init__(self, slots: int, slot_bytes: int, max_consumers: int = 64,
-                 device: int | None = None, control: str = "device"):
+                 device: int | None = None, control: str = "device", writers: int = 1):
         L = load()
         if device is None:
             dev = ctypes.c_int(0)
             call("tsb_get_device", ctypes.byref(dev))
             device = dev.value
         h = ctypes.c_void_p()
-        call("tsb_ring_create", device, slots, slot_bytes, max_consumers, ctypes.byref(h))
+        call("tsb_ring_create_ex", device, slots, slot_bytes, max_consumers, writers,
+             ctypes.byref(h))
+        self.writers = writers
         self._init(h, slots, slot_bytes, max_consumers, device, imported=False)
         self._L = L
         self.ctl = None
         if control == "host":
-            nb = L.tsb_ring_control_bytes(slots, max_consumers)
+            nb = L.tsb_ring_control_bytes_ex(slots, max_consumers, writers)
             self.ctl = _HostControl(f"tsbc-{os.getpid()}-{id(self) & 0xFFFFFF:x}", nb, True)
             call("tsb_ring_attach_host_control", self._h, self.ctl.addr, nb, 1)
         elif control != "device":
@@ -131,22 +136,25 @@ class DeviceRing:
 
     @classmethod
     def import_handle(cls, handle: bytes, slots: int, slot_bytes: int, max_consumers: int,
-                      control_name: str = "-"):
-        """Open a ring exported by another process on this GPU (CUDA IPC); with a
-        host control block, map the same shm segment."""
+                      control_name: str = "-", writers: int = 1):
+        """Open a ring exported by another process (CUDA IPC; on this GPU, or on
+        a peer GPU -- then its slots are written/read over NVLink); with a host
+        control block, map the same shm segment."""
         if len(handle) != IPC_HANDLE_BYTES:
             raise ValueError("IPC handle must be 64 bytes")
         L = load()
         buf = ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES)
         h = ctypes.c_void_p()
-        call("tsb_ring_import", buf, slots, slot_bytes, max_consumers, ctypes.byref(h))
+        call("tsb_ring_import_ex", buf, slots, slot_bytes, max_consumers, writers,
+             ctypes.byref(h))
         self = cls.__new__(cls)
+        self.writers = writers
         dev = ctypes.c_int(0)
         call("tsb_get_device", ctypes.byref(dev))
         self._init(h, slots, slot_bytes, max_consumers, dev.value, imported=True)
         self.ctl = None
         if control_name and control_name != "-":
-            nb = L.tsb_ring_control_bytes(slots, max_consumers)
+            nb = L.tsb_ring_control_bytes_ex(slots, max_consumers, writers)
             self.ctl = _HostControl(control_name, nb, False)
             call("tsb_ring_attach_host_control", self._h, self.ctl.addr, nb, 0)
         return self
@@ -170,7 +178,11 @@ class DeviceRing:
 
     # -- device sync words ----------------------------------------------------
     def publish(self, slot: int, seq: int, stream=None) -> None:
+        """Every writer's shard of the slot holds seq."""
         call("tsb_ring_publish", self._h, slot, seq, _stream(stream))
+
+    def publish_shard(self, slot: int, writer: int, seq: int, stream=None) -> None:
+        call("tsb_ring_publish_shard", self._h, slot, writer, seq, _stream(stream))
 
     def wait_ready(self, slot: int, seq: int, stream=None) -> None:
         call("tsb_ring_wait_ready", self._h, slot, seq, _stream(stream))
@@ -258,3 +270,21 @@ def consume_range(ring: DeviceRing, consumer: int, seq0: int, n: int, events=Non
                   stream=None) -> None:
     """Native consumer loop: wait_ready -> ack for n batches (tsb_consume_range)."""
     call("tsb_consume_range", ring._h, consumer, seq0, n, _ev_array(events), _stream(stream))
+
+
+def produce_group(rings, local: int, args, shard: int, n_shards: int, seq0: int, batch0: int,
+                  n: int, live_per_ring, stream=None) -> None:
+    """Sharded ingest + fused fan-out (tsb_produce_group): writer ``shard`` of
+    ``n_shards`` produces its rows of n batches of one epoch straight into the
+    same slot of every ring in ``rings`` (own device's ring = rings[local],
+    peers opened over CUDA IPC); the calling thread blocks on the host gate."""
+    rings = list(rings)
+    ptrs = (ctypes.c_void_p * len(rings))(*[r._h.value if hasattr(r._h, "value") else r._h
+                                           for r in rings])
+    flat = [c for lv in live_per_ring for c in lv]
+    live = (ctypes.c_int * max(1, len(flat)))(*flat)
+    counts = (ctypes.c_int * len(rings))(*[len(lv) for lv in live_per_ring])
+    if len(live_per_ring) != len(rings):
+        raise ValueError("one live list per ring")
+    call("tsb_produce_group", ptrs, len(rings), local, ctypes.byref(args), shard, n_shards, seq0,
+         batch0, n, live, counts, _stream(stream))
