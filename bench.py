@@ -11,9 +11,14 @@ collate/augment (RandomCrop pad 16 + HFlip with params from the reference RNG,
 ImageNet normalise) to float32 NCHW written into the device ring; consumers in
 other processes map the ring over CUDA IPC and release slots with
 device-counted acks.  A step = one batch of 256 produced and delivered to all
-4 consumers.  N > 1: one independent producer + 4 consumers per GPU (weak
-scaling; the units -- batches -- are sharded across ranks, no data-path
-collective).
+4 consumers.  N > 1 (one rank per GPU): still one logical producer -- every
+rank collates its B/N rows of each batch and the collate kernel stores them
+straight into the same slot of every rank's ring over NVLink (sharded ingest
++ the all-gather fused into the producing kernel); each GPU's
+4 consumers get every whole batch (weak scaling in delivered samples: the
+consumer count grows with N).  Test hook: TSB_BENCH_SAME_DEVICE=1 +
+TSB_BENCH_BACKEND=gloo put every rank on cuda:0 (peers = IPC allocations on
+one GPU) so the N > 1 path runs on a one-GPU box.
 
 value: delivered samples/s summed over all consumers (the reference's
 aggregate metric, bs/harness.py:574 + bs/cli.py:220-236), inputs resident in
@@ -51,6 +56,7 @@ PAD = 16
 OUT_BYTES = C * H * W * 4          # f32 NCHW per sample
 ALG_BYTES_PER_SAMPLE = SAMPLE_BYTES + OUT_BYTES  # 752,640 B read + write (collate)
 METRIC = "delivered samples/sec (all consumers)"
+NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
 WORKLOAD = ("C2: 1 producer + 4 same-GPU consumers via CUDA IPC zero copy, 224x224x3 u8 store "
             "-> ResNet-50-shaped f32 NCHW (crop pad16 + hflip from the reference RNG + ImageNet "
             "normalise), batch 256")
@@ -200,7 +206,7 @@ def device_consumer(dev, handle, slots, slot_bytes, max_consumers, cursor, warmu
 
 
 def host_consumer(dev, handle, control, slots, slot_bytes, max_consumers, cursor, warmup, steps,
-                  q):
+                  q, writers=1):
     """The reference consumer (bs/cli.py:252-258: map, ack, never read the
     payload): maps the ring over CUDA IPC; waits and releases through the
     host-shared control block, so it never touches its GPU channel."""
@@ -209,7 +215,7 @@ def host_consumer(dev, handle, control, slots, slot_bytes, max_consumers, cursor
     torch.cuda.set_device(dev)
     from paper_2409_18749_b200.ring import DeviceRing
 
-    ring = DeviceRing.import_handle(handle, slots, slot_bytes, max_consumers, control)
+    ring = DeviceRing.import_handle(handle, slots, slot_bytes, max_consumers, control, writers)
     q.put(("ready", cursor))
     times = []
     for seq in range(1, warmup + steps + 1):
@@ -256,31 +262,49 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = local
+    dev = 0 if os.environ.get("TSB_BENCH_SAME_DEVICE") == "1" else local
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("TSB_BENCH_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec, StoreSource,
                                        TensorProducer)
     from paper_2409_18749_b200 import dataplane as dp
     from paper_2409_18749_b200._lib import GATE_HOST
-    from paper_2409_18749_b200.ring import DeviceRing, produce_range, sync_mode
+    from paper_2409_18749_b200.ring import DeviceRing, produce_group, produce_range
 
     K, Wm = args.steps, args.warmup
     ctx = mp.get_context("spawn")
 
     # ---- device-resident run (value) ----
+    # One logical producer: at N GPUs every rank ingests and collates its 1/N
+    # shard of each batch and the collate kernel stores it straight into the
+    # same slot of every rank's ring (own HBM + peers over NVLink: the
+    # all-gather fused into the producing kernel, tsb_produce_group); each
+    # rank's 4 consumers see every whole batch.  N = 1 is exactly C2.
     store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="hbm")
     ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
     loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
-    ring = DeviceRing(RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, device=dev, control="host")
+    ring = DeviceRing(RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, device=dev, control="host",
+                      writers=world)
     handle = ring.export()
+    rings = [ring]
+    if world > 1:
+        infos = [None] * world
+        torch.distributed.all_gather_object(infos, (rank, handle, ring.control_name))
+        rings = []
+        for r, h_r, ctl_r in sorted(infos):
+            rings.append(ring if r == rank else DeviceRing.import_handle(
+                h_r, RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, ctl_r, writers=world))
     q = ctx.Queue()
     procs = [ctx.Process(target=host_consumer,
                          args=(dev, handle, ring.control_name, RING_SLOTS, loader.batch_nbytes,
-                               N_CONSUMERS, k, Wm, K, q))
+                               N_CONSUMERS, k, Wm, K, q, world))
              for k in range(N_CONSUMERS)]
     for p in procs:
         p.start()
@@ -290,7 +314,7 @@ def run_ours(args):
     live = list(range(N_CONSUMERS))
     L = len(loader)
 
-    def produce(seq0, n, events=None):
+    def produce(seq0, n):
         """Enqueue n batches starting at global seq0 (1-based), across epochs."""
         done = 0
         while done < n:
@@ -299,8 +323,11 @@ def run_ours(args):
             m = min(n - done, L - bi)
             a = loader.produce_args(epoch)
             a.gate = GATE_HOST  # gate on the host-shared cursors; PDL-chained kernels
-            evs = None if events is None else events[2 * done:2 * (done + m)]
-            produce_range(ring, a, q0, bi, m, live, events=evs, stream=stream)
+            if world == 1:
+                produce_range(ring, a, q0, bi, m, live, stream=stream)
+            else:
+                produce_group(rings, rank, a, rank, world, q0, bi, m, [live] * world,
+                              stream=stream)
             done += m
 
     produce(1, Wm)
@@ -329,12 +356,16 @@ def run_ours(args):
     # kernel's average launch duration is the timed region / K
     avg_launch_ms = ms / K
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t.item())
+        torch.distributed.barrier()  # peers are done writing into our ring
     else:
         ms_max = ms
     value = world * N_CONSUMERS * B * K / (ms_max / 1e3)
+    for r in rings:
+        if r is not ring:
+            r.close()
     ring.close()
     del store, loader
 
@@ -342,35 +373,52 @@ def run_ours(args):
     e2e = run_e2e(args, ctx, dev, rank, world)
 
     peak, peak_src = measured_hbm_peak()
-    achieved = B * ALG_BYTES_PER_SAMPLE / (avg_launch_ms / 1e3) / 1e9
+    if world == 1:
+        achieved = B * ALG_BYTES_PER_SAMPLE / (avg_launch_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
+                    "kernel": "collate_augment_kernel<f32,C=3>",
+                    "alg_bytes_per_launch": B * ALG_BYTES_PER_SAMPLE,
+                    "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src}
+    else:
+        # binding link: each rank's NVLink egress, its shard stored into N-1 peers
+        egress = (B // world) * OUT_BYTES * (world - 1)
+        achieved = egress / (ms_max / K / 1e3) / 1e9
+        roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_GBS,
+                    "unit": "GB/s", "frac": round(achieved / NVLINK_GBS, 4), "traffic": None,
+                    "kernel": "collate_augment_kernel<f32,C=3,MULTI> (fused all-gather)",
+                    "alg_bytes_per_launch": egress, "avg_launch_ms": round(ms_max / K, 5),
+                    "peak_source": "B200_PROFILING.md measured peer copy, per direction per GPU",
+                    "hbm_achieved_gbs": round(
+                        (B // world) * SAMPLE_BYTES / (ms_max / K / 1e3) / 1e9 +
+                        B * OUT_BYTES / (ms_max / K / 1e3) / 1e9, 1)}
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
         "steps": K, "warmup": Wm, "ms_per_step": round(ms_max / K, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: SplitMix64 DirectorySource-equivalent store (reference RNG), "
                 "reference Fisher-Yates epoch order",
-        "config": {"workload": WORKLOAD, "global_batch": B * world, "batch_per_gpu": B,
+        "config": {"workload": WORKLOAD, "global_batch": B, "batch_per_gpu": B,
                    "consumers_per_gpu": N_CONSUMERS, "samples_per_epoch": N_SAMPLES,
                    "ring_slots": RING_SLOTS, "sample": "224x224x3 u8 -> 3x224x224 f32",
                    "store": "HBM-resident (value) / pinned host (e2e)",
                    "l2": "inputs larger than L2: 2.47 GB store, 1.2 GB ring of 8 slots",
-                   "parallelism": f"weak: {world} independent producer(s), 4 IPC consumers each",
+                   "parallelism": (f"sharded ingest over {world} GPUs (each collates B/{world} rows "
+                                   "of every batch) + all-gather fused into the collate kernel "
+                                   "(P2P stores into every rank's ring slot); 4 IPC consumers "
+                                   "per GPU" if world > 1 else "1 producer, 4 IPC consumers"),
                    "sync": "slot-reuse gate on the host-shared release cursors (producer thread "
                            "blocks, never the stream); fused publish (release store from the "
                            "kernel's last CTA); consecutive batches chained with programmatic "
                            "dependent launch; consumers: host wait + host ack (map-and-ack, "
                            "bs/cli.py:252-258)"},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(), "kernel": "collate_augment_kernel<f32,C=3>",
-                     "alg_bytes_per_launch": B * ALG_BYTES_PER_SAMPLE,
-                     "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src},
+        "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": K,
         "clocks": clk,
         "extra": {"producer_ms": round(ms, 3),
                   "consumer_rates_samples_s": {str(k): round(v, 1) for k, v in consumer_rates.items()},
-                  "produced_samples_per_s": round(world * B * K / (ms_max / 1e3), 1)},
+                  "produced_samples_per_s": round(B * K / (ms_max / 1e3), 1)},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
@@ -422,7 +470,8 @@ def run_e2e(args, ctx, dev, rank, world):
     wall = time.monotonic() - t_start
     value = sum(rates.values())
     if world > 1:
-        t = torch.tensor([value], device="cuda")
+        t = torch.tensor([value], device="cuda" if os.environ.get("TSB_BENCH_BACKEND", "nccl")
+                         == "nccl" else "cpu")
         torch.distributed.all_reduce(t)
         value = float(t.item())
     return {"value": round(value, 1), "unit": "samples/s",
