@@ -48,6 +48,11 @@ int tsb_device_count(int *n);
 int tsb_set_device(int dev);
 int tsb_get_device(int *dev);
 int tsb_device_info(int dev, int *sm_count, int *cc_major, int *cc_minor, size_t *hbm_bytes);
+/* Load every kernel of the library into the current device's context now
+ * (no lazy loading: a first launch must never wait for the device to go
+ * idle while a stream is parked on a ring wait).  Called per device by the
+ * ring constructors. */
+int tsb_preload_kernels(void);
 
 /* ---- memory & streams (plumbing; no torch) -------------------------------- */
 int tsb_malloc(void **p, size_t bytes);                 /* device HBM */
@@ -166,6 +171,13 @@ int tsb_ring_sync_mode(void);
 size_t tsb_ring_control_bytes(int slots, int max_consumers);
 size_t tsb_ring_control_bytes_ex(int slots, int max_consumers, int writers);
 int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int init);
+/* Host flow gate (host control block): block the caller until every live
+ * cursor has released `need` (wrap-around GEQ; evicted cursors pass).
+ * timeout_us < 0 = forever; TSB_ERR_STALE on timeout.  A producer that gates
+ * here keeps device waits out of its streams -- no stream is ever parked on
+ * a value another stream of the same process has yet to write. */
+int tsb_ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need,
+                       int64_t timeout_us);
 /* Host consumer: spin until ready[slot] >= seq (timeout_us < 0 = forever). */
 int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeout_us);
 
@@ -185,6 +197,16 @@ int tsb_collate_augment_fanout(const void *src, const int64_t *d_indices, int64_
  * wrapping) into out. */
 int tsb_rebatch_gather(const void *ring_base, int64_t ring_samples, int64_t sample_bytes,
                        int64_t first, int64_t count, void *out, void *stream);
+/* Rebatch window (heterogeneous consumers): a consumer
+ * batch = epoch-stream samples [first, first+count) of a producer whose
+ * slots hold `per_slot` samples laid out [inputs][targets] (sl/abi.py:27-31
+ * pair layout).  slots[0..n_slots) = bases of the producer slots the window
+ * touches, in stream order (slot 0 holds sample first).  out = [count
+ * inputs][count targets].  Used when the window straddles producer slots;
+ * windows inside one slot are zero-copy views. */
+int tsb_rebatch_window(const void *const *slots, int n_slots, int64_t first, int64_t count,
+                       int64_t per_slot, int64_t in_sample_bytes, int64_t tgt_sample_bytes,
+                       void *out, void *stream);
 
 /* ---- native producer/consumer loops (replace the per-batch host work of
  *      Producer._try_announce, producer.py:506-534, and

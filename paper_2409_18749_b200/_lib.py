@@ -40,6 +40,7 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_get_device": (i32, [ctypes.POINTER(i32)]),
     "tsb_device_info": (i32, [i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                               ctypes.POINTER(sz)]),
+    "tsb_preload_kernels": (i32, []),
     "tsb_malloc": (i32, [pp, sz]),
     "tsb_free": (i32, [vp]),
     "tsb_host_alloc": (i32, [pp, sz]),
@@ -92,6 +93,7 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_ring_control_bytes": (sz, [i32, i32]),
     "tsb_ring_attach_host_control": (i32, [vp, vp, sz, i32]),
     "tsb_ring_host_wait_ready": (i32, [vp, i32, u64, i64]),
+    "tsb_ring_host_gate": (i32, [vp, ctypes.POINTER(i32), i32, u64, i64]),
     "tsb_ring_create_ex": (i32, [i32, i32, sz, i32, i32, pp]),
     "tsb_ring_import_ex": (i32, [vp, i32, sz, i32, i32, pp]),
     "tsb_ring_writers": (i32, [vp, ctypes.POINTER(i32)]),
@@ -101,6 +103,7 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_collate_augment_fanout": (i32, [vp, vp, i64, i32, i32, i32, i32, i32, u64, u64, fp, fp,
                                          i32, pp, i32, vp]),
     "tsb_rebatch_gather": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+    "tsb_rebatch_window": (i32, [pp, i32, i64, i64, i64, i64, i64, vp, vp]),
 }
 
 class ProduceArgs(ctypes.Structure):
@@ -192,3 +195,17 @@ def stream_handle(stream) -> ctypes.c_void_p:
 
 def exported_symbols() -> list[str]:
     return list(SIGNATURES)
+
+
+_preloaded: set = set()
+
+
+def preload(device: int) -> None:
+    """Eager-load the library's kernels in `device`'s context (once)."""
+    if device in _preloaded:
+        return
+    import torch
+
+    with torch.cuda.device(device):
+        call("tsb_preload_kernels")
+    _preloaded.add(device)

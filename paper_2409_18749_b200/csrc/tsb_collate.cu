@@ -559,18 +559,24 @@ int launch_ca_c(int c, const uint8_t *src, const int64_t *idx, CaGeom g, int fli
     }
 }
 
+// HBM of the launching device (TMA staging); peer HBM and pinned host memory
+// take the LDG staging path.
 int is_device_memory(const void *p) {
     // one-entry cache: a producer launches over the same store every batch
     static thread_local const void *last_p = nullptr;
+    static thread_local int last_dev = -1;
     static thread_local int last_v = 0;
-    if (p == last_p) return last_v;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (p == last_p && cur == last_dev) return last_v;
     cudaPointerAttributes a;
     int v = 0;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess)
         cudaGetLastError();
     else
-        v = a.type == cudaMemoryTypeDevice;
+        v = a.type == cudaMemoryTypeDevice && a.device == cur;
     last_p = p;
+    last_dev = cur;
     last_v = v;
     return v;
 }
@@ -903,3 +909,30 @@ int tsb_collate_augment_fanout(const void *src, const int64_t *d_indices, int64_
 }
 
 }  // extern "C"
+
+namespace tsb {
+template <int K>
+void preload_ca() {
+    touch_kernel(collate_augment_kernel<K, 1, false>);
+    touch_kernel(collate_augment_kernel<K, 2, false>);
+    touch_kernel(collate_augment_kernel<K, 3, false>);
+    touch_kernel(collate_augment_kernel<K, 4, false>);
+    touch_kernel(collate_augment_kernel<K, 1, true>);
+    touch_kernel(collate_augment_kernel<K, 2, true>);
+    touch_kernel(collate_augment_kernel<K, 3, true>);
+    touch_kernel(collate_augment_kernel<K, 4, true>);
+}
+void preload_collate() {
+    touch_kernel(fill_kernel);
+    touch_kernel(gather_v16_kernel);
+    touch_kernel(gather_v1_kernel);
+    touch_kernel(aug_params_kernel);
+    preload_ca<TSB_OUT_U8>();
+    preload_ca<TSB_OUT_F32>();
+    preload_ca<TSB_OUT_BF16>();
+    touch_kernel(passthrough_multi_kernel<false, false>);
+    touch_kernel(passthrough_multi_kernel<false, true>);
+    touch_kernel(passthrough_multi_kernel<true, false>);
+    touch_kernel(passthrough_multi_kernel<true, true>);
+}
+}  // namespace tsb

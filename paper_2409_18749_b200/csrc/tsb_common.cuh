@@ -140,3 +140,16 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, ui
         : "memory");
 }
 }  // namespace tsb
+
+namespace tsb {
+// Force eager loading of this file's kernels in the current context: a lazily
+// loaded kernel's first launch can wait for the device to go idle, which
+// deadlocks when a stream is parked on a ring wait that this very launch
+// would satisfy (e.g. an in-process consumer's first rebatch gather).
+template <typename F>
+inline void touch_kernel(F f) {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(f)) != cudaSuccess)
+        cudaGetLastError();
+}
+}  // namespace tsb

@@ -181,3 +181,20 @@ int tsb_epoch_order(int64_t n, uint64_t shuffle_seed, uint64_t epoch, int reshuf
 }
 
 }  // extern "C"
+
+namespace tsb {
+void preload_collate();
+void preload_crc32();
+void preload_fanout();
+void preload_ring();
+}  // namespace tsb
+
+extern "C" int tsb_preload_kernels(void) {
+    int dev = -1;
+    TSB_CUDA(cudaGetDevice(&dev));
+    tsb::preload_collate();
+    tsb::preload_crc32();
+    tsb::preload_fanout();
+    tsb::preload_ring();
+    return TSB_OK;
+}

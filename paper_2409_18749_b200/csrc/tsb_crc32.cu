@@ -207,3 +207,10 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
 }
 
 }  // extern "C"
+
+namespace tsb {
+void preload_crc32() {
+    touch_kernel(crc_init_kernel);
+    touch_kernel(crc_kernel);
+}
+}  // namespace tsb

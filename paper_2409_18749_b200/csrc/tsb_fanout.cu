@@ -74,9 +74,72 @@ __global__ void __launch_bounds__(RB_THREADS)
     }
 }
 
+// Rebatch window: consumer batch = stream samples [first, first+count) of a
+// producer whose slots hold `per_slot` samples laid out [inputs][targets]
+// (the pair layout of sl/abi.py:27-31).  slots[k] = base of the k-th
+// producer slot the window touches (first / per_slot is slot 0).  Output:
+// [count inputs][count targets].  One CTA row per window sample, 16 B
+// vectors when aligned.
+constexpr int RW_MAX_SLOTS = 32;
+struct SlotList {
+    const uint8_t *p[RW_MAX_SLOTS];
+};
+
+__global__ void __launch_bounds__(RB_THREADS)
+    rebatch_window_kernel(SlotList sl, int64_t first, int64_t per_slot, int64_t in_sb,
+                          int64_t tg_sb, int64_t count, uint8_t *__restrict__ out, int vec) {
+    const int64_t j = blockIdx.y;
+    const int64_t pos = first + j;
+    const int64_t k = pos / per_slot - first / per_slot, i = pos % per_slot;
+    const uint8_t *slot = sl.p[k];
+    // input part, then target part of sample j
+    for (int part = 0; part < 2; ++part) {
+        const int64_t sb = part ? tg_sb : in_sb;
+        if (!sb) continue;
+        const uint8_t *in = part ? slot + per_slot * in_sb + i * tg_sb : slot + i * in_sb;
+        uint8_t *o = part ? out + count * in_sb + j * tg_sb : out + j * in_sb;
+        const int64_t b0 = (int64_t)blockIdx.x * RB_BYTES_PER_CTA;
+        const int64_t b1 = min(b0 + RB_BYTES_PER_CTA, sb);
+        if (vec) {
+            for (int64_t q = b0 + 16 * threadIdx.x; q < b1; q += 16 * RB_THREADS)
+                st_v4(o + q, ld_nc_v4(in + q));
+        } else {
+            for (int64_t q = b0 + threadIdx.x; q < b1; q += RB_THREADS) o[q] = in[q];
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+int tsb_rebatch_window(const void *const *slots, int n_slots, int64_t first, int64_t count,
+                       int64_t per_slot, int64_t in_sample_bytes, int64_t tgt_sample_bytes,
+                       void *out, void *stream) {
+    TSB_CHECK(slots && out, "null pointer");
+    TSB_CHECK(per_slot > 0 && first >= 0 && count >= 0 && count <= 65535 && in_sample_bytes > 0 &&
+                  tgt_sample_bytes >= 0,
+              "bad rebatch window");
+    if (!count) return TSB_OK;
+    const int64_t need = (first + count - 1) / per_slot - first / per_slot + 1;
+    TSB_CHECK(n_slots >= need && n_slots <= RW_MAX_SLOTS, "window needs %lld slots, got %d (max %d)",
+              (long long)need, n_slots, RW_MAX_SLOTS);
+    SlotList sl{};
+    bool vec = (in_sample_bytes % 16 == 0) && (tgt_sample_bytes % 16 == 0) &&
+               (((uintptr_t)out & 15) == 0) && ((per_slot * in_sample_bytes) % 16 == 0);
+    for (int k = 0; k < n_slots; ++k) {
+        TSB_CHECK(slots[k], "null slot %d", k);
+        sl.p[k] = static_cast<const uint8_t *>(slots[k]);
+        vec = vec && (((uintptr_t)slots[k] & 15) == 0);
+    }
+    const int64_t mx = in_sample_bytes > tgt_sample_bytes ? in_sample_bytes : tgt_sample_bytes;
+    dim3 grid((unsigned)((mx + RB_BYTES_PER_CTA - 1) / RB_BYTES_PER_CTA), (unsigned)count);
+    rebatch_window_kernel<<<grid, RB_THREADS, 0, as_stream(stream)>>>(
+        sl, first, per_slot, in_sample_bytes, tgt_sample_bytes, count, static_cast<uint8_t *>(out),
+        vec ? 1 : 0);
+    TSB_LAUNCH_CHECK();
+    return TSB_OK;
+}
 
 int tsb_fanout(const void *src, void *const *dsts, int n_dst, size_t bytes, void *stream) {
     TSB_CHECK(src && dsts && n_dst >= 1 && n_dst <= FO_MAX, "n_dst must be 1..%d", FO_MAX);
@@ -124,3 +187,12 @@ int tsb_rebatch_gather(const void *ring_base, int64_t ring_samples, int64_t samp
 }
 
 }  // extern "C"
+
+namespace tsb {
+void preload_fanout() {
+    touch_kernel(fanout_v16_kernel);
+    touch_kernel(fanout_tail_kernel);
+    touch_kernel(rebatch_kernel);
+    touch_kernel(rebatch_window_kernel);
+}
+}  // namespace tsb

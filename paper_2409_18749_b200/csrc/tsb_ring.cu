@@ -470,6 +470,36 @@ int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, v
     }
     return dev_wait(r, addrs, n_live, seq, stream);
 }
+int tsb_ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need,
+                       int64_t timeout_us) {
+    TSB_CHECK(r && r->h_ctl, "host gate needs a host control block");
+    TSB_CHECK(live || n_live == 0, "null live list");
+    if (timeout_us < 0) return ring_host_gate(r, live, n_live, need);
+    struct timespec t0, t;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int i = 0; i < n_live; ++i) {
+        TSB_CHECK(live[i] >= 0 && live[i] < r->max_consumers, "bad consumer %d", live[i]);
+        const uint64_t *h = r->h_ctl + (size_t)r->slots * r->writers + live[i];
+        int64_t spins = 0;
+        while ((int64_t)(__atomic_load_n(h, __ATOMIC_ACQUIRE) - need) < 0) {
+            if (++spins < 2048) {
+                __builtin_ia32_pause();
+                continue;
+            }
+            clock_gettime(CLOCK_MONOTONIC, &t);
+            const int64_t us = (t.tv_sec - t0.tv_sec) * 1000000 + (t.tv_nsec - t0.tv_nsec) / 1000;
+            if (us > timeout_us) {
+                set_error("timed out gating seq %llu on consumer %d", (unsigned long long)need,
+                          live[i]);
+                return TSB_ERR_STALE;
+            }
+            struct timespec ns = {0, 5000};
+            nanosleep(&ns, nullptr);
+        }
+    }
+    return TSB_OK;
+}
+
 int tsb_ring_evict(tsb_ring *r, int consumer) {
     TSB_CHECK(r && consumer >= 0 && consumer < r->max_consumers, "bad consumer %d", consumer);
     // "+inf" for every wait: far ahead of any sequence, yet positive under the
@@ -497,3 +527,10 @@ int tsb_ring_read_ready(tsb_ring *r, int slot, uint64_t *out) {
 }
 
 }  // extern "C"
+
+namespace tsb {
+void preload_ring() {
+    touch_kernel(signal_kernel);
+    touch_kernel(wait_kernel);
+}
+}  // namespace tsb

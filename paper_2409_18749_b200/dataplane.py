@@ -147,6 +147,15 @@ def fanout(src, dsts, nbytes: int, stream=None) -> None:
     call("tsb_fanout", ptr(src), arr, len(dsts), nbytes, current_stream(stream))
 
 
+def rebatch_window(slot_ptrs, first: int, count: int, per_slot: int, in_sample_bytes: int,
+                   tgt_sample_bytes: int, out, stream=None) -> None:
+    """Consumer batch = stream samples [first, first+count) gathered from the
+    producer slots it straddles (tsb_rebatch_window)."""
+    arr = (ctypes.c_void_p * len(slot_ptrs))(*[int(p) for p in slot_ptrs])
+    call("tsb_rebatch_window", arr, len(slot_ptrs), first, count, per_slot, in_sample_bytes,
+         tgt_sample_bytes, ptr(out), current_stream(stream))
+
+
 def rebatch_gather(ring_base, ring_samples: int, sample_bytes: int, first: int, count: int,
                    out, stream=None) -> None:
     call("tsb_rebatch_gather", ptr(ring_base), ring_samples, sample_bytes, first, count,
@@ -157,6 +166,7 @@ __all__ = [
     "OUT_U8", "OUT_F32", "OUT_BF16", "ptr", "mix64", "derive_key", "permutation",
     "epoch_order", "norm_consts", "fill_synthetic", "make_store", "gather", "aug_params",
     "collate_augment", "collate_augment_fanout", "crc32", "fanout", "rebatch_gather",
+    "rebatch_window",
 ]
 
 
@@ -194,3 +204,16 @@ class DeviceEvent:
             load().tsb_event_destroy(self.handle)
         except Exception:
             pass
+
+
+# -- peers (multi-GPU fan-out) -------------------------------------------------
+
+def can_access_peer(dev: int, peer: int) -> bool:
+    v = ctypes.c_int(0)
+    call("tsb_can_access_peer", dev, peer, ctypes.byref(v))
+    return bool(v.value)
+
+
+def enable_peer(dev: int, peer: int) -> None:
+    """Kernels on `dev` may load/store `peer`'s HBM (NVLink P2P); idempotent."""
+    call("tsb_enable_peer", dev, peer)

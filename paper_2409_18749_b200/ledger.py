@@ -36,6 +36,26 @@ def seq_of(epoch: int, index: int, epoch_len: int) -> int:
     return epoch * epoch_len + index + 1
 
 
+def rebatch_epoch_len(samples_per_epoch: int, producer_epoch_len: int, per_slot: int,
+                      batch_size: int) -> int:
+    """Batches per epoch of a consumer with its own batch size: the reference's
+    drop-last ``N // b`` (pipeline.py:77-79), capped by the samples the
+    producer's own drop-last epoch covers (producer_epoch_len * per_slot)."""
+    covered = producer_epoch_len * per_slot
+    n = min(samples_per_epoch, covered) if samples_per_epoch else covered
+    return n // batch_size
+
+
+def window_slots(batch_size: int, per_slot: int) -> int:
+    """Most producer slots one consumer batch window (starting at a multiple
+    of batch_size) can touch."""
+    if per_slot % batch_size == 0:
+        return 1
+    if batch_size % per_slot == 0:
+        return batch_size // per_slot
+    return -(-batch_size // per_slot) + 1
+
+
 @dataclass
 class ConsumerRecord:
     consumer_id: int
@@ -48,6 +68,11 @@ class ConsumerRecord:
     conn: object = None
     bcast: object = None
     replay: list = field(default_factory=list)
+    device: int = -1             # the consumer's GPU
+    ring: int = 0                # index of the producer ring it maps (one per GPU)
+    batch_size: int = 0          # own batch size (0 = the producer's)
+    ack_epoch: int = -1          # heterogeneous consumers: producer batches acked so far
+    ack_k: int = 0
 
 
 class Ledger:

@@ -28,7 +28,22 @@ shm block -- evictions and map-and-ack consumers never touch a GPU channel;
 missing barrier is the start race noted in SURVEY.md §4), ``checksum``
 (device CRC-32 of every batch into Announce.checksum), ``rubberband_fraction``
 (late-join replay window, bs/producer.py:119-135; 0 = facade behaviour),
-``device``.
+``device``; ``devices`` + ``fanout`` (multi-GPU, below).
+
+Multi-GPU (``devices=[0, 1, ...]``): one ring per device, each
+consumer maps the ring of its own GPU (``SharedLoader(device=...)``, Join v2).
+``fanout="sharded"`` (default): every device collates its 1/G rows of each
+batch and the kernel stores them into the same slot of every device's ring
+(P2P stores over NVLink/NVSwitch -- the all-gather fused into the producing
+kernel, ``tsb_produce_group``); ``fanout="star"``: the first device produces
+the whole batch into every ring (the literal single-producer fan-out).
+
+Heterogeneous consumers (``SharedLoader(batch_size=b)``): each receives
+exactly the reference's batches for its own batch size -- samples
+``order[j*b:(j+1)*b]`` of the batch-size-independent epoch order
+(bs/pipeline.py:113-123), drop-last ``N // b`` -- as zero-copy windows of the
+producer's slots, or gathered by the rebatch kernel when a window straddles
+two slots.
 """
 
 from __future__ import annotations
@@ -42,12 +57,14 @@ import numpy as np
 from . import dataplane as dp
 from . import segment as sg
 from .errors import ProducerClosed
-from .ledger import ConsumerRecord, Ledger, admission_code, retention_window, seq_of
-from .ring import DeviceRing
+from .ledger import (ConsumerRecord, Ledger, admission_code, rebatch_epoch_len, retention_window,
+                     seq_of, window_slots)
+from ._lib import GATE_HOST
+from .ring import DeviceRing, produce_group, produce_range
 from .transport import Conn, endpoints_from_env, listen
-from .wire import (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT, PROTOCOL_VERSION, Ack, Announce,
-                   Bye, DType, EpochEnd, EpochStart, Heartbeat, Join, Shutdown, Welcome, dtype_of,
-                   encode)
+from .wire import (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT, SUPPORTED_VERSIONS, Ack,
+                   Announce, Bye, DType, EpochEnd, EpochStart, Heartbeat, Join, Shutdown, Welcome,
+                   dtype_of, encode)
 
 MONITOR_ID = 0  # bs/producer.py:52-54: passive broadcast observers
 _RINGS: dict[int, DeviceRing] = {}  # ring_id -> ring, for same-process consumers
@@ -63,7 +80,8 @@ class TensorProducer:
                  pause_poll_s: float = 0.05, *, ring_slots: int | None = None,
                  min_consumers: int = 1, checksum: bool = False,
                  rubberband_fraction: float = 0.0, max_consumers: int = 64,
-                 device: int | None = None, control: str = "host"):
+                 device: int | None = None, control: str = "host", devices=None,
+                 fanout: str = "sharded"):
         import torch
 
         if not hasattr(data_loader, "__len__"):
@@ -85,6 +103,23 @@ class TensorProducer:
         self._ring_slots = ring_slots
         self._control = control
         self.device = torch.cuda.current_device() if device is None else device
+        self._devices = [int(d) for d in devices] if devices else [self.device]
+        if not 1 <= len(self._devices) <= 8:
+            raise ValueError("1..8 devices")
+        self.device = self._devices[0]
+        if fanout not in ("sharded", "star"):
+            raise ValueError("fanout must be 'sharded' or 'star'")
+        self._multi = len(self._devices) > 1
+        if self._multi and control != "host":
+            raise ValueError("multi-GPU rings need control='host' (host-shared control words)")
+        self._sharded = self._multi and fanout == "sharded"
+        self._rings: dict[int, DeviceRing] = {}
+        self._streams: dict = {}
+        self._descriptors: dict[int, sg.RingDescriptor] = {}
+        self._ring_ids: dict[int, int] = {}
+        self._orders: dict = {}
+        self._per_slot = 0   # producer batch size (samples per slot)
+        self._samples = 0    # samples per epoch
         self._epoch = 0
         self._announced_in_epoch = 0
         self._epoch_started = False
@@ -102,10 +137,11 @@ class TensorProducer:
         self._ring: DeviceRing | None = None
         self._stream = None
         self._events = []
-        self._retained: dict[int, Announce] = {}  # seq -> announce (rubberband prefix)
+        self._retained: dict[int, dict] = {}  # seq -> {device: announce} (rubberband prefix)
         self._retention_active = False
         self.ring_id = (os.getpid() << 20) ^ (id(self) & 0xFFFFF)
         self.stats = {"announced": 0, "acks": 0, "evictions": 0}
+        self.drops: list[tuple[int, str, float]] = []  # (consumer_id, reason, time) event log
 
     # -- ring -------------------------------------------------------------
     def _batch_nbytes_hint(self) -> int | None:
@@ -119,27 +155,86 @@ class TensorProducer:
                 raise ValueError(f"batch of {nbytes} B exceeds the ring slot "
                                  f"({self._ring.slot_bytes} B); batch shapes must be fixed")
             return
+        window = retention_window(self._fraction, max(1, len(self._loader)))
+        slots = self._ring_slots or max(self._depth + 2 + window, 4)
+        if slots <= window:
+            raise ValueError(f"ring_slots={slots} must exceed the rubberband window {window}")
+        if self._multi:
+            from . import dataplane as dp
+
+            for a in set(self._devices):  # kernels on a store into (and read from) b over NVLink
+                for b in set(self._devices):
+                    if a != b:
+                        if not dp.can_access_peer(a, b):
+                            raise ValueError(f"GPU {a} cannot access GPU {b} (no P2P)")
+                        dp.enable_peer(a, b)
+        writers = len(self._devices) if self._sharded else 1
+        for k, d in enumerate(self._devices):
+            with torch.cuda.device(d):
+                # cursor index max_consumers is the producer's retention cursor
+                ring = DeviceRing(slots, nbytes, self._max_consumers + 1, device=d,
+                                  control=self._control, writers=writers)
+                self._rings[k] = ring
+                self._streams[k] = torch.cuda.Stream(device=d)
+                rid = self.ring_id if k == 0 else (self.ring_id ^ (k << 44))
+                self._ring_ids[k] = rid
+                _RINGS[rid] = ring
+        self._ring = self._rings[0]
+        self._stream = self._streams[0]
         with torch.cuda.device(self.device):
-            window = retention_window(self._fraction, max(1, len(self._loader)))
-            slots = self._ring_slots or max(self._depth + 2 + window, 4)
-            if slots <= window:
-                raise ValueError(f"ring_slots={slots} must exceed the rubberband window {window}")
-            # cursor index max_consumers is the producer's retention cursor
-            self._ring = DeviceRing(slots, nbytes, self._max_consumers + 1, device=self.device,
-                                    control=self._control)
-            self._stream = torch.cuda.Stream(device=self.device)
             self._events = [torch.cuda.Event() for _ in range(slots)]
             self._crc = torch.zeros(slots, dtype=torch.int32, device=f"cuda:{self.device}")
             self._crc_host = torch.zeros(slots, dtype=torch.int32).pin_memory()
-            _RINGS[self.ring_id] = self._ring
-            self._descriptor = sg.RingDescriptor(
-                self.ring_id, os.getpid(), self.device, slots, nbytes, self._max_consumers + 1,
-                self._ring.export(), self._ring.control_name)
         self._lock.notify_all()
+
+    def _descriptor_for(self, k: int) -> sg.RingDescriptor:
+        """Ring k (on self._devices[k]) as a consumer maps it."""
+        if k not in self._descriptors:
+            ring = self._rings[k]
+            self._descriptors[k] = sg.RingDescriptor(
+                self._ring_ids[k], os.getpid(), self._devices[k], ring.slots, ring.slot_bytes,
+                self._max_consumers + 1, ring.export(), ring.control_name, ring.writers,
+                self._per_slot, self._samples)
+        return self._descriptors[k]
+
+    def _ring_for_device(self, dev: int) -> int | None:
+        """Ring index serving a consumer on `dev` (least loaded if several)."""
+        ks = [k for k, d in enumerate(self._devices) if d == dev]
+        if not ks:
+            return None
+        load = {k: sum(1 for r in self._consumers.values() if r.ring == k) for k in ks}
+        return min(ks, key=lambda k: (load[k], k))
 
     @property
     def ring(self) -> DeviceRing | None:
         return self._ring
+
+    @property
+    def rings(self) -> dict:
+        return dict(self._rings)
+
+    def _set_geometry(self, first_batch=None) -> None:
+        """Producer batch size and samples per epoch (rebatch descriptors)."""
+        if self._per_slot:
+            return
+        ds = getattr(self._loader, "dataset", None)
+        if ds is not None and hasattr(ds, "batch_size"):
+            self._per_slot = int(ds.batch_size)
+            self._samples = int(getattr(ds, "samples_per_epoch", 0))
+        elif first_batch is not None:
+            shape = getattr(first_batch[0], "shape", ())
+            self._per_slot = int(shape[0]) if len(shape) else 1
+            self._samples = self._per_slot * len(self._loader)
+
+    def _rebatch_ok(self, b: int) -> bool:
+        """A consumer batch size is servable when the drop-last epoch has a
+        batch of it and a window fits the ring next to the producer's run-ahead."""
+        if not self._per_slot or b <= 0:
+            return False
+        L = max(1, len(self._loader))
+        if rebatch_epoch_len(self._samples, L, self._per_slot, b) < 1:
+            return False
+        return window_slots(b, self._per_slot) + 1 <= self._ring.slots
 
     @property
     def _retention_cursor(self) -> int:
@@ -153,6 +248,7 @@ class TensorProducer:
         hint = self._batch_nbytes_hint()
         if hint is not None:
             with self._lock:
+                self._set_geometry()
                 self._ensure_ring(hint)
         for ep, handler in ((self._broadcast_ep, self._accept_broadcast),
                             (self._aggregate_ep, self._accept_aggregate)):
@@ -229,9 +325,23 @@ class TensorProducer:
                     return cid
                 rec.last_heartbeat = now
                 L = max(1, len(self._loader))
-                seq = seq_of(msg.epoch, msg.batch_index, L)
-                self._ledger.ack(msg.consumer_id, seq)
-                rec.ack_seq = max(rec.ack_seq, seq)
+                if rec.batch_size and rec.batch_size != self._per_slot:
+                    # heterogeneous consumer: its batch j fully covers the producer
+                    # batches before (j+1)*b // B; its last batch covers the epoch
+                    if rec.ack_epoch != msg.epoch:
+                        rec.ack_epoch, rec.ack_k = msg.epoch, 0
+                    lc = rebatch_epoch_len(self._samples, L, self._per_slot, rec.batch_size)
+                    upto = L if msg.batch_index >= lc - 1 else min(
+                        L, (msg.batch_index + 1) * rec.batch_size // self._per_slot)
+                    for k in range(rec.ack_k, upto):
+                        self._ledger.ack(msg.consumer_id, seq_of(msg.epoch, k, L))
+                    rec.ack_k = max(rec.ack_k, upto)
+                    if upto:
+                        rec.ack_seq = max(rec.ack_seq, seq_of(msg.epoch, upto - 1, L))
+                else:
+                    seq = seq_of(msg.epoch, msg.batch_index, L)
+                    self._ledger.ack(msg.consumer_id, seq)
+                    rec.ack_seq = max(rec.ack_seq, seq)
                 self.stats["acks"] += 1
                 self._ledger.sample_drift(now, self._consumers.values())
                 self._lock.notify_all()
@@ -245,7 +355,7 @@ class TensorProducer:
         return cid
 
     def _handle_join(self, conn: Conn, msg: Join, now: float):
-        if msg.protocol_version != PROTOCOL_VERSION or msg.consumer_id == MONITOR_ID:
+        if msg.protocol_version not in SUPPORTED_VERSIONS or msg.consumer_id == MONITOR_ID:
             conn.close()
             return None
         # broadcast identification may lag the Join: wait briefly for it
@@ -269,16 +379,25 @@ class TensorProducer:
         if self._next_cursor >= self._max_consumers:
             conn.close()  # cursor table exhausted
             return None
+        dev = self.device if msg.device < 0 else msg.device
+        bsz = msg.batch_size if msg.batch_size != self._per_slot else 0
+        k = self._ring_for_device(dev)
+        if k is None or (bsz and not self._rebatch_ok(bsz)):
+            conn.close()  # no ring on that GPU / batch size not servable: no Welcome
+            return None
         rec = ConsumerRecord(consumer_id=cid, cursor=self._next_cursor, last_heartbeat=now,
-                             join_epoch=self._epoch, conn=conn, bcast=bcast)
+                             join_epoch=self._epoch, conn=conn, bcast=bcast, device=dev,
+                             batch_size=bsz, ring=k)
         self._next_cursor += 1
         L = max(1, len(self._loader))
         progress = self._announced_in_epoch if self._epoch_started else 0
         code = admission_code(progress, L, self._fraction)
         q0 = seq_of(self._epoch, 0, L)
+        if bsz and code == ADMIT_RUBBERBAND:
+            code = ADMIT_WAIT  # replayed slots are producer batches; rebatching starts at an epoch
         if code in (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND):
             rec.admitted = True
-            self._ring.set_cursor(rec.cursor, q0 - 1)
+            self._rings[k].set_cursor(rec.cursor, q0 - 1)
             welcome = Welcome(cid, self._epoch, L, progress if code == ADMIT_RUBBERBAND else 0,
                               self._depth, code)
         else:
@@ -287,15 +406,15 @@ class TensorProducer:
         self._consumers[cid] = rec
         try:
             # ring descriptor first (private channel), then the Welcome
-            conn.send(Announce(sg.RING_EPOCH, rec.cursor, self._descriptor.name(), 0, DType.U8,
-                               (0,), 0))
+            conn.send(Announce(sg.RING_EPOCH, rec.cursor, self._descriptor_for(k).name(), 0,
+                               DType.U8, (0,), 0))
             conn.send(welcome)
             if code == ADMIT_RUBBERBAND:
                 for q in range(q0, q0 + progress):
-                    ann = self._retained.get(q)
-                    if ann is not None:
+                    anns = self._retained.get(q)
+                    if anns is not None:
                         self._ledger.pending.setdefault(q, set()).add(cid)
-                        conn.send(ann)
+                        conn.send(anns[k])
         except OSError:
             self._drop(cid, "disconnect")
         self._lock.notify_all()
@@ -305,8 +424,9 @@ class TensorProducer:
         rec = self._consumers.pop(cid, None)
         if rec is None:
             return
-        if self._ring is not None:
-            self._ring.evict(rec.cursor)  # unblocks every device wait on this consumer
+        self.drops.append((cid, reason, time.monotonic()))
+        if rec.ring in self._rings:
+            self._rings[rec.ring].evict(rec.cursor)  # unblocks every wait on this consumer
         self._ledger.remove_consumer(cid)
         if reason == "timeout":
             self.stats["evictions"] += 1
@@ -356,6 +476,7 @@ class TensorProducer:
         if it is not None and L > 0:
             first = next(it)  # fixes the slot size before any consumer is admitted
             with self._lock:
+                self._set_geometry(first)
                 self._ensure_ring(self._pair_nbytes(first))
         with self._lock:
             need = 1 if self._barrier_met else self._min_consumers
@@ -393,20 +514,22 @@ class TensorProducer:
                 if rec.waiting_for_epoch == self._epoch:
                     rec.waiting_for_epoch = None
                     rec.admitted = True
-                    if self._ring is not None:
-                        self._ring.set_cursor(rec.cursor, q0 - 1)
+                    if rec.ring in self._rings:
+                        self._rings[rec.ring].set_cursor(rec.cursor, q0 - 1)
             self._epoch_started = True
             self._announced_in_epoch = 0
             self._retained.clear()
             window = retention_window(self._fraction, L)
-            if window > 0 and self._ring is not None:
-                self._ring.set_cursor(self._retention_cursor, q0 - 1)
+            if window > 0 and self._rings:
+                for ring in self._rings.values():
+                    ring.set_cursor(self._retention_cursor, q0 - 1)
                 self._retention_active = True
             self._send_all(EpochStart(self._epoch, L))
 
     def _drop_retention(self) -> None:
-        if self._retention_active and self._ring is not None:
-            self._ring.evict(self._retention_cursor)
+        if self._retention_active:
+            for ring in self._rings.values():
+                ring.evict(self._retention_cursor)
         self._retention_active = False
 
     def _publish(self, index: int, batch) -> None:
@@ -430,30 +553,52 @@ class TensorProducer:
         with self._lock:
             self._ensure_ring(nbytes)
             self._lock.wait_for(lambda: self._admitted() or self._closed)
-            live = [r.cursor for r in self._admitted()]
+            admitted = self._admitted()
+            live_by_ring = {k: [r.cursor for r in admitted if r.ring == k]
+                            for k in range(len(self._devices))}
             if self._retention_active:
-                live.append(self._retention_cursor)
+                for lv in live_by_ring.values():
+                    lv.append(self._retention_cursor)
         ring, stream = self._ring, self._stream
         slot = ring.slot_of(q)
-        # bound host run-ahead: batch q-S (same slot) must have been published
-        if q > ring.slots:
-            self._events[slot].synchronize()
-        with torch.cuda.device(self.device), torch.cuda.stream(stream):
-            ring.wait_free(live, q - ring.slots, stream)
-            base = ring.slot_ptr(slot)
-            if self._device_loader:
-                self._loader.produce_into(base, self._epoch, index, stream)
-            else:
-                view = ring.view(slot, (nbytes,), torch.uint8)
-                view[:in_bytes].copy_(inp.contiguous().reshape(-1).view(torch.uint8),
-                                      non_blocking=True)
-                view[in_bytes:nbytes].copy_(tgt.contiguous().reshape(-1).view(torch.uint8),
-                                            non_blocking=True)
-            if self._checksum:
-                dp.crc32(base, nbytes, self._crc[slot:slot + 1], stream)
-                self._crc_host[slot:slot + 1].copy_(self._crc[slot:slot + 1], non_blocking=True)
-            ring.publish(slot, q, stream)
-            self._events[slot].record(stream)
+        host_gated = all(r.host_control for r in self._rings.values())
+        if host_gated:
+            # flow gate on the host-shared cursors: the producer's streams never
+            # park on a device wait, so no stream of this process (in-process
+            # consumers included) can be blocked behind one
+            self._host_gate(q, live_by_ring)
+        if self._multi and self._device_loader and not self._checksum:
+            self._publish_group(q, index)
+        elif self._device_loader and host_gated and not self._checksum:
+            a = self._loader.produce_args(self._epoch)  # fused collate + target + publish
+            a.gate = GATE_HOST
+            with torch.cuda.device(self.device):
+                produce_range(ring, a, q, index, 1, [], stream=stream)
+        else:
+            if not host_gated and q > ring.slots:
+                # bound host run-ahead: batch q-S (same slot) must have been published
+                self._events[slot].synchronize()
+            for k, d in enumerate(self._devices):
+                r, st = self._rings[k], self._streams[k]
+                with torch.cuda.device(d), torch.cuda.stream(st):
+                    if not host_gated:
+                        r.wait_free(live_by_ring[k], q - r.slots, st)
+                    base = r.slot_ptr(slot)
+                    if self._device_loader:
+                        self._loader.produce_into(base, self._epoch, index, st)
+                    else:
+                        view = r.view(slot, (nbytes,), torch.uint8)
+                        view[:in_bytes].copy_(inp.contiguous().reshape(-1).view(torch.uint8),
+                                              non_blocking=True)
+                        view[in_bytes:nbytes].copy_(
+                            tgt.contiguous().reshape(-1).view(torch.uint8), non_blocking=True)
+                    if self._checksum and k == 0:
+                        dp.crc32(base, nbytes, self._crc[slot:slot + 1], st)
+                        self._crc_host[slot:slot + 1].copy_(self._crc[slot:slot + 1],
+                                                            non_blocking=True)
+                    r.publish(slot, q, st)
+                    if k == 0:
+                        self._events[slot].record(st)
         crc = 0
         if self._checksum:
             self._events[slot].synchronize()
@@ -462,18 +607,77 @@ class TensorProducer:
                                          in_bytes)
         header = sg.pack_header(self._epoch, index, DType.U8, (nbytes,), nbytes, crc,
                                 reserved=reserved, extra_slots=(*in_shape, *tg_shape))
-        ann = Announce(self._epoch, index, sg.slot_name(self.ring_id, slot, header), nbytes,
-                       DType.U8, (nbytes,), crc)
+        anns = {k: Announce(self._epoch, index, sg.slot_name(self._ring_ids[k], slot, header),
+                            nbytes, DType.U8, (nbytes,), crc) for k in self._rings}
         with self._lock:
             self._ledger.add(q, [r.consumer_id for r in self._admitted()])
-            self._send_all(ann)
+            self._send_announces(anns)
             self._announced_in_epoch = index + 1
             self.stats["announced"] += 1
             window = retention_window(self._fraction, L)
             if self._retention_active:
-                self._retained[q] = ann
+                self._retained[q] = anns
                 if self._announced_in_epoch >= window:
                     self._drop_retention()
+
+    def _order_on(self, dev: int, epoch: int):
+        """The epoch order resident on `dev` (a shard's kernel reads its indices locally)."""
+        import torch
+
+        key = (dev, epoch)
+        if key not in self._orders:
+            for k in [k for k in self._orders if k[1] != epoch]:
+                del self._orders[k]
+            host, _ = self._loader.order(epoch)
+            self._orders[key] = torch.from_numpy(host).to(f"cuda:{dev}")
+        return self._orders[key]
+
+    def _host_gate(self, q: int, live_by_ring) -> None:
+        """Block until every live consumer of every ring released batch q-S."""
+        need = q - self._ring.slots
+        if need <= 0:
+            return
+        for k, ring in self._rings.items():
+            while not ring.host_gate(live_by_ring[k], need, timeout_s=0.1):
+                if self._closed:
+                    raise ProducerClosed("producer closed while waiting for consumers")
+
+    def _publish_group(self, q: int, index: int) -> None:
+        """Multi-GPU: every device produces its shard of the batch straight into
+        the slot of every device's ring (sharded), or the first device produces
+        the whole batch into every ring (star); publish is fused into the kernel
+        and the flow gate runs on the host (tsb_produce_group)."""
+        import torch
+
+        G = len(self._devices)
+        rings = [self._rings[k] for k in range(G)]
+        live = [[] for _ in range(G)]  # gated on the host already (_host_gate)
+        writers = list(range(G)) if self._sharded else [0]
+        for g, k in enumerate(writers):
+            d = self._devices[k]
+            with torch.cuda.device(d):
+                a = self._loader.produce_args(self._epoch)
+                order = self._order_on(d, self._epoch)
+                a.d_order = order.data_ptr()
+                a.gate = GATE_HOST
+                produce_group(rings, k, a, g, len(writers), q, index, 1, live,
+                              stream=self._streams[k])
+
+    def _send_announces(self, anns: dict) -> None:
+        """Announce a batch: each consumer gets the slot name of its own GPU's ring."""
+        data = {d: encode(a) for d, a in anns.items()}
+        for rec in list(self._consumers.values()):
+            if rec.bcast is None:
+                continue
+            try:
+                rec.bcast.send_raw(data[rec.ring])
+            except OSError:
+                self._drop(rec.consumer_id, "disconnect")
+        for c in list(self._monitors):
+            try:
+                c.send_raw(data[0])
+            except OSError:
+                self._monitors.remove(c)
 
     # -- shutdown ---------------------------------------------------------------
     def join(self, drain_timeout_s: float = 10.0) -> None:
@@ -487,10 +691,10 @@ class TensorProducer:
         # device drain: every live consumer released the last batch (bounded wait)
         if self._ring is not None:
             with self._lock:
-                cursors = [r.cursor for r in self._admitted()]
+                cursors = [(self._rings[r.ring], r.cursor) for r in self._admitted()]
             final = seq_of(self._epoch, 0, max(1, len(self._loader))) - 1
             while cursors and time.monotonic() < deadline:
-                if all(self._ring.read_cursor(c) >= final for c in cursors):
+                if all(ring.read_cursor(c) >= final for ring, c in cursors):
                     break
                 time.sleep(0.005)
         with self._lock:
@@ -509,12 +713,13 @@ class TensorProducer:
     def close(self) -> None:
         """Release the device ring (after join()).  Consumers must be gone."""
         self.join(0.0)
-        if self._stream is not None:
-            self._stream.synchronize()
-        if self._ring is not None:
-            _RINGS.pop(self.ring_id, None)
-            self._ring.close()
-            self._ring = None
+        for st in self._streams.values():
+            st.synchronize()
+        for d, ring in self._rings.items():
+            _RINGS.pop(self._ring_ids[d], None)
+            ring.close()
+        self._rings.clear()
+        self._ring = None
 
     def __del__(self):
         try:

@@ -100,6 +100,7 @@ class DeviceRing:
             dev = ctypes.c_int(0)
             call("tsb_get_device", ctypes.byref(dev))
             device = dev.value
+        _lib.preload(device)
         h = ctypes.c_void_p()
         call("tsb_ring_create_ex", device, slots, slot_bytes, max_consumers, writers,
              ctypes.byref(h))
@@ -143,11 +144,15 @@ class DeviceRing:
         if len(handle) != IPC_HANDLE_BYTES:
             raise ValueError("IPC handle must be 64 bytes")
         L = load()
+        cur = ctypes.c_int(0)
+        call("tsb_get_device", ctypes.byref(cur))
+        _lib.preload(cur.value)
         buf = ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES)
         h = ctypes.c_void_p()
         call("tsb_ring_import_ex", buf, slots, slot_bytes, max_consumers, writers,
              ctypes.byref(h))
         self = cls.__new__(cls)
+        self._L = L
         self.writers = writers
         dev = ctypes.c_int(0)
         call("tsb_get_device", ctypes.byref(dev))
@@ -218,6 +223,24 @@ class DeviceRing:
         """Spin on the host until the slot holds seq (no GPU channel involved)."""
         call("tsb_ring_host_wait_ready", self._h, slot, seq,
              -1 if timeout_s < 0 else int(timeout_s * 1e6))
+
+    def host_gate(self, live, need: int, timeout_s: float = -1.0) -> bool:
+        """Block until every live cursor released `need` (host control block);
+        False on timeout."""
+        if need <= 0:
+            return True
+        live = list(live)
+        arr = (ctypes.c_int * max(1, len(live)))(*live)
+        rc = self._L.tsb_ring_host_gate(self._h, arr, len(live), need,
+                                        -1 if timeout_s < 0 else int(timeout_s * 1e6))
+        if rc == _lib.TSB_ERR_STALE:
+            return False
+        _lib.check(rc, "tsb_ring_host_gate")
+        return True
+
+    @property
+    def host_control(self) -> bool:
+        return self.ctl is not None
 
     def host_ack(self, consumer: int, seq: int) -> None:
         """Release up to seq from the host (consumer finished with the batch)."""

@@ -12,7 +12,12 @@ The ring itself (CUDA-IPC handle + geometry) is described once per consumer
 by a private "ring descriptor" announce with ``epoch == RING_EPOCH``
 (0xFFFFFFFF), ``batch_index`` = the consumer's device cursor index and
 
-    tsbr:<ring_id>:<pid>:<device>:<slots>:<slot_bytes>:<max_consumers>:<b64(ipc)>
+    tsbr:<ring_id>:<pid>:<device>:<slots>:<slot_bytes>:<max_consumers>:<ctl>:<b64(ipc)>
+    tsbr2:<...same...>:<ctl>:<writers>:<per_slot>:<samples>:<b64(ipc)>
+
+(v2: ``writers`` ready words per slot -- sharded ingest; ``per_slot`` =
+producer batch size and ``samples`` = samples per epoch, for consumers that
+rebatch to their own batch size; the ring is the one on the consumer's GPU).
 
 Reference consumers ignore it (epoch mismatch, sl/loader.py:155-156).
 Pair encoding (input+target in one blob) follows sl/abi.py:27-31,291-308:
@@ -136,17 +141,29 @@ class RingDescriptor:
     max_consumers: int
     ipc_handle: bytes
     control: str = "-"  # host-shared control block (shm name) or "-" (device words)
+    writers: int = 1
+    per_slot: int = 0   # producer batch size (samples per slot); 0 = unknown
+    samples: int = 0    # samples per epoch; 0 = unknown
 
     def name(self) -> str:
-        n = (f"tsbr:{self.ring_id:x}:{self.pid}:{self.device}:{self.slots}:{self.slot_bytes}:"
-             f"{self.max_consumers}:{self.control}:{_b64(self.ipc_handle)}")
+        head = (f"{self.ring_id:x}:{self.pid}:{self.device}:{self.slots}:{self.slot_bytes}:"
+                f"{self.max_consumers}:{self.control}")
+        if self.writers == 1 and not self.per_slot and not self.samples:
+            n = f"tsbr:{head}:{_b64(self.ipc_handle)}"
+        else:
+            n = (f"tsbr2:{head}:{self.writers}:{self.per_slot}:{self.samples}:"
+                 f"{_b64(self.ipc_handle)}")
         assert len(n) <= 255
         return n
 
     @classmethod
     def parse(cls, name: str) -> "RingDescriptor | None":
-        if not name.startswith("tsbr:"):
-            return None
-        _, rid, pid, dev, slots, sb, mc, ctl, h = name.split(":", 8)
-        return cls(int(rid, 16), int(pid), int(dev), int(slots), int(sb), int(mc),
-                   base64.b64decode(h), ctl)
+        if name.startswith("tsbr:"):
+            _, rid, pid, dev, slots, sb, mc, ctl, h = name.split(":", 8)
+            return cls(int(rid, 16), int(pid), int(dev), int(slots), int(sb), int(mc),
+                       base64.b64decode(h), ctl)
+        if name.startswith("tsbr2:"):
+            _, rid, pid, dev, slots, sb, mc, ctl, wr, ps, ns, h = name.split(":", 11)
+            return cls(int(rid, 16), int(pid), int(dev), int(slots), int(sb), int(mc),
+                       base64.b64decode(h), ctl, int(wr), int(ps), int(ns))
+        return None

@@ -11,6 +11,11 @@ Additions (behind the same frame format):
 * ``DType.BF16 = 5`` (2 bytes) -- the reference's closed set is 0..4
   (wire.py:49-74); only this implementation emits it.
 * device-slot URIs in ``Announce.segment_name`` (see ``segment.py``).
+* Join v2 (``protocol_version == 2``): the v1 body ``u64 consumer_id | u16
+  version`` followed by ``i16 device | u32 batch_size`` -- the consumer's GPU
+  (which device ring it maps) and its own batch size (heterogeneous
+  consumers, 0 = the producer's).  v1 Joins (the reference's) decode as
+  before, with device = -1 and batch_size = 0.
 """
 
 from __future__ import annotations
@@ -21,6 +26,8 @@ from dataclasses import dataclass
 from enum import IntEnum
 
 PROTOCOL_VERSION = 1
+JOIN_V2 = 2
+SUPPORTED_VERSIONS = (PROTOCOL_VERSION, JOIN_V2)
 MAX_FRAME_BODY = 65536
 MAX_SEGMENT_NAME = 255
 MAX_NDIM = 8
@@ -78,6 +85,8 @@ def dtype_of(obj) -> DType:
 class Join:
     consumer_id: int
     protocol_version: int = PROTOCOL_VERSION
+    device: int = -1        # v2 only
+    batch_size: int = 0     # v2 only
 
 
 @dataclass(frozen=True)
@@ -150,6 +159,7 @@ ANNOUNCE_KIND = 3
 KIND = {cls: k for k, (cls, _) in _FIXED.items()}
 KIND[Announce] = ANNOUNCE_KIND
 _HEAD = struct.Struct("<IB")
+_JOIN_V2 = struct.Struct("<QHhI")
 
 
 def checksum(data) -> int:
@@ -189,11 +199,18 @@ def encode(msg) -> bytes:
         nd = len(msg.shape)
         body = struct.pack(f"<IQH{len(name)}sQBB{nd}QI", msg.epoch, msg.batch_index, len(name),
                            name, msg.byte_len, int(msg.dtype), nd, *msg.shape, msg.checksum)
+    elif kind == 1 and msg.protocol_version >= JOIN_V2:
+        if not (-1 <= msg.device < 32768 and 0 <= msg.batch_size < (1 << 32)):
+            raise EncodeError("Join v2 device/batch_size out of range")
+        body = _JOIN_V2.pack(msg.consumer_id, msg.protocol_version, msg.device, msg.batch_size)
     else:
         cls, st = _FIXED[kind]
         if cls is EpochStart and msg.epoch_len <= 0:
             raise EncodeError("epoch_len must be > 0")
-        body = st.pack(*(getattr(msg, f) for f in cls.__dataclass_fields__))
+        if cls is Join and (msg.device != -1 or msg.batch_size != 0):
+            raise EncodeError("device/batch_size need protocol_version >= 2")
+        fields = ("consumer_id", "protocol_version") if cls is Join else cls.__dataclass_fields__
+        body = st.pack(*(getattr(msg, f) for f in fields))
     return _HEAD.pack(len(body) + 1, kind) + body
 
 
@@ -212,6 +229,11 @@ def decode(frame: bytes):
     end = 4 + length
     if kind == ANNOUNCE_KIND:
         msg, used = _decode_announce(frame)
+    elif kind == 1 and length - 1 == _JOIN_V2.size:
+        cid, ver, dev, bsz = _JOIN_V2.unpack_from(frame, 5)
+        if ver < JOIN_V2:
+            raise DecodeError(13, f"Join v{ver} body carries v2 fields")
+        msg, used = Join(cid, ver, dev, bsz), 5 + _JOIN_V2.size
     elif kind in _FIXED:
         cls, st = _FIXED[kind]
         if 5 + st.size > end:

@@ -1,0 +1,151 @@
+"""Facade on the GPU, multi-ring and heterogeneous consumers.
+
+* ``TensorProducer(devices=[...])``: one ring per device, consumers map the
+  ring of their own GPU (Join v2).  On the one-GPU test box the device list
+  is ``[0, 0]`` -- two rings on one GPU, consumers spread over them -- which
+  exercises the sharded writers (two streams, fused all-gather into both
+  rings) and the star path exactly as on separate GPUs, minus NVLink.
+* ``SharedLoader(batch_size=b)`` (config C4): each consumer receives exactly
+  the reference's batches for its own b -- samples ``order[j*b:(j+1)*b]``,
+  ``N // b`` per epoch (bs/pipeline.py:77-79,113-123) -- zero-copy windows or
+  rebatch-kernel gathers across slot boundaries; checked against the oracle.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec,  # noqa: E402
+                                   SharedLoader, StoreSource, TensorProducer)
+
+H, W, C, PAD = 32, 64, 3, 4
+
+
+@pytest.fixture
+def endpoints(tmp_path):
+    return f"unix:{tmp_path}/mb.sock", f"unix:{tmp_path}/ma.sock"
+
+
+def _loader(N, B, out_dtype="float32", seed=2):
+    store = StoreSource.synthetic(seed, N, (H, W, C))
+    return CollateLoader(DatasetSpec(store, N, B, shuffle_seed=3),
+                         AugmentSpec(pad=PAD, flip=True, out_dtype=out_dtype, seed=1))
+
+
+def _consume(loader, epochs, out):
+    # each in-process consumer orders its waits/acks on its own stream (one
+    # process per consumer gets that for free; threads sharing the legacy
+    # default stream would serialise one consumer's wait before another's ack)
+    try:
+        with torch.cuda.stream(torch.cuda.Stream()):
+            for _ in range(epochs):
+                ep = []
+                for inp, tgt in loader:
+                    x = inp.view(torch.int16) if inp.dtype == torch.bfloat16 else inp
+                    ep.append((x.cpu().numpy().copy(), tgt.cpu().numpy().copy()))
+                out.append(ep)
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        out.append(traceback.format_exc())
+    finally:
+        loader.close()
+
+
+def _want(oracle, N, seed, epoch, idx, kind):
+    store_h = oracle.make_store(seed, N, H * W * C)
+    scale, bias = oracle.norm_consts()
+    return oracle.collate_augment(store_h, idx, H, W, C, PAD, True, 1, epoch, kind, scale, bias)
+
+
+def _run(endpoints, ld, consumers_kw, epochs, **pkw):
+    b, a = endpoints
+    producer = TensorProducer(ld, broadcast=b, aggregate=a, heartbeat_timeout_s=20.0,
+                              min_consumers=len(consumers_kw), **pkw)
+
+    def run():
+        for _ in range(epochs):
+            for _ in producer:
+                pass
+        producer.join(30)
+
+    pt = threading.Thread(target=run, daemon=True)
+    pt.start()
+    outs = [[] for _ in consumers_kw]
+    ts = [threading.Thread(target=_consume, args=(SharedLoader(b, a, consumer_id=100 + i, **kw),
+                                                   epochs, outs[i]))
+          for i, kw in enumerate(consumers_kw)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(180)
+        assert not t.is_alive(), "consumer hung"
+    pt.join(60)
+    return producer, outs
+
+
+@pytest.mark.parametrize("fanout", ["sharded", "star"])
+@pytest.mark.parametrize("out_dtype,kind", [("float32", 1), ("bfloat16", 2)])
+def test_multi_ring_producer_every_consumer_gets_every_batch(endpoints, oracle, fanout,
+                                                             out_dtype, kind):
+    N, B = 48, 8
+    ld = _loader(N, B, out_dtype)
+    producer, outs = _run(endpoints, ld, [{"device": 0}] * 3, epochs=2, devices=[0, 0],
+                          fanout=fanout, ring_slots=3)
+    for got in outs:
+        assert len(got) == 2 and not isinstance(got[0], str), got
+        for e, ep in enumerate(got):
+            order = oracle.epoch_order(N, 3, e)
+            assert len(ep) == N // B
+            for j, (inp, tgt) in enumerate(ep):
+                idx = order[j * B:(j + 1) * B]
+                np.testing.assert_array_equal(tgt, idx)
+                want = _want(oracle, N, 2, e, idx, kind)
+                np.testing.assert_array_equal(inp if kind == 1 else inp.view(np.uint16), want)
+    producer.close()
+
+
+def test_heterogeneous_batch_sizes_match_reference_batches(endpoints, oracle):
+    """C4 shape: consumers with b in {8, 16, 32, 64, 24} on a producer of B=32:
+    zero-copy sub-windows (8, 16), the producer's own batches (32), windows
+    spanning two slots (64) and straddling ones (24) gathered by the rebatch
+    kernel.  Each consumer's epoch = N // b batches = order[j*b:(j+1)*b]."""
+    N, B = 128, 32
+    ld = _loader(N, B, "float32", seed=5)
+    sizes = [8, 16, 32, 64, 24]
+    producer, outs = _run(endpoints, ld, [{"batch_size": b} for b in sizes], epochs=2,
+                          ring_slots=4)
+    for b, got in zip(sizes, outs):
+        assert len(got) == 2 and not isinstance(got[0], str), (b, got, producer.drops)
+        for e, ep in enumerate(got):
+            order = oracle.epoch_order(N, 3, e)
+            assert len(ep) == N // b, (b, len(ep))
+            for j, (inp, tgt) in enumerate(ep):
+                idx = order[j * b:(j + 1) * b]
+                np.testing.assert_array_equal(tgt, idx, err_msg=f"b={b} epoch {e} batch {j}")
+                assert inp.shape == (b, C, H, W)
+                np.testing.assert_array_equal(inp, _want(oracle, N, 5, e, idx, 1))
+    producer.close()
+
+
+def test_unservable_batch_size_is_refused(endpoints):
+    """A window that cannot fit the ring next to the producer's run-ahead gets
+    no Welcome (StreamError), like any refused Join."""
+    from paper_2409_18749_b200.errors import StreamError
+
+    N, B = 64, 8
+    ld = _loader(N, B)
+    b, a = endpoints
+    producer = TensorProducer(ld, broadcast=b, aggregate=a, ring_slots=3)
+    producer._start()
+    loader = SharedLoader(b, a, consumer_id=7, batch_size=40, connect_timeout_s=3)
+    with pytest.raises(StreamError):
+        next(iter(loader))
+    producer.join(0)
+    producer.close()
