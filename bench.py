@@ -295,12 +295,9 @@ def run_ours(args):
     handle = ring.export()
     rings = [ring]
     if world > 1:
-        infos = [None] * world
-        torch.distributed.all_gather_object(infos, (rank, handle, ring.control_name))
-        rings = []
-        for r, h_r, ctl_r in sorted(infos):
-            rings.append(ring if r == rank else DeviceRing.import_handle(
-                h_r, RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, ctl_r, writers=world))
+        from paper_2409_18749_b200 import group
+
+        rings = group.open_group(ring, group.exchange(group.describe(ring, rank)), rank)
     q = ctx.Queue()
     procs = [ctx.Process(target=host_consumer,
                          args=(dev, handle, ring.control_name, RING_SLOTS, loader.batch_nbytes,

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
+from typing import NamedTuple
 
 from .wire import ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT
 
@@ -54,6 +55,25 @@ def window_slots(batch_size: int, per_slot: int) -> int:
     if batch_size % per_slot == 0:
         return batch_size // per_slot
     return -(-batch_size // per_slot) + 1
+
+
+class WindowPlan(NamedTuple):
+    k0: int              # first producer batch (slot) the window touches
+    k1: int              # last one
+    offset: int          # sample offset of the window inside batch k0
+    zero_copy: bool      # inside one slot: a view, held until the next step
+    release_before: int  # producer batches [0, release_before) are free before this step
+    release_after: int   # gathered windows: batches [0, release_after) are free after the gather
+
+
+def rebatch_window_plan(j: int, batch_size: int, per_slot: int) -> WindowPlan:
+    """Batch j of a consumer with its own batch size b = stream samples
+    [j*b, (j+1)*b) of the epoch order (the reference's batch for b,
+    pipeline.py:113-123), laid over producer batches of per_slot samples."""
+    first = j * batch_size
+    k0, k1 = first // per_slot, (first + batch_size - 1) // per_slot
+    return WindowPlan(k0, k1, first - k0 * per_slot, k0 == k1, k0,
+                      (first + batch_size) // per_slot)
 
 
 @dataclass
