@@ -214,6 +214,15 @@ int tsb_rebatch_window(const void *const *slots, int n_slots, int64_t first, int
 #define TSB_SRC_AUGMENT 0   /* store -> fused collate/augment            */
 #define TSB_SRC_GATHER 1    /* store -> passthrough gather (DirectorySource) */
 #define TSB_SRC_SYNTHETIC 2 /* SplitMix64 generator (SyntheticSource)    */
+/* Staged PCIe ingest for pinned-host stores (copy engine, double-buffered
+ * HBM staging; one cudaMemcpyBatchAsync of the batch's sample rows). */
+typedef struct tsb_ingest tsb_ingest;
+int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int depth,
+                      tsb_ingest **out);
+int tsb_ingest_destroy(tsb_ingest *g);
+/* 1 if the batched-copy driver API is in use, 0 if per-sample copies. */
+int tsb_ingest_batch_api(tsb_ingest *g, int *used);
+
 typedef struct {
     int mode;                /* TSB_SRC_*                                     */
     const void *src;         /* store base: HBM or pinned host (NULL synthetic) */
@@ -235,6 +244,11 @@ typedef struct {
                                 thread blocks until the slot is free, the stream
                                 carries only kernels and consecutive fused batches
                                 chain with programmatic dependent launch */
+    tsb_ingest *ingest;      /* non-null (with h_order, src = pinned host store):
+                                each batch's sample rows cross PCIe by the copy
+                                engine into HBM staging first (augment), or
+                                straight into the slot (gather) */
+    const int64_t *h_order;  /* host copy of d_order (row addresses for ingest) */
 } tsb_produce_args;
 #define TSB_GATE_DEVICE 0
 #define TSB_GATE_HOST 1

@@ -104,6 +104,9 @@ SIGNATURES: dict[str, tuple] = {
                                          i32, pp, i32, vp]),
     "tsb_rebatch_gather": (i32, [vp, i64, i64, i64, i64, vp, vp]),
     "tsb_rebatch_window": (i32, [pp, i32, i64, i64, i64, i64, i64, vp, vp]),
+    "tsb_ingest_create": (i32, [i32, i64, i64, i32, pp]),
+    "tsb_ingest_destroy": (i32, [vp]),
+    "tsb_ingest_batch_api": (i32, [vp, ctypes.POINTER(i32)]),
 }
 
 class ProduceArgs(ctypes.Structure):
@@ -116,6 +119,7 @@ class ProduceArgs(ctypes.Structure):
         ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
         ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
         ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int), ("gate", ctypes.c_int),
+        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p),
     ]
 
 

@@ -155,6 +155,7 @@ class CollateLoader:
         self.with_target = with_target
         self.device = torch.cuda.current_device() if device is None else device
         self._order = _EpochOrder()
+        self._ingest = None  # staged copy-engine ingest (pinned-host stores)
         self.epoch = 0  # the epoch __iter__ produces next
         src = dataset.source
         if augment is not None:
@@ -261,6 +262,10 @@ class CollateLoader:
         a.with_target = int(self.with_target)
         a.input_bytes = self.input_nbytes
         a.d_crc = 0 if with_crc is None else with_crc.data_ptr()
+        if isinstance(src, StoreSource) and src.location == "pinned":
+            host, _ = self.order(epoch)
+            a.ingest = self._ingest_handle()
+            a.h_order = host.ctypes.data
         for i in range(4):
             a.scale[i], a.bias[i] = 1.0, 0.0
         if isinstance(src, SyntheticSource):
@@ -278,6 +283,15 @@ class CollateLoader:
                     a.scale[i], a.bias[i] = float(self._scale[i]), float(self._bias[i])
         return a
 
+    def _ingest_handle(self) -> int:
+        """Copy-engine ingest (double-buffered HBM staging) for a pinned store."""
+        if self._ingest is None:
+            from . import _lib
+
+            self._ingest = _Ingest(self.device, self.dataset.batch_size,
+                                   self.dataset.source.sample_nbytes)
+        return self._ingest.handle
+
     def __iter__(self):
         """Standalone (non-shared) iteration: fresh device tensors per batch."""
         import torch
@@ -291,3 +305,32 @@ class CollateLoader:
             inp = inp.view(self.input_shape)
             tgt = buf[self.input_nbytes:].view(torch.int64) if self.with_target else None
             yield inp, tgt
+
+
+class _Ingest:
+    """tsb_ingest: staged PCIe ingest (one cudaMemcpyBatchAsync per batch)."""
+
+    def __init__(self, device: int, max_batch: int, sample_bytes: int, depth: int = 2):
+        import ctypes
+
+        from . import _lib
+
+        h = ctypes.c_void_p()
+        _lib.call("tsb_ingest_create", device, max_batch, sample_bytes, depth, ctypes.byref(h))
+        self.handle = h.value
+        self._lib = _lib
+
+    def batch_api(self) -> bool:
+        import ctypes
+
+        v = ctypes.c_int(0)
+        self._lib.call("tsb_ingest_batch_api", self.handle, ctypes.byref(v))
+        return bool(v.value)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.load().tsb_ingest_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass

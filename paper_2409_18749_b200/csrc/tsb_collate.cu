@@ -179,6 +179,7 @@ struct Epi {
     unsigned int *counter;   // device completion counter (reset by the last CTA); nullptr = no publish
     int pdl;                 // launch as a programmatic dependent of the previous batch
     int sys_fence;           // destinations on other devices: order stores at system scope
+    const int64_t *tgt_idx;  // sample indices written as the target (nullptr = the gather indices)
 };
 
 __device__ __forceinline__ void pdl_launch_dependents() {
@@ -187,9 +188,10 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 __device__ __forceinline__ void write_targets(const Epi &ep, const int64_t *__restrict__ idx, int b,
                                               int tid, int nthreads) {
+    const int64_t *src = ep.tgt_idx ? ep.tgt_idx : idx;
     for (int d = 0; d < ep.n; ++d)
         if (ep.tgt[d])
-            for (int i = tid; i < b; i += nthreads) ep.tgt[d][i] = idx[i];
+            for (int i = tid; i < b; i += nthreads) ep.tgt[d][i] = src[i];
 }
 
 // Last CTA to finish publishes the slot: every thread orders its stores
@@ -620,10 +622,12 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     g.vec_ldg = aligned_rows && (g.io % 4 == 0);
     // rows per item (measured on B200, B=256 224x224x3): enough output per item to
     // amortise the per-item pipeline handoff -- f32 R=4 (10.7 KB out), bf16/u8 R=16.
+    // (profiles/r1/sweep_collate.txt: f32 R=4 x3 stages 37.2 us, bf16 R=16 x2 22.6 us,
+    // u8 R=16 x3 16.9 us per B=256 batch)
     int R = out_kind == TSB_OUT_F32 ? 4 : 16;
     while (R > 1 && (int64_t)R > h) R >>= 1;
     while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R >>= 1;
-    int nstage = 4;
+    int nstage = out_kind == TSB_OUT_BF16 ? 2 : 3;
     if (const char *e = getenv("TSB_CA_R")) R = atoi(e);          // tuning knobs
     if (const char *e = getenv("TSB_CA_STAGES")) nstage = atoi(e);
     TSB_CHECK(R >= 1 && R <= 64 && (R & (R - 1)) == 0, "rows per item must be a power of 2 <= 64");
@@ -741,7 +745,8 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
-                            int pdl, void *stream) {
+                            int pdl, void *stream, const int32_t *d_params,
+                            const int64_t *tgt_idx) {
     Dsts d{};
     d.p[0] = out;
     d.n = 1;
@@ -752,8 +757,9 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     ep.seq = seq;
     ep.counter = counter;
     ep.pdl = pdl;
+    ep.tgt_idx = tgt_idx;
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
-                          out_kind, nullptr, d, stream, ep);
+                          out_kind, d_params, d, stream, ep);
 }
 
 // One batch shard into n destinations (fan-out), fused target copy + publish:

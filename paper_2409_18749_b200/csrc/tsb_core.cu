@@ -187,6 +187,7 @@ void preload_collate();
 void preload_crc32();
 void preload_fanout();
 void preload_ring();
+void preload_ingest();
 }  // namespace tsb
 
 extern "C" int tsb_preload_kernels(void) {
@@ -196,5 +197,6 @@ extern "C" int tsb_preload_kernels(void) {
     tsb::preload_crc32();
     tsb::preload_fanout();
     tsb::preload_ring();
+    tsb::preload_ingest();
     return TSB_OK;
 }

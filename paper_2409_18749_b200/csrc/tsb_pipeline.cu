@@ -22,7 +22,16 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
-                            int pdl, void *stream);
+                            int pdl, void *stream, const int32_t *d_params,
+                            const int64_t *tgt_idx);
+int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
+                 void *dst, void *stream, int *k_out, bool after_stream);
+int ingest_release(tsb_ingest *g, int k, void *stream);
+uint8_t *ingest_staging(tsb_ingest *g, int k);
+int64_t *ingest_indices(tsb_ingest *g, int k);
+int32_t *ingest_params(tsb_ingest *g, int k);
+int64_t *ingest_identity(tsb_ingest *g);
+int64_t ingest_sample_bytes(tsb_ingest *g);
 }  // namespace tsb
 
 extern "C" {
@@ -50,6 +59,11 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     static const bool no_pdl = getenv("TSB_NO_PDL") && atoi(getenv("TSB_NO_PDL"));      // A/B knobs
     static const bool no_fused = getenv("TSB_NO_FUSED") && atoi(getenv("TSB_NO_FUSED"));
     bool prev_fused = false;
+    const bool staged = a->ingest && a->h_order && !ev;
+    if (staged)
+        TSB_CHECK(ingest_sample_bytes(a->ingest) == a->sample_bytes,
+                  "ingest staging is for %lld-byte samples, not %lld",
+                  (long long)ingest_sample_bytes(a->ingest), (long long)a->sample_bytes);
     for (int i = 0; i < n; ++i) {
         const uint64_t q = seq0 + (uint64_t)i;
         const int slot = (int)((q - 1) % (uint64_t)slots);
@@ -74,7 +88,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         }
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i]), s));
         int rc = TSB_OK;
-        bool published = false;
+        bool published = false, staged_target = false;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
                 if (!a->d_crc && !no_fused && ring_writers(r) == 1) {  // fused epilogue: target copy + publish from the kernel
@@ -86,10 +100,29 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                                      a->input_bytes)
                                        : nullptr;
                     const int pdl = prev_fused && host_gate && !ev && !no_pdl;
+                    if (staged) {  // copy-engine ingest into HBM staging, then collate it
+                        int k = 0;
+                        if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, nullptr,
+                                               stream, &k, false)))
+                            return rc;
+                        int32_t *params = ingest_params(a->ingest, k);
+                        if ((rc = tsb_aug_params(a->seed, a->epoch, ingest_indices(a->ingest, k),
+                                                 b, a->pad, a->flip, params, stream)))
+                            return rc;
+                        rc = collate_augment_publish(ingest_staging(a->ingest, k),
+                                                     ingest_identity(a->ingest), b, a->h, a->w,
+                                                     a->c, a->pad, a->flip, a->seed, a->epoch,
+                                                     a->scale, a->bias, a->out_kind, out, tgt,
+                                                     ready, q, counter, 0, stream, params,
+                                                     ingest_indices(a->ingest, k));
+                        if (!rc) rc = ingest_release(a->ingest, k, stream);
+                        published = true;
+                        break;
+                    }
                     rc = collate_augment_publish(a->src, idx, b, a->h, a->w, a->c, a->pad,
                                                  a->flip, a->seed, a->epoch, a->scale, a->bias,
                                                  a->out_kind, out, tgt, ready, q, counter, pdl,
-                                                 stream);
+                                                 stream, nullptr, nullptr);
                     published = true;
                     break;
                 }
@@ -98,6 +131,20 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                          nullptr, out, stream);
                 break;
             case TSB_SRC_GATHER:
+                if (staged) {  // copy engine straight into the slot (no kernel)
+                    int k = 0;
+                    if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, out, stream,
+                                           &k, !host_gate)))
+                        return rc;
+                    if (a->with_target) {
+                        TSB_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(out) + a->input_bytes,
+                                                 ingest_indices(a->ingest, k), 8 * b,
+                                                 cudaMemcpyDeviceToDevice, s));
+                        staged_target = true;
+                    }
+                    rc = ingest_release(a->ingest, k, stream);
+                    break;
+                }
                 rc = tsb_gather(a->src, idx, b, a->sample_bytes, out, stream);
                 break;
             case TSB_SRC_SYNTHETIC:
@@ -110,7 +157,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         prev_fused = published;
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
         if (published) continue;
-        if (a->with_target)
+        if (a->with_target && !staged_target)
             TSB_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(out) + a->input_bytes, idx, 8 * b,
                                      cudaMemcpyDeviceToDevice, s));
         if (a->d_crc)

@@ -178,3 +178,59 @@ def test_host_gate_needs_host_control():
     with pytest.raises(ValueError, match="host control"):
         produce_range(ring, a, 1, 0, 1, [0])
     ring.close()
+
+
+@pytest.mark.parametrize("mode", ["augment_f32", "augment_bf16", "gather"])
+def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode):
+    """Pinned-host store: each batch's scattered sample rows cross PCIe by the
+    copy engine (cudaMemcpyBatchAsync) into HBM staging (augment) or straight
+    into the slot (gather); results identical to the oracle."""
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    h, w, c, B, N, S, n = 32, 64, 3, 8, 64, 3, 12
+    store = StoreSource.synthetic(9, N, (h, w, c), location="pinned")
+    aug = None if mode == "gather" else AugmentSpec(
+        pad=4, flip=True, out_dtype="float32" if mode == "augment_f32" else "bfloat16", seed=2)
+    ld = CollateLoader(DatasetSpec(store, N, B, shuffle_seed=1), aug)
+    ring = DeviceRing(S, ld.batch_nbytes, 1, control="host")
+    ring.set_cursor(0, 0)
+    store_h = oracle.make_store(9, N, h * w * c)
+    scale, bias = oracle.norm_consts()
+    kind = {"augment_f32": 1, "augment_bf16": 2}.get(mode)
+    L = len(ld)
+    got = {}
+    import threading
+
+    def consumer():
+        for q in range(1, n + 1):
+            slot = ring.slot_of(q)
+            ring.host_wait_ready(slot, q, timeout_s=60)
+            got[q] = ring.view(slot, (ld.batch_nbytes,), torch.uint8).cpu().numpy().copy()
+            ring.host_ack(0, q)
+
+    t = threading.Thread(target=consumer)
+    t.start()
+    ps = torch.cuda.Stream()
+    q = 1
+    while q <= n:
+        epoch, bi = divmod(q - 1, L)
+        m = min(n - q + 1, L - bi)
+        a = ld.produce_args(epoch)
+        assert a.ingest and a.h_order
+        a.gate = GATE_HOST
+        produce_range(ring, a, q, bi, m, [0], stream=ps)
+        q += m
+    ps.synchronize()
+    t.join(60)
+    assert not t.is_alive()
+    for q in range(1, n + 1):
+        epoch, bi = divmod(q - 1, L)
+        idx = oracle.epoch_order(N, 1, epoch)[bi * B:(bi + 1) * B]
+        if kind is None:
+            want = oracle.gather(store_h, idx, h * w * c)
+        else:
+            want = oracle.collate_augment(store_h, idx, h, w, c, 4, True, 2, epoch, kind,
+                                          scale, bias)
+        assert got[q][:ld.input_nbytes].tobytes() == want.tobytes(), q
+        np.testing.assert_array_equal(got[q][ld.input_nbytes:].view(np.int64), idx)
+    ring.close()
