@@ -145,10 +145,33 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                     rc = ingest_release(a->ingest, k, stream);
                     break;
                 }
-                rc = tsb_gather(a->src, idx, b, a->sample_bytes, out, stream);
-                break;
+                [[fallthrough]];
             case TSB_SRC_SYNTHETIC:
-                rc = tsb_fill_synthetic(out, idx, b, a->seed, a->epoch, a->sample_bytes, stream);
+                if (!a->d_crc && !no_fused && ring_writers(r) == 1 && a->sample_bytes % 16 == 0 &&
+                    ((uintptr_t)out & 15) == 0) {
+                    // one persistent passthrough launch: samples + target + slot publish
+                    uint64_t *ready = nullptr;
+                    unsigned int *counter = nullptr;
+                    if ((rc = ring_publish_ptrs(r, slot, 0, &ready, &counter))) return rc;
+                    int64_t *tgt = a->with_target
+                                       ? reinterpret_cast<int64_t *>(static_cast<uint8_t *>(out) +
+                                                                     a->input_bytes)
+                                       : nullptr;
+                    void *outs[1] = {out};
+                    int64_t *tgts[1] = {tgt};
+                    uint64_t *readys[1] = {ready};
+                    const int pdl = prev_fused && host_gate && !ev && !no_pdl;
+                    rc = produce_multi(a->mode, a->src, idx, b, a->h, a->w, a->c, a->pad, a->flip,
+                                       a->seed, a->epoch, a->scale, a->bias, a->out_kind,
+                                       a->sample_bytes, outs, tgts, readys, 1, counter, q, pdl, 0,
+                                       stream);
+                    published = true;
+                    break;
+                }
+                rc = a->mode == TSB_SRC_GATHER
+                         ? tsb_gather(a->src, idx, b, a->sample_bytes, out, stream)
+                         : tsb_fill_synthetic(out, idx, b, a->seed, a->epoch, a->sample_bytes,
+                                              stream);
                 break;
             default:
                 TSB_CHECK(false, "bad produce mode %d", a->mode);
