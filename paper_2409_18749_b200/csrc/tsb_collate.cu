@@ -274,6 +274,33 @@ __device__ __forceinline__ float byte_to_float(const uint32_t *wv) {
     const uint32_t bits = __byte_perm(wv[K >> 2], 0x4B000000u, sel);
     return __uint_as_float(bits) - 8388608.0f;  // (2^23 + u) - 2^23, exact
 }
+// Paired fp32 arithmetic (FADD2/FMUL2 on sm_100).  Explicit-rounding PTX
+// (.rn) is never contracted into FFMA2, so each lane keeps the oracle's two
+// roundings fl(fl(u*s)+b); the CUDA float2 intrinsics did get fused.
+__device__ __forceinline__ uint64_t pack_f32x2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack_f32x2(uint64_t v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t add_rn_f32x2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t mul_rn_f32x2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t byte_bits(const uint32_t *wv) {
+    constexpr uint32_t sel = (K & 3) | (4u << 4) | (5u << 8) | (7u << 12);
+    return __byte_perm(wv[K >> 2], 0x4B000000u, sel);
+}
 template <int K>
 __device__ __forceinline__ uint32_t byte_at(const uint32_t *wv) {
     return (wv[K >> 2] >> (8 * (K & 3))) & 0xFFu;
@@ -298,8 +325,22 @@ __device__ __forceinline__ uint4 make_vec(const uint32_t *wv, float sc, float bi
                           b[8] | (b[9] << 8) | (b[10] << 16) | (b[11] << 24),
                           b[12] | (b[13] << 8) | (b[14] << 16) | (b[15] << 24));
     } else {
-        float f[P] = {__fadd_rn(
-            __fmul_rn(byte_to_float<Emit<OUT_KIND, C, FLIP, 0>::kidx(Qs, CH)>(wv), sc), bi)...};
+        // PRMT byte -> float bits 2^23+u; then paired fp32 ops (FADD2/FMUL2 on sm_100,
+        // per-lane IEEE round-to-nearest, no contraction): (2^23+u)-2^23 is exact,
+        // then fl(fl(u*sc)+bi) exactly as the oracle's two roundings.
+        const uint32_t bits[P] = {byte_bits<Emit<OUT_KIND, C, FLIP, 0>::kidx(Qs, CH)>(wv)...};
+        float f[P];
+        const uint64_t k23 = pack_f32x2(-8388608.0f, -8388608.0f);
+        const uint64_t sc2 = pack_f32x2(sc, sc);
+#pragma unroll
+        for (int i = 0; i < P; i += 2) {
+            uint64_t u = pack_f32x2(__uint_as_float(bits[i]), __uint_as_float(bits[i + 1]));
+            u = mul_rn_f32x2(add_rn_f32x2(u, k23), sc2);
+            float m0, m1;
+            unpack_f32x2(u, m0, m1);
+            f[i] = __fadd_rn(m0, bi);  // scalar .rn add: keeps the product's rounding
+            f[i + 1] = __fadd_rn(m1, bi);
+        }
         if constexpr (OUT_KIND == TSB_OUT_F32) {
             return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
                               __float_as_uint(f[3]));

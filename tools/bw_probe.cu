@@ -27,6 +27,35 @@ __global__ void mix_k(const uint4 *in, uint4 *out, size_t n16, int ratio) {
     }
 }
 
+__global__ void write_cs_k(uint4 *out, size_t n16, uint32_t v) {
+    size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += stride)
+        asm volatile("st.global.cs.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(out + i), "r"(v) : "memory");
+}
+// TMA bulk stores: each CTA streams `chunk`-byte pieces of its smem buffer to
+// global, grid-strided; lane 0 of each warp owns every 8th chunk.
+__global__ void tma_write_k(uint8_t *out, size_t bytes, int chunk) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    for (int i = threadIdx.x; i < chunk * 8 / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(sm)[i] = make_uint4(7, 7, 7, 7);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t nchunks = bytes / chunk;
+    if (lane == 0) {
+        int issued = 0;
+        for (size_t c = (size_t)blockIdx.x * 8 + warp; c < nchunks; c += (size_t)gridDim.x * 8) {
+            const uint8_t *src = sm + (size_t)warp * chunk;
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + c * chunk),
+                         "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(chunk)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (++issued >= 4) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
 int main() {
     const size_t N = 38535168;  // bytes of one u8 batch (256 x 150528)
     uint4 *a, *b;
@@ -60,5 +89,18 @@ int main() {
     time("mix 1:2 (u8->bf16) 115MB", 3.0 * N, [&] { mix_k<<<g, t>>>(a, b, N / 16, 2); });
     time("mix 1:1 (u8->u8) 77MB", 2.0 * N, [&] { mix_k<<<g, t>>>(a, b, N / 16, 1); });
     time("memset 154MB", 4.0 * N, [&] { cudaMemsetAsync(b, 0, 4 * N); });
+    time("write_only st.cs 154MB", 4.0 * N, [&] { write_cs_k<<<g, t>>>(b, 4 * N / 16, 7); });
+    for (int chunk : {4096, 8192, 16384}) {
+        cudaFuncSetAttribute(tma_write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * chunk);
+        char name[64];
+        snprintf(name, sizeof name, "tma_write %dB chunks 154MB", chunk);
+        for (int ctas : {1, 2}) {
+            char nm[80];
+            snprintf(nm, sizeof nm, "%s x%d/SM", name, ctas);
+            time(nm, 4.0 * N, [&] {
+                tma_write_k<<<sms * ctas, 256, 8 * chunk>>>(reinterpret_cast<uint8_t *>(b), 4 * N, chunk);
+            });
+        }
+    }
     return 0;
 }
