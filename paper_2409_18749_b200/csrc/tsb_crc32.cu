@@ -7,13 +7,15 @@
 //   raw(A||B) = x^(8|B|) * raw(A)  xor  raw(B)          (raw = zero-init CRC)
 //   crc(M)    = raw(M) xor x^(8|M|) * 0xFFFFFFFF xor 0xFFFFFFFF
 // and raw(0^z || M) = raw(M), so the message is front-padded (virtually) to a
-// whole number of 2 KB units.  Each warp owns one unit: every lane runs the
-// byte-table CRC over its 64 B (table replicated 32x in shared memory so lane
-// l always hits bank l -- conflict-free), a 5-level shuffle tree combines the
-// 32 lane CRCs, the unit CRC is shifted by the bytes that follow it, and the
-// shifted values are XOR-reduced (XOR is associative/commutative) with one
-// atomicXor per warp.  Multiplication by a constant x^k mod P uses 4-bit
-// tables (8 nibbles x 16 entries).  HBM-bound: one read of the data.
+// whole number of 2 KB units.  Each warp owns a contiguous run of units;
+// every lane runs two slice-by-4 chains through its 64 B of each unit (the
+// four 256-entry tables replicated 32x in shared memory, 128 KB, so lane l
+// always hits bank l -- conflict-free), carrying each chain across the gap
+// to its next piece with one constant multiply; one 5-level shuffle tree per
+// run combines the lanes, the run is shifted once by the units after it, and
+// runs are XOR-reduced (XOR is associative/commutative) with one atomicXor
+// per warp.  Multiplication by a constant x^k mod P uses 4-bit
+// tables (8 nibbles x 16 entries).  One read of the data.
 #include <mutex>
 
 #include "tsb_common.cuh"
@@ -24,14 +26,16 @@ namespace {
 
 constexpr uint32_t POLY = 0xEDB88320u;
 constexpr int UNIT = 2048;        // bytes per warp unit
-constexpr int LANE_BYTES = 64;    // bytes per lane
+constexpr int LANE_BYTES = 64;    // bytes per lane and unit (two 32-byte chains)
 constexpr int TREE_LEVELS = 5;    // 32 lanes
-constexpr int SHIFT_BITS = 32;    // unit-shift tables: 2048 * 2^k, k < 32
+constexpr int SHIFT_BITS = 40;    // unit-shift tables: UNIT * 2^k, k < 40
 constexpr int NT = 8 * 16;        // u32 per nibble table
-constexpr int CRC_THREADS = 256;
+constexpr int CRC_THREADS = 1024;  // one CTA (32 warps) per SM: the lane-replicated tables take 128 KB
 
-__device__ uint32_t g_byte_tab[256];
+__device__ uint32_t g_slice_tab[4 * 256];
 __device__ uint32_t g_tree_tab[TREE_LEVELS * NT];
+__device__ uint32_t g_half_tab[NT];
+__device__ uint32_t g_gap_tab[NT];
 __device__ uint32_t g_shift_tab[SHIFT_BITS * NT];
 
 uint32_t h_multmodp(uint32_t a, uint32_t b) {
@@ -69,21 +73,35 @@ int ensure_tables() {
     TSB_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
     if (dev < 64 && g_ready[dev]) return TSB_OK;
-    static uint32_t bt[256], tt[TREE_LEVELS * NT], st[SHIFT_BITS * NT];
-    for (uint32_t i = 0; i < 256; ++i) {
+    static uint32_t sl[4 * 256], tt[TREE_LEVELS * NT], ht[NT], gt[NT], st[SHIFT_BITS * NT];
+    for (uint32_t i = 0; i < 256; ++i) {  // T0: the byte table (zlib's crc_table[0])
         uint32_t r = i;
         for (int k = 0; k < 8; ++k) r = (r >> 1) ^ (POLY & (0u - (r & 1u)));
-        bt[i] = r;
+        sl[i] = r;
     }
+    for (int t = 1; t < 4; ++t)  // slice-by-4: T_t[i] = T_{t-1}[i] >> 8 ^ T0[T_{t-1}[i] & 0xff]
+        for (uint32_t i = 0; i < 256; ++i)
+            sl[t * 256 + i] = (sl[(t - 1) * 256 + i] >> 8) ^ sl[sl[(t - 1) * 256 + i] & 0xFFu];
     for (int k = 0; k < TREE_LEVELS; ++k) h_nibble_table(h_x8n((uint64_t)LANE_BYTES << k), tt + k * NT);
+    h_nibble_table(h_x8n(LANE_BYTES / 2), ht);
+    h_nibble_table(h_x8n(UNIT - LANE_BYTES / 2), gt);
     for (int k = 0; k < SHIFT_BITS; ++k) h_nibble_table(h_x8n((uint64_t)UNIT << k), st + k * NT);
-    TSB_CUDA(cudaMemcpyToSymbol(g_byte_tab, bt, sizeof(bt)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_slice_tab, sl, sizeof(sl)));
     TSB_CUDA(cudaMemcpyToSymbol(g_tree_tab, tt, sizeof(tt)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_half_tab, ht, sizeof(ht)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_gap_tab, gt, sizeof(gt)));
     TSB_CUDA(cudaMemcpyToSymbol(g_shift_tab, st, sizeof(st)));
     if (dev < 64) g_ready[dev] = true;
     return TSB_OK;
 }
 
+// same product with a lane-replicated table (t already offset by the lane)
+__device__ __forceinline__ uint32_t mul_nib_rep(uint32_t v, const uint32_t *t) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r ^= t[(j * 16 + ((v >> (4 * j)) & 15u)) << 5];
+    return r;
+}
 __device__ __forceinline__ uint32_t mul_nib(uint32_t v, const uint32_t *t) {
     uint32_t r = 0;
 #pragma unroll
@@ -92,77 +110,108 @@ __device__ __forceinline__ uint32_t mul_nib(uint32_t v, const uint32_t *t) {
 }
 
 struct CrcSmem {
-    uint32_t rep[256 * 32];  // rep[i*32 + lane] = byte_tab[i]
+    uint32_t rep[4 * 256 * 32];  // rep[(t*256 + i)*32 + lane] = T_t[i]: lane l always hits bank l
     uint32_t tree[TREE_LEVELS * NT];
+    uint32_t half[NT];
+    uint32_t gap[NT * 32];  // lane-replicated like rep: gap[(j*16 + nib)*32 + lane]
     uint32_t shift[SHIFT_BITS * NT];
 };
 
 __global__ void crc_init_kernel(uint32_t *out, uint32_t c) { *out = c; }
 
+// slice-by-4 step of the raw (zero-init) reflected CRC over one little-endian word
+__device__ __forceinline__ uint32_t crc_word(const uint32_t *rep, uint32_t c, uint32_t w) {
+    const uint32_t x = c ^ w;
+    return rep[(3 * 256 + (x & 0xFFu)) << 5] ^ rep[(2 * 256 + ((x >> 8) & 0xFFu)) << 5] ^
+           rep[(1 * 256 + ((x >> 16) & 0xFFu)) << 5] ^ rep[(x >> 24) << 5];
+}
+
+// Each warp owns a contiguous run of 2 KB units and lane l always takes bytes
+// [64l, 64l+64) of each unit, as two 32-byte slice-by-4 chains.  A chain
+// runs across the whole run: before each next piece its state is multiplied
+// by x^(8*(2048-32)) (the gap to its next piece), so after the run lane l
+// holds sum_u raw(piece(u,l)) * x^(8*2048*(u_last-u)).  One shuffle tree per
+// run then shifts lane l by the 64*(31-l) bytes after its pieces, and lane 0
+// shifts the run by the units after it; one atomicXor per warp.
 __global__ void __launch_bounds__(CRC_THREADS)
     crc_kernel(const uint8_t *__restrict__ data, uint64_t n, uint64_t z, uint64_t n_units,
                int vec, uint32_t *out) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     CrcSmem &sm = *reinterpret_cast<CrcSmem *>(smem_raw);
-    for (int i = threadIdx.x; i < 256 * 32; i += CRC_THREADS) sm.rep[i] = g_byte_tab[i >> 5];
+    // replicate the 4x256 slice tables 32x: one global load per entry, the 32
+    // copies written in a rotated order so a warp's stores hit 32 banks
+    for (int e = threadIdx.x; e < 4 * 256; e += CRC_THREADS) {
+        const uint32_t v = g_slice_tab[e];
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) sm.rep[e * 32 + ((l + e) & 31)] = v;
+    }
     for (int i = threadIdx.x; i < TREE_LEVELS * NT; i += CRC_THREADS) sm.tree[i] = g_tree_tab[i];
+    for (int i = threadIdx.x; i < NT; i += CRC_THREADS) sm.half[i] = g_half_tab[i];
+    for (int e = threadIdx.x; e < NT; e += CRC_THREADS) {
+        const uint32_t v = g_gap_tab[e];
+        for (int l = 0; l < 32; ++l) sm.gap[e * 32 + ((l + e) & 31)] = v;
+    }
     for (int i = threadIdx.x; i < SHIFT_BITS * NT; i += CRC_THREADS) sm.shift[i] = g_shift_tab[i];
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * CRC_THREADS + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * CRC_THREADS) >> 5;
+    const uint64_t per = (n_units + nwarps - 1) / nwarps;
+    const uint64_t u0 = warp * per, u1 = u0 + per < n_units ? u0 + per : n_units;
+    if (u0 >= u1) return;
     const uint32_t *rep = sm.rep + lane;
-    uint32_t acc = 0;
+    const uint32_t *gap = sm.gap + lane;
+    uint32_t c0 = 0, c1 = 0;
 
-    for (uint64_t u = warp; u < n_units; u += nwarps) {
-        // virtual byte position of this lane's chunk (front-padded by z zeros)
+    for (uint64_t u = u0; u < u1; ++u) {
+        c0 = mul_nib_rep(c0, gap);
+        c1 = mul_nib_rep(c1, gap);
+        // virtual byte position of this lane's piece (front-padded by z zeros)
         const int64_t vpos = (int64_t)(u * UNIT + (uint64_t)lane * LANE_BYTES) - (int64_t)z;
-        uint32_t c = 0;
         if (vec && vpos >= 0) {
             const uint4 *p = reinterpret_cast<const uint4 *>(data + vpos);
-            uint4 q[4];
+            constexpr int NV = LANE_BYTES / 16, HW = LANE_BYTES / 8;  // vectors, words per chain
+            uint4 q[NV];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) q[k] = ld_nc_v4(p + k);
+            for (int k = 0; k < NV; ++k) q[k] = ld_nc_v4(p + k);
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(q);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint32_t wv[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        c = rep[((c ^ (wv[j] >> (8 * b))) & 0xFFu) << 5] ^ (c >> 8);
-                }
+            for (int j = 0; j < HW; ++j) {
+                c0 = crc_word(rep, c0, w[j]);
+                c1 = crc_word(rep, c1, w[HW + j]);
             }
         } else {
             for (int k = 0; k < LANE_BYTES; ++k) {
                 const int64_t p = vpos + k;
                 const uint32_t byte = (p >= 0 && (uint64_t)p < n) ? data[p] : 0u;
-                c = rep[((c ^ byte) & 0xFFu) << 5] ^ (c >> 8);
+                if (k < LANE_BYTES / 2)
+                    c0 = rep[((c0 ^ byte) & 0xFFu) << 5] ^ (c0 >> 8);
+                else
+                    c1 = rep[((c1 ^ byte) & 0xFFu) << 5] ^ (c1 >> 8);
             }
-        }
-        // combine the 32 lane CRCs (each covers 64 B) in address order
-#pragma unroll
-        for (int k = 0; k < TREE_LEVELS; ++k) {
-            const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, c, 1 << k);
-            if (lane & (1 << k))
-                c = mul_nib(other, sm.tree + k * NT) ^ c;  // other is the left half
-            else
-                c = mul_nib(c, sm.tree + k * NT) ^ other;
-        }
-        // shift by the whole units that follow this one
-        uint64_t q = n_units - 1 - u;
-        if (lane == 0) {
-            int k = 0;
-            while (q) {
-                if (q & 1) c = mul_nib(c, sm.shift + k * NT);
-                q >>= 1;
-                ++k;
-            }
-            acc ^= c;
         }
     }
-    if (lane == 0 && acc) atomicXor(out, acc);
+    uint32_t c = mul_nib(c0, sm.half) ^ c1;  // raw(A||B) = x^(8|B|) raw(A) ^ raw(B)
+    // combine the 32 lanes (each covers 64 B of every unit) in address order
+#pragma unroll
+    for (int k = 0; k < TREE_LEVELS; ++k) {
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, c, 1 << k);
+        if (lane & (1 << k))
+            c = mul_nib(other, sm.tree + k * NT) ^ c;  // other is the left half
+        else
+            c = mul_nib(c, sm.tree + k * NT) ^ other;
+    }
+    if (lane == 0) {
+        uint64_t q = n_units - u1;  // shift by the units after this warp's run
+        int k = 0;
+        while (q) {
+            if (q & 1) c = mul_nib(c, sm.shift + k * NT);
+            q >>= 1;
+            ++k;
+        }
+        if (c) atomicXor(out, c);
+    }
 }
 
 }  // namespace
@@ -198,7 +247,7 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
     }
     const uint64_t warps_per_block = CRC_THREADS / 32;
     uint64_t blocks = (n_units + warps_per_block - 1) / warps_per_block;
-    const uint64_t cap = (uint64_t)sm_count() * 4;  // persistent: ~4 CTAs per SM
+    const uint64_t cap = (uint64_t)sm_count();  // persistent: one CTA per SM
     if (blocks > cap) blocks = cap;
     crc_kernel<<<(unsigned)blocks, CRC_THREADS, smem, s>>>(static_cast<const uint8_t *>(data), n, z,
                                                            n_units, vec, d_out);
