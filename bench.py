@@ -427,6 +427,12 @@ def run_ours(args):
 
 
 def run_e2e(args, ctx, dev, rank, world):
+    """e2e through the public API.  N = 1: TensorProducer over a pinned-host
+    store (copy-engine ingest) and 4 SharedLoader processes.  N > 1: rank 0
+    runs ONE TensorProducer(devices=[every rank's GPU]) -- each GPU ingests
+    its 1/N rows of every batch over its own PCIe link and the collate kernel
+    stores them into every GPU's ring (fused all-gather) -- and every rank
+    runs 4 SharedLoader(device=its GPU) consumers."""
     import torch
 
     from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec, StoreSource,
@@ -434,36 +440,53 @@ def run_e2e(args, ctx, dev, rank, world):
 
     K, Wm = args.steps, args.warmup
     tmp = f"/tmp/tsb-bench-{os.getpid()}"
+    if world > 1:  # one endpoint pair for the whole job, created by rank 0
+        obj = [tmp]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        tmp = obj[0]
+        devs = [None] * world
+        torch.distributed.all_gather_object(devs, dev)
     os.makedirs(tmp, exist_ok=True)
     bcast, agg = f"unix:{tmp}/b.sock", f"unix:{tmp}/a.sock"
-    store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="pinned")
-    ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
-    loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
-    producer = TensorProducer(loader, bcast, agg, min_consumers=N_CONSUMERS, ring_slots=RING_SLOTS,
-                              heartbeat_timeout_s=60.0)
+    producer = None
+    if rank == 0:
+        store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="pinned")
+        ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
+        loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
+        producer = TensorProducer(loader, bcast, agg, min_consumers=N_CONSUMERS * world,
+                                  ring_slots=RING_SLOTS, heartbeat_timeout_s=60.0,
+                                  devices=devs if world > 1 else None)
+        producer._start()  # listeners up before any rank's consumers dial
+    if world > 1:
+        torch.distributed.barrier()
     q = ctx.Queue()
-    procs = [ctx.Process(target=api_consumer, args=(dev, bcast, agg, 1000 + k, Wm, K, q))
+    procs = [ctx.Process(target=api_consumer,
+                         args=(dev, bcast, agg, 1000 + 100 * rank + k, Wm, K, q))
              for k in range(N_CONSUMERS)]
     for p in procs:
         p.start()
     total = Wm + K
     t_start = time.monotonic()
     produced = 0
-    while produced < total:
-        for _ in producer:
-            produced += 1
-            if produced >= total:
-                break
-    producer.join(drain_timeout_s=60)
+    if producer is not None:
+        while produced < total:
+            for _ in producer:
+                produced += 1
+                if produced >= total:
+                    break
+        producer.join(drain_timeout_s=60)
     rates = {}
     for _ in procs:
-        msg = q.get(timeout=300)
+        msg = q.get(timeout=600)
         while msg[0] != "done":
-            msg = q.get(timeout=300)
+            msg = q.get(timeout=600)
         rates[msg[1]] = msg[2]
     for p in procs:
         p.join(60)
-    producer.close()
+    if world > 1:
+        torch.distributed.barrier()  # every consumer is done before the rings go
+    if producer is not None:
+        producer.close()
     wall = time.monotonic() - t_start
     value = sum(rates.values())
     if world > 1:
@@ -471,12 +494,17 @@ def run_e2e(args, ctx, dev, rank, world):
                          == "nccl" else "cpu")
         torch.distributed.all_reduce(t)
         value = float(t.item())
+    path = ("TensorProducer(CollateLoader(pinned-host StoreSource)) -> 4 SharedLoader processes "
+            "(CUDA IPC); each batch's rows cross PCIe by the copy engine; consumers .item() one "
+            "element per batch")
+    if world > 1:
+        path = (f"one TensorProducer(devices={world} GPUs, sharded ingest: each GPU reads its "
+                "1/N rows of every batch from pinned host memory, fused all-gather into every "
+                "ring) -> 4 SharedLoader(device=g) processes per GPU; consumers .item() per batch")
     return {"value": round(value, 1), "unit": "samples/s",
             "h2d_bytes_per_step": B * SAMPLE_BYTES,
-            "d2h_bytes_per_step": 4 * N_CONSUMERS,
-            "path": "TensorProducer(CollateLoader(pinned-host StoreSource)) -> 4 SharedLoader "
-                    "processes (CUDA IPC); kernel reads samples over PCIe; consumers .item() "
-                    "one element per batch",
+            "d2h_bytes_per_step": 4 * N_CONSUMERS * world,
+            "path": path,
             "per_consumer": {str(k): round(v, 1) for k, v in rates.items()},
             "wall_s": round(wall, 2), "batches_produced": produced}
 
