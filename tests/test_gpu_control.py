@@ -1,0 +1,181 @@
+"""Control-plane parity on the device ring: the
+reference's integration tests (pkg/tests/test_producer_consumer.py:231-414)
+re-run against the B200 facade -- backpressure / drift bound, eviction that
+unblocks survivors (cursor sentinel), rubberband replay from retained ring
+slots, late join waiting for the next epoch, and exactly-once in-order
+delivery."""
+
+import threading
+import time
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2409_18749_b200 import SharedLoader, TensorProducer  # noqa: E402
+
+
+class SeqLoader:
+    """(input, target) batches whose target carries the global batch number."""
+
+    def __init__(self, n, batch=4, delay_s=0.0):
+        self.n, self.batch, self.delay_s = n, batch, delay_s  # delay_s: simulated prep cost
+        self.epoch = 0
+
+    def __len__(self):
+        return self.n
+
+    def __iter__(self):
+        e = self.epoch
+        self.epoch += 1
+        for i in range(self.n):
+            if self.delay_s:
+                time.sleep(self.delay_s)
+            inp = np.full((self.batch, 16), e * 1000 + i, dtype=np.float32)
+            yield inp, np.array([e, i] + [0] * (self.batch - 2), dtype=np.int64)
+
+
+def expected(epochs, n, start_epoch=0):
+    return [(e, i) for e in range(start_epoch, epochs) for i in range(n)]
+
+
+@pytest.fixture
+def endpoints(tmp_path):
+    return f"unix:{tmp_path}/cb.sock", f"unix:{tmp_path}/ca.sock"
+
+
+def run_producer(loader, endpoints, epochs, **kw):
+    b, a = endpoints
+    producer = TensorProducer(loader, broadcast=b, aggregate=a, **kw)
+
+    def run():
+        for _ in range(epochs):
+            for _ in producer:
+                pass
+        producer.join(20)
+
+    t = threading.Thread(target=run, daemon=True)
+    t.start()
+    return producer, t
+
+
+def consume(endpoints, cid, epochs, out, delay_s=0.0, stop_after=None, **kw):
+    loader = SharedLoader(*endpoints, consumer_id=cid, **kw)
+    out["loader"] = loader
+    seq = out.setdefault("seq", [])
+    with torch.cuda.stream(torch.cuda.Stream()):
+        for _ in range(epochs):
+            for inp, tgt in loader:
+                t = tgt.cpu().numpy()
+                v = float(inp[0, 0].item())
+                assert v == t[0] * 1000 + t[1]  # input paired with its own target
+                seq.append((int(t[0]), int(t[1])))
+                if delay_s:
+                    time.sleep(delay_s)
+                if stop_after is not None and len(seq) >= stop_after:
+                    return  # stalled: stops fetching (holds its slot) ...
+            if loader.finished:
+                break
+    loader.close()
+
+
+def test_slow_consumer_backpressure(endpoints):
+    """Drift bound (criterion 4): the producer runs at most ring_slots batches
+    ahead of the slowest consumer's releases."""
+    producer, pt = run_producer(SeqLoader(12), endpoints, 1, buffer_depth=2, ring_slots=4)
+    out = {}
+    w = threading.Thread(target=consume, args=(endpoints, 1, 1, out), kwargs={"delay_s": 0.05})
+    w.start()
+    time.sleep(0.3)
+    announced, fetched = producer.stats["announced"], len(out.get("seq", []))
+    assert announced <= fetched + 4
+    w.join(30)
+    pt.join(30)
+    assert out["seq"] == expected(1, 12)
+    producer.close()
+
+
+def test_exactly_once_in_order_three_consumers_two_epochs(endpoints):
+    producer, pt = run_producer(SeqLoader(20), endpoints, 2, min_consumers=3, ring_slots=4)
+    outs = [{} for _ in range(3)]
+    ts = [threading.Thread(target=consume, args=(endpoints, 10 + k, 2, outs[k]))
+          for k in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(60)
+    pt.join(30)
+    for o in outs:
+        assert o["seq"] == expected(2, 20)
+    assert producer.stats["announced"] == 40
+    producer.close()
+
+
+def test_eviction_unblocks_survivors(endpoints):
+    """Criterion 7: a consumer that stops fetching and heartbeating is evicted
+    after the timeout; its cursor becomes the sentinel, so the device ring
+    stops waiting for it and the survivor gets every batch."""
+    producer, pt = run_producer(SeqLoader(40), endpoints, 1, min_consumers=2, ring_slots=4,
+                                heartbeat_timeout_s=0.5)
+    victim, survivor = {}, {}
+
+    def run_victim():
+        consume(endpoints, 2, 1, victim, stop_after=3, heartbeat_interval_s=0.1)
+        victim["loader"].finished = True  # heartbeats stop too (process "hung")
+
+    vt = threading.Thread(target=run_victim)
+    st = threading.Thread(target=consume, args=(endpoints, 1, 1, survivor),
+                          kwargs={"heartbeat_interval_s": 0.1})
+    vt.start()
+    st.start()
+    vt.join(30)
+    st.join(60)
+    pt.join(60)
+    assert producer.stats["evictions"] == 1
+    assert survivor["seq"] == expected(1, 40)
+    assert victim["seq"] == expected(1, 40)[:3]
+    producer.close()
+
+
+def test_rubberband_join_gets_full_epoch(endpoints):
+    """A consumer joining inside the rubberband window (fraction of the epoch)
+    is admitted at once and replayed the retained slots from the ring: it
+    sees the full epoch, then keeps streaming the next one."""
+    producer, pt = run_producer(SeqLoader(16, delay_s=0.05), endpoints, 2,
+                                rubberband_fraction=0.25, ring_slots=8)
+    base, joiner = {}, {}
+    bt = threading.Thread(target=consume, args=(endpoints, 1, 2, base), kwargs={"delay_s": 0.02})
+    bt.start()
+    deadline = time.time() + 30
+    while producer.stats["announced"] < 2 and time.time() < deadline:
+        time.sleep(0.002)
+    assert producer.stats["announced"] < 4  # still inside the window of ceil(0.25*16) = 4
+    consume(endpoints, 2, 2, joiner)
+    bt.join(60)
+    pt.join(60)
+    assert base["seq"] == expected(2, 16)
+    assert joiner["seq"] == expected(2, 16)
+    assert joiner["loader"].welcome.admitted == 1  # ADMIT_RUBBERBAND
+    producer.close()
+
+
+def test_late_join_waits_for_next_epoch(endpoints):
+    producer, pt = run_producer(SeqLoader(20), endpoints, 2, rubberband_fraction=0.05,
+                                ring_slots=4)
+    base, joiner = {}, {}
+    bt = threading.Thread(target=consume, args=(endpoints, 1, 2, base), kwargs={"delay_s": 0.01})
+    bt.start()
+    deadline = time.time() + 30
+    while producer.stats["announced"] < 6 and time.time() < deadline:
+        time.sleep(0.002)
+    consume(endpoints, 2, 1, joiner)
+    bt.join(60)
+    pt.join(60)
+    assert base["seq"] == expected(2, 20)
+    assert joiner["seq"] == expected(2, 20, start_epoch=1)
+    assert joiner["loader"].welcome.admitted == 0  # ADMIT_WAIT
+    producer.close()
