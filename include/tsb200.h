@@ -282,6 +282,47 @@ int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_
                       int shard, int n_shards, uint64_t seq0, int64_t batch0, int n,
                       const int *live, const int *n_live, void *stream);
 
+/* ---- control-plane codec (host; wire.py:1-11,77-156,199-341) ------------
+ * The reference's 9-message frame format, byte-identical, plus DType 5 (bf16)
+ * and Join v2 (device, batch_size).  One struct carries every kind; unused
+ * fields are ignored on encode and zero (device = -1) on decode. */
+#define TSB_MSG_JOIN 1
+#define TSB_MSG_WELCOME 2
+#define TSB_MSG_ANNOUNCE 3
+#define TSB_MSG_ACK 4
+#define TSB_MSG_HEARTBEAT 5
+#define TSB_MSG_EPOCH_START 6
+#define TSB_MSG_EPOCH_END 7
+#define TSB_MSG_BYE 8
+#define TSB_MSG_SHUTDOWN 9
+typedef struct {
+    uint8_t kind;
+    uint64_t consumer_id;
+    uint16_t protocol_version;
+    int16_t device;              /* Join v2 */
+    uint32_t batch_size;         /* Join v2 */
+    uint32_t epoch;
+    uint64_t epoch_len;
+    uint64_t next_batch_index;
+    uint16_t buffer_depth;
+    uint8_t admitted;
+    uint64_t batch_index;
+    uint64_t monotonic_millis;
+    uint16_t name_len;
+    char segment_name[256];
+    uint64_t byte_len;
+    uint8_t dtype;
+    uint8_t ndim;
+    uint64_t shape[8];
+    uint32_t checksum;
+} tsb_msg;
+/* Encode one frame into out[0..cap); *len = frame bytes.  TSB_ERR_INVALID on
+ * a wire-invariant violation (EncodeError, wire.py:33-38). */
+int tsb_wire_encode(const tsb_msg *m, uint8_t *out, size_t cap, size_t *len);
+/* Decode exactly one complete frame; TSB_ERR_CORRUPT with *err_off = the
+ * failing byte offset (DecodeError(offset, cause), wire.py:41-46). */
+int tsb_wire_decode(const uint8_t *frame, size_t len, tsb_msg *m, size_t *err_off);
+
 #ifdef __cplusplus
 }
 #endif

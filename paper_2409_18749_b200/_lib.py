@@ -126,11 +126,28 @@ class ProduceArgs(ctypes.Structure):
 GATE_DEVICE, GATE_HOST = 0, 1
 
 
+class Msg(ctypes.Structure):
+    """Mirror of tsb_msg (include/tsb200.h)."""
+    _fields_ = [
+        ("kind", ctypes.c_uint8), ("consumer_id", ctypes.c_uint64),
+        ("protocol_version", ctypes.c_uint16), ("device", ctypes.c_int16),
+        ("batch_size", ctypes.c_uint32), ("epoch", ctypes.c_uint32),
+        ("epoch_len", ctypes.c_uint64), ("next_batch_index", ctypes.c_uint64),
+        ("buffer_depth", ctypes.c_uint16), ("admitted", ctypes.c_uint8),
+        ("batch_index", ctypes.c_uint64), ("monotonic_millis", ctypes.c_uint64),
+        ("name_len", ctypes.c_uint16), ("segment_name", ctypes.c_char * 256),
+        ("byte_len", ctypes.c_uint64), ("dtype", ctypes.c_uint8), ("ndim", ctypes.c_uint8),
+        ("shape", ctypes.c_uint64 * 8), ("checksum", ctypes.c_uint32),
+    ]
+
+
 SRC_AUGMENT, SRC_GATHER, SRC_SYNTHETIC = 0, 1, 2
 
 SIGNATURES["tsb_produce_range"] = (i32, [vp, ctypes.POINTER(ProduceArgs), u64, i64, i32,
                                          ctypes.POINTER(i32), i32, pp, vp])
 SIGNATURES["tsb_consume_range"] = (i32, [vp, i32, u64, i32, pp, vp])
+SIGNATURES["tsb_wire_encode"] = (i32, [ctypes.POINTER(Msg), vp, sz, ctypes.POINTER(sz)])
+SIGNATURES["tsb_wire_decode"] = (i32, [vp, sz, ctypes.POINTER(Msg), ctypes.POINTER(sz)])
 SIGNATURES["tsb_produce_group"] = (i32, [pp, i32, i32, ctypes.POINTER(ProduceArgs), i32, i32, u64,
                                          i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp])
 
