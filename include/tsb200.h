@@ -223,6 +223,25 @@ int tsb_ingest_destroy(tsb_ingest *g);
 /* 1 if the batched-copy driver API is in use, 0 if per-sample copies. */
 int tsb_ingest_batch_api(tsb_ingest *g, int *used);
 
+/* JPEG sample source (NEW; the paper's decode step, in
+ * front of the reference's DirectorySource, pipeline.py:45-54,190-210):
+ * nvJPEG batched decode (NVJPG hardware engines when available) of a store
+ * of encoded files held in host memory, to interleaved RGB u8 in HBM.
+ * libnvjpeg is opened at run time (TSB_ERR_UNSUPPORTED when absent). */
+typedef struct tsb_jpeg tsb_jpeg;
+int tsb_jpeg_available(int *ok);
+/* backend: 0 = hardware (NVJPG) if present, else GPU-assisted Huffman, else
+ * default; 1 = default (hybrid); 2 = hardware only */
+int tsb_jpeg_create(int dev, int64_t max_batch, int h, int w, int backend, tsb_jpeg **out);
+int tsb_jpeg_backend(tsb_jpeg *j, int *backend);  /* 1 = default, 2 = hardware, 3 = GPU Huffman */
+/* The store: files[i] / lengths[i] = encoded sample i (host memory the
+ * caller keeps alive); every file must decode to h x w. */
+int tsb_jpeg_attach_store(tsb_jpeg *j, const uint8_t *const *files, const size_t *lengths,
+                          int64_t n);
+/* Decode files h_indices[0..b) into out (b x h*w*3 u8 RGB, device) on stream. */
+int tsb_jpeg_decode(tsb_jpeg *j, const int64_t *h_indices, int64_t b, void *out, void *stream);
+int tsb_jpeg_destroy(tsb_jpeg *j);
+
 typedef struct {
     int mode;                /* TSB_SRC_*                                     */
     const void *src;         /* store base: HBM or pinned host (NULL synthetic) */
@@ -249,6 +268,9 @@ typedef struct {
                                 engine into HBM staging first (augment), or
                                 straight into the slot (gather) */
     const int64_t *h_order;  /* host copy of d_order (row addresses for ingest) */
+    tsb_jpeg *jpeg;          /* non-null (with h_order): samples are JPEG files,
+                                decoded per batch into HBM staging (augment) or
+                                straight into the slot (gather); src unused */
 } tsb_produce_args;
 #define TSB_GATE_DEVICE 0
 #define TSB_GATE_HOST 1

@@ -27,7 +27,8 @@ def __getattr__(name):
         from .ring import DeviceRing
 
         return DeviceRing
-    if name in ("CollateLoader", "StoreSource", "SyntheticSource", "DatasetSpec", "AugmentSpec"):
+    if name in ("CollateLoader", "StoreSource", "SyntheticSource", "DatasetSpec", "AugmentSpec",
+                "JpegSource"):
         from . import collate
 
         return getattr(collate, name)

@@ -107,6 +107,12 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_ingest_create": (i32, [i32, i64, i64, i32, pp]),
     "tsb_ingest_destroy": (i32, [vp]),
     "tsb_ingest_batch_api": (i32, [vp, ctypes.POINTER(i32)]),
+    "tsb_jpeg_available": (i32, [ctypes.POINTER(i32)]),
+    "tsb_jpeg_create": (i32, [i32, i64, i32, i32, i32, pp]),
+    "tsb_jpeg_backend": (i32, [vp, ctypes.POINTER(i32)]),
+    "tsb_jpeg_attach_store": (i32, [vp, pp, ctypes.POINTER(sz), i64]),
+    "tsb_jpeg_decode": (i32, [vp, vp, i64, vp, vp]),
+    "tsb_jpeg_destroy": (i32, [vp]),
 }
 
 class ProduceArgs(ctypes.Structure):
@@ -119,7 +125,7 @@ class ProduceArgs(ctypes.Structure):
         ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
         ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
         ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int), ("gate", ctypes.c_int),
-        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p),
+        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p), ("jpeg", ctypes.c_void_p),
     ]
 
 

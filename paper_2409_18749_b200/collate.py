@@ -85,6 +85,97 @@ class StoreSource:
         return cls(host, sample_shape, dtype)
 
 
+class JpegSource:
+    """A store of JPEG files (one per sample, all decoding to the same h x w RGB)
+    held in pinned host memory, decoded per batch on the GPU by nvJPEG (B200
+    NVJPG engines when present) -- the paper's decode step
+    in front of the reference's DirectorySource (pipeline.py:45-54,190-210).
+    Samples are u8 HWC (h, w, 3) after decode."""
+
+    def __init__(self, files, height: int, width: int, backend: str = "auto"):
+        import torch
+
+        self.sample_shape = (int(height), int(width), 3)
+        self.dtype = DType.U8
+        self.num_samples = len(files)
+        if not self.num_samples:
+            raise ValueError("empty JPEG store")
+        lens = np.array([len(f) for f in files], dtype=np.int64)
+        offs = np.zeros(len(files) + 1, dtype=np.int64)
+        np.cumsum(lens, out=offs[1:])
+        self.blob = torch.empty(int(offs[-1]), dtype=torch.uint8).pin_memory()
+        view = self.blob.numpy()
+        for i, f in enumerate(files):
+            view[offs[i]:offs[i + 1]] = np.frombuffer(f, dtype=np.uint8)
+        self.offsets, self.lengths = offs, lens
+        self.backend = {"auto": 0, "default": 1, "hardware": 2}[backend]
+        self._decoders = {}
+
+    @property
+    def sample_nbytes(self) -> int:
+        return int(np.prod(self.sample_shape))
+
+    @classmethod
+    def from_directory(cls, path: str, height: int, width: int, **kw):
+        """Files of a directory in sorted name order (write_directory_dataset order)."""
+        import os
+
+        names = sorted(n for n in os.listdir(path) if not n.startswith("."))
+        files = []
+        for n in names:
+            with open(os.path.join(path, n), "rb") as fh:
+                files.append(fh.read())
+        return cls(files, height, width, **kw)
+
+    def decoder(self, device: int, max_batch: int):
+        """tsb_jpeg handle for `device` with this store attached (cached)."""
+        key = (device, max_batch)
+        if key not in self._decoders:
+            self._decoders[key] = _JpegDecoder(self, device, max_batch)
+        return self._decoders[key]
+
+
+class _JpegDecoder:
+    def __init__(self, src: "JpegSource", device: int, max_batch: int):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = _lib
+        h, w, _ = src.sample_shape
+        hd = ctypes.c_void_p()
+        _lib.call("tsb_jpeg_create", device, max_batch, h, w, src.backend, ctypes.byref(hd))
+        self.handle = hd.value
+        base = src.blob.data_ptr()
+        n = src.num_samples
+        ptrs = (ctypes.c_void_p * n)(*[base + int(o) for o in src.offsets[:-1]])
+        lens = (ctypes.c_size_t * n)(*[int(x) for x in src.lengths])
+        _lib.call("tsb_jpeg_attach_store", self.handle, ptrs, lens, n)
+        self._keep = (src, ptrs, lens)
+
+    @property
+    def backend(self) -> str:
+        import ctypes
+
+        v = ctypes.c_int(0)
+        self._lib.call("tsb_jpeg_backend", self.handle, ctypes.byref(v))
+        return {2: "hardware", 3: "gpu_hybrid"}.get(v.value, "default")
+
+    def decode(self, indices, out, stream=None) -> None:
+        """Decode store samples `indices` (host ints) into `out` (device u8)."""
+        idx = np.ascontiguousarray(indices, dtype=np.int64)
+        self._lib.call("tsb_jpeg_decode", self.handle, idx.ctypes.data, len(idx), dp.ptr(out),
+                       dp.current_stream(stream))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.load().tsb_jpeg_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 @dataclass(frozen=True)
 class DatasetSpec:
     source: object
@@ -101,7 +192,7 @@ class DatasetSpec:
         if isinstance(self.source, SyntheticSource) and self.source.sample_nbytes % 8:
             raise ValueError("synthetic sample size must be a multiple of 8 bytes "
                              f"(got {self.source.sample_nbytes})")
-        if isinstance(self.source, StoreSource) and \
+        if isinstance(self.source, (StoreSource, JpegSource)) and \
                 self.samples_per_epoch > self.source.num_samples:
             raise ValueError("samples_per_epoch exceeds the store")
 
@@ -162,7 +253,7 @@ class CollateLoader:
             if DType(src.dtype) != DType.U8 or len(src.sample_shape) != 3:
                 raise ValueError("augment needs uint8 HWC samples")
             if isinstance(src, SyntheticSource):
-                raise ValueError("augment reads from a StoreSource")
+                raise ValueError("augment reads from a StoreSource or a JpegSource")
             self._scale, self._bias = (dp.norm_consts(augment.mean, augment.std)
                                        if augment.normalize and augment.out_kind != dp.OUT_U8
                                        else (None, None))
@@ -235,7 +326,9 @@ class CollateLoader:
         b = d.batch_size
         didx = dorder[batch_index * b:(batch_index + 1) * b]
         src = d.source
-        if isinstance(src, SyntheticSource):
+        if isinstance(src, JpegSource):
+            self._produce_jpeg(src, out_ptr, epoch, batch_index, didx, stream)
+        elif isinstance(src, SyntheticSource):
             dp.fill_synthetic(out_ptr, didx, b, src.seed, epoch, src.sample_nbytes, stream)
         elif self.augment is None:
             dp.gather(src.samples, didx, b, src.sample_nbytes, out_ptr, stream)
@@ -247,6 +340,30 @@ class CollateLoader:
                                stream=stream)
         if self.with_target:
             dp.memcpy_async(out_ptr + self.input_nbytes, didx, 8 * b, stream)
+
+    def _produce_jpeg(self, src, out_ptr, epoch, batch_index, didx, stream) -> None:
+        """nvJPEG decode of the batch's files; augment from the decoded staging
+        (params keyed by the real sample indices, source rows = batch rows)."""
+        import torch
+
+        b = self.dataset.batch_size
+        dec = src.decoder(self.device, b)
+        host_idx = self.indices(epoch, batch_index)
+        if self.augment is None:
+            dec.decode(host_idx, out_ptr, stream)
+            return
+        if getattr(self, "_jpeg_stage", None) is None:
+            dev = f"cuda:{self.device}"
+            self._jpeg_stage = torch.empty(b * src.sample_nbytes, dtype=torch.uint8, device=dev)
+            self._jpeg_params = torch.empty(3 * b, dtype=torch.int32, device=dev)
+            self._jpeg_rows = torch.arange(b, dtype=torch.int64, device=dev)
+        a = self.augment
+        h, w, c = src.sample_shape
+        dec.decode(host_idx, self._jpeg_stage, stream)
+        dp.aug_params(a.seed, epoch, didx, b, a.pad, a.flip, self._jpeg_params, stream)
+        dp.collate_augment(self._jpeg_stage, self._jpeg_rows, b, h, w, c, a.pad, a.flip, a.seed,
+                           epoch, a.out_kind, out_ptr, scale=self._scale, bias=self._bias,
+                           d_params=self._jpeg_params, stream=stream)
 
     def produce_args(self, epoch: int, with_crc=None):
         """tsb_produce_args for the native range producer (ring.produce_range)."""
@@ -266,16 +383,21 @@ class CollateLoader:
             host, _ = self.order(epoch)
             a.ingest = self._ingest_handle()
             a.h_order = host.ctypes.data
+        if isinstance(src, JpegSource):
+            host, _ = self.order(epoch)
+            a.jpeg = src.decoder(self.device, d.batch_size).handle
+            a.h_order = host.ctypes.data
         for i in range(4):
             a.scale[i], a.bias[i] = 1.0, 0.0
+        samples = getattr(src, "samples", None)  # JpegSource: decoded per batch, no raw store
         if isinstance(src, SyntheticSource):
             a.mode, a.seed = _lib.SRC_SYNTHETIC, src.seed
         elif self.augment is None:
-            a.mode, a.src = _lib.SRC_GATHER, src.samples.data_ptr()
+            a.mode, a.src = _lib.SRC_GATHER, 0 if samples is None else samples.data_ptr()
         else:
             aug = self.augment
             h, w, c = src.sample_shape
-            a.mode, a.src = _lib.SRC_AUGMENT, src.samples.data_ptr()
+            a.mode, a.src = _lib.SRC_AUGMENT, 0 if samples is None else samples.data_ptr()
             a.h, a.w, a.c, a.pad, a.flip, a.out_kind = h, w, c, aug.pad, int(aug.flip), aug.out_kind
             a.seed = aug.seed
             if self._scale is not None:

@@ -188,6 +188,7 @@ void preload_crc32();
 void preload_fanout();
 void preload_ring();
 void preload_ingest();
+void preload_jpeg();
 }  // namespace tsb
 
 extern "C" int tsb_preload_kernels(void) {
@@ -198,5 +199,6 @@ extern "C" int tsb_preload_kernels(void) {
     tsb::preload_fanout();
     tsb::preload_ring();
     tsb::preload_ingest();
+    tsb::preload_jpeg();
     return TSB_OK;
 }

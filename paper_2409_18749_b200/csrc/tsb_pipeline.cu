@@ -32,6 +32,13 @@ int64_t *ingest_indices(tsb_ingest *g, int k);
 int32_t *ingest_params(tsb_ingest *g, int k);
 int64_t *ingest_identity(tsb_ingest *g);
 int64_t ingest_sample_bytes(tsb_ingest *g);
+int jpeg_decode(tsb_jpeg *j, const int64_t *h_idx, int64_t b, void *out, void *stream);
+int jpeg_upload_indices(tsb_jpeg *j, const int64_t *h_idx, int64_t b, void *stream);
+uint8_t *jpeg_staging(tsb_jpeg *j);
+int64_t *jpeg_indices(tsb_jpeg *j);
+int32_t *jpeg_params(tsb_jpeg *j);
+int64_t *jpeg_identity(tsb_jpeg *j);
+int64_t jpeg_sample_bytes(tsb_jpeg *j);
 }  // namespace tsb
 
 extern "C" {
@@ -59,7 +66,17 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     static const bool no_pdl = getenv("TSB_NO_PDL") && atoi(getenv("TSB_NO_PDL"));      // A/B knobs
     static const bool no_fused = getenv("TSB_NO_FUSED") && atoi(getenv("TSB_NO_FUSED"));
     bool prev_fused = false;
-    const bool staged = a->ingest && a->h_order && !ev;
+    const bool jpeg = a->jpeg && a->h_order;
+    if (jpeg) {
+        TSB_CHECK(a->mode == TSB_SRC_AUGMENT || a->mode == TSB_SRC_GATHER,
+                  "a JPEG source feeds the augment or gather modes");
+        TSB_CHECK(jpeg_sample_bytes(a->jpeg) == a->sample_bytes,
+                  "decoder geometry (%lld B) does not match the samples (%lld B)",
+                  (long long)jpeg_sample_bytes(a->jpeg), (long long)a->sample_bytes);
+        TSB_CHECK(!a->d_crc && !no_fused && ring_writers(r) == 1,
+                  "the JPEG source needs the fused single-writer path (no per-batch CRC)");
+    }
+    const bool staged = !jpeg && a->ingest && a->h_order && !ev;
     if (staged)
         TSB_CHECK(ingest_sample_bytes(a->ingest) == a->sample_bytes,
                   "ingest staging is for %lld-byte samples, not %lld",
@@ -100,6 +117,23 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                                      a->input_bytes)
                                        : nullptr;
                     const int pdl = prev_fused && host_gate && !ev && !no_pdl;
+                    if (jpeg) {  // nvJPEG decode into HBM staging, then collate it
+                        const int64_t *hb = a->h_order + bi * b;
+                        if ((rc = jpeg_upload_indices(a->jpeg, hb, b, stream))) return rc;
+                        if ((rc = jpeg_decode(a->jpeg, hb, b, jpeg_staging(a->jpeg), stream)))
+                            return rc;
+                        int32_t *params = jpeg_params(a->jpeg);
+                        if ((rc = tsb_aug_params(a->seed, a->epoch, jpeg_indices(a->jpeg), b,
+                                                 a->pad, a->flip, params, stream)))
+                            return rc;
+                        rc = collate_augment_publish(jpeg_staging(a->jpeg), jpeg_identity(a->jpeg),
+                                                     b, a->h, a->w, a->c, a->pad, a->flip, a->seed,
+                                                     a->epoch, a->scale, a->bias, a->out_kind, out,
+                                                     tgt, ready, q, counter, 0, stream, params,
+                                                     jpeg_indices(a->jpeg));
+                        published = true;
+                        break;
+                    }
                     if (staged) {  // copy-engine ingest into HBM staging, then collate it
                         int k = 0;
                         if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, nullptr,
@@ -131,6 +165,18 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                          nullptr, out, stream);
                 break;
             case TSB_SRC_GATHER:
+                if (jpeg) {  // decode straight into the slot (u8 HWC), then target + publish
+                    const int64_t *hb = a->h_order + bi * b;
+                    if ((rc = jpeg_upload_indices(a->jpeg, hb, b, stream))) return rc;
+                    if ((rc = jpeg_decode(a->jpeg, hb, b, out, stream))) return rc;
+                    if (a->with_target) {
+                        TSB_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(out) + a->input_bytes,
+                                                 jpeg_indices(a->jpeg), 8 * b,
+                                                 cudaMemcpyDeviceToDevice, s));
+                        staged_target = true;
+                    }
+                    break;
+                }
                 if (staged) {  // copy engine straight into the slot (no kernel)
                     int k = 0;
                     if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, out, stream,

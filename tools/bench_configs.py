@@ -191,6 +191,33 @@ def main():
                         "8 consumers (one GPU)", reference_cpu=REF["c5_llm_k8"])
         print(json.dumps(r), flush=True)
         del ld
+    if "jpeg" in which:
+        import io
+
+        import numpy as np
+        from PIL import Image
+
+        from paper_2409_18749_b200 import JpegSource
+
+        rng = np.random.default_rng(0)
+        yy, xx = np.mgrid[0:224, 0:224].astype(np.float32)
+        files = []
+        for i in range(1024):
+            f = rng.uniform(0.02, 0.2, 3)
+            img = np.stack([127 + 100 * np.sin(f[c] * xx + i) * np.cos(f[c] * yy)
+                            for c in range(3)], -1)
+            img = np.clip(img + rng.normal(0, 6, img.shape), 0, 255).astype(np.uint8)
+            b = io.BytesIO()
+            Image.fromarray(img).save(b, format="JPEG", quality=90)
+            files.append(b.getvalue())
+        src = JpegSource(files, 224, 224)
+        ld = CollateLoader(DatasetSpec(src, 1024, 256), AugmentSpec(out_dtype="bfloat16"))
+        r = device_run(ld, 4, min(K, 64), Wm)
+        r.update(config="JPEG store (1024 x 224x224 q90 4:2:0, ~%d KB/file) -> nvJPEG batched "
+                        "decode (%s) -> crop/flip/normalise bf16, B=256, 4 consumers"
+                        % (sum(map(len, files)) // len(files) // 1024,
+                           src.decoder(0, 256).backend))
+        print(json.dumps(r), flush=True)
     if "c4" in which:
         r = c4()
         r.update(config="C4 (one GPU): consumers with b=64/128/256/512 (2 each) on one producer "
