@@ -6,6 +6,7 @@
 // (no contraction -> no tensor cores): 128-bit coalesced accesses, source rows
 // staged through shared memory, grids of thousands of CTAs.
 #include <stdlib.h>
+#include <string.h>
 
 #include <utility>
 
@@ -163,6 +164,7 @@ struct CaGeom {
     int nstage;        // pipeline depth (shared-memory stages)
     int use_tma;
     int vec_ldg;       // 16B LDG staging allowed
+    int use_direct;    // collate_direct_kernel (TSB_CA_IMPL=direct A/B)
     int64_t plane;     // h*w
     int64_t sample_bytes;
 };
@@ -539,10 +541,146 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     publish_epilogue(ep, tid, CA_THREADS);
 }
 
+template <int OUT_KIND, int C, bool MULTI, bool FLIP, int... CHs>
+__device__ __forceinline__ void emit_window(const uint32_t *wv, const Norm &norm, const Dsts &dsts,
+                                            int64_t off, int64_t plane_bytes,
+                                            std::integer_sequence<int, CHs...>) {
+    (emit_channel<OUT_KIND, C, MULTI, FLIP, CHs>(wv, norm, dsts, off, plane_bytes), ...);
+}
+
+// ---------------------------------------------------------------------------
+// Direct collate/augment (A/B candidate, TSB_CA_IMPL=direct): no shared-memory
+// staging.  A flat grid-stride walk over the batch's output groups (sample,
+// row, P consecutive output pixels); each thread loads the group's source
+// window as predicated 32-bit words straight from HBM (L1-cached: neighbouring
+// groups share words), realigns with a funnel shift, and emits like the TMA
+// kernel.  Rows are whole 32-bit words (row_bytes % 4 == 0), so a word is
+// either inside the source row or entirely in the zero padding: out-of-range
+// words load as 0, which is exactly the crop's zero fill.  Per-sample crop /
+// flip params are derived by every CTA for the whole batch into shared memory.
+constexpr int DC_THREADS = 256;
+constexpr int DC_MAX_B = 1024;
+
+struct DcPar {
+    int oy, ox, fl, pad_;
+    int64_t src_off;
+};
+
+template <int OUT_KIND, int C, bool MULTI>
+__global__ void __launch_bounds__(DC_THREADS)
+    collate_direct_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
+                          CaGeom g, int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
+                          const int32_t *__restrict__ params, Dsts dsts, Epi ep) {
+    using T = OutTraits<OUT_KIND>;
+    constexpr int P = T::P;
+    constexpr int NB = P * C;
+    constexpr int NW = NB / 4 + 1;
+    __shared__ DcPar par[DC_MAX_B];
+    const int tid = threadIdx.x;
+    for (int s = tid; s < g.b; s += DC_THREADS) {
+        DcPar p;
+        if (params) {
+            p.oy = params[3 * s];
+            p.ox = params[3 * s + 1];
+            p.fl = params[3 * s + 2];
+        } else {
+            derive_aug(aug_mixed, epoch, idx[s], g.pad, flip_en, p.oy, p.ox, p.fl);
+        }
+        p.src_off = idx[s] * g.sample_bytes;
+        par[s] = p;
+    }
+    if (blockIdx.x == 0) write_targets(ep, idx, g.b, tid, DC_THREADS);
+    __syncthreads();
+    const int G = g.groups;                  // groups per output row
+    const int64_t HG = (int64_t)g.h * G;     // groups per sample
+    const int64_t total = (int64_t)g.b * HG;
+    const int row_words = g.row_bytes >> 2;
+    const int64_t plane_bytes = g.plane * T::ELEM;
+    const uint32_t stride = gridDim.x * DC_THREADS;
+    const uint32_t hg = (uint32_t)HG, gg = (uint32_t)G;  // launcher guarantees total < 2^31
+    for (uint32_t gi = blockIdx.x * DC_THREADS + tid; gi < (uint32_t)total; gi += stride) {
+        const int s = (int)(gi / hg);
+        const uint32_t r = gi - (uint32_t)s * hg;
+        const int y = (int)(r / gg);
+        const int x0 = (int)(r - (uint32_t)y * gg) * P;
+        const DcPar p = par[s];
+        const int sy = y + p.oy - g.pad;
+        const bool rowok = (unsigned)sy < (unsigned)g.h;
+        const int sx0 = (p.fl ? (g.w - x0 - P) : x0) + p.ox - g.pad;
+        const int a = sx0 * C;                 // window start, bytes from the row start
+        const int wa = a >> 2;                 // floor (arithmetic shift)
+        const int sh = (a & 3) * 8;
+        const uint32_t *row = reinterpret_cast<const uint32_t *>(
+            src + p.src_off + (int64_t)(rowok ? sy : 0) * g.row_bytes);
+        uint32_t raw[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const int wi = wa + i;
+            raw[i] = (rowok && (unsigned)wi < (unsigned)row_words) ? __ldg(row + wi) : 0u;
+        }
+        uint32_t wv[NW - 1];
+#pragma unroll
+        for (int i = 0; i < NW - 1; ++i) wv[i] = __funnelshift_r(raw[i], raw[i + 1], sh);
+        const int64_t off = ((int64_t)s * C * g.plane + (int64_t)y * g.w + x0) * T::ELEM;
+        if (!p.fl)
+            emit_window<OUT_KIND, C, MULTI, false>(wv, norm, dsts, off, plane_bytes,
+                                                   std::make_integer_sequence<int, C>{});
+        else
+            emit_window<OUT_KIND, C, MULTI, true>(wv, norm, dsts, off, plane_bytes,
+                                                  std::make_integer_sequence<int, C>{});
+    }
+    pdl_launch_dependents();
+    publish_epilogue(ep, tid, DC_THREADS);
+}
+
+template <int K, int C, bool MULTI>
+int launch_direct(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
+                  uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
+                  cudaStream_t s, const Epi &ep) {
+    auto kern = collate_direct_kernel<K, C, MULTI>;
+    static int occ_cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) dev = 63;
+    if (!occ_cache[dev]) {
+        int occ = 0;
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, DC_THREADS, 0));
+        occ_cache[dev] = occ > 0 ? occ : 1;
+    }
+    const int64_t groups = (int64_t)g.b * g.h * g.groups;
+    const int64_t need = (groups + DC_THREADS - 1) / DC_THREADS;
+    const int64_t cap = (int64_t)sm_count() * occ_cache[dev];
+    const int grid = (int)(need < cap ? need : cap);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(DC_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ep.pdl ? 1 : 0;
+    TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, src, idx, g, flip, aug_mixed, epoch, norm, params,
+                                dsts, ep));
+    return TSB_OK;
+}
+
+int direct_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TSB_CA_IMPL");
+        v = (e && strcmp(e, "direct") == 0) ? 1 : 0;
+    }
+    return v;
+}
+
 template <int K, int C, bool MULTI>
 int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
               uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
               size_t smem, cudaStream_t s, const Epi &ep) {
+    if (g.use_direct)
+        return launch_direct<K, C, MULTI>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
+                                          s, ep);
     auto kern = collate_augment_kernel<K, C, MULTI>;
     static int occ_cache[64] = {0};
     static size_t smem_cache[64] = {0};
@@ -661,6 +799,9 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     g.use_tma = aligned_rows && is_device_memory(src);
     if (const char *e = getenv("TSB_CA_NOTMA")) g.use_tma = g.use_tma && !atoi(e);
     g.vec_ldg = aligned_rows && (g.io % 4 == 0);
+    g.use_direct = direct_enabled() && is_device_memory(src) && (g.row_bytes % 4 == 0) &&
+                   (g.sample_bytes % 4 == 0) && (((uintptr_t)src & 3) == 0) && b <= DC_MAX_B &&
+                   b * (int64_t)h * (w / vec) < (1ll << 31);
     // rows per item (measured on B200, B=256 224x224x3): enough output per item to
     // amortise the per-item pipeline handoff -- f32 R=4 (10.7 KB out), bf16/u8 R=16.
     // (profiles/r1/sweep_collate.txt: f32 R=4 x3 stages 37.2 us, bf16 R=16 x2 22.6 us,
