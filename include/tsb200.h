@@ -268,6 +268,9 @@ typedef struct {
                                 engine into HBM staging first (augment), or
                                 straight into the slot (gather) */
     const int64_t *h_order;  /* host copy of d_order (row addresses for ingest) */
+    int chain;               /* 1: the previous operation on `stream` was a fused
+                                produce kernel (so the call's first batch may chain
+                                with programmatic dependent launch too) */
     tsb_jpeg *jpeg;          /* non-null (with h_order): samples are JPEG files,
                                 decoded per batch into HBM staging (augment) or
                                 straight into the slot (gather); src unused */

@@ -125,7 +125,8 @@ class ProduceArgs(ctypes.Structure):
         ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
         ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
         ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int), ("gate", ctypes.c_int),
-        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p), ("jpeg", ctypes.c_void_p),
+        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p), ("chain", ctypes.c_int),
+        ("jpeg", ctypes.c_void_p),
     ]
 
 

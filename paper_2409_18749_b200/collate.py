@@ -366,7 +366,18 @@ class CollateLoader:
                            d_params=self._jpeg_params, stream=stream)
 
     def produce_args(self, epoch: int, with_crc=None):
-        """tsb_produce_args for the native range producer (ring.produce_range)."""
+        """tsb_produce_args for the native range producer (ring.produce_range).
+        Cached per epoch: callers that edit per-call fields take a copy
+        (``_lib.ProduceArgs.from_buffer_copy``)."""
+        key = (epoch, None if with_crc is None else with_crc.data_ptr())
+        cached = getattr(self, "_args_cache", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        a = self._build_args(epoch, with_crc)
+        self._args_cache = (key, a)
+        return a
+
+    def _build_args(self, epoch: int, with_crc=None):
         from . import _lib
 
         _, dorder = self.order(epoch)

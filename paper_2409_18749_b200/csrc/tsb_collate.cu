@@ -813,7 +813,7 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     if (const char *e = getenv("TSB_CA_R")) R = atoi(e);          // tuning knobs
     if (const char *e = getenv("TSB_CA_STAGES")) nstage = atoi(e);
     TSB_CHECK(R >= 1 && R <= 64 && (R & (R - 1)) == 0, "rows per item must be a power of 2 <= 64");
-    TSB_CHECK(nstage >= 2 && nstage <= MAX_STAGES, "stages must be 2..%d", MAX_STAGES);
+    TSB_CHECK(nstage >= 1 && nstage <= MAX_STAGES, "stages must be 1..%d", MAX_STAGES);
     if (R > h) R = 1;
     TSB_CHECK(R * g.groups <= MAX_SLOTS * CA_THREADS, "image width %d too large", w);
     while (nstage > 2 && (size_t)(nstage * R + 1) * g.rs + 2048 > 64 * 1024) --nstage;

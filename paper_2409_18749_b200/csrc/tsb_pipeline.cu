@@ -65,7 +65,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     const bool host_gate = a->gate == TSB_GATE_HOST;
     static const bool no_pdl = getenv("TSB_NO_PDL") && atoi(getenv("TSB_NO_PDL"));      // A/B knobs
     static const bool no_fused = getenv("TSB_NO_FUSED") && atoi(getenv("TSB_NO_FUSED"));
-    bool prev_fused = false;
+    bool prev_fused = a->chain != 0;
     const bool jpeg = a->jpeg && a->h_order;
     if (jpeg) {
         TSB_CHECK(a->mode == TSB_SRC_AUGMENT || a->mode == TSB_SRC_GATHER,

@@ -51,6 +51,7 @@ from __future__ import annotations
 import os
 import threading
 import time
+from collections import deque
 
 import numpy as np
 
@@ -142,6 +143,13 @@ class TensorProducer:
         self.ring_id = (os.getpid() << 20) ^ (id(self) & 0xFFFFF)
         self.stats = {"announced": 0, "acks": 0, "evictions": 0}
         self.drops: list[tuple[int, str, float]] = []  # (consumer_id, reason, time) event log
+        self._chain_ok = False  # PDL across produce calls (previous op = our fused kernel)
+        # wire Acks are queued by the reader threads without taking the lock and
+        # folded into the ledger in bulk by the producer (_drain_acks): one lock
+        # round and one drift sample per batch instead of per ack
+        self._ack_q: deque = deque()
+        self._hdr_key = None
+        self._hdr_reserved = b""
 
     # -- ring -------------------------------------------------------------
     def _batch_nbytes_hint(self) -> int | None:
@@ -316,43 +324,61 @@ class TensorProducer:
 
     def _handle(self, conn: Conn, msg, cid):
         now = time.monotonic()
+        if isinstance(msg, Ack):
+            self._ack_q.append((msg, now))  # deque.append is atomic: no lock on the hot path
+            return cid
         with self._lock:
             if isinstance(msg, Join):
                 return self._handle_join(conn, msg, now)
-            if isinstance(msg, Ack):
-                rec = self._consumers.get(msg.consumer_id)
-                if rec is None or not rec.admitted:
-                    return cid
-                rec.last_heartbeat = now
-                L = max(1, len(self._loader))
-                if rec.batch_size and rec.batch_size != self._per_slot:
-                    # heterogeneous consumer: its batch j fully covers the producer
-                    # batches before (j+1)*b // B; its last batch covers the epoch
-                    if rec.ack_epoch != msg.epoch:
-                        rec.ack_epoch, rec.ack_k = msg.epoch, 0
-                    lc = rebatch_epoch_len(self._samples, L, self._per_slot, rec.batch_size)
-                    upto = L if msg.batch_index >= lc - 1 else min(
-                        L, (msg.batch_index + 1) * rec.batch_size // self._per_slot)
-                    for k in range(rec.ack_k, upto):
-                        self._ledger.ack(msg.consumer_id, seq_of(msg.epoch, k, L))
-                    rec.ack_k = max(rec.ack_k, upto)
-                    if upto:
-                        rec.ack_seq = max(rec.ack_seq, seq_of(msg.epoch, upto - 1, L))
-                else:
-                    seq = seq_of(msg.epoch, msg.batch_index, L)
-                    self._ledger.ack(msg.consumer_id, seq)
-                    rec.ack_seq = max(rec.ack_seq, seq)
-                self.stats["acks"] += 1
-                self._ledger.sample_drift(now, self._consumers.values())
-                self._lock.notify_all()
-            elif isinstance(msg, Heartbeat):
+            if isinstance(msg, Heartbeat):
                 rec = self._consumers.get(msg.consumer_id)
                 if rec is not None:
                     rec.last_heartbeat = now
             elif isinstance(msg, Bye):
+                self._drain_acks()
                 if msg.consumer_id in self._consumers:
                     self._drop(msg.consumer_id, "bye")
         return cid
+
+    def _drain_acks(self) -> None:
+        """Fold queued wire Acks into the ledger (caller holds the lock)."""
+        q = self._ack_q
+        if not q:
+            return
+        L = max(1, len(self._loader))
+        n, last = 0, None
+        while q:
+            try:
+                msg, now = q.popleft()
+            except IndexError:
+                break
+            last = now
+            rec = self._consumers.get(msg.consumer_id)
+            if rec is None or not rec.admitted:
+                continue
+            rec.last_heartbeat = max(rec.last_heartbeat, now)
+            n += 1
+            if rec.batch_size and rec.batch_size != self._per_slot:
+                # heterogeneous consumer: its batch j fully covers the producer
+                # batches before (j+1)*b // B; its last batch covers the epoch
+                if rec.ack_epoch != msg.epoch:
+                    rec.ack_epoch, rec.ack_k = msg.epoch, 0
+                lc = rebatch_epoch_len(self._samples, L, self._per_slot, rec.batch_size)
+                upto = L if msg.batch_index >= lc - 1 else min(
+                    L, (msg.batch_index + 1) * rec.batch_size // self._per_slot)
+                for k in range(rec.ack_k, upto):
+                    self._ledger.ack(msg.consumer_id, seq_of(msg.epoch, k, L))
+                rec.ack_k = max(rec.ack_k, upto)
+                if upto:
+                    rec.ack_seq = max(rec.ack_seq, seq_of(msg.epoch, upto - 1, L))
+            else:
+                seq = seq_of(msg.epoch, msg.batch_index, L)
+                self._ledger.ack(msg.consumer_id, seq)
+                rec.ack_seq = max(rec.ack_seq, seq)
+        self.stats["acks"] += n
+        if n:
+            self._ledger.sample_drift(last, self._consumers.values())
+            self._lock.notify_all()
 
     def _handle_join(self, conn: Conn, msg: Join, now: float):
         if msg.protocol_version not in SUPPORTED_VERSIONS or msg.consumer_id == MONITOR_ID:
@@ -440,6 +466,7 @@ class TensorProducer:
             time.sleep(self._poll)
             now = time.monotonic()
             with self._lock:
+                self._drain_acks()
                 for cid in [c for c, r in self._consumers.items()
                             if now - r.last_heartbeat > self._hb_timeout]:
                     self._drop(cid, "timeout")
@@ -572,12 +599,15 @@ class TensorProducer:
         elif self._device_loader and host_gated and not self._checksum:
             a = self._loader.produce_args(self._epoch)  # fused collate + target + publish
             a.gate = GATE_HOST
+            a.chain = int(self._chain_ok)  # the stream's previous op was our fused kernel
             with torch.cuda.device(self.device):
                 produce_range(ring, a, q, index, 1, [], stream=stream)
+            self._chain_ok = True
         else:
             if not host_gated and q > ring.slots:
                 # bound host run-ahead: batch q-S (same slot) must have been published
                 self._events[slot].synchronize()
+            self._chain_ok = False
             for k, d in enumerate(self._devices):
                 r, st = self._rings[k], self._streams[k]
                 with torch.cuda.device(d), torch.cuda.stream(st):
@@ -603,13 +633,17 @@ class TensorProducer:
         if self._checksum:
             self._events[slot].synchronize()
             crc = int(self._crc_host[slot]) & 0xFFFFFFFF
-        reserved = sg.pack_pair_reserved(int(in_dt), len(in_shape), int(tg_dt), len(tg_shape),
-                                         in_bytes)
+        hkey = (int(in_dt), in_shape, int(tg_dt), tg_shape, in_bytes, nbytes)
+        if self._hdr_key != hkey:  # the pair layout is fixed for a loader: pack it once
+            self._hdr_key = hkey
+            self._hdr_reserved = sg.pack_pair_reserved(int(in_dt), len(in_shape), int(tg_dt),
+                                                       len(tg_shape), in_bytes)
         header = sg.pack_header(self._epoch, index, DType.U8, (nbytes,), nbytes, crc,
-                                reserved=reserved, extra_slots=(*in_shape, *tg_shape))
+                                reserved=self._hdr_reserved, extra_slots=(*in_shape, *tg_shape))
         anns = {k: Announce(self._epoch, index, sg.slot_name(self._ring_ids[k], slot, header),
                             nbytes, DType.U8, (nbytes,), crc) for k in self._rings}
         with self._lock:
+            self._drain_acks()
             self._ledger.add(q, [r.consumer_id for r in self._admitted()])
             self._send_announces(anns)
             self._announced_in_epoch = index + 1
@@ -638,7 +672,10 @@ class TensorProducer:
         if need <= 0:
             return
         for k, ring in self._rings.items():
-            while not ring.host_gate(live_by_ring[k], need, timeout_s=0.1):
+            live = live_by_ring[k]
+            if ring.released(live, need):  # the common case: no wait, no native call
+                continue
+            while not ring.host_gate(live, need, timeout_s=0.1):
                 if self._closed:
                     raise ProducerClosed("producer closed while waiting for consumers")
 
@@ -656,7 +693,9 @@ class TensorProducer:
         for g, k in enumerate(writers):
             d = self._devices[k]
             with torch.cuda.device(d):
-                a = self._loader.produce_args(self._epoch)
+                from ._lib import ProduceArgs
+
+                a = ProduceArgs.from_buffer_copy(self._loader.produce_args(self._epoch))
                 order = self._order_on(d, self._epoch)
                 a.d_order = order.data_ptr()
                 a.gate = GATE_HOST
@@ -686,7 +725,12 @@ class TensorProducer:
             return
         deadline = time.monotonic() + drain_timeout_s
         with self._lock:
-            self._lock.wait_for(lambda: not self._ledger.pending, timeout=drain_timeout_s)
+            while time.monotonic() < deadline:
+                self._drain_acks()
+                if not self._ledger.pending:
+                    break
+                self._lock.wait(0.002)
+            self._drain_acks()
             self._send_all(Shutdown())
         # device drain: every live consumer released the last batch (bounded wait)
         if self._ring is not None:

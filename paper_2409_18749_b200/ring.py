@@ -242,6 +242,26 @@ class DeviceRing:
     def host_control(self) -> bool:
         return self.ctl is not None
 
+    @property
+    def cursor_words(self):
+        """numpy u64 view of the release cursors in the host-shared control
+        block (read-only use: the fast path of a host flow gate)."""
+        v = getattr(self, "_cursor_view", None)
+        if v is None:
+            import numpy as np
+
+            off = 8 * self.slots * self.writers
+            v = np.frombuffer(self.ctl.mm, dtype=np.uint64, count=self.max_consumers, offset=off)
+            self._cursor_view = v
+        return v
+
+    def released(self, live, need: int) -> bool:
+        """True if every live cursor has released `need` (wrap-around GEQ)."""
+        if not live:
+            return True
+        cur = self.cursor_words
+        return all(((int(cur[c]) - need) & 0xFFFFFFFFFFFFFFFF) < (1 << 63) for c in live)
+
     def host_ack(self, consumer: int, seq: int) -> None:
         """Release up to seq from the host (consumer finished with the batch)."""
         call("tsb_ring_set_cursor", self._h, consumer, seq)

@@ -56,6 +56,41 @@ __global__ void tma_write_k(uint8_t *out, size_t bytes, int chunk) {
     }
 }
 
+// phased 1:ratio mix: each CTA loads a CHUNK-byte tile into smem with one
+// TMA bulk copy, then writes it `ratio` times with 16 B stores (reads and
+// writes of a CTA are separated in time, not interleaved per thread)
+template <int CHUNK>
+__global__ void phased_mix_k(const uint8_t *in, uint8_t *out, size_t n, int ratio) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ __align__(8) uint64_t bar;
+    const size_t nchunks = n / CHUNK;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar)), "r"(CHUNK) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"((uint32_t)__cvta_generic_to_shared(sm)), "l"(in + c * CHUNK), "r"(CHUNK),
+                         "r"((uint32_t)__cvta_generic_to_shared(&bar)) : "memory");
+        }
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(&bar)), "r"(phase) : "memory");
+        phase ^= 1;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(sm);
+        for (int r = 0; r < ratio; ++r) {
+            uint4 *o = reinterpret_cast<uint4 *>(out + ((size_t)r * n) + c * CHUNK);
+            for (int i = threadIdx.x; i < CHUNK / 16; i += blockDim.x) o[i] = s4[i];
+        }
+        __syncthreads();
+    }
+}
+
 int main() {
     const size_t N = 38535168;  // bytes of one u8 batch (256 x 150528)
     uint4 *a, *b;
@@ -90,6 +125,20 @@ int main() {
     time("mix 1:1 (u8->u8) 77MB", 2.0 * N, [&] { mix_k<<<g, t>>>(a, b, N / 16, 1); });
     time("memset 154MB", 4.0 * N, [&] { cudaMemsetAsync(b, 0, 4 * N); });
     time("write_only st.cs 154MB", 4.0 * N, [&] { write_cs_k<<<g, t>>>(b, 4 * N / 16, 7); });
+    cudaFuncSetAttribute(phased_mix_k<16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
+    cudaFuncSetAttribute(phased_mix_k<65536>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    for (int per : {4, 8}) {
+        char nm[80];
+        snprintf(nm, sizeof nm, "phased 1:4 16KB x%d/SM", per);
+        time(nm, 5.0 * N, [&] { phased_mix_k<16384><<<sms * per, 256, 16384>>>(reinterpret_cast<const uint8_t *>(a), reinterpret_cast<uint8_t *>(b), N, 4); });
+        snprintf(nm, sizeof nm, "phased 1:2 16KB x%d/SM", per);
+        time(nm, 3.0 * N, [&] { phased_mix_k<16384><<<sms * per, 256, 16384>>>(reinterpret_cast<const uint8_t *>(a), reinterpret_cast<uint8_t *>(b), N, 2); });
+    }
+    for (int per : {2, 3}) {
+        char nm[80];
+        snprintf(nm, sizeof nm, "phased 1:4 64KB x%d/SM", per);
+        time(nm, 5.0 * N, [&] { phased_mix_k<65536><<<sms * per, 512, 65536>>>(reinterpret_cast<const uint8_t *>(a), reinterpret_cast<uint8_t *>(b), N, 4); });
+    }
     for (int chunk : {4096, 8192, 16384}) {
         cudaFuncSetAttribute(tma_write_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * chunk);
         char name[64];

@@ -1,0 +1,97 @@
+"""Delivered samples/s through the public API with an HBM-resident store:
+TensorProducer(CollateLoader) -> K SharedLoader consumer processes (host sync,
+map-and-ack).  Shows the facade's per-batch host cost next to bench.py's
+native-loop value."""
+import json
+import multiprocessing as mp
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def consumer(bcast, agg, cid, n, q, sync):
+    import torch
+
+    torch.cuda.set_device(0)
+    from paper_2409_18749_b200 import SharedLoader
+
+    ld = SharedLoader(bcast, agg, consumer_id=cid, sync=sync)
+    prof = None
+    if os.environ.get("TSB_PROFILE_CONSUMER") and cid == 100:
+        import cProfile
+
+        prof = cProfile.Profile()
+        prof.enable()
+    ts = []
+    while len(ts) < n:
+        for inp, tgt in ld:
+            ts.append(time.monotonic())
+            if len(ts) >= n:
+                break
+        if ld.finished:
+            break
+    ld.close()
+    if prof is not None:
+        import pstats
+
+        prof.disable()
+        with open(os.environ["TSB_PROFILE_CONSUMER"], "w") as fh:
+            pstats.Stats(prof, stream=fh).sort_stats("tottime").print_stats(25)
+    w = ts[len(ts) // 4:]
+    q.put((len(w) - 1) / (w[-1] - w[0]) if len(w) > 1 else 0.0)
+
+
+def main():
+    import torch
+
+    torch.cuda.set_device(0)
+    from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec, StoreSource,
+                                       TensorProducer)
+
+    B, K, n = 256, 4, int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    sync = sys.argv[2] if len(sys.argv) > 2 else "host"
+    store = StoreSource.synthetic(0, 16384, (224, 224, 3), location="hbm")
+    ld = CollateLoader(DatasetSpec(store, 16384, B), AugmentSpec(out_dtype="float32"))
+    tmp = f"/tmp/tsb-fr-{os.getpid()}"
+    os.makedirs(tmp, exist_ok=True)
+    b, a = f"unix:{tmp}/b.sock", f"unix:{tmp}/a.sock"
+    prod = TensorProducer(ld, b, a, min_consumers=K, ring_slots=8, heartbeat_timeout_s=60)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=consumer, args=(b, a, 100 + k, n, q, sync)) for k in range(K)]
+    for p in ps:
+        p.start()
+    done, t0 = 0, None
+    prof = None
+    while done < n:
+        for _ in prod:
+            done += 1
+            if done == n // 4:
+                t0 = time.monotonic()
+                if os.environ.get("TSB_PROFILE_PRODUCER"):
+                    import cProfile
+
+                    prof = cProfile.Profile()
+                    prof.enable()
+            if done >= n:
+                break
+    t1 = time.monotonic()
+    if prof is not None:
+        import pstats
+
+        prof.disable()
+        with open(os.environ["TSB_PROFILE_PRODUCER"], "w") as fh:
+            pstats.Stats(prof, stream=fh).sort_stats("tottime").print_stats(30)
+    prod.join(60)
+    rates = [q.get(timeout=300) for _ in ps]
+    prod.close()
+    print(json.dumps({"consumer_batches_per_s": [round(r, 1) for r in rates],
+                      "delivered_samples_per_s": round(sum(rates) * B, 1),
+                      "producer_loop_batches_per_s": round((n - n // 4) / (t1 - t0), 1),
+                      "sync": sync}))
+
+
+if __name__ == "__main__":
+    main()

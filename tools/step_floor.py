@@ -1,7 +1,8 @@
 """Where does a producer step go?  Per-batch device time of the native loop
 (tsb_produce_range) vs the bare collate kernel in a CUDA graph, per output
 kind.  Knobs (env, read once): TSB_NO_PDL, TSB_NO_FUSED.
-usage: python tools/step_floor.py <f32|bf16|u8> <mode>  mode: graph|host|device"""
+usage: python tools/step_floor.py <f32|bf16|u8> <mode>  mode: graph|host|host1|device
+(host1: one batch per tsb_produce_range call, the facade's pattern)"""
 import json
 import sys
 
@@ -39,24 +40,31 @@ if mode == "graph":
         g.replay()
     e1.record()
 else:
-    ring = DeviceRing(8, ld.batch_nbytes, 1, control="host" if mode == "host" else "device")
+    ring = DeviceRing(8, ld.batch_nbytes, 1, control="device" if mode == "device" else "host")
+
+    per_call = 1 if mode == "host1" else 1 << 30
 
     def run(q0, n):
         q = q0
         while q < q0 + n:
             ep, bi = divmod(q - 1, L)
-            m = min(q0 + n - q, L - bi)
+            m = min(q0 + n - q, L - bi, per_call)
             a = ld.produce_args(ep)
-            a.gate = GATE_HOST if mode == "host" else GATE_DEVICE
+            a.gate = GATE_DEVICE if mode == "device" else GATE_HOST
             produce_range(ring, a, q, bi, m, [], stream=s)
             q += m
+
+    import time as _t
 
     run(1, 16)
     s.synchronize()
     e0.record(s)
+    h0 = _t.perf_counter()
     run(17, K)
+    host_us = (_t.perf_counter() - h0) * 1e6 / K
     e1.record(s)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / K
 print(json.dumps({"kind": kind, "mode": mode, "us_per_batch": round(ms * 1000, 2),
+                  "host_enqueue_us_per_batch": round(host_us, 2) if mode != "graph" else None,
                   "Msamples_s": round(B / ms / 1e3, 3)}))
