@@ -24,7 +24,7 @@ into a ring slot with one kernel launch + one tiny D2D copy.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 

@@ -3,7 +3,6 @@
 import json
 import multiprocessing as mp
 import sys
-import time
 
 import torch
 

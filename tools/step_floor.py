@@ -10,7 +10,6 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2409_18749_b200 import AugmentSpec, CollateLoader, DatasetSpec, StoreSource  # noqa: E402
-from paper_2409_18749_b200 import dataplane as dp  # noqa: E402
 from paper_2409_18749_b200._lib import GATE_DEVICE, GATE_HOST  # noqa: E402
 from paper_2409_18749_b200.ring import DeviceRing, produce_range  # noqa: E402
 
