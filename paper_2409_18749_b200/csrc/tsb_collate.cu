@@ -165,6 +165,8 @@ struct CaGeom {
     int use_tma;
     int vec_ldg;       // 16B LDG staging allowed
     int use_direct;    // collate_direct_kernel (TSB_CA_IMPL=direct A/B)
+    int st_cs;         // streaming (evict-first) output stores (TSB_CA_ST=plain disables)
+    int ld_hint;       // L2 evict-first policy on the TMA source loads (TSB_CA_LDHINT=0 disables)
     int64_t plane;     // h*w
     int64_t sample_bytes;
 };
@@ -222,6 +224,8 @@ __device__ __forceinline__ void publish_epilogue(const Epi &ep, int tid, int nth
         }
     }
 }
+
+__constant__ int g_st_cs;  // streaming output stores (TSB_CA_ST), set once per device
 
 struct ItemPar {
     int s, oy, ox, fl;
@@ -361,7 +365,10 @@ __device__ __forceinline__ void emit_channel(const uint32_t *wv, const Norm &nor
                                                     std::make_integer_sequence<int, P>{});
     const int64_t o = off + CH * plane_bytes;
     if constexpr (!MULTI) {
-        st_v4(static_cast<uint8_t *>(dsts.p[0]) + o, v);
+        if (g_st_cs)
+            st_cs_v4(static_cast<uint8_t *>(dsts.p[0]) + o, v);
+        else
+            st_v4(static_cast<uint8_t *>(dsts.p[0]) + o, v);
     } else {
 #pragma unroll
         for (int d = 0; d < MAX_DST; ++d)
@@ -450,9 +457,18 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
                     fence_proxy_async();
                     mbar_arrive_expect_tx(&full[st],
                                           (uint32_t)max(0, hi - lo) * (uint32_t)g.row_bytes);
-                    for (int r = lo; r < hi; ++r)
-                        tma_load_1d(dst + (r - sy_first) * g.rs, sample + (int64_t)r * g.row_bytes,
-                                    (uint32_t)g.row_bytes, &full[st]);
+                    if (g.ld_hint) {
+                        const uint64_t pol = l2_evict_first_policy();
+                        for (int r = lo; r < hi; ++r)
+                            tma_load_1d_hint(dst + (r - sy_first) * g.rs,
+                                             sample + (int64_t)r * g.row_bytes,
+                                             (uint32_t)g.row_bytes, &full[st], pol);
+                    } else {
+                        for (int r = lo; r < hi; ++r)
+                            tma_load_1d(dst + (r - sy_first) * g.rs,
+                                        sample + (int64_t)r * g.row_bytes, (uint32_t)g.row_bytes,
+                                        &full[st]);
+                    }
                 }
             } else {
                 if (g.vec_ldg) {
@@ -799,6 +815,28 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     g.use_tma = aligned_rows && is_device_memory(src);
     if (const char *e = getenv("TSB_CA_NOTMA")) g.use_tma = g.use_tma && !atoi(e);
     g.vec_ldg = aligned_rows && (g.io % 4 == 0);
+    {
+        static int knobs = -1;  // A/B knobs, read once per process
+        static int st_cs = 0, ld_hint = 0;
+        if (knobs < 0) {
+            // defaults (profiles/r1/cache_hints_ab.txt): streaming evict-first output
+            // stores + an L2 evict-first policy on the single-use source rows
+            const char *e1 = getenv("TSB_CA_ST");
+            const char *e2 = getenv("TSB_CA_LDHINT");
+            st_cs = !(e1 && strcmp(e1, "plain") == 0);
+            ld_hint = !(e2 && atoi(e2) == 0);
+            knobs = 1;
+        }
+        g.st_cs = st_cs;
+        g.ld_hint = ld_hint;
+        static int set_dev[64] = {0};
+        int dv = 0;
+        cudaGetDevice(&dv);
+        if (dv < 64 && !set_dev[dv]) {
+            TSB_CUDA(cudaMemcpyToSymbol(g_st_cs, &st_cs, sizeof(int)));
+            set_dev[dv] = 1;
+        }
+    }
     g.use_direct = direct_enabled() && is_device_memory(src) && (g.row_bytes % 4 == 0) &&
                    (g.sample_bytes % 4 == 0) && (((uintptr_t)src & 3) == 0) && b <= DC_MAX_B &&
                    b * (int64_t)h * (w / vec) < (1ll << 31);
