@@ -348,6 +348,29 @@ int tsb_wire_encode(const tsb_msg *m, uint8_t *out, size_t cap, size_t *len);
  * failing byte offset (DecodeError(offset, cause), wire.py:41-46). */
 int tsb_wire_decode(const uint8_t *frame, size_t len, tsb_msg *m, size_t *err_off);
 
+/* ---- native control-plane hub (bs/producer.py:379-438 readers + broadcast) --
+ * One epoll thread reads every admitted consumer's aggregate socket and
+ * decodes Ack / Heartbeat / Bye frames natively; the producer drains them
+ * in bulk.  tsb_hub_broadcast writes one frame to many sockets.  The caller
+ * keeps owning the fds (remove before closing). */
+typedef struct tsb_hub tsb_hub;
+typedef struct {
+    uint8_t kind;          /* TSB_MSG_ACK / _HEARTBEAT / _BYE, or 0 = connection closed */
+    uint64_t consumer_id;  /* from the frame (0 for kind 0) */
+    uint32_t epoch;
+    uint64_t batch_index;
+    int64_t t_us;          /* CLOCK_MONOTONIC at receipt */
+    int32_t fd;
+} tsb_hub_event;
+int tsb_hub_create(tsb_hub **out);
+/* Start reading fd for consumer_id; `pending` = bytes already read from it. */
+int tsb_hub_add(tsb_hub *h, int fd, uint64_t consumer_id, const uint8_t *pending, size_t n);
+int tsb_hub_remove(tsb_hub *h, int fd);
+int tsb_hub_drain(tsb_hub *h, tsb_hub_event *out, int cap, int *n);
+/* Blocking sends of one frame to fds[0..n); failed[i] = 1 on error (peer gone). */
+int tsb_hub_broadcast(const int *fds, int n, const uint8_t *frame, size_t len, int *failed);
+int tsb_hub_destroy(tsb_hub *h);
+
 #ifdef __cplusplus
 }
 #endif

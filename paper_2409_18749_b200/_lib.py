@@ -153,6 +153,19 @@ SRC_AUGMENT, SRC_GATHER, SRC_SYNTHETIC = 0, 1, 2
 SIGNATURES["tsb_produce_range"] = (i32, [vp, ctypes.POINTER(ProduceArgs), u64, i64, i32,
                                          ctypes.POINTER(i32), i32, pp, vp])
 SIGNATURES["tsb_consume_range"] = (i32, [vp, i32, u64, i32, pp, vp])
+class HubEvent(ctypes.Structure):
+    """Mirror of tsb_hub_event (include/tsb200.h)."""
+    _fields_ = [("kind", ctypes.c_uint8), ("consumer_id", ctypes.c_uint64),
+                ("epoch", ctypes.c_uint32), ("batch_index", ctypes.c_uint64),
+                ("t_us", ctypes.c_int64), ("fd", ctypes.c_int32)]
+
+
+SIGNATURES["tsb_hub_create"] = (i32, [pp])
+SIGNATURES["tsb_hub_add"] = (i32, [vp, i32, u64, vp, sz])
+SIGNATURES["tsb_hub_remove"] = (i32, [vp, i32])
+SIGNATURES["tsb_hub_drain"] = (i32, [vp, ctypes.POINTER(HubEvent), i32, ctypes.POINTER(i32)])
+SIGNATURES["tsb_hub_broadcast"] = (i32, [ctypes.POINTER(i32), i32, vp, sz, ctypes.POINTER(i32)])
+SIGNATURES["tsb_hub_destroy"] = (i32, [vp])
 SIGNATURES["tsb_wire_encode"] = (i32, [ctypes.POINTER(Msg), vp, sz, ctypes.POINTER(sz)])
 SIGNATURES["tsb_wire_decode"] = (i32, [vp, sz, ctypes.POINTER(Msg), ctypes.POINTER(sz)])
 SIGNATURES["tsb_produce_group"] = (i32, [pp, i32, i32, ctypes.POINTER(ProduceArgs), i32, i32, u64,

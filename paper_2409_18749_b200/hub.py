@@ -1,0 +1,70 @@
+"""Native control-plane hub (csrc/tsb_hub.cpp): per-batch socket work of the
+producer -- decoding every consumer's wire Acks and writing every Announce --
+off the interpreter lock.  The handshake stays in Python (transport.Conn);
+an admitted consumer's aggregate socket is handed to the hub."""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .wire import Ack, Bye, Heartbeat
+
+KIND_CLOSED = 0
+_KINDS = {4: Ack, 5: Heartbeat, 8: Bye}
+
+
+class Hub:
+    def __init__(self, cap: int = 4096):
+        h = ctypes.c_void_p()
+        _lib.call("tsb_hub_create", ctypes.byref(h))
+        self._h = h.value
+        self._buf = (_lib.HubEvent * cap)()
+        self._cap = cap
+        self._n = ctypes.c_int(0)
+        self._L = _lib.load()
+
+    def add(self, fd: int, consumer_id: int, pending: bytes = b"") -> None:
+        buf = ctypes.create_string_buffer(pending, len(pending)) if pending else None
+        _lib.call("tsb_hub_add", self._h, fd, consumer_id, buf, len(pending))
+
+    def remove(self, fd: int) -> None:
+        if self._h:  # (closed hub: nothing is read anymore)
+            _lib.call("tsb_hub_remove", self._h, fd)
+
+    def drain(self):
+        """[(kind, consumer_id, epoch, batch_index, t_monotonic_s, fd)] received so far;
+        kind is the wire kind (4 Ack, 5 Heartbeat, 8 Bye) or 0 = connection closed."""
+        out = []
+        while self._h:
+            _lib.check(self._L.tsb_hub_drain(self._h, self._buf, self._cap,
+                                             ctypes.byref(self._n)), "tsb_hub_drain")
+            n = self._n.value
+            b = self._buf
+            out.extend((b[i].kind, b[i].consumer_id, b[i].epoch, b[i].batch_index,
+                        b[i].t_us * 1e-6, b[i].fd) for i in range(n))
+            if n < self._cap:
+                return out
+        return out
+
+    @staticmethod
+    def broadcast(fds, frame: bytes) -> list:
+        """Send `frame` to every fd; returns the fds whose send failed."""
+        n = len(fds)
+        if not n:
+            return []
+        arr = (ctypes.c_int * n)(*fds)
+        failed = (ctypes.c_int * n)()
+        _lib.call("tsb_hub_broadcast", arr, n, frame, len(frame), failed)
+        return [fds[i] for i in range(n) if failed[i]]
+
+    def close(self) -> None:
+        h, self._h = self._h, None
+        if h:
+            self._L.tsb_hub_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -62,7 +62,8 @@ from .ledger import (ConsumerRecord, Ledger, admission_code, rebatch_epoch_len, 
                      seq_of, window_slots)
 from ._lib import GATE_HOST
 from .ring import DeviceRing, produce_group, produce_range
-from .transport import Conn, endpoints_from_env, listen
+from .hub import Hub
+from .transport import HANDOFF, Conn, endpoints_from_env, listen
 from .wire import (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT, SUPPORTED_VERSIONS, Ack,
                    Announce, Bye, DType, EpochEnd, EpochStart, Heartbeat, Join, Shutdown, Welcome,
                    dtype_of, encode)
@@ -148,6 +149,10 @@ class TensorProducer:
         # folded into the ledger in bulk by the producer (_drain_acks): one lock
         # round and one drift sample per batch instead of per ack
         self._ack_q: deque = deque()
+        # native control-plane hub: admitted consumers' aggregate sockets are read
+        # (Acks, Heartbeats, Bye) and Announces written without the interpreter
+        self._hub = Hub()
+        self._hub_fds: dict[int, int] = {}  # fd -> consumer id
         self._hdr_key = None
         self._hdr_reserved = b""
 
@@ -312,6 +317,18 @@ class TensorProducer:
 
             def on_msg(m, conn=conn, state=state):
                 state["cid"] = self._handle(conn, m, state["cid"])
+                if isinstance(m, Join):
+                    with self._lock:
+                        rec = self._consumers.get(state["cid"])
+                        if rec is not None and rec.conn is conn:
+                            return HANDOFF  # admitted: the hub reads this socket from now on
+                return None
+
+            def on_handoff(pending, conn=conn, state=state):
+                with self._lock:
+                    fd = conn.sock.fileno()
+                    self._hub_fds[fd] = state["cid"]
+                    self._hub.add(fd, state["cid"], pending)
 
             def on_close(conn=conn, state=state):
                 with self._lock:
@@ -320,7 +337,7 @@ class TensorProducer:
                     if rec is not None and rec.conn is conn:
                         self._drop(cid, "disconnect")
 
-            conn.start_reader(on_msg, on_close, "agg-reader")
+            conn.start_reader(on_msg, on_close, "agg-reader", on_handoff)
 
     def _handle(self, conn: Conn, msg, cid):
         now = time.monotonic()
@@ -340,8 +357,31 @@ class TensorProducer:
                     self._drop(msg.consumer_id, "bye")
         return cid
 
-    def _drain_acks(self) -> None:
+    def _drain_hub(self) -> None:
+        """Hub events: Acks join the ack queue; heartbeats, Byes and closed
+        sockets are applied here (caller holds the lock)."""
+        for kind, cid, epoch, bi, t, fd in self._hub.drain():
+            if kind == 4:
+                self._ack_q.append((Ack(cid, epoch, bi), t))
+            elif kind == 5:
+                rec = self._consumers.get(cid)
+                if rec is not None:
+                    rec.last_heartbeat = max(rec.last_heartbeat, t)
+            elif kind == 8:
+                self._drain_acks(hub=False)
+                if cid in self._consumers:
+                    self._drop(cid, "bye")
+            else:  # connection closed / protocol error
+                owner = self._hub_fds.pop(fd, None)
+                rec = self._consumers.get(owner)
+                if rec is not None and rec.conn is not None and rec.conn.sock.fileno() == fd:
+                    self._drain_acks(hub=False)
+                    self._drop(owner, "disconnect")
+
+    def _drain_acks(self, hub: bool = True) -> None:
         """Fold queued wire Acks into the ledger (caller holds the lock)."""
+        if hub:
+            self._drain_hub()
         q = self._ack_q
         if not q:
             return
@@ -456,6 +496,10 @@ class TensorProducer:
         self._ledger.remove_consumer(cid)
         if reason == "timeout":
             self.stats["evictions"] += 1
+        if rec.conn is not None and not rec.conn.closed:
+            fd = rec.conn.sock.fileno()
+            if self._hub_fds.pop(fd, None) is not None:
+                self._hub.remove(fd)  # stop reading before the fd can be reused
         for c in (rec.conn, rec.bcast if close_bcast else None):
             if c is not None:
                 c.close()
@@ -705,13 +749,15 @@ class TensorProducer:
     def _send_announces(self, anns: dict) -> None:
         """Announce a batch: each consumer gets the slot name of its own GPU's ring."""
         data = {d: encode(a) for d, a in anns.items()}
-        for rec in list(self._consumers.values()):
-            if rec.bcast is None:
-                continue
-            try:
-                rec.bcast.send_raw(data[rec.ring])
-            except OSError:
-                self._drop(rec.consumer_id, "disconnect")
+        by_ring: dict[int, list] = {}
+        for rec in self._consumers.values():
+            if rec.bcast is not None and not rec.bcast.closed:
+                by_ring.setdefault(rec.ring, []).append(rec)
+        for k, recs in by_ring.items():  # one native call per ring: no per-consumer Python
+            failed = set(Hub.broadcast([r.bcast.sock.fileno() for r in recs], data[k]))
+            for r in recs:
+                if r.bcast.sock.fileno() in failed:
+                    self._drop(r.consumer_id, "disconnect")
         for c in list(self._monitors):
             try:
                 c.send_raw(data[0])
@@ -759,6 +805,8 @@ class TensorProducer:
         self.join(0.0)
         for st in self._streams.values():
             st.synchronize()
+        with self._lock:  # the sweeper drains the hub under the same lock
+            self._hub.close()
         for d, ring in self._rings.items():
             _RINGS.pop(self._ring_ids[d], None)
             ring.close()

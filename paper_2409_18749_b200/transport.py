@@ -78,6 +78,9 @@ def dial(endpoint: str, timeout: float) -> socket.socket:
             time.sleep(0.02)
 
 
+HANDOFF = object()  # on_msg return value: stop the Python reader, hand the socket off
+
+
 class Conn:
     """A socket with a send lock and a frame reader thread."""
 
@@ -93,7 +96,13 @@ class Conn:
         with self._lock:
             self.sock.sendall(data)
 
-    def start_reader(self, on_msg, on_close, name: str = "reader") -> threading.Thread:
+    def start_reader(self, on_msg, on_close, name: str = "reader",
+                     on_handoff=None) -> threading.Thread:
+        """Read frames on a thread.  If on_msg returns ``HANDOFF`` the thread
+        stops reading (the socket stays open) and ``on_handoff(pending_bytes)``
+        gets what was already read past that frame -- used to pass an admitted
+        consumer's socket to the native hub."""
+
         def run():
             dec = wire.FrameDecoder()
             try:
@@ -101,12 +110,15 @@ class Conn:
                     data = self.sock.recv(65536)
                     if not data:
                         break
-                    for m in dec.feed(data):
-                        on_msg(m)
+                    msgs = dec.feed(data)
+                    for i, m in enumerate(msgs):
+                        if on_msg(m) is HANDOFF and on_handoff is not None:
+                            rest = b"".join(wire.encode(x) for x in msgs[i + 1:])
+                            on_handoff(rest + dec.take_pending())
+                            return
             except (OSError, ValueError):
                 pass
-            finally:
-                on_close()
+            on_close()
 
         t = threading.Thread(target=run, name=name, daemon=True)
         t.start()

@@ -317,6 +317,12 @@ class FrameDecoder:
     def pending_bytes(self) -> int:
         return len(self._buf)
 
+    def take_pending(self) -> bytes:
+        """Bytes received past the last complete frame (and forget them)."""
+        b = bytes(self._buf)
+        self._buf.clear()
+        return b
+
 
 # reference-compatible aliases
 encode_message = encode

@@ -50,7 +50,8 @@ def main():
     from paper_2409_18749_b200 import (AugmentSpec, CollateLoader, DatasetSpec, StoreSource,
                                        TensorProducer)
 
-    B, K, n = 256, 4, int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    B, n = 256, int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    K = int(os.environ.get("TSB_CONSUMERS", 4))
     sync = sys.argv[2] if len(sys.argv) > 2 else "host"
     store = StoreSource.synthetic(0, 16384, (224, 224, 3), location="hbm")
     ld = CollateLoader(DatasetSpec(store, 16384, B), AugmentSpec(out_dtype="float32"))
@@ -90,7 +91,7 @@ def main():
     print(json.dumps({"consumer_batches_per_s": [round(r, 1) for r in rates],
                       "delivered_samples_per_s": round(sum(rates) * B, 1),
                       "producer_loop_batches_per_s": round((n - n // 4) / (t1 - t0), 1),
-                      "sync": sync}))
+                      "sync": sync, "consumers": K}))
 
 
 if __name__ == "__main__":
