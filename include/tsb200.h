@@ -306,6 +306,16 @@ int tsb_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, void **ev
 int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_produce_args *a,
                       int shard, int n_shards, uint64_t seq0, int64_t batch0, int n,
                       const int *live, const int *n_live, void *stream);
+/* One process driving every writer (TensorProducer(devices=...)): for each
+ * of n batches, one host gate over all rings, then writer w (of n_writers =
+ * the shard count) produces its shard on devices[w] / streams[w] with
+ * args[w] (its device's order and store pointers) into all rings;
+ * rings[locals[w]] is the ring on devices[w].  One call per batch range
+ * instead of one per writer and batch. */
+int tsb_produce_group_multi(tsb_ring *const *rings, int n_rings, const tsb_produce_args *args,
+                            const int *locals, const int *devices, void *const *streams,
+                            int n_writers, uint64_t seq0, int64_t batch0, int n, const int *live,
+                            const int *n_live);
 
 /* ---- control-plane codec (host; wire.py:1-11,77-156,199-341) ------------
  * The reference's 9-message frame format, byte-identical, plus DType 5 (bf16)

@@ -320,11 +320,49 @@ int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_
         if (int rc = produce_multi(a->mode, a->src, idx, bs, a->h, a->w, a->c, a->pad, a->flip,
                                    a->seed, a->epoch, a->scale, a->bias, a->out_kind,
                                    a->sample_bytes, outs, tgts, readys, n_rings, counter, q,
-                                   i > 0, sys_fence, stream))
+                                   i > 0 || a->chain, sys_fence, stream))
             return rc;
     }
     (void)s;
     return TSB_OK;
+}
+
+int tsb_produce_group_multi(tsb_ring *const *rings, int n_rings, const tsb_produce_args *args,
+                            const int *locals, const int *devices, void *const *streams,
+                            int n_writers, uint64_t seq0, int64_t batch0, int n, const int *live,
+                            const int *n_live) {
+    TSB_CHECK(rings && args && locals && devices && streams && n_live, "null argument");
+    TSB_CHECK(n_writers >= 1 && n_writers <= TSB_MAX_DST, "writers must be 1..%d", TSB_MAX_DST);
+    int slots = 0;
+    if (int rc = tsb_ring_geometry(rings[0], &slots, nullptr, nullptr)) return rc;
+    int prev = 0;
+    TSB_CUDA(cudaGetDevice(&prev));
+    int no_live[TSB_MAX_DST] = {0};
+    int rc = TSB_OK;
+    for (int i = 0; i < n && rc == TSB_OK; ++i) {
+        const uint64_t q = seq0 + (uint64_t)i;
+        if (q > (uint64_t)slots) {  // one host gate for the batch, over every ring
+            int off = 0;
+            for (int k = 0; k < n_rings && rc == TSB_OK; ++k) {
+                rc = ring_host_gate(rings[k], live + off, n_live[k], q - (uint64_t)slots);
+                off += n_live[k];
+            }
+        }
+        for (int w = 0; w < n_writers && rc == TSB_OK; ++w) {
+            if (cudaSetDevice(devices[w]) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("cudaSetDevice(%d) failed", devices[w]);
+                rc = TSB_ERR_CUDA;
+                break;
+            }
+            tsb_produce_args a = args[w];
+            a.chain = args[w].chain || i > 0;  // each writer's stream carries only its kernels
+            rc = tsb_produce_group(rings, n_rings, locals[w], &a, w, n_writers, q, batch0 + i, 1,
+                                   nullptr, no_live, streams[w]);
+        }
+    }
+    cudaSetDevice(prev);
+    return rc;
 }
 
 }  // extern "C"

@@ -61,7 +61,7 @@ from .errors import ProducerClosed
 from .ledger import (ConsumerRecord, Ledger, admission_code, rebatch_epoch_len, retention_window,
                      seq_of, window_slots)
 from ._lib import GATE_HOST
-from .ring import DeviceRing, produce_group, produce_range
+from .ring import DeviceRing, produce_group_multi, produce_range
 from .hub import Hub
 from .transport import HANDOFF, Conn, endpoints_from_env, listen
 from .wire import (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT, SUPPORTED_VERSIONS, Ack,
@@ -731,20 +731,27 @@ class TensorProducer:
         import torch
 
         G = len(self._devices)
-        rings = [self._rings[k] for k in range(G)]
-        live = [[] for _ in range(G)]  # gated on the host already (_host_gate)
         writers = list(range(G)) if self._sharded else [0]
-        for g, k in enumerate(writers):
-            d = self._devices[k]
-            with torch.cuda.device(d):
-                from ._lib import ProduceArgs
+        key = (self._epoch, tuple(writers))
+        if getattr(self, "_group_cache", (None,))[0] != key:
+            from ._lib import ProduceArgs
 
-                a = ProduceArgs.from_buffer_copy(self._loader.produce_args(self._epoch))
-                order = self._order_on(d, self._epoch)
-                a.d_order = order.data_ptr()
+            base = self._loader.produce_args(self._epoch)
+            args = []
+            for k in writers:
+                a = ProduceArgs.from_buffer_copy(base)
+                a.d_order = self._order_on(self._devices[k], self._epoch).data_ptr()
                 a.gate = GATE_HOST
-                produce_group(rings, k, a, g, len(writers), q, index, 1, live,
-                              stream=self._streams[k])
+                args.append(a)
+            self._group_cache = (key, args)
+        args = self._group_cache[1]
+        for a in args:
+            a.chain = int(self._chain_ok)  # each writer's stream: previous op was its kernel
+        produce_group_multi([self._rings[k] for k in range(G)], args, writers,
+                            [self._devices[k] for k in writers],
+                            [self._streams[k] for k in writers], q, index, 1,
+                            [[] for _ in range(G)])  # gated on the host already (_host_gate)
+        self._chain_ok = True
 
     def _send_announces(self, anns: dict) -> None:
         """Announce a batch: each consumer gets the slot name of its own GPU's ring."""

@@ -331,3 +331,22 @@ def produce_group(rings, local: int, args, shard: int, n_shards: int, seq0: int,
         raise ValueError("one live list per ring")
     call("tsb_produce_group", ptrs, len(rings), local, ctypes.byref(args), shard, n_shards, seq0,
          batch0, n, live, counts, _stream(stream))
+
+
+def produce_group_multi(rings, args_list, locals_, devices, streams, seq0: int, batch0: int,
+                        n: int, live_per_ring) -> None:
+    """All writers of a single-process multi-GPU producer in one native call
+    (tsb_produce_group_multi); the calling thread blocks on the host gate."""
+    rings = list(rings)
+    W = len(args_list)
+    ptrs = (ctypes.c_void_p * len(rings))(*[r._h.value if hasattr(r._h, "value") else r._h
+                                           for r in rings])
+    arr = (_lib.ProduceArgs * W)(*args_list)
+    loc = (ctypes.c_int * W)(*locals_)
+    devs = (ctypes.c_int * W)(*devices)
+    sts = (ctypes.c_void_p * W)(*[_stream(s).value for s in streams])
+    flat = [c for lv in live_per_ring for c in lv]
+    live = (ctypes.c_int * max(1, len(flat)))(*flat)
+    counts = (ctypes.c_int * len(rings))(*[len(lv) for lv in live_per_ring])
+    call("tsb_produce_group_multi", ptrs, len(rings), arr, loc, devs, sts, W, seq0, batch0, n,
+         live, counts)
