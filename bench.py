@@ -218,12 +218,8 @@ def host_consumer(dev, handle, control, slots, slot_bytes, max_consumers, cursor
 
     ring = DeviceRing.import_handle(handle, slots, slot_bytes, max_consumers, control, writers)
     q.put(("ready", cursor))
-    times = []
-    for seq in range(1, warmup + steps + 1):
-        ring.host_wait_ready((seq - 1) % slots, seq)
-        if seq > warmup:
-            times.append(time.monotonic())
-        ring.host_ack(cursor, seq)
+    ring.host_consume_range(cursor, 1, warmup, timestamps=False)
+    times = ring.host_consume_range(cursor, warmup + 1, steps)  # native wait -> stamp -> ack
     rate = (len(times) - 1) / (times[-1] - times[0]) * B if len(times) > 1 else 0.0
     q.put(("done", cursor, rate))
     ring.close()

@@ -178,6 +178,10 @@ int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int 
  * a value another stream of the same process has yet to write. */
 int tsb_ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need,
                        int64_t timeout_us);
+/* Native map-and-ack consumer loop (bs/cli.py:252-258): for n batches from
+ * seq0, spin until the slot is ready, record the fetch time (CLOCK_MONOTONIC
+ * us, t_us may be NULL) and release it. */
+int tsb_ring_host_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, int64_t *t_us);
 /* Host consumer: spin until ready[slot] >= seq (timeout_us < 0 = forever). */
 int tsb_ring_host_wait_ready(tsb_ring *r, int slot, uint64_t seq, int64_t timeout_us);
 
@@ -268,6 +272,11 @@ typedef struct {
                                 engine into HBM staging first (augment), or
                                 straight into the slot (gather) */
     const int64_t *h_order;  /* host copy of d_order (row addresses for ingest) */
+    int persistent;          /* 1 (passthrough modes, host-control ring): the whole
+                                range is ONE cooperative persistent launch whose
+                                CTAs gate on the release cursors themselves -- no
+                                host launch per batch.  Consumers must not need
+                                this process's SMs to release slots. */
     int chain;               /* 1: the previous operation on `stream` was a fused
                                 produce kernel (so the call's first batch may chain
                                 with programmatic dependent launch too) */

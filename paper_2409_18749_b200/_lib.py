@@ -94,6 +94,7 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_ring_attach_host_control": (i32, [vp, vp, sz, i32]),
     "tsb_ring_host_wait_ready": (i32, [vp, i32, u64, i64]),
     "tsb_ring_host_gate": (i32, [vp, ctypes.POINTER(i32), i32, u64, i64]),
+    "tsb_ring_host_consume_range": (i32, [vp, i32, u64, i32, vp]),
     "tsb_ring_create_ex": (i32, [i32, i32, sz, i32, i32, pp]),
     "tsb_ring_import_ex": (i32, [vp, i32, sz, i32, i32, pp]),
     "tsb_ring_writers": (i32, [vp, ctypes.POINTER(i32)]),
@@ -125,7 +126,8 @@ class ProduceArgs(ctypes.Structure):
         ("epoch", ctypes.c_uint64), ("scale", ctypes.c_float * 4), ("bias", ctypes.c_float * 4),
         ("with_target", ctypes.c_int), ("input_bytes", ctypes.c_int64),
         ("d_crc", ctypes.c_void_p), ("wait_stride", ctypes.c_int), ("gate", ctypes.c_int),
-        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p), ("chain", ctypes.c_int),
+        ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p), ("persistent", ctypes.c_int),
+        ("chain", ctypes.c_int),
         ("jpeg", ctypes.c_void_p),
     ]
 

@@ -940,6 +940,131 @@ __global__ void __launch_bounds__(PT_THREADS)
     publish_epilogue(ep, tid, PT_THREADS);
 }
 
+// Persistent passthrough producer: ONE launch produces n consecutive batches
+// of a ring (gather from a store or the SplitMix64 source).  Each CTA gates
+// itself on the host-shared release cursors (ld.acquire.sys; the last value
+// seen is cached, so the common case costs no read), copies its share of the
+// batch, and the last CTA to finish a batch publishes the slot -- no host
+// launch per batch, so small batches are no longer bound by the launch rate.
+// CTAs never wait on each other, only on consumers, so the grid must be
+// co-resident (cooperative launch).  Consumers must not need this process's
+// SMs to release slots (host consumers, or other processes).
+constexpr int PER_MAX_LIVE = 16;
+struct PersistArgs {
+    const uint8_t *src;
+    const int64_t *order;      // epoch order (device)
+    int64_t b, sb;
+    uint64_t seed, epoch;
+    uint8_t *ring_base;
+    int64_t slot_stride;
+    int slots;
+    uint64_t *ready;           // [slots] (single writer)
+    const uint64_t *cursors;   // release cursors (device-visible, host-shared)
+    unsigned int *counters;    // [slots]
+    unsigned long long *gate;  // device word: every live cursor has released this much
+    int live[PER_MAX_LIVE];
+    int n_live;
+    int64_t input_bytes;
+    int with_target;
+    uint64_t seq0;
+    int64_t batch0;
+    int n;
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <bool SYNTH>
+__global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(PersistArgs a) {
+    const int tid = threadIdx.x;
+    const int chunks = (int)((a.sb + PT_CHUNK - 1) / PT_CHUNK);
+    const int items = (int)a.b * chunks;
+    const int64_t nvec = a.sb >> 4;
+    constexpr int U = PT_CHUNK / 16 / PT_THREADS;
+    uint64_t known = 0;  // thread 0: every live cursor is known to have released `known`
+    for (int i = 0; i < a.n; ++i) {
+        const uint64_t q = a.seq0 + (uint64_t)i;
+        const int slot = (int)((q - 1) % (uint64_t)a.slots);
+        if (tid == 0 && q > (uint64_t)a.slots) {
+            // CTA 0 alone reads the host-shared cursors (a PCIe round trip) and
+            // publishes the verified release level in a device word; the other
+            // CTAs wait on that word in L2 -- no flood of host reads
+            const uint64_t need = q - (uint64_t)a.slots;
+            while ((int64_t)(known - need) < 0) {
+                if (blockIdx.x == 0) {
+                    uint64_t lo = need + (1ull << 61);
+                    for (int j = 0; j < a.n_live; ++j) {
+                        const uint64_t c = ld_acquire_sys_u64(a.cursors + a.live[j]);
+                        if ((int64_t)(c - lo) < 0) lo = c;  // min under wrap-around order
+                    }
+                    if ((int64_t)(lo - need) >= 0) {
+                        atomicMax(a.gate, (unsigned long long)lo);
+                        known = lo;
+                    } else {
+                        __nanosleep(500);
+                    }
+                } else {
+                    uint64_t g;
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(g) : "l"(a.gate)
+                                 : "memory");
+                    known = g;
+                    if ((int64_t)(known - need) < 0) __nanosleep(100);
+                }
+            }
+        }
+        __syncthreads();  // the slot is free for this CTA's stores
+        const int64_t *idx = a.order + (a.batch0 + i) * a.b;
+        uint8_t *out = a.ring_base + (int64_t)slot * a.slot_stride;
+        if (blockIdx.x == 0 && a.with_target) {
+            int64_t *tgt = reinterpret_cast<int64_t *>(out + a.input_bytes);
+            for (int k = tid; k < a.b; k += PT_THREADS) tgt[k] = idx[k];
+        }
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            const int sidx = it / chunks, c = it - sidx * chunks;
+            const int64_t v0 = (int64_t)c * (PT_CHUNK / 16);
+            const int64_t v1 = min(v0 + PT_CHUNK / 16, nvec);
+            const uint64_t key = SYNTH ? derive_key(a.seed, a.epoch, (uint64_t)idx[sidx]) : 0;
+            const uint8_t *in = SYNTH ? nullptr : a.src + idx[sidx] * a.sb;
+            uint8_t *o = out + (int64_t)sidx * a.sb;
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t k = v0 + tid + u * PT_THREADS;
+                if (k < v1) {
+                    if constexpr (SYNTH) {
+                        const uint64_t w0 = mix64(key + (uint64_t)(2 * k + 1) * GAMMA);
+                        const uint64_t w1 = mix64(key + (uint64_t)(2 * k + 2) * GAMMA);
+                        v[u] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1,
+                                          (uint32_t)(w1 >> 32));
+                    } else {
+                        v[u] = ld_nc_v4(in + 16 * k);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t k = v0 + tid + u * PT_THREADS;
+                if (k < v1) st_v4(o + 16 * k, v[u]);
+            }
+        }
+        // batch i done by this CTA: the last CTA publishes the slot
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned int prev = atomicAdd(a.counters + slot, 1u);
+            if (prev == gridDim.x - 1) {
+                a.counters[slot] = 0u;
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.ready + slot), "l"(q)
+                             : "memory");
+            }
+        }
+    }
+}
+
 template <typename Kern, typename... Args>
 int launch_maybe_pdl(Kern kern, int grid, int block, size_t smem, cudaStream_t s, bool pdl,
                      Args... args) {
@@ -1019,7 +1144,9 @@ int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int 
     const int64_t chunks = (sample_bytes + PT_CHUNK - 1) / PT_CHUNK;
     int64_t items = b * chunks;
     TSB_CHECK(items < (1ll << 31), "too many work items");
-    const int64_t cap = (int64_t)sm_count() * 8;
+    static int per_sm = -1;  // CTAs per SM (TSB_PT_PER_SM A/B knob)
+    if (per_sm < 0) per_sm = getenv("TSB_PT_PER_SM") ? atoi(getenv("TSB_PT_PER_SM")) : 8;
+    const int64_t cap = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 8);
     const int grid = (int)(items < 1 ? 1 : (items < cap ? items : cap));
     auto s = as_stream(stream);
     const auto *s8 = static_cast<const uint8_t *>(src);
@@ -1036,6 +1163,71 @@ int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int 
                                 s8, idx, sample_bytes, bb, seed, epoch, d, ep);
     return launch_maybe_pdl(passthrough_multi_kernel<false, true>, grid, PT_THREADS, 0, s, pdl, s8,
                             idx, sample_bytes, bb, seed, epoch, d, ep);
+}
+// n batches of a passthrough source in one cooperative persistent launch
+int produce_persistent(int mode, const void *src, const int64_t *order, int64_t b,
+                       int64_t sample_bytes, uint64_t seed, uint64_t epoch, uint8_t *ring_base,
+                       int64_t slot_stride, int slots, uint64_t *ready, const uint64_t *cursors,
+                       unsigned int *counters, const int *live, int n_live, int64_t input_bytes,
+                       int with_target, uint64_t seq0, int64_t batch0, int n, void *stream) {
+    TSB_CHECK(mode == TSB_SRC_GATHER || mode == TSB_SRC_SYNTHETIC,
+              "the persistent producer serves the passthrough modes");
+    TSB_CHECK(sample_bytes % 16 == 0 && ((uintptr_t)ring_base & 15) == 0 &&
+                  slot_stride % 16 == 0,
+              "persistent producer needs 16-byte samples and slots");
+    TSB_CHECK(n_live <= PER_MAX_LIVE, "at most %d live consumers", PER_MAX_LIVE);
+    TSB_CHECK(b >= 1 && b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK) < (1ll << 31),
+              "bad batch");
+    if (n <= 0) return TSB_OK;
+    PersistArgs a{};
+    a.src = static_cast<const uint8_t *>(src);
+    a.order = order;
+    a.b = b;
+    a.sb = sample_bytes;
+    a.seed = seed;
+    a.epoch = epoch;
+    a.ring_base = ring_base;
+    a.slot_stride = slot_stride;
+    a.slots = slots;
+    a.ready = ready;
+    a.cursors = cursors;
+    a.counters = counters;
+    // per-device gate word (reset in stream order before every persistent launch)
+    static unsigned long long *gate_words[64] = {nullptr};
+    int dev = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    TSB_CHECK(dev < 64, "device index");
+    if (!gate_words[dev]) TSB_CUDA(cudaMalloc(&gate_words[dev], 256));
+    a.gate = gate_words[dev];
+    TSB_CUDA(cudaMemsetAsync(a.gate, 0, sizeof(unsigned long long), as_stream(stream)));
+    for (int j = 0; j < n_live; ++j) a.live[j] = live[j];
+    a.n_live = n_live;
+    a.input_bytes = input_bytes;
+    a.with_target = with_target;
+    a.seq0 = seq0;
+    a.batch0 = batch0;
+    a.n = n;
+    const bool synth = mode == TSB_SRC_SYNTHETIC;
+    auto kern = synth ? persistent_passthrough_kernel<true> : persistent_passthrough_kernel<false>;
+    int occ = 0;
+    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT_THREADS, 0));
+    const int64_t items = b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK);
+    static int per_sm = -1;  // CTAs per SM: fewer CTAs = fewer same-address completion atomics
+    if (per_sm < 0) per_sm = getenv("TSB_PT_PER_SM") ? atoi(getenv("TSB_PT_PER_SM")) : 2;
+    int64_t cap = (int64_t)sm_count() * (occ > 0 ? occ : 1);
+    if (per_sm > 0 && (int64_t)sm_count() * per_sm < cap) cap = (int64_t)sm_count() * per_sm;
+    const int grid = (int)(items < cap ? items : cap);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(PT_THREADS);
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: CTAs gate independently
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    return TSB_OK;
 }
 }  // namespace tsb
 
@@ -1160,5 +1352,7 @@ void preload_collate() {
     touch_kernel(passthrough_multi_kernel<false, true>);
     touch_kernel(passthrough_multi_kernel<true, false>);
     touch_kernel(passthrough_multi_kernel<true, true>);
+    touch_kernel(persistent_passthrough_kernel<false>);
+    touch_kernel(persistent_passthrough_kernel<true>);
 }
 }  // namespace tsb

@@ -11,6 +11,13 @@ namespace tsb {
 int ring_publish_ptrs(tsb_ring *r, int slot, int writer, uint64_t **ready, unsigned int **counter);
 int ring_writers(const tsb_ring *r);
 int ring_phys_device(const tsb_ring *r);
+void ring_internals(tsb_ring *r, uint8_t **base, int64_t *stride, uint64_t **ready,
+                    uint64_t **cursors, unsigned int **counters);
+int produce_persistent(int mode, const void *src, const int64_t *order, int64_t b,
+                       int64_t sample_bytes, uint64_t seed, uint64_t epoch, uint8_t *ring_base,
+                       int64_t slot_stride, int slots, uint64_t *ready, const uint64_t *cursors,
+                       unsigned int *counters, const int *live, int n_live, int64_t input_bytes,
+                       int with_target, uint64_t seq0, int64_t batch0, int n, void *stream);
 int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int h, int w, int c,
                   int pad, int flip, uint64_t seed, uint64_t epoch, const float *scale,
                   const float *bias, int out_kind, int64_t sample_bytes, void *const *outs,
@@ -77,6 +84,21 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                   "the JPEG source needs the fused single-writer path (no per-batch CRC)");
     }
     const bool staged = !jpeg && a->ingest && a->h_order && !ev;
+    if (a->persistent) {  // one cooperative launch for the whole range, gated on the device
+        TSB_CHECK(ring_has_host_control(r) && ring_writers(r) == 1 && !staged && !jpeg &&
+                      !a->d_crc && !ev,
+                  "the persistent producer needs a host-control single-writer ring, a "
+                  "device-resident passthrough source and no CRC / events");
+        uint8_t *base = nullptr;
+        int64_t sstride = 0;
+        uint64_t *ready = nullptr, *cursors = nullptr;
+        unsigned int *counters = nullptr;
+        ring_internals(r, &base, &sstride, &ready, &cursors, &counters);
+        return produce_persistent(a->mode, a->src, a->d_order, a->batch_size, a->sample_bytes,
+                                  a->seed, a->epoch, base, sstride, slots, ready, cursors,
+                                  counters, live, n_live, a->input_bytes, a->with_target, seq0,
+                                  batch0, n, stream);
+    }
     if (staged)
         TSB_CHECK(ingest_sample_bytes(a->ingest) == a->sample_bytes,
                   "ingest staging is for %lld-byte samples, not %lld",

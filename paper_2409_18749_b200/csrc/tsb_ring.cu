@@ -230,6 +230,14 @@ int ring_publish_ptrs(tsb_ring *r, int slot, int writer, uint64_t **ready,
 }
 int ring_writers(const tsb_ring *r) { return r->writers; }
 int ring_phys_device(const tsb_ring *r) { return r->phys_dev; }
+void ring_internals(tsb_ring *r, uint8_t **base, int64_t *stride, uint64_t **ready,
+                    uint64_t **cursors, unsigned int **counters) {
+    *base = r->base;
+    *stride = (int64_t)r->slot_stride;
+    *ready = r->ready;
+    *cursors = r->cursor;
+    *counters = r->counters;
+}
 
 bool ring_has_host_control(const tsb_ring *r) { return r && r->h_ctl; }
 
@@ -470,6 +478,24 @@ int tsb_ring_wait_free(tsb_ring *r, const int *live, int n_live, uint64_t seq, v
     }
     return dev_wait(r, addrs, n_live, seq, stream);
 }
+int tsb_ring_host_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, int64_t *t_us) {
+    TSB_CHECK(r && r->h_ctl && consumer >= 0 && consumer < r->max_consumers && n >= 0,
+              "needs a host control block and a valid consumer");
+    uint64_t *cur = r->h_ctl + (size_t)r->slots * r->writers + consumer;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t q = seq0 + (uint64_t)i;
+        const int slot = (int)((q - 1) % (uint64_t)r->slots);
+        if (int rc = tsb_ring_host_wait_ready(r, slot, q, -1)) return rc;
+        if (t_us) {
+            struct timespec t;
+            clock_gettime(CLOCK_MONOTONIC, &t);
+            t_us[i] = (int64_t)t.tv_sec * 1000000 + t.tv_nsec / 1000;
+        }
+        __atomic_store_n(cur, q, __ATOMIC_RELEASE);  // map-and-ack: release at once
+    }
+    return TSB_OK;
+}
+
 int tsb_ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need,
                        int64_t timeout_us) {
     TSB_CHECK(r && r->h_ctl, "host gate needs a host control block");

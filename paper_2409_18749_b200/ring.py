@@ -262,6 +262,15 @@ class DeviceRing:
         cur = self.cursor_words
         return all(((int(cur[c]) - need) & 0xFFFFFFFFFFFFFFFF) < (1 << 63) for c in live)
 
+    def host_consume_range(self, consumer: int, seq0: int, n: int, timestamps: bool = True):
+        """Native map-and-ack loop over n batches; returns fetch times (s) or None."""
+        import numpy as np
+
+        t = np.empty(max(n, 1), dtype=np.int64) if timestamps else None
+        call("tsb_ring_host_consume_range", self._h, consumer, seq0, n,
+             None if t is None else t.ctypes.data)
+        return None if t is None else t[:n] * 1e-6
+
     def host_ack(self, consumer: int, seq: int) -> None:
         """Release up to seq from the host (consumer finished with the batch)."""
         call("tsb_ring_set_cursor", self._h, consumer, seq)

@@ -234,3 +234,54 @@ def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode):
         assert got[q][:ld.input_nbytes].tobytes() == want.tobytes(), q
         np.testing.assert_array_equal(got[q][ld.input_nbytes:].view(np.int64), idx)
     ring.close()
+
+
+@pytest.mark.parametrize("mode", ["gather", "synthetic"])
+def test_persistent_producer_matches_reference(golden, mode):
+    """One cooperative persistent launch produces a whole range of batches,
+    gating each slot on the host-shared cursors from the device; a host
+    consumer (map-and-ack) checks every batch against the reference's CRCs."""
+    import threading
+    import zlib
+
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    cases = {(c["epoch"], c["batch_index"]): c for c in golden["prepare_batch"]
+             if c["name"] == "img_b64"}
+    if mode == "synthetic":
+        src = SyntheticSource(0, (224, 224, 3), DType.U8)
+    else:
+        src = StoreSource.synthetic(0, 1024, (224, 224, 3))
+    ld = CollateLoader(DatasetSpec(src, 1024, 64, shuffle_seed=0))
+    ring = DeviceRing(3, ld.batch_nbytes, 2, control="host")  # 3 slots: forces device-side gating
+    ring.set_cursor(0, 0)
+    ring.evict(1)
+    L, n = len(ld), 16
+    crcs = {}
+
+    def consumer():
+        for q in range(1, n + 1):
+            s = ring.slot_of(q)
+            ring.host_wait_ready(s, q, timeout_s=60)
+            v = ring.view(s, (ld.batch_nbytes,), torch.uint8).cpu().numpy()
+            crcs[q] = (zlib.crc32(v[:ld.input_nbytes].tobytes()),
+                       v[ld.input_nbytes:].view(np.int64).copy())
+            ring.host_ack(0, q)
+
+    t = threading.Thread(target=consumer)
+    t.start()
+    a = ld.produce_args(0)
+    a.gate = GATE_HOST
+    a.persistent = 1
+    ps = torch.cuda.Stream()
+    produce_range(ring, a, 1, 0, n, [0, 1], stream=ps)
+    ps.synchronize()
+    t.join(60)
+    assert not t.is_alive() and len(crcs) == n
+    assert L >= n
+    for (e, bi), c in cases.items():
+        if e == 0 and bi < n:
+            assert crcs[bi + 1][0] == c["crc32"]
+    np.testing.assert_array_equal(crcs[1][1], cases[(0, 0)]["indices"])
+    a.persistent = 0
+    ring.close()

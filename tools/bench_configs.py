@@ -30,7 +30,7 @@ REF = {  # reference CPU path, shared mode, aggregate delivered samples/s (BASEL
 }
 
 
-def device_run(loader, n_consumers, steps, warmup, slots=8):
+def device_run(loader, n_consumers, steps, warmup, slots=8, persistent=False):
     """value: delivered samples/s of the native producer loop (device time)."""
     import torch
 
@@ -60,6 +60,7 @@ def device_run(loader, n_consumers, steps, warmup, slots=8):
             m = min(n - done, L - bi)
             a = loader.produce_args(ep)
             a.gate = GATE_HOST
+            a.persistent = int(persistent)
             produce_range(ring, a, q0, bi, m, list(range(n_consumers)), stream=s)
             done += m
 
@@ -149,6 +150,8 @@ def main():
     ap.add_argument("--steps", type=int, default=512)
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--only", default="c1,c2bf16,c5video,c5llm,c4")
+    ap.add_argument("--persistent", action="store_true",
+                    help="passthrough configs (C1, C5) as one persistent launch per range")
     args = ap.parse_args()
     import torch
 
@@ -163,8 +166,9 @@ def main():
     if "c1" in which:
         store = StoreSource.synthetic(0, N, (224, 224, 3), location="hbm")
         ld = CollateLoader(DatasetSpec(store, N, 64))
-        r = device_run(ld, 2, K, Wm)
-        r.update(config="C1: 224x224x3 u8 passthrough (DirectorySource gather), B=64, 2 consumers",
+        r = device_run(ld, 2, K, Wm, persistent=args.persistent)
+        r.update(config="C1: 224x224x3 u8 passthrough (DirectorySource gather), B=64, 2 consumers"
+                 + (" [persistent]" if args.persistent else ""),
                  reference_cpu=REF["c1"])
         print(json.dumps(r), flush=True)
         del store, ld
@@ -179,14 +183,14 @@ def main():
     if "c5video" in which:
         ld = CollateLoader(DatasetSpec(StoreSource.synthetic(0, 4096, (16, 3, 112, 112)), 4096,
                                        16))
-        r = device_run(ld, 8, K, Wm)
+        r = device_run(ld, 8, K, Wm, persistent=args.persistent)
         r.update(config="C5 video: (16,3,112,112) u8 clips, B=16, 8 consumers (one GPU)",
                  reference_cpu=REF["c5_video_k8"])
         print(json.dumps(r), flush=True)
         del ld
     if "c5llm" in which:
         ld = CollateLoader(DatasetSpec(SyntheticSource(0, (2048,), DType.I32), N, 256))
-        r = device_run(ld, 8, K, Wm)
+        r = device_run(ld, 8, K, Wm, persistent=args.persistent)
         r.update(config="C5 LLM: (2048,) int32 tokens (SyntheticSource on device), B=256, "
                         "8 consumers (one GPU)", reference_cpu=REF["c5_llm_k8"])
         print(json.dumps(r), flush=True)
