@@ -18,6 +18,7 @@ scale, bias = dp.norm_consts()
 kind = {"f32": 1, "bf16": 2, "u8": 0}
 out = torch.empty(B * c * h * w * 4, dtype=torch.uint8, device="cuda")
 crc = torch.zeros(1, dtype=torch.int32, device="cuda")
+out2 = torch.empty(B * c * h * w * 2, dtype=torch.uint8, device="cuda")
 torch.cuda.synchronize()
 for i in range(iters):
     idx = order[(i % 64) * B:((i % 64) + 1) * B]
@@ -28,5 +29,8 @@ for i in range(iters):
         dp.crc32(out, B * c * h * w * 4, crc)
     elif what == "gather":
         dp.gather(store, idx, B, sb, out)
+    elif what == "fanout2_bf16":  # collate MULTI: one pass into two destination slots
+        dp.collate_augment_fanout(store, idx, B, h, w, c, 16, True, 0, 0, kind["bf16"],
+                                  [out, out2], scale=scale, bias=bias)
 torch.cuda.synchronize()
 print("done", what)
