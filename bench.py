@@ -614,6 +614,11 @@ def run_reference(args):
 
 
 def main():
+    # a wedged multi-process run (a peer rank or consumer died) must end, not hang
+    import faulthandler
+
+    faulthandler.dump_traceback_later(float(os.environ.get("TSB_BENCH_WATCHDOG_S", 1500)),
+                                      exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2048)

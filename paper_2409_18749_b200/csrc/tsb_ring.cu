@@ -252,6 +252,12 @@ bool ring_has_host_control(const tsb_ring *r) { return r && r->h_ctl; }
 int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need) {
     TSB_CHECK(r && r->h_ctl, "host gate needs a host control block");
     if (n_live <= 0 || need == 0) return TSB_OK;
+    // a consumer that never releases (and is never evicted) must not wedge the
+    // producer forever: TSB_GATE_TIMEOUT_S (default 600 s) turns it into an error
+    static const double limit_s = getenv("TSB_GATE_TIMEOUT_S") ? atof(getenv("TSB_GATE_TIMEOUT_S"))
+                                                                 : 600.0;
+    struct timespec t0, t;
+    bool started = false;
     for (int i = 0; i < n_live; ++i) {
         TSB_CHECK(live[i] >= 0 && live[i] < r->max_consumers, "bad consumer %d", live[i]);
         const uint64_t *h = r->h_ctl + (size_t)r->slots * r->writers + live[i];
@@ -259,9 +265,20 @@ int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need) {
         while ((int64_t)(__atomic_load_n(h, __ATOMIC_ACQUIRE) - need) < 0) {
             if (++spins < 2048) {
                 __builtin_ia32_pause();
-            } else {
-                struct timespec ns = {0, 5000};
-                nanosleep(&ns, nullptr);
+                continue;
+            }
+            struct timespec ns = {0, 5000};
+            nanosleep(&ns, nullptr);
+            if ((spins & 1023) == 0) {
+                clock_gettime(CLOCK_MONOTONIC, &t);
+                if (!started) {
+                    t0 = t;
+                    started = true;
+                } else if ((t.tv_sec - t0.tv_sec) + 1e-9 * (t.tv_nsec - t0.tv_nsec) > limit_s) {
+                    set_error("flow gate: consumer %d has not released seq %llu for %.0f s",
+                              live[i], (unsigned long long)need, limit_s);
+                    return TSB_ERR_STALE;
+                }
             }
         }
     }
