@@ -149,3 +149,65 @@ def test_unservable_batch_size_is_refused(endpoints):
         next(iter(loader))
     producer.join(0)
     producer.close()
+
+
+CHILD = r"""
+import sys, zlib
+sys.path.insert(0, {root!r})
+import torch
+torch.cuda.set_device(0)
+from paper_2409_18749_b200 import SharedLoader
+loader = SharedLoader({b!r}, {a!r}, consumer_id={cid}, device=0, sync={sync!r})
+out = []
+for epoch in range(2):
+    for inp, tgt in loader:
+        out.append((zlib.crc32(inp.view(torch.int16).cpu().numpy().tobytes()), int(tgt[0])))
+loader.close()
+print("CRCS", out)
+"""
+
+
+@pytest.mark.parametrize("sync", ["device", "host"])
+def test_multi_ring_consumers_in_other_processes(endpoints, oracle, sync):
+    """Sharded two-ring producer; consumer processes map their ring over CUDA
+    IPC from the v2 ring descriptor (two writers per slot) and see every batch."""
+    import os
+    import subprocess
+    import sys
+    import zlib
+
+    N, B = 32, 8
+    ld = _loader(N, B, "bfloat16")
+    b, a = endpoints
+    producer = TensorProducer(ld, broadcast=b, aggregate=a, heartbeat_timeout_s=30.0,
+                              min_consumers=2, devices=[0, 0], ring_slots=3)
+
+    def run():
+        for _ in range(2):
+            for _ in producer:
+                pass
+        producer.join(30)
+
+    pt = threading.Thread(target=run, daemon=True)
+    pt.start()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    procs = [subprocess.Popen([sys.executable, "-c", CHILD.format(root=root, b=b, a=a, cid=cid,
+                                                                   sync=sync)],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for cid in (91, 92)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    pt.join(60)
+    rings_used = {r.ring for r in producer._consumers.values()}
+    want = []
+    for e in range(2):
+        order = oracle.epoch_order(N, 3, e)
+        for j in range(N // B):
+            idx = order[j * B:(j + 1) * B]
+            x = _want(oracle, N, 2, e, idx, 2)
+            want.append((zlib.crc32(x.tobytes()), int(idx[0])))
+    for p, (out, err) in zip(procs, outs):
+        assert p.returncode == 0, err[-2000:]
+        line = [ln for ln in out.splitlines() if ln.startswith("CRCS")][0]
+        assert eval(line[5:]) == want
+    assert len(rings_used) <= 2
+    producer.close()
