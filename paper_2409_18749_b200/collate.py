@@ -67,6 +67,66 @@ class StoreSource:
         return "hbm" if self.samples.is_cuda else "pinned"
 
     @classmethod
+    def from_directory(cls, path: str, sample_shape, dtype: DType = DType.U8,
+                       location: str = "pinned"):
+        """A DirectorySource (pipeline.py:45-54): equally sized binary files in
+        ``manifest.txt`` order (else sorted ``sample-*.bin``), read once into
+        pinned host memory (kept there, or copied to HBM).  Size errors follow
+        pipeline.py:196-209."""
+        import os
+
+        import torch
+
+        sb = int(np.prod(sample_shape)) * DType(dtype).size
+        man = os.path.join(path, "manifest.txt")
+        if os.path.exists(man):
+            with open(man, encoding="utf-8") as fh:
+                names = [ln.strip() for ln in fh if ln.strip()]
+        else:
+            names = sorted(n for n in os.listdir(path) if n.startswith("sample-"))
+        if not names:
+            raise ValueError(f"empty directory dataset at {path}")
+        host = torch.empty(len(names) * sb, dtype=torch.uint8).pin_memory()
+        view = memoryview(host.numpy())
+        for i, name in enumerate(names):
+            fp = os.path.join(path, name)
+            try:
+                with open(fp, "rb") as fh:
+                    n = fh.readinto(view[i * sb:(i + 1) * sb])
+                    extra = fh.read(1)
+            except FileNotFoundError:
+                raise ValueError(f"missing sample {i}: {fp}") from None
+            if n != sb or extra:
+                raise ValueError(f"sample {i} ({fp}) is {n + len(extra)}+ bytes, expected {sb}")
+        if location == "pinned":
+            return cls(host, sample_shape, dtype)
+        return cls(host.to("cuda"), sample_shape, dtype)
+
+    @staticmethod
+    def write_directory(path: str, num_samples: int, sample_bytes: int, seed: int = 0) -> None:
+        """write_directory_dataset (pipeline.py:139-155): file i is the
+        SplitMix64 stream keyed derive_key(seed, 0, i), generated on the GPU;
+        ``sample-%08d.bin`` files plus ``manifest.txt``."""
+        import os
+
+        import torch
+
+        if sample_bytes % 8:
+            raise ValueError("sample_bytes must be a multiple of 8")
+        os.makedirs(path, exist_ok=True)
+        dev = torch.empty(num_samples * sample_bytes, dtype=torch.uint8, device="cuda")
+        dp.make_store(dev, seed, num_samples, sample_bytes)
+        host = dev.cpu().numpy()
+        names = []
+        for i in range(num_samples):
+            name = f"sample-{i:08d}.bin"
+            with open(os.path.join(path, name), "wb") as fh:
+                fh.write(host[i * sample_bytes:(i + 1) * sample_bytes].tobytes())
+            names.append(name)
+        with open(os.path.join(path, "manifest.txt"), "w", encoding="utf-8") as fh:
+            fh.write("\n".join(names) + "\n")
+
+    @classmethod
     def synthetic(cls, seed: int, num_samples: int, sample_shape, dtype: DType = DType.U8,
                   location: str = "hbm"):
         """Store whose file i = fill(derive_key(seed, 0, i)) (pipeline.py:139-155)."""

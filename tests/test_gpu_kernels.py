@@ -245,3 +245,32 @@ def test_zero_copy_view_is_the_slot():
     assert a.data_ptr() == b.data_ptr() == ring.slot_ptr(1)
     torch.cuda.synchronize()
     assert float(a.sum()) == 3.5 * 1024
+
+
+def test_directory_source_files_and_batches_match_reference(golden, tmp_path):
+    """StoreSource.write_directory / from_directory (pipeline.py:45-54,139-155,
+    190-210): the files equal the reference's write_directory_dataset bytes
+    and the gathered batches equal its prepare_batch (golden CRCs)."""
+    import zlib
+
+    from paper_2409_18749_b200 import CollateLoader, DatasetSpec, StoreSource
+
+    d = golden["directory"]
+    StoreSource.write_directory(str(tmp_path), d["num_samples"], d["sample_bytes"], d["seed"])
+    for i, want in enumerate(d["file_crc32"]):
+        data = (tmp_path / f"sample-{i:08d}.bin").read_bytes()
+        assert zlib.crc32(data) == want
+    for location in ("pinned", "hbm"):
+        store = StoreSource.from_directory(str(tmp_path), (d["sample_bytes"],),
+                                           location=location)
+        ld = CollateLoader(DatasetSpec(store, d["num_samples"], d["batch_size"],
+                                       shuffle_seed=d["shuffle_seed"]))
+        for case in d["batches"]:
+            buf = torch.empty(ld.batch_nbytes, dtype=torch.uint8, device="cuda")
+            ld.produce_into(buf.data_ptr(), case["epoch"], case["batch_index"])
+            got = buf.cpu().numpy()
+            assert zlib.crc32(got[:ld.input_nbytes].tobytes()) == case["crc32"]
+            np.testing.assert_array_equal(got[ld.input_nbytes:].view(np.int64), case["indices"])
+    (tmp_path / "sample-00000003.bin").write_bytes(b"short")
+    with pytest.raises(ValueError, match="expected"):
+        StoreSource.from_directory(str(tmp_path), (d["sample_bytes"],))
