@@ -315,6 +315,19 @@ int tsb_consume_range(tsb_ring *r, int consumer, uint64_t seq0, int n, void **ev
 int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_produce_args *a,
                       int shard, int n_shards, uint64_t seq0, int64_t batch0, int n,
                       const int *live, const int *n_live, void *stream);
+/* Two-stage multi-GPU production, stage 2 (NEW): stage 1 is
+ * tsb_produce_group in TSB_SRC_GATHER mode into per-GPU INPUT rings (the
+ * compact u8 rows cross NVLink: 1x the input instead of the 2-4x larger
+ * f32/bf16 outputs), target = the real sample indices.  Stage 2, per GPU,
+ * for each batch q: host-wait until every writer's shard is in in_ring,
+ * host-gate out_ring's slot on its live consumers, collate/augment the
+ * staged rows into out_ring's slot (params keyed by the staged indices) with
+ * the fused publish, then release the input slot from the stream
+ * (in_ring cursor in_consumer := q).  a: augment geometry of the OUTPUT and
+ * a->ingest for the param / identity tables. */
+int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
+                        const tsb_produce_args *a, uint64_t seq0, int n, const int *live,
+                        int n_live, void *stream);
 /* One process driving every writer (TensorProducer(devices=...)): for each
  * of n batches, one host gate over all rings, then writer w (of n_writers =
  * the shard count) produces its shard on devices[w] / streams[w] with

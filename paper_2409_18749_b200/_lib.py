@@ -155,6 +155,8 @@ SRC_AUGMENT, SRC_GATHER, SRC_SYNTHETIC = 0, 1, 2
 SIGNATURES["tsb_produce_range"] = (i32, [vp, ctypes.POINTER(ProduceArgs), u64, i64, i32,
                                          ctypes.POINTER(i32), i32, pp, vp])
 SIGNATURES["tsb_consume_range"] = (i32, [vp, i32, u64, i32, pp, vp])
+SIGNATURES["tsb_restage_collate"] = (i32, [vp, i32, vp, ctypes.POINTER(ProduceArgs), u64, i32,
+                                           ctypes.POINTER(i32), i32, vp])
 SIGNATURES["tsb_produce_group_multi"] = (i32, [pp, i32, ctypes.POINTER(ProduceArgs),
                                                ctypes.POINTER(i32), ctypes.POINTER(i32), pp, i32,
                                                u64, i64, i32, ctypes.POINTER(i32),

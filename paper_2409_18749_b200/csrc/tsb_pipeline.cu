@@ -387,4 +387,55 @@ int tsb_produce_group_multi(tsb_ring *const *rings, int n_rings, const tsb_produ
     return rc;
 }
 
+int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
+                        const tsb_produce_args *a, uint64_t seq0, int n, const int *live,
+                        int n_live, void *stream) {
+    TSB_CHECK(in_ring && out_ring && a && a->ingest, "null argument (tables come from a->ingest)");
+    TSB_CHECK(a->mode == TSB_SRC_AUGMENT, "stage 2 collates/augments the staged rows");
+    TSB_CHECK(ring_has_host_control(in_ring) && ring_has_host_control(out_ring) &&
+                  ring_writers(out_ring) == 1,
+              "host-control rings; the output ring has one writer");
+    TSB_CHECK(seq0 >= 1 && n >= 0, "bad range");
+    const int64_t b = a->batch_size;
+    const int64_t sb = a->sample_bytes;
+    int in_slots = 0, out_slots = 0;
+    size_t in_stride = 0, out_stride = 0;
+    if (int rc = tsb_ring_geometry(in_ring, &in_slots, &in_stride, nullptr)) return rc;
+    if (int rc = tsb_ring_geometry(out_ring, &out_slots, &out_stride, nullptr)) return rc;
+    TSB_CHECK(in_stride >= (size_t)(b * sb + 8 * b), "input slot too small for %lld rows + targets",
+              (long long)b);
+    const size_t out_bytes = (size_t)a->input_bytes + (a->with_target ? 8 * (size_t)b : 0);
+    TSB_CHECK(out_stride >= out_bytes, "output slot too small");
+    for (int i = 0; i < n; ++i) {
+        const uint64_t q = seq0 + (uint64_t)i;
+        const int islot = (int)((q - 1) % (uint64_t)in_slots);
+        const int oslot = (int)((q - 1) % (uint64_t)out_slots);
+        // every writer's shard of batch q is in the input slot (host-side wait)
+        if (int rc = tsb_ring_host_wait_ready(in_ring, islot, q, -1)) return rc;
+        if (q > (uint64_t)out_slots)
+            if (int rc = ring_host_gate(out_ring, live, n_live, q - (uint64_t)out_slots)) return rc;
+        void *in = nullptr, *out = nullptr;
+        if (int rc = tsb_ring_slot_ptr(in_ring, islot, &in)) return rc;
+        if (int rc = tsb_ring_slot_ptr(out_ring, oslot, &out)) return rc;
+        const int64_t *ridx = reinterpret_cast<const int64_t *>(static_cast<uint8_t *>(in) + b * sb);
+        int32_t *params = ingest_params(a->ingest, 0);
+        if (int rc = tsb_aug_params(a->seed, a->epoch, ridx, b, a->pad, a->flip, params, stream))
+            return rc;
+        uint64_t *ready = nullptr;
+        unsigned int *counter = nullptr;
+        if (int rc = ring_publish_ptrs(out_ring, oslot, 0, &ready, &counter)) return rc;
+        int64_t *tgt = a->with_target
+                           ? reinterpret_cast<int64_t *>(static_cast<uint8_t *>(out) + a->input_bytes)
+                           : nullptr;
+        if (int rc = collate_augment_publish(in, ingest_identity(a->ingest), b, a->h, a->w, a->c,
+                                             a->pad, a->flip, a->seed, a->epoch, a->scale, a->bias,
+                                             a->out_kind, out, tgt, ready, q, counter, 0, stream,
+                                             params, ridx))
+            return rc;
+        // the kernel has read the staged rows: release the input slot (stream-ordered)
+        if (int rc = tsb_ring_ack(in_ring, in_consumer, q, stream)) return rc;
+    }
+    return TSB_OK;
+}
+
 }  // extern "C"

@@ -359,3 +359,12 @@ def produce_group_multi(rings, args_list, locals_, devices, streams, seq0: int, 
     counts = (ctypes.c_int * len(rings))(*[len(lv) for lv in live_per_ring])
     call("tsb_produce_group_multi", ptrs, len(rings), arr, loc, devs, sts, W, seq0, batch0, n,
          live, counts)
+
+
+def restage_collate(in_ring: DeviceRing, in_consumer: int, out_ring: DeviceRing, args,
+                    seq0: int, n: int, live, stream=None) -> None:
+    """Stage 2 of two-stage multi-GPU production (tsb_restage_collate)."""
+    live = list(live)
+    arr = (ctypes.c_int * max(1, len(live)))(*live)
+    call("tsb_restage_collate", in_ring._h, in_consumer, out_ring._h, ctypes.byref(args), seq0, n,
+         arr, len(live), _stream(stream))

@@ -231,3 +231,87 @@ def test_group_cross_process_ipc():
     for p in procs:
         p.join(60)
     assert results == {r: "ok" for r in range(world)}, results
+
+
+@pytest.mark.parametrize("out_dtype,kind", [("float32", 1), ("bfloat16", 2)])
+def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind):
+    """Two-stage multi-GPU production: stage 1 all-gathers the compact u8 rows
+    into every GPU's input ring (passthrough group, G writers); stage 2 on
+    each GPU collates the staged rows into its own output ring
+    (tsb_restage_collate).  G = 2 'GPUs' on device 0, threads as ranks."""
+    from paper_2409_18749_b200._lib import GATE_HOST
+    from paper_2409_18749_b200.collate import _Ingest
+    from paper_2409_18749_b200.ring import restage_collate
+
+    h, w, c, B, N, G, n = 32, 64, 3, 8, 64, 2, 12
+    store = StoreSource.synthetic(8, N, (h, w, c))
+    gather_ld = CollateLoader(DatasetSpec(store, N, B, shuffle_seed=6))
+    aug_ld = CollateLoader(DatasetSpec(store, N, B, shuffle_seed=6),
+                           AugmentSpec(pad=4, flip=True, out_dtype=out_dtype, seed=2))
+    in_rings = [DeviceRing(3, gather_ld.batch_nbytes, 1, control="host", writers=G)
+                for _ in range(G)]
+    out_rings = [DeviceRing(3, aug_ld.batch_nbytes, 1, control="host") for _ in range(G)]
+    for r in in_rings + out_rings:
+        r.set_cursor(0, 0)
+    tables = [_Ingest(0, B, h * w * c) for _ in range(G)]
+    L = len(aug_ld)
+    errors, got = [], {g: {} for g in range(G)}
+
+    def stage1(g):
+        try:
+            s = torch.cuda.Stream()
+            q = 1
+            while q <= n:
+                e, bi = divmod(q - 1, L)
+                m = min(n - q + 1, L - bi)
+                a = gather_ld.produce_args(e)
+                produce_group(in_rings, g, a, g, G, q, bi, m, [[0]] * G, stream=s)
+                q += m
+            s.synchronize()
+        except Exception as ex:  # noqa: BLE001
+            errors.append(("stage1", g, repr(ex)))
+
+    def stage2(g):
+        try:
+            s = torch.cuda.Stream()
+            q = 1
+            while q <= n:
+                e, bi = divmod(q - 1, L)
+                m = min(n - q + 1, L - bi)
+                from paper_2409_18749_b200._lib import ProduceArgs
+
+                a = ProduceArgs.from_buffer_copy(aug_ld.produce_args(e))
+                a.ingest = tables[g].handle
+                a.gate = GATE_HOST
+                restage_collate(in_rings[g], 0, out_rings[g], a, q, m, [0], stream=s)
+                q += m
+            s.synchronize()
+        except Exception as ex:  # noqa: BLE001
+            errors.append(("stage2", g, repr(ex)))
+
+    def consumer(g):
+        r = out_rings[g]
+        for q in range(1, n + 1):
+            r.host_wait_ready(r.slot_of(q), q, timeout_s=60)
+            got[g][q] = r.view(r.slot_of(q), (aug_ld.batch_nbytes,), torch.uint8).cpu().numpy()
+            r.host_ack(0, q)
+
+    ts = [threading.Thread(target=f, args=(g,)) for f in (stage1, stage2, consumer)
+          for g in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+        assert not t.is_alive(), "two-stage pipeline hung"
+    assert not errors, errors
+    store_h = oracle.make_store(8, N, h * w * c)
+    scale, bias = oracle.norm_consts()
+    for q in range(1, n + 1):
+        e, bi = divmod(q - 1, L)
+        idx = oracle.epoch_order(N, 6, e)[bi * B:(bi + 1) * B]
+        x = oracle.collate_augment(store_h, idx, h, w, c, 4, True, 2, e, kind, scale, bias)
+        want = np.concatenate([x.reshape(-1).view(np.uint8), idx.astype("<i8").view(np.uint8)])
+        for g in range(G):
+            assert got[g][q].tobytes() == want.tobytes(), (g, q)
+    for r in in_rings + out_rings:
+        r.close()
