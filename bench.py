@@ -273,32 +273,52 @@ def run_ours(args):
                                        TensorProducer)
     from paper_2409_18749_b200 import dataplane as dp
     from paper_2409_18749_b200._lib import GATE_HOST
-    from paper_2409_18749_b200.ring import DeviceRing, produce_group, produce_range
+    from paper_2409_18749_b200._lib import ProduceArgs
+    from paper_2409_18749_b200.ring import (DeviceRing, produce_group, produce_range,
+                                            restage_collate)
 
     K, Wm = args.steps, args.warmup
     ctx = mp.get_context("spawn")
 
     # ---- device-resident run (value) ----
-    # One logical producer: at N GPUs every rank ingests and collates its 1/N
-    # shard of each batch and the collate kernel stores it straight into the
-    # same slot of every rank's ring (own HBM + peers over NVLink: the
-    # all-gather fused into the producing kernel, tsb_produce_group); each
-    # rank's 4 consumers see every whole batch.  N = 1 is exactly C2.
+    # One logical producer.  N = 1 is exactly C2.  At N GPUs (default
+    # TSB_BENCH_FANOUT=inputs, two-stage): every rank gathers its 1/N rows of
+    # each batch (compact u8) into the same slot of every rank's INPUT ring
+    # (own HBM + peers over NVLink, tsb_produce_group), then each rank
+    # collates the whole staged batch locally into its output ring
+    # (tsb_restage_collate) -- 1x the input crosses NVLink instead of the 4x
+    # larger f32 output.  TSB_BENCH_FANOUT=outputs: the collate kernel itself
+    # stores its 1/N output rows into every rank's output ring (fused
+    # all-gather of the outputs).  Each rank's 4 consumers see every batch.
+    fanout = os.environ.get("TSB_BENCH_FANOUT", "inputs") if world > 1 else "none"
     store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="hbm")
     ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
     loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
+    out_writers = world if fanout == "outputs" else 1
     ring = DeviceRing(RING_SLOTS, loader.batch_nbytes, N_CONSUMERS, device=dev, control="host",
-                      writers=world)
+                      writers=out_writers)
     handle = ring.export()
     rings = [ring]
+    in_ring, in_rings, gather_ld, tables = None, None, None, None
     if world > 1:
         from paper_2409_18749_b200 import group
 
-        rings = group.open_group(ring, group.exchange(group.describe(ring, rank)), rank)
+        if fanout == "outputs":
+            rings = group.open_group(ring, group.exchange(group.describe(ring, rank)), rank)
+        else:
+            from paper_2409_18749_b200.collate import _Ingest
+
+            gather_ld = CollateLoader(ds)  # u8 rows + target indices (stage 1)
+            in_ring = DeviceRing(4, gather_ld.batch_nbytes, 1, device=dev, control="host",
+                                 writers=world)
+            in_ring.set_cursor(0, 0)
+            in_rings = group.open_group(in_ring, group.exchange(group.describe(in_ring, rank)),
+                                        rank)
+            tables = _Ingest(dev, B, SAMPLE_BYTES)
     q = ctx.Queue()
     procs = [ctx.Process(target=host_consumer,
                          args=(dev, handle, ring.control_name, RING_SLOTS, loader.batch_nbytes,
-                               N_CONSUMERS, k, Wm, K, q, world))
+                               N_CONSUMERS, k, Wm, K, q, out_writers))
              for k in range(N_CONSUMERS)]
     for p in procs:
         p.start()
@@ -308,21 +328,41 @@ def run_ours(args):
     live = list(range(N_CONSUMERS))
     L = len(loader)
 
-    def produce(seq0, n):
-        """Enqueue n batches starting at global seq0 (1-based), across epochs."""
+    def chunks(seq0, n):
         done = 0
         while done < n:
             q0 = seq0 + done
             epoch, bi = divmod(q0 - 1, L)
             m = min(n - done, L - bi)
+            yield q0, epoch, bi, m
+            done += m
+
+    def stage1(seq0, n, s1):
+        for q0, epoch, bi, m in chunks(seq0, n):
+            produce_group(in_rings, rank, gather_ld.produce_args(epoch), rank, world, q0, bi, m,
+                          [[0]] * world, stream=s1)
+
+    def produce(seq0, n):
+        """Enqueue n batches starting at global seq0 (1-based), across epochs."""
+        feeder = None
+        if fanout == "inputs":  # stage 1 runs beside stage 2 on its own thread + stream
+            s1 = torch.cuda.Stream()
+            feeder = threading.Thread(target=stage1, args=(seq0, n, s1))
+            feeder.start()
+        for q0, epoch, bi, m in chunks(seq0, n):
             a = loader.produce_args(epoch)
             a.gate = GATE_HOST  # gate on the host-shared cursors; PDL-chained kernels
             if world == 1:
                 produce_range(ring, a, q0, bi, m, live, stream=stream)
-            else:
+            elif fanout == "outputs":
                 produce_group(rings, rank, a, rank, world, q0, bi, m, [live] * world,
                               stream=stream)
-            done += m
+            else:
+                a2 = ProduceArgs.from_buffer_copy(a)
+                a2.ingest = tables.handle
+                restage_collate(in_ring, 0, ring, a2, q0, m, live, stream=stream)
+        if feeder is not None:
+            feeder.join()
 
     produce(1, Wm)
     stream.synchronize()
@@ -357,9 +397,11 @@ def run_ours(args):
     else:
         ms_max = ms
     value = world * N_CONSUMERS * B * K / (ms_max / 1e3)
-    for r in rings:
-        if r is not ring:
+    for r in rings + (in_rings or []):
+        if r is not ring and r is not in_ring:
             r.close()
+    if in_ring is not None:
+        in_ring.close()
     ring.close()
     del store, loader
 
@@ -375,17 +417,21 @@ def run_ours(args):
                     "alg_bytes_per_launch": B * ALG_BYTES_PER_SAMPLE,
                     "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src}
     else:
-        # binding link: each rank's NVLink egress, its shard stored into N-1 peers
-        egress = (B // world) * OUT_BYTES * (world - 1)
+        # binding link: each rank's NVLink egress -- its 1/N rows stored into the
+        # N-1 peers' rings (u8 input rows for the two-stage path, f32 outputs else)
+        row_bytes = SAMPLE_BYTES if fanout == "inputs" else OUT_BYTES
+        egress = (B // world) * row_bytes * (world - 1)
         achieved = egress / (ms_max / K / 1e3) / 1e9
         roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_GBS,
                     "unit": "GB/s", "frac": round(achieved / NVLINK_GBS, 4), "traffic": None,
-                    "kernel": "collate_augment_kernel<f32,C=3,MULTI> (fused all-gather)",
+                    "kernel": ("passthrough_multi_kernel (u8 row all-gather) + local "
+                               "collate_augment_kernel<f32>" if fanout == "inputs" else
+                               "collate_augment_kernel<f32,C=3,MULTI> (fused all-gather)"),
                     "alg_bytes_per_launch": egress, "avg_launch_ms": round(ms_max / K, 5),
                     "peak_source": "B200_PROFILING.md measured peer copy, per direction per GPU",
+                    "fanout": fanout,
                     "hbm_achieved_gbs": round(
-                        (B // world) * SAMPLE_BYTES / (ms_max / K / 1e3) / 1e9 +
-                        B * OUT_BYTES / (ms_max / K / 1e3) / 1e9, 1)}
+                        B * ALG_BYTES_PER_SAMPLE / (ms_max / K / 1e3) / 1e9, 1)}
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
         "steps": K, "warmup": Wm, "ms_per_step": round(ms_max / K, 4), "higher_is_better": True,
@@ -397,10 +443,15 @@ def run_ours(args):
                    "ring_slots": RING_SLOTS, "sample": "224x224x3 u8 -> 3x224x224 f32",
                    "store": "HBM-resident (value) / pinned host (e2e)",
                    "l2": "inputs larger than L2: 2.47 GB store, 1.2 GB ring of 8 slots",
-                   "parallelism": (f"sharded ingest over {world} GPUs (each collates B/{world} rows "
-                                   "of every batch) + all-gather fused into the collate kernel "
-                                   "(P2P stores into every rank's ring slot); 4 IPC consumers "
-                                   "per GPU" if world > 1 else "1 producer, 4 IPC consumers"),
+                   "parallelism": (
+                       (f"two-stage: every rank gathers B/{world} u8 rows of each batch into "
+                        "every rank's input ring (P2P stores over NVLink), then collates the "
+                        "whole batch locally; 4 IPC consumers per GPU")
+                       if fanout == "inputs" else
+                       (f"sharded ingest over {world} GPUs (each collates B/{world} rows of "
+                        "every batch) + all-gather fused into the collate kernel (P2P stores "
+                        "into every rank's ring slot); 4 IPC consumers per GPU")
+                       if world > 1 else "1 producer, 4 IPC consumers"),
                    "sync": "slot-reuse gate on the host-shared release cursors (producer thread "
                            "blocks, never the stream); fused publish (release store from the "
                            "kernel's last CTA); consecutive batches chained with programmatic "
@@ -408,7 +459,9 @@ def run_ours(args):
                            "bs/cli.py:252-258)"},
         "roofline": roofline,
         "e2e": e2e,
-        "gpu_launches": K,
+        # per step: the collate (N=1, outputs fan-out); the row gather + param
+        # table + collate (two-stage)
+        "gpu_launches": K if fanout != "inputs" else 3 * K,
         "clocks": clk,
         "extra": {"producer_ms": round(ms, 3),
                   "consumer_rates_samples_s": {str(k): round(v, 1) for k, v in consumer_rates.items()},
