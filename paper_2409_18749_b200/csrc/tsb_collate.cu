@@ -167,6 +167,8 @@ struct CaGeom {
     int use_direct;    // collate_direct_kernel (TSB_CA_IMPL=direct A/B)
     int st_cs;         // streaming (evict-first) output stores (TSB_CA_ST=plain disables)
     int ld_hint;       // L2 evict-first policy on the TMA source loads (TSB_CA_LDHINT=0 disables)
+    int blocked;       // CTA c walks a contiguous run of items (TSB_CA_ORDER=blocked), else round-robin
+    int occ_cap;       // resident CTAs per SM cap (TSB_CA_OCC; 0 = occupancy limit)
     int64_t plane;     // h*w
     int64_t sample_bytes;
 };
@@ -413,7 +415,18 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     ItemPar *par = reinterpret_cast<ItemPar *>(empty + g.nstage);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int nk = (g.items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    // this CTA's items: item(k) = i0 + k * istep
+    int nk, i0, istep;
+    if (g.blocked) {
+        const int base = g.items / (int)gridDim.x, rem = g.items % (int)gridDim.x;
+        nk = base + ((int)blockIdx.x < rem);
+        i0 = (int)blockIdx.x * base + min((int)blockIdx.x, rem);
+        istep = 1;
+    } else {
+        nk = (g.items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+        i0 = (int)blockIdx.x;
+        istep = (int)gridDim.x;
+    }
 
     // zero all stages + the zero row once: borders are never overwritten
     {
@@ -423,7 +436,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     }
     // crop/flip params + source offsets of this CTA's items, derived in parallel
     for (int k = tid; k < min(nk, META_CAP); k += blockDim.x)
-        par[k] = item_par(g, blockIdx.x + k * gridDim.x, idx, params, aug_mixed, epoch, flip_en);
+        par[k] = item_par(g, i0 + k * istep, idx, params, aug_mixed, epoch, flip_en);
     if (tid == 0) {
         for (int i = 0; i < g.nstage; ++i) {
             mbar_init(&full[i], g.use_tma ? 1 : 32);
@@ -435,8 +448,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
 
     auto get_par = [&](int k) -> ItemPar {
         return k < META_CAP ? par[k]
-                            : item_par(g, blockIdx.x + k * gridDim.x, idx, params, aug_mixed,
-                                       epoch, flip_en);
+                            : item_par(g, i0 + k * istep, idx, params, aug_mixed, epoch, flip_en);
     };
 
     if (warp == NCW) {
@@ -444,7 +456,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
         for (int k = 0; k < nk; ++k) {
             const int st = k % g.nstage;
             if (k >= g.nstage) mbar_wait(&empty[st], ((k / g.nstage) - 1) & 1);
-            const int item = blockIdx.x + k * gridDim.x;
+            const int item = i0 + k * istep;
             const ItemPar p = get_par(k);
             const int y0 = (item - p.s * g.nrb) << g.log2r;
             const int nrows = min(g.R, g.h - y0);
@@ -510,7 +522,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     const int dx = (CA_THREADS - dr * g.groups) * P;
     for (int k = 0; k < nk; ++k) {
         const int st = k % g.nstage;
-        const int item = blockIdx.x + k * gridDim.x;
+        const int item = i0 + k * istep;
         const ItemPar p = get_par(k);
         const int y0 = (item - p.s * g.nrb) << g.log2r;
         const int nrows = min(g.R, g.h - y0);
@@ -710,7 +722,8 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
         occ_cache[dev] = occ > 0 ? occ : 1;
         smem_cache[dev] = smem;
     }
-    const int slots = sm_count() * occ_cache[dev];
+    const int occ = g.occ_cap > 0 && g.occ_cap < occ_cache[dev] ? g.occ_cap : occ_cache[dev];
+    const int slots = sm_count() * occ;
     const int grid = g.items < slots ? g.items : slots;
     if (ep.pdl) {
         cudaLaunchConfig_t cfg{};
@@ -841,15 +854,22 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
                    (g.sample_bytes % 4 == 0) && (((uintptr_t)src & 3) == 0) && b <= DC_MAX_B &&
                    b * (int64_t)h * (w / vec) < (1ll << 31);
     // rows per item (measured on B200, B=256 224x224x3): enough output per item to
-    // amortise the per-item pipeline handoff -- f32 R=4 (10.7 KB out), bf16/u8 R=16.
-    // (profiles/r1/sweep_collate.txt: f32 R=4 x3 stages 37.2 us, bf16 R=16 x2 22.6 us,
-    // u8 R=16 x3 16.9 us per B=256 batch)
-    int R = out_kind == TSB_OUT_F32 ? 4 : 16;
+    // amortise the per-item pipeline handoff -- f32 R=8 (21.5 KB out) with 2
+    // resident CTAs per SM (below), bf16/u8 R=16 (profiles/r1/sweep_collate.txt,
+    // sweep_collate_occ.txt, bench_f32_occ_ab.txt).
+    int R = out_kind == TSB_OUT_F32 ? 8 : 16;
     while (R > 1 && (int64_t)R > h) R >>= 1;
     while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R >>= 1;
     int nstage = out_kind == TSB_OUT_BF16 ? 2 : 3;
-    if (const char *e = getenv("TSB_CA_R")) R = atoi(e);          // tuning knobs
+    const char *env_R = getenv("TSB_CA_R");
+    if (env_R) R = atoi(env_R);                                    // tuning knobs
     if (const char *e = getenv("TSB_CA_STAGES")) nstage = atoi(e);
+    {
+        const char *e1 = getenv("TSB_CA_ORDER");
+        const char *e2 = getenv("TSB_CA_OCC");
+        g.blocked = e1 && strcmp(e1, "blocked") == 0;
+        g.occ_cap = e2 ? atoi(e2) : 0;
+    }
     TSB_CHECK(R >= 1 && R <= 64 && (R & (R - 1)) == 0, "rows per item must be a power of 2 <= 64");
     TSB_CHECK(nstage >= 1 && nstage <= MAX_STAGES, "stages must be 1..%d", MAX_STAGES);
     if (R > h) R = 1;
@@ -864,8 +884,27 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     TSB_CHECK(b * (int64_t)g.nrb < (1ll << 31), "too many work items");
     g.items = (int)(b * g.nrb);
     g.slots = R * g.groups;
-    const size_t smem = (size_t)(nstage * R + 1) * g.rs + 2 * nstage * sizeof(uint64_t) +
-                        META_CAP * sizeof(ItemPar);
+    size_t smem = (size_t)(nstage * R + 1) * g.rs + 2 * nstage * sizeof(uint64_t) +
+                  META_CAP * sizeof(ItemPar);
+    // Resident CTAs per SM: reserve shared memory so at most `resident` CTAs
+    // fit on an SM.  f32: 2 CTAs of 8-row stages -- longer read bursts between
+    // the 4x larger write streams -- and the next PDL-launched batch's CTAs
+    // only take an SM's slots as this batch's CTAs retire, instead of
+    // co-running beside them (bench: 36.8 vs 37.4 us per B=256 batch at the
+    // old R=4 / full occupancy; profiles/r1/bench_f32_occ_ab.txt).
+    int resident = out_kind == TSB_OUT_F32 && !env_R ? 2 : 0;
+    if (const char *e = getenv("TSB_CA_RESIDENT")) resident = atoi(e);
+    if (resident > 0) {
+        static int smem_sm = 0;
+        if (!smem_sm) {
+            int dv = 0;
+            cudaGetDevice(&dv);
+            TSB_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dv));
+        }
+        // the runtime reserves 1 KB of shared memory per resident CTA
+        const size_t want = (size_t)smem_sm / (size_t)resident - 1024 - 128;
+        if (want > smem && want <= 200 * 1024) smem = want;
+    }
     TSB_CHECK(smem <= 200 * 1024, "row too wide for shared staging (%zu B)", smem);
     const uint64_t aug_mixed = mix64(aug_seed ^ AUG_DOMAIN);
     const auto *s8 = static_cast<const uint8_t *>(src);
