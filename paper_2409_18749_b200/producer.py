@@ -14,9 +14,12 @@ Differences behind the same API (B200 data plane):
   segment per batch; a ``CollateLoader`` writes each batch straight into its
   slot with the fused collate/augment kernel, any other loader's (input,
   target) pairs are copied in once;
-* release is device-counted: consumers advance a cursor word from their own
-  CUDA stream; the producer's stream waits on the cursors before reusing a
-  slot -- no host round trip on the data path;
+* release is counted in cursor words: consumers advance their cursor (from
+  their own CUDA stream, or a host store into the host-shared control block);
+  before reusing a slot the producer thread checks the cursors on the host
+  (control="host": the producer's streams never wait on a device word) or its
+  stream waits on them (control="device"); the Ack frames still feed the
+  reference's ledger bookkeeping;
 * the reference's wire protocol is kept byte-for-byte (Join/Welcome/Announce/
   Ack/Heartbeat/EpochStart/EpochEnd/Bye/Shutdown); the Announce's segment
   name carries the slot and its 80-byte segment header (segment.py).
@@ -132,6 +135,12 @@ class TensorProducer:
         self._monitors: list[Conn] = []
         self._ledger = Ledger()
         self._next_cursor = 0
+        # cursor words of departed consumers, reused after a quarantine: a
+        # consumer that left (Bye, closed socket, rejoin) may still have one ack
+        # store in flight.  Timed-out consumers' words are never reused -- a hung
+        # process can wake up and store its old cursor (bs/producer.py:203-219
+        # evicts; here the word stays the eviction sentinel for good).
+        self._free_cursors: deque = deque()  # (cursor, free time)
         self._closed = False
         self._started = False
         self._listeners = []
@@ -442,19 +451,19 @@ class TensorProducer:
             if self._closed:
                 conn.close()
                 return None
-        if self._next_cursor >= self._max_consumers:
-            conn.close()  # cursor table exhausted
-            return None
         dev = self.device if msg.device < 0 else msg.device
         bsz = msg.batch_size if msg.batch_size != self._per_slot else 0
         k = self._ring_for_device(dev)
         if k is None or (bsz and not self._rebatch_ok(bsz)):
             conn.close()  # no ring on that GPU / batch size not servable: no Welcome
             return None
-        rec = ConsumerRecord(consumer_id=cid, cursor=self._next_cursor, last_heartbeat=now,
+        cursor = self._alloc_cursor(now)
+        if cursor is None:
+            conn.close()  # cursor table exhausted
+            return None
+        rec = ConsumerRecord(consumer_id=cid, cursor=cursor, last_heartbeat=now,
                              join_epoch=self._epoch, conn=conn, bcast=bcast, device=dev,
                              batch_size=bsz, ring=k)
-        self._next_cursor += 1
         L = max(1, len(self._loader))
         progress = self._announced_in_epoch if self._epoch_started else 0
         code = admission_code(progress, L, self._fraction)
@@ -486,13 +495,30 @@ class TensorProducer:
         self._lock.notify_all()
         return cid
 
+    @property
+    def cursor_quarantine_s(self) -> float:
+        """How long a departed consumer's cursor word rests before reuse."""
+        return 2 * self._hb_timeout
+
+    def _alloc_cursor(self, now: float) -> int | None:
+        """A cursor index valid in every ring (the cursor tables are parallel)."""
+        if self._free_cursors and now - self._free_cursors[0][1] >= self.cursor_quarantine_s:
+            return self._free_cursors.popleft()[0]
+        if self._next_cursor < self._max_consumers:
+            self._next_cursor += 1
+            return self._next_cursor - 1
+        return None
+
     def _drop(self, cid: int, reason: str, close_bcast: bool = True) -> None:
         rec = self._consumers.pop(cid, None)
         if rec is None:
             return
-        self.drops.append((cid, reason, time.monotonic()))
+        now = time.monotonic()
+        self.drops.append((cid, reason, now))
         if rec.ring in self._rings:
             self._rings[rec.ring].evict(rec.cursor)  # unblocks every wait on this consumer
+        if reason != "timeout":
+            self._free_cursors.append((rec.cursor, now))
         self._ledger.remove_consumer(cid)
         if reason == "timeout":
             self.stats["evictions"] += 1

@@ -179,3 +179,36 @@ def test_late_join_waits_for_next_epoch(endpoints):
     assert joiner["seq"] == expected(2, 20, start_epoch=1)
     assert joiner["loader"].welcome.admitted == 0  # ADMIT_WAIT
     producer.close()
+
+
+def test_consumer_churn_reuses_cursor_words(endpoints):
+    """More consumers over a job's life than cursor words: a departed
+    consumer's word (Bye) is reused after the quarantine, so a long-running
+    producer keeps admitting newcomers.  An anchor consumer stays for the
+    whole run (with no admitted consumer the producer pauses, as the
+    reference's does, sl/producer.py:282-285); five newcomers in turn share
+    the one remaining word, each receiving one whole epoch."""
+    E = 100
+    producer, pt = run_producer(SeqLoader(8, delay_s=0.01), endpoints, E, ring_slots=4,
+                                max_consumers=2, heartbeat_timeout_s=0.25)
+    anchor = {}
+    at = threading.Thread(target=consume, args=(endpoints, 1, E, anchor),
+                          kwargs={"heartbeat_interval_s": 0.05})
+    at.start()
+    deadline = time.time() + 30
+    while producer.stats["announced"] < 1 and time.time() < deadline:
+        time.sleep(0.002)
+    cursors = []
+    for k in range(5):
+        out = {}
+        consume(endpoints, 100 + k, 1, out, heartbeat_interval_s=0.05)
+        cursors.append(out["loader"]._cursor)
+        e0 = out["seq"][0][0]
+        assert out["seq"] == [(e0, i) for i in range(8)]  # one whole epoch, in order
+        time.sleep(producer.cursor_quarantine_s + 0.1)
+    assert cursors == [1] * 5 and anchor["loader"]._cursor == 0  # 6 consumers on 2 words
+    assert len(producer.drops) == 5 and all(d[1] in ("bye", "disconnect") for d in producer.drops)
+    at.join(60)
+    pt.join(60)
+    assert anchor["seq"] == expected(E, 8)
+    producer.close()
