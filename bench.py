@@ -590,7 +590,15 @@ def cpu_baseline(seconds: float = 15.0):
             break
     dt = time.monotonic() - t0
     produced = n * B / dt
+    # the same step on one thread (the CPU augment oracle on
+    # 1 thread and on nproc threads), a few batches
+    t1, n1 = time.monotonic(), 0
+    while n1 < 1 or (time.monotonic() - t1 < min(3.0, seconds / 5) and n1 < 20):
+        cpu_reference_step(o, store, order, n1 % (n_store // B), 1, out, scale, bias)
+        n1 += 1
+    produced_1t = n1 * B / (time.monotonic() - t1)
     return {"value": round(produced * N_CONSUMERS, 1), "unit": "samples/s", "cores": nthreads,
+            "single_thread_produced_samples_per_s": round(produced_1t, 1),
             "kind": "port",
             "sample": f"{n} batches x {B} samples ({dt:.1f} s): oracle C/OpenMP collate+augment "
                       f"f32 NCHW + CRC-32 per batch, {nthreads} threads; delivered = "
