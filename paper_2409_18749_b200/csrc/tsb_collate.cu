@@ -693,6 +693,28 @@ int launch_direct(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, ui
     return TSB_OK;
 }
 
+// A/B and tuning knobs (environment), read once per process: the launch
+// path runs per batch and must not walk the environment every time.
+struct CaKnobs {
+    int notma = 0;
+    int R = 0, stages = 0;     // 0 = per-kind default
+    int blocked = 0, occ = 0;  // item order, grid cap (CTAs per SM)
+    int resident = -1;         // -1 = per-kind default
+};
+const CaKnobs &ca_knobs() {
+    static const CaKnobs k = [] {
+        CaKnobs v;
+        if (const char *e = getenv("TSB_CA_NOTMA")) v.notma = atoi(e);
+        if (const char *e = getenv("TSB_CA_R")) v.R = atoi(e);
+        if (const char *e = getenv("TSB_CA_STAGES")) v.stages = atoi(e);
+        if (const char *e = getenv("TSB_CA_ORDER")) v.blocked = strcmp(e, "blocked") == 0;
+        if (const char *e = getenv("TSB_CA_OCC")) v.occ = atoi(e);
+        if (const char *e = getenv("TSB_CA_RESIDENT")) v.resident = atoi(e);
+        return v;
+    }();
+    return k;
+}
+
 int direct_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -825,8 +847,9 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     g.groups = w / vec;
     const bool aligned_rows = (g.row_bytes % 16 == 0) && (((uintptr_t)src & 15) == 0) &&
                               (g.sample_bytes % 16 == 0);
-    g.use_tma = aligned_rows && is_device_memory(src);
-    if (const char *e = getenv("TSB_CA_NOTMA")) g.use_tma = g.use_tma && !atoi(e);
+    const CaKnobs &kn = ca_knobs();
+    const bool src_dev = is_device_memory(src);
+    g.use_tma = aligned_rows && src_dev && !kn.notma;
     g.vec_ldg = aligned_rows && (g.io % 4 == 0);
     {
         static int knobs = -1;  // A/B knobs, read once per process
@@ -850,7 +873,7 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
             set_dev[dv] = 1;
         }
     }
-    g.use_direct = direct_enabled() && is_device_memory(src) && (g.row_bytes % 4 == 0) &&
+    g.use_direct = direct_enabled() && src_dev && (g.row_bytes % 4 == 0) &&
                    (g.sample_bytes % 4 == 0) && (((uintptr_t)src & 3) == 0) && b <= DC_MAX_B &&
                    b * (int64_t)h * (w / vec) < (1ll << 31);
     // rows per item (measured on B200, B=256 224x224x3): enough output per item to
@@ -861,15 +884,10 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     while (R > 1 && (int64_t)R > h) R >>= 1;
     while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R >>= 1;
     int nstage = out_kind == TSB_OUT_BF16 ? 2 : 3;
-    const char *env_R = getenv("TSB_CA_R");
-    if (env_R) R = atoi(env_R);                                    // tuning knobs
-    if (const char *e = getenv("TSB_CA_STAGES")) nstage = atoi(e);
-    {
-        const char *e1 = getenv("TSB_CA_ORDER");
-        const char *e2 = getenv("TSB_CA_OCC");
-        g.blocked = e1 && strcmp(e1, "blocked") == 0;
-        g.occ_cap = e2 ? atoi(e2) : 0;
-    }
+    if (kn.R) R = kn.R;  // tuning knobs
+    if (kn.stages) nstage = kn.stages;
+    g.blocked = kn.blocked;
+    g.occ_cap = kn.occ;
     TSB_CHECK(R >= 1 && R <= 64 && (R & (R - 1)) == 0, "rows per item must be a power of 2 <= 64");
     TSB_CHECK(nstage >= 1 && nstage <= MAX_STAGES, "stages must be 1..%d", MAX_STAGES);
     if (R > h) R = 1;
@@ -892,8 +910,8 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     // only take an SM's slots as this batch's CTAs retire, instead of
     // co-running beside them (bench: 36.8 vs 37.4 us per B=256 batch at the
     // old R=4 / full occupancy; profiles/r1/bench_f32_occ_ab.txt).
-    int resident = out_kind == TSB_OUT_F32 && !env_R ? 2 : 0;
-    if (const char *e = getenv("TSB_CA_RESIDENT")) resident = atoi(e);
+    int resident = out_kind == TSB_OUT_F32 && !kn.R ? 2 : 0;
+    if (kn.resident >= 0) resident = kn.resident;
     if (resident > 0) {
         static int smem_sm = 0;
         if (!smem_sm) {
