@@ -525,6 +525,11 @@ def run_e2e(args, ctx, dev, rank, world):
                 if produced >= total:
                     break
         producer.join(drain_timeout_s=60)
+    h2d = B * SAMPLE_BYTES  # every sample row (sharded multi-GPU ingest)
+    if producer is not None and world == 1 and loader._ingest is not None and produced:
+        # copy-engine ingest counts what it enqueued: the rows the crop reads,
+        # plus the index and parameter uploads
+        h2d = int(round(loader._ingest.bytes_enqueued() / produced))
     rates = {}
     for _ in procs:
         msg = q.get(timeout=600)
@@ -545,14 +550,15 @@ def run_e2e(args, ctx, dev, rank, world):
         torch.distributed.all_reduce(t)
         value = float(t.item())
     path = ("TensorProducer(CollateLoader(pinned-host StoreSource)) -> 4 SharedLoader processes "
-            "(CUDA IPC); each batch's rows cross PCIe by the copy engine; consumers .item() one "
-            "element per batch")
+            "(CUDA IPC); each batch's sample rows that the crop reads cross PCIe by the copy "
+            "engine, with the host-derived crop/flip table; consumers .item() one element per "
+            "batch")
     if world > 1:
         path = (f"one TensorProducer(devices={world} GPUs, sharded ingest: each GPU reads its "
                 "1/N rows of every batch from pinned host memory, fused all-gather into every "
                 "ring) -> 4 SharedLoader(device=g) processes per GPU; consumers .item() per batch")
     return {"value": round(value, 1), "unit": "samples/s",
-            "h2d_bytes_per_step": B * SAMPLE_BYTES,
+            "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * N_CONSUMERS * world,
             "path": path,
             "per_consumer": {str(k): round(v, 1) for k, v in rates.items()},

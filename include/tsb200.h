@@ -226,6 +226,10 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
 int tsb_ingest_destroy(tsb_ingest *g);
 /* 1 if the batched-copy driver API is in use, 0 if per-sample copies. */
 int tsb_ingest_batch_api(tsb_ingest *g, int *used);
+/* Host->device bytes this ingest has enqueued so far (sample rows + index and
+ * parameter uploads).  Augment batches copy only the source rows the crop
+ * reads: h - |oy - pad| of the h rows of each sample. */
+int tsb_ingest_bytes(tsb_ingest *g, uint64_t *bytes);
 
 /* JPEG sample source (NEW; the paper's decode step, in
  * front of the reference's DirectorySource, pipeline.py:45-54,190-210):

@@ -108,6 +108,7 @@ SIGNATURES: dict[str, tuple] = {
     "tsb_ingest_create": (i32, [i32, i64, i64, i32, pp]),
     "tsb_ingest_destroy": (i32, [vp]),
     "tsb_ingest_batch_api": (i32, [vp, ctypes.POINTER(i32)]),
+    "tsb_ingest_bytes": (i32, [vp, ctypes.POINTER(ctypes.c_uint64)]),
     "tsb_jpeg_available": (i32, [ctypes.POINTER(i32)]),
     "tsb_jpeg_create": (i32, [i32, i64, i32, i32, i32, pp]),
     "tsb_jpeg_backend": (i32, [vp, ctypes.POINTER(i32)]),

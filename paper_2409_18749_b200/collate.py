@@ -520,6 +520,14 @@ class _Ingest:
         self._lib.call("tsb_ingest_batch_api", self.handle, ctypes.byref(v))
         return bool(v.value)
 
+    def bytes_enqueued(self) -> int:
+        """Host->device bytes enqueued so far (tsb_ingest_bytes)."""
+        import ctypes
+
+        v = ctypes.c_uint64(0)
+        self._lib.call("tsb_ingest_bytes", self.handle, ctypes.byref(v))
+        return int(v.value)
+
     def __del__(self):
         try:
             if self.handle:

@@ -92,11 +92,7 @@ __global__ void gather_v1_kernel(const uint8_t *__restrict__ src, const int64_t 
 //   oy = mix64(ka+1G) % (2P+1), ox = mix64(ka+2G) % (2P+1), flip = mix64(ka+3G) & 1
 __device__ __forceinline__ void derive_aug(uint64_t aug_mixed, uint64_t epoch, int64_t index,
                                            int pad, int flip_en, int &oy, int &ox, int &fl) {
-    const uint64_t ka = derive_key(aug_mixed, epoch, (uint64_t)index);
-    const uint64_t m = (uint64_t)(2 * pad + 1);
-    oy = (int)(mix64(ka + GAMMA) % m);
-    ox = (int)(mix64(ka + 2 * GAMMA) % m);
-    fl = flip_en ? (int)(mix64(ka + 3 * GAMMA) & 1) : 0;
+    derive_aug_host(aug_mixed, epoch, index, pad, flip_en, oy, ox, fl);
 }
 
 __global__ void aug_params_kernel(uint64_t aug_mixed, uint64_t epoch,

@@ -61,6 +61,27 @@ __host__ __device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t 
     return h;
 }
 
+// Augment params of one sample (SURVEY.md §8a A6'), host and device:
+//   ka = derive_key(mix64(aug_seed ^ AUG_DOMAIN), epoch, idx)
+//   oy = mix64(ka+1G) % (2P+1), ox = mix64(ka+2G) % (2P+1), flip = mix64(ka+3G) & 1
+__host__ __device__ __forceinline__ void derive_aug_host(uint64_t aug_mixed, uint64_t epoch,
+                                                         int64_t index, int pad, int flip_en,
+                                                         int &oy, int &ox, int &fl) {
+    const uint64_t ka = derive_key(aug_mixed, epoch, (uint64_t)index);
+    const uint64_t m = (uint64_t)(2 * pad + 1);
+    oy = (int)(mix64(ka + GAMMA) % m);
+    ox = (int)(mix64(ka + 2 * GAMMA) % m);
+    fl = flip_en ? (int)(mix64(ka + 3 * GAMMA) & 1) : 0;
+}
+
+// Crop geometry for a crop-aware ingest (tsb_ingest.cu): which source rows of
+// each staged sample the collate kernel will read.
+struct IngestCrop {
+    uint64_t aug_mixed;  // mix64(aug_seed ^ AUG_DOMAIN)
+    uint64_t epoch;
+    int h, row_bytes, pad, flip;
+};
+
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int sm_count() {

@@ -28,6 +28,8 @@ struct tsb_ingest {
     int32_t *d_params;    // [depth][max_batch][3] crop/flip table
     int64_t *d_identity;  // [max_batch] 0..max_batch-1 (rows of a staged batch)
     int64_t *h_idx;       // [depth][max_batch] pinned upload buffer
+    int32_t *h_params;    // [depth][max_batch][3] pinned upload buffer (crop-aware batches)
+    uint64_t bytes;       // H2D bytes enqueued (tsb_ingest_bytes)
     cudaStream_t stream;  // copy-engine stream
     std::vector<cudaEvent_t> done, freed;
     std::vector<int> used;
@@ -51,8 +53,16 @@ void preload_ingest() { touch_kernel(iota_kernel); }
 // Enqueue the H2D copy of batch rows h_idx[0..b) of `host_store` on the
 // ingest stream, into staging buffer k (or `dst` when non-null), plus the
 // index upload; `stream` waits for it.  Returns k.
+//
+// With `crop` (augment batches): the crop/flip params of every sample are
+// derived here on the host -- the same pure function of (aug seed, epoch,
+// sample index) the device uses (SURVEY.md §8a A6') -- and uploaded with the
+// indices, and only the source rows the crop reads cross PCIe: output row y
+// reads source row y + oy - pad, so rows [max(0, oy-pad), min(h, h+oy-pad))
+// of each sample (on average 8.2 of 224 rows fewer at pad 16).  The collate
+// kernel loads exactly those rows of a staged sample, never the others.
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
-                 void *dst, void *stream, int *k_out, bool after_stream) {
+                 void *dst, void *stream, int *k_out, bool after_stream, const IngestCrop *crop) {
     TSB_CHECK(g && host_store && h_idx && k_out, "null argument");
     TSB_CHECK(b >= 1 && b <= g->max_batch, "batch %lld exceeds the ingest capacity %lld",
               (long long)b, (long long)g->max_batch);
@@ -73,10 +83,28 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
                        : g->staging + (size_t)k * (size_t)(g->max_batch * g->sample_bytes);
     const uint8_t *src = static_cast<const uint8_t *>(host_store);
     const size_t sb = (size_t)g->sample_bytes;
+    int32_t *hp = g->h_params + (size_t)k * g->max_batch * 3;
+    size_t nbytes = 0;
     for (int64_t i = 0; i < b; ++i) {
-        g->dsts[i] = out + (size_t)i * sb;
-        g->srcs[i] = const_cast<uint8_t *>(src + (size_t)h_idx[i] * sb);
-        g->sizes[i] = sb;
+        size_t off = 0, len = sb;
+        if (crop) {
+            int oy = 0, ox = 0, fl = 0;
+            derive_aug_host(crop->aug_mixed, crop->epoch, h_idx[i], crop->pad, crop->flip, oy, ox,
+                            fl);
+            hp[3 * i] = oy;
+            hp[3 * i + 1] = ox;
+            hp[3 * i + 2] = fl;
+            const int lo = oy - crop->pad > 0 ? oy - crop->pad : 0;
+            const int hi = crop->h + oy - crop->pad < crop->h ? crop->h + oy - crop->pad : crop->h;
+            // a sample cropped out entirely (pad >= h) still gets a 1-byte copy
+            // (the batch API takes no empty entries); the kernel reads none of it
+            off = hi > lo ? (size_t)lo * (size_t)crop->row_bytes : 0;
+            len = hi > lo ? (size_t)(hi - lo) * (size_t)crop->row_bytes : 1;
+        }
+        g->dsts[i] = out + (size_t)i * sb + off;
+        g->srcs[i] = const_cast<uint8_t *>(src + (size_t)h_idx[i] * sb + off);
+        g->sizes[i] = len;
+        nbytes += g->sizes[i];
     }
     bool done = false;
     if (g->batch_api) {
@@ -99,6 +127,14 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
                                      g->stream));
     TSB_CUDA(cudaMemcpyAsync(g->d_idx + (size_t)k * g->max_batch, hk, sizeof(int64_t) * (size_t)b,
                              cudaMemcpyHostToDevice, g->stream));
+    nbytes += sizeof(int64_t) * (size_t)b;
+    if (crop) {
+        TSB_CUDA(cudaMemcpyAsync(g->d_params + (size_t)k * g->max_batch * 3, hp,
+                                 sizeof(int32_t) * 3 * (size_t)b, cudaMemcpyHostToDevice,
+                                 g->stream));
+        nbytes += sizeof(int32_t) * 3 * (size_t)b;
+    }
+    g->bytes += nbytes;
     TSB_CUDA(cudaEventRecord(g->done[k], g->stream));
     TSB_CUDA(cudaStreamWaitEvent(as_stream(stream), g->done[k], 0));
     *k_out = k;
@@ -139,6 +175,8 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
     if (e == cudaSuccess) e = cudaMalloc(&g->d_params, sizeof(int32_t) * 3 * max_batch * depth);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_identity, sizeof(int64_t) * max_batch);
     if (e == cudaSuccess) e = cudaHostAlloc(&g->h_idx, sizeof(int64_t) * max_batch * depth, 0);
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(&g->h_params, sizeof(int32_t) * 3 * max_batch * depth, 0);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         set_error("ingest allocation: %s", cudaGetErrorString(e));
@@ -174,6 +212,7 @@ int tsb_ingest_destroy(tsb_ingest *g) {
     cudaFree(g->d_params);
     cudaFree(g->d_identity);
     if (g->h_idx) cudaFreeHost(g->h_idx);
+    if (g->h_params) cudaFreeHost(g->h_params);
     delete g;
     return TSB_OK;
 }
@@ -181,6 +220,12 @@ int tsb_ingest_destroy(tsb_ingest *g) {
 int tsb_ingest_batch_api(tsb_ingest *g, int *used) {
     TSB_CHECK(g && used, "null argument");
     *used = g->batch_api;
+    return TSB_OK;
+}
+
+int tsb_ingest_bytes(tsb_ingest *g, uint64_t *bytes) {
+    TSB_CHECK(g && bytes, "null argument");
+    *bytes = g->bytes;
     return TSB_OK;
 }
 

@@ -32,7 +32,8 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             int pdl, void *stream, const int32_t *d_params,
                             const int64_t *tgt_idx);
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
-                 void *dst, void *stream, int *k_out, bool after_stream);
+                 void *dst, void *stream, int *k_out, bool after_stream,
+                 const IngestCrop *crop = nullptr);
 int ingest_release(tsb_ingest *g, int k, void *stream);
 uint8_t *ingest_staging(tsb_ingest *g, int k);
 int64_t *ingest_indices(tsb_ingest *g, int k);
@@ -157,14 +158,15 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                         break;
                     }
                     if (staged) {  // copy-engine ingest into HBM staging, then collate it
+                        // crop-aware: only the rows the crop reads cross PCIe, and the
+                        // param table is derived on the host and uploaded with the indices
+                        const IngestCrop crop{mix64(a->seed ^ AUG_DOMAIN), a->epoch, a->h,
+                                              a->w * a->c, a->pad, a->flip};
                         int k = 0;
                         if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, nullptr,
-                                               stream, &k, false)))
+                                               stream, &k, false, &crop)))
                             return rc;
                         int32_t *params = ingest_params(a->ingest, k);
-                        if ((rc = tsb_aug_params(a->seed, a->epoch, ingest_indices(a->ingest, k),
-                                                 b, a->pad, a->flip, params, stream)))
-                            return rc;
                         rc = collate_augment_publish(ingest_staging(a->ingest, k),
                                                      ingest_identity(a->ingest), b, a->h, a->w,
                                                      a->c, a->pad, a->flip, a->seed, a->epoch,

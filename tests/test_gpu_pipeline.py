@@ -180,23 +180,29 @@ def test_host_gate_needs_host_control():
     ring.close()
 
 
-@pytest.mark.parametrize("mode", ["augment_f32", "augment_bf16", "gather"])
-def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode):
+@pytest.mark.parametrize("mode,h,pad", [("augment_f32", 32, 4), ("augment_bf16", 32, 4),
+                                        ("gather", 32, 4), ("augment_f32", 8, 12),
+                                        ("augment_u8", 24, 24)])
+def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode, h, pad):
     """Pinned-host store: each batch's scattered sample rows cross PCIe by the
     copy engine (cudaMemcpyBatchAsync) into HBM staging (augment) or straight
-    into the slot (gather); results identical to the oracle."""
+    into the slot (gather); results identical to the oracle.  Augment
+    batches copy only the rows the crop reads (the staging buffers keep the
+    previous batches' other rows, which the kernel must never read) -- down
+    to samples cropped out entirely when pad >= h."""
     from paper_2409_18749_b200._lib import GATE_HOST
 
-    h, w, c, B, N, S, n = 32, 64, 3, 8, 64, 3, 12
+    w, c, B, N, S, n = 64, 3, 8, 64, 3, 12
     store = StoreSource.synthetic(9, N, (h, w, c), location="pinned")
-    aug = None if mode == "gather" else AugmentSpec(
-        pad=4, flip=True, out_dtype="float32" if mode == "augment_f32" else "bfloat16", seed=2)
+    out_dtype = {"augment_f32": "float32", "augment_bf16": "bfloat16", "augment_u8": "uint8"}
+    aug = None if mode == "gather" else AugmentSpec(pad=pad, flip=True, out_dtype=out_dtype[mode],
+                                                    seed=2)
     ld = CollateLoader(DatasetSpec(store, N, B, shuffle_seed=1), aug)
     ring = DeviceRing(S, ld.batch_nbytes, 1, control="host")
     ring.set_cursor(0, 0)
     store_h = oracle.make_store(9, N, h * w * c)
     scale, bias = oracle.norm_consts()
-    kind = {"augment_f32": 1, "augment_bf16": 2}.get(mode)
+    kind = {"augment_f32": 1, "augment_bf16": 2, "augment_u8": 0}.get(mode)
     L = len(ld)
     got = {}
     import threading
@@ -229,10 +235,21 @@ def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode):
         if kind is None:
             want = oracle.gather(store_h, idx, h * w * c)
         else:
-            want = oracle.collate_augment(store_h, idx, h, w, c, 4, True, 2, epoch, kind,
+            want = oracle.collate_augment(store_h, idx, h, w, c, pad, True, 2, epoch, kind,
                                           scale, bias)
         assert got[q][:ld.input_nbytes].tobytes() == want.tobytes(), q
         np.testing.assert_array_equal(got[q][ld.input_nbytes:].view(np.int64), idx)
+    sent = ld._ingest.bytes_enqueued() - 8 * B * n  # less the index uploads
+    if kind is None:
+        assert sent == n * B * h * w * c
+    else:  # the rows the crop reads, plus the 12-byte param rows
+        rows = 0
+        for q in range(1, n + 1):
+            epoch, bi = divmod(q - 1, L)
+            idx = oracle.epoch_order(N, 1, epoch)[bi * B:(bi + 1) * B]
+            d = h - np.abs(oracle.aug_params(2, epoch, idx, pad)[:, 0].astype(np.int64) - pad)
+            rows += int(np.where(d > 0, d * w * c, 1).sum())  # cropped-out sample: 1 byte
+        assert sent == rows + 12 * B * n
     ring.close()
 
 
