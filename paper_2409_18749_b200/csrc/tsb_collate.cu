@@ -148,7 +148,7 @@ struct Dsts {
 struct CaGeom {
     int h, w, b;
     int pad;
-    int log2r, R;      // rows per item (power of two)
+    int R;             // rows per item
     int nrb;           // row blocks per sample
     int items;         // b * nrb
     int rs;            // shared row stride (bytes)
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
             if (k >= g.nstage) mbar_wait(&empty[st], ((k / g.nstage) - 1) & 1);
             const int item = i0 + k * istep;
             const ItemPar p = get_par(k);
-            const int y0 = (item - p.s * g.nrb) << g.log2r;
+            const int y0 = (item - p.s * g.nrb) * g.R;
             const int nrows = min(g.R, g.h - y0);
             const int sy_first = y0 + p.oy - g.pad;
             const int lo = max(sy_first, 0), hi = min(sy_first + nrows, g.h);
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
         const int st = k % g.nstage;
         const int item = i0 + k * istep;
         const ItemPar p = get_par(k);
-        const int y0 = (item - p.s * g.nrb) << g.log2r;
+        const int y0 = (item - p.s * g.nrb) * g.R;
         const int nrows = min(g.R, g.h - y0);
         const int sy_first = y0 + p.oy - g.pad;
         const int lo = max(sy_first, 0), hi = min(sy_first + nrows, g.h);
@@ -872,41 +872,42 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     g.use_direct = direct_enabled() && src_dev && (g.row_bytes % 4 == 0) &&
                    (g.sample_bytes % 4 == 0) && (((uintptr_t)src & 3) == 0) && b <= DC_MAX_B &&
                    b * (int64_t)h * (w / vec) < (1ll << 31);
-    // rows per item (measured on B200, B=256 224x224x3): enough output per item to
-    // amortise the per-item pipeline handoff -- f32 R=8 (21.5 KB out) with 2
-    // resident CTAs per SM (below), bf16/u8 R=16 (profiles/r1/sweep_collate.txt,
-    // sweep_collate_occ.txt, bench_f32_occ_ab.txt).
-    int R = out_kind == TSB_OUT_F32 ? 8 : 16;
-    while (R > 1 && (int64_t)R > h) R >>= 1;
-    while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R >>= 1;
-    int nstage = out_kind == TSB_OUT_BF16 ? 2 : 3;
+    // Rows per item (measured on B200, B=256 224x224x3, inside the PDL-chained
+    // producer loop; profiles/r1/collate_rows_sweep.txt): items of ~45 rows --
+    // each sample split into ceil(h/45) nearly equal row blocks, 5 for 224 --
+    // with 2 stages (73 KB of shared memory, 3 CTAs per SM).  Long items keep
+    // each CTA's write streams long (R rows x w per channel plane) between its
+    // read bursts; f32 32.2 us (0.91 of the HBM peak), bf16 22.3, u8 18.4 per
+    // batch, against 36.9 / 24.4 / 19.8 at the earlier power-of-two R.
+    int R;
+    {
+        const int nb = (h + 44) / 45;
+        R = (h + nb - 1) / nb;
+    }
+    while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R = (R + 1) / 2;
+    int nstage = 2;
     if (kn.R) R = kn.R;  // tuning knobs
     if (kn.stages) nstage = kn.stages;
     g.blocked = kn.blocked;
     g.occ_cap = kn.occ;
-    TSB_CHECK(R >= 1 && R <= 64 && (R & (R - 1)) == 0, "rows per item must be a power of 2 <= 64");
+    TSB_CHECK(R >= 1 && R <= 256, "rows per item must be 1..256");
     TSB_CHECK(nstage >= 1 && nstage <= MAX_STAGES, "stages must be 1..%d", MAX_STAGES);
     if (R > h) R = 1;
     TSB_CHECK(R * g.groups <= MAX_SLOTS * CA_THREADS, "image width %d too large", w);
     while (nstage > 2 && (size_t)(nstage * R + 1) * g.rs + 2048 > 64 * 1024) --nstage;
-    while (R > 1 && (size_t)(nstage * R + 1) * g.rs + 2048 > 200 * 1024) R >>= 1;
+    while (R > 1 && (size_t)(nstage * R + 1) * g.rs + 2048 > 200 * 1024) R = (R + 1) / 2;
     g.R = R;
     g.nstage = nstage;
-    g.log2r = 0;
-    while ((1 << g.log2r) < R) ++g.log2r;
     g.nrb = (h + R - 1) / R;
     TSB_CHECK(b * (int64_t)g.nrb < (1ll << 31), "too many work items");
     g.items = (int)(b * g.nrb);
     g.slots = R * g.groups;
     size_t smem = (size_t)(nstage * R + 1) * g.rs + 2 * nstage * sizeof(uint64_t) +
                   META_CAP * sizeof(ItemPar);
-    // Resident CTAs per SM: reserve shared memory so at most `resident` CTAs
-    // fit on an SM.  f32: 2 CTAs of 8-row stages -- longer read bursts between
-    // the 4x larger write streams -- and the next PDL-launched batch's CTAs
-    // only take an SM's slots as this batch's CTAs retire, instead of
-    // co-running beside them (bench: 36.8 vs 37.4 us per B=256 batch at the
-    // old R=4 / full occupancy; profiles/r1/bench_f32_occ_ab.txt).
-    int resident = out_kind == TSB_OUT_F32 && !kn.R ? 2 : 0;
+    // Resident CTAs per SM (A/B knob TSB_CA_RESIDENT): reserve shared memory so
+    // at most `resident` CTAs fit on an SM.  With 45-row items the natural 3
+    // per SM wins (2: 35.0 us; profiles/r1/collate_rows_sweep.txt).
+    int resident = 0;
     if (kn.resident >= 0) resident = kn.resident;
     if (resident > 0) {
         static int smem_sm = 0;
