@@ -696,6 +696,7 @@ struct CaKnobs {
     int R = 0, stages = 0;     // 0 = per-kind default
     int blocked = 0, occ = 0;  // item order, grid cap (CTAs per SM)
     int resident = -1;         // -1 = per-kind default
+    int grid = 0;              // absolute grid size (A/B; 0 = SMs x resident CTAs)
 };
 const CaKnobs &ca_knobs() {
     static const CaKnobs k = [] {
@@ -706,6 +707,7 @@ const CaKnobs &ca_knobs() {
         if (const char *e = getenv("TSB_CA_ORDER")) v.blocked = strcmp(e, "blocked") == 0;
         if (const char *e = getenv("TSB_CA_OCC")) v.occ = atoi(e);
         if (const char *e = getenv("TSB_CA_RESIDENT")) v.resident = atoi(e);
+        if (const char *e = getenv("TSB_CA_GRID")) v.grid = atoi(e);
         return v;
     }();
     return k;
@@ -741,7 +743,8 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
         smem_cache[dev] = smem;
     }
     const int occ = g.occ_cap > 0 && g.occ_cap < occ_cache[dev] ? g.occ_cap : occ_cache[dev];
-    const int slots = sm_count() * occ;
+    int slots = sm_count() * occ;
+    if (ca_knobs().grid > 0 && ca_knobs().grid < slots) slots = ca_knobs().grid;
     const int grid = g.items < slots ? g.items : slots;
     if (ep.pdl) {
         cudaLaunchConfig_t cfg{};

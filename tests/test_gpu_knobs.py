@@ -1,8 +1,8 @@
 """The collate kernel's tuning / A/B knobs keep it bit-exact.
 
 The knobs (TSB_CA_R rows per item, TSB_CA_STAGES pipeline depth,
-TSB_CA_ORDER item order, TSB_CA_OCC grid cap, TSB_CA_RESIDENT resident CTAs
-per SM, TSB_CA_NOTMA cooperative staging, TSB_CA_IMPL=direct staging-free
+TSB_CA_ORDER item order, TSB_CA_OCC grid cap, TSB_CA_GRID absolute grid,
+TSB_CA_RESIDENT resident CTAs per SM, TSB_CA_NOTMA cooperative staging, TSB_CA_IMPL=direct staging-free
 kernel, TSB_CA_ST / TSB_CA_LDHINT cache hints) are read once per process, so
 each configuration runs in a child process that prints the CRC-32 of the
 collated batch; the parent checks it against the oracle's bytes."""
@@ -48,6 +48,7 @@ KNOBS = [
     {"TSB_CA_R": "2", "TSB_CA_STAGES": "4", "TSB_CA_ORDER": "blocked"},
     {"TSB_CA_R": "32", "TSB_CA_STAGES": "2", "TSB_CA_OCC": "1"},
     {"TSB_CA_RESIDENT": "3", "TSB_CA_ORDER": "blocked"},
+    {"TSB_CA_R": "7", "TSB_CA_STAGES": "3", "TSB_CA_GRID": "5"},
     {"TSB_CA_NOTMA": "1"},
     {"TSB_CA_IMPL": "direct"},
     {"TSB_CA_ST": "plain", "TSB_CA_LDHINT": "0"},
