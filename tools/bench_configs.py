@@ -91,17 +91,21 @@ def c4_consumer(bcast, agg, cid, b, epochs, q):
 
     loader = SharedLoader(bcast, agg, consumer_id=cid, batch_size=b, sync="host")
     q.put(("ready", cid))
-    times, n = [], 0
+    rates, n = [], 0
     for _ in range(epochs):
+        times = []
         for inp, tgt in loader:
             times.append(time.monotonic())
             n += 1
+        if len(times) > 1:  # the reference's per-epoch rate (bs/cli.py:220-236)
+            rates.append((len(times) - 1) / (times[-1] - times[0]) * b)
     loader.close()
-    rate = (len(times) - 1) / (times[-1] - times[0]) * b if len(times) > 1 else 0.0
+    # mean over epochs, as bs/harness.py:611-617 (the first epoch includes start-up)
+    rate = sum(rates[1:]) / len(rates[1:]) if len(rates) > 1 else (rates[0] if rates else 0.0)
     q.put(("done", cid, b, rate, n))
 
 
-def c4(epochs=3):
+def c4(epochs=5):
     """Heterogeneous consumers b in {64,128,256,512} (2 each) on one producer
     of B=512 bf16 batches: every consumer gets the reference's batches for its
     own b (zero-copy windows); per-consumer rate by the reference formula."""
