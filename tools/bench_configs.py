@@ -100,8 +100,7 @@ def c4_consumer(bcast, agg, cid, b, epochs, q):
         if len(times) > 1:  # the reference's per-epoch rate (bs/cli.py:220-236)
             rates.append((len(times) - 1) / (times[-1] - times[0]) * b)
     loader.close()
-    # mean over epochs, as bs/harness.py:611-617 (the first epoch includes start-up)
-    rate = sum(rates[1:]) / len(rates[1:]) if len(rates) > 1 else (rates[0] if rates else 0.0)
+    rate = sum(rates) / len(rates) if rates else 0.0  # mean over epochs, bs/harness.py:611-617
     q.put(("done", cid, b, rate, n))
 
 
