@@ -131,7 +131,17 @@ __global__ void aug_params_kernel(uint64_t aug_mixed, uint64_t epoch,
 // in parallel by warp 0 in the prologue (or read from a param table).
 // Sources TMA cannot address (pinned host memory, unaligned rows) use the
 // same loop with cooperative 16-byte LDG staging instead.
-constexpr int CA_THREADS = 256;
+// Consumer threads per CTA (+1 producer warp): 128 for f32 (31.8 vs 32.3 us
+// per B=256 batch), 256 for bf16/u8 (22.2 vs 23.5 us at 128);
+// profiles/r1/collate_threads_ab.txt.
+#ifndef TSB_CA_THREADS
+#define TSB_CA_THREADS 256
+#endif
+#ifndef TSB_CA_THREADS_F32
+#define TSB_CA_THREADS_F32 128
+#endif
+constexpr int CA_THREADS = TSB_CA_THREADS;
+constexpr int CA_THREADS_F32 = TSB_CA_THREADS_F32;
 constexpr int MAX_DST = 8;
 constexpr int MAX_STAGES = 16;
 constexpr int MAX_SLOTS = 64;      // slots per thread per item
@@ -394,14 +404,14 @@ __device__ __forceinline__ void emit_pixels(const uint32_t *smem_words, uint32_t
     (emit_channel<OUT_KIND, C, MULTI, FLIP, CHs>(wv, norm, dsts, off, plane_bytes), ...);
 }
 
-template <int OUT_KIND, int C, bool MULTI>
-__global__ void __launch_bounds__(CA_THREADS + 32)
+template <int OUT_KIND, int C, bool MULTI, int NT>
+__global__ void __launch_bounds__(NT + 32)
     collate_augment_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
                            CaGeom g, int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
                            const int32_t *__restrict__ params, Dsts dsts, Epi ep) {
     using T = OutTraits<OUT_KIND>;
     constexpr int P = T::P;
-    constexpr int NCW = CA_THREADS / 32;  // consumer warps; warp NCW is the producer
+    constexpr int NCW = NT / 32;  // consumer warps; warp NCW is the producer
     extern __shared__ __align__(128) uint8_t smem[];
     const int stage_bytes = g.R * g.rs;
     const uint32_t *smem_words = reinterpret_cast<const uint32_t *>(smem);
@@ -509,13 +519,13 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     }
 
     // ---------------- consumer warps: emit normalised NCHW ------------------
-    if (blockIdx.x == 0) write_targets(ep, idx, g.b, tid, CA_THREADS);
+    if (blockIdx.x == 0) write_targets(ep, idx, g.b, tid, NT);
     const int64_t plane_bytes = g.plane * T::ELEM;
-    // first slot of this thread; further slots every CA_THREADS (no divisions in the loop)
+    // first slot of this thread; further slots every NT (no divisions in the loop)
     const int r_first = tid / g.groups;
     const int x_first = (tid - r_first * g.groups) * P;
-    const int dr = CA_THREADS / g.groups;
-    const int dx = (CA_THREADS - dr * g.groups) * P;
+    const int dr = NT / g.groups;
+    const int dx = (NT - dr * g.groups) * P;
     for (int k = 0; k < nk; ++k) {
         const int st = k % g.nstage;
         const int item = i0 + k * istep;
@@ -528,7 +538,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
         mbar_wait(&full[st], (k / g.nstage) & 1);
         int r = r_first, x0 = x_first;
 #pragma unroll 1
-        for (int sl = tid; sl < g.slots; sl += CA_THREADS) {
+        for (int sl = tid; sl < g.slots; sl += NT) {
             if (r < nrows) {
                 const int sy = sy_first + r;
                 const uint32_t row_off = (sy >= lo && sy < hi)
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(CA_THREADS + 32)
     // different ring slot, and its gate was checked on the host, so it never
     // needs this grid's results (no griddepcontrol.wait anywhere).
     pdl_launch_dependents();
-    publish_epilogue(ep, tid, CA_THREADS);
+    publish_epilogue(ep, tid, NT);
 }
 
 template <int OUT_KIND, int C, bool MULTI, bool FLIP, int... CHs>
@@ -729,7 +739,8 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
     if (g.use_direct)
         return launch_direct<K, C, MULTI>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
                                           s, ep);
-    auto kern = collate_augment_kernel<K, C, MULTI>;
+    constexpr int NT = K == TSB_OUT_F32 ? CA_THREADS_F32 : CA_THREADS;
+    auto kern = collate_augment_kernel<K, C, MULTI, NT>;
     static int occ_cache[64] = {0};
     static size_t smem_cache[64] = {0};
     int dev = 0;
@@ -738,7 +749,7 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
     if (smem_cache[dev] != smem) {
         TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
-        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CA_THREADS + 32, smem));
+        TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 32, smem));
         occ_cache[dev] = occ > 0 ? occ : 1;
         smem_cache[dev] = smem;
     }
@@ -749,7 +760,7 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
     if (ep.pdl) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(CA_THREADS + 32);
+        cfg.blockDim = dim3(NT + 32);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -761,7 +772,7 @@ int launch_ca(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
                                     dsts, ep));
         return TSB_OK;
     }
-    kern<<<grid, CA_THREADS + 32, smem, s>>>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
+    kern<<<grid, NT + 32, smem, s>>>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
                                              ep);
     TSB_LAUNCH_CHECK();
     return TSB_OK;
@@ -887,7 +898,8 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
         const int nb = (h + 44) / 45;
         R = (h + nb - 1) / nb;
     }
-    while (R > 1 && R * g.groups > MAX_SLOTS * CA_THREADS) R = (R + 1) / 2;
+    const int nt = out_kind == TSB_OUT_F32 ? CA_THREADS_F32 : CA_THREADS;
+    while (R > 1 && R * g.groups > MAX_SLOTS * nt) R = (R + 1) / 2;
     int nstage = 2;
     if (kn.R) R = kn.R;  // tuning knobs
     if (kn.stages) nstage = kn.stages;
@@ -896,7 +908,7 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     TSB_CHECK(R >= 1 && R <= 256, "rows per item must be 1..256");
     TSB_CHECK(nstage >= 1 && nstage <= MAX_STAGES, "stages must be 1..%d", MAX_STAGES);
     if (R > h) R = 1;
-    TSB_CHECK(R * g.groups <= MAX_SLOTS * CA_THREADS, "image width %d too large", w);
+    TSB_CHECK(R * g.groups <= MAX_SLOTS * nt, "image width %d too large", w);
     while (nstage > 2 && (size_t)(nstage * R + 1) * g.rs + 2048 > 64 * 1024) --nstage;
     while (R > 1 && (size_t)(nstage * R + 1) * g.rs + 2048 > 200 * 1024) R = (R + 1) / 2;
     g.R = R;
@@ -1388,14 +1400,15 @@ int tsb_collate_augment_fanout(const void *src, const int64_t *d_indices, int64_
 namespace tsb {
 template <int K>
 void preload_ca() {
-    touch_kernel(collate_augment_kernel<K, 1, false>);
-    touch_kernel(collate_augment_kernel<K, 2, false>);
-    touch_kernel(collate_augment_kernel<K, 3, false>);
-    touch_kernel(collate_augment_kernel<K, 4, false>);
-    touch_kernel(collate_augment_kernel<K, 1, true>);
-    touch_kernel(collate_augment_kernel<K, 2, true>);
-    touch_kernel(collate_augment_kernel<K, 3, true>);
-    touch_kernel(collate_augment_kernel<K, 4, true>);
+    constexpr int NT = K == TSB_OUT_F32 ? CA_THREADS_F32 : CA_THREADS;
+    touch_kernel(collate_augment_kernel<K, 1, false, NT>);
+    touch_kernel(collate_augment_kernel<K, 2, false, NT>);
+    touch_kernel(collate_augment_kernel<K, 3, false, NT>);
+    touch_kernel(collate_augment_kernel<K, 4, false, NT>);
+    touch_kernel(collate_augment_kernel<K, 1, true, NT>);
+    touch_kernel(collate_augment_kernel<K, 2, true, NT>);
+    touch_kernel(collate_augment_kernel<K, 3, true, NT>);
+    touch_kernel(collate_augment_kernel<K, 4, true, NT>);
 }
 void preload_collate() {
     touch_kernel(fill_kernel);
