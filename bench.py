@@ -430,6 +430,9 @@ def run_ours(args):
                     "alg_bytes_per_launch": egress, "avg_launch_ms": round(ms_max / K, 5),
                     "peak_source": "B200_PROFILING.md measured peer copy, per direction per GPU",
                     "fanout": fanout,
+                    **({"note": "TSB_BENCH_SAME_DEVICE test mode: every rank on one GPU, no "
+                                "NVLink traffic; frac is not a link utilisation"}
+                       if os.environ.get("TSB_BENCH_SAME_DEVICE") else {}),
                     "hbm_achieved_gbs": round(
                         B * ALG_BYTES_PER_SAMPLE / (ms_max / K / 1e3) / 1e9, 1)}
     result = {
