@@ -212,3 +212,65 @@ def test_consumer_churn_reuses_cursor_words(endpoints):
     pt.join(60)
     assert anchor["seq"] == expected(E, 8)
     producer.close()
+
+
+def test_zero_consumers_idle(endpoints):
+    """With no consumer the producer announces nothing (it waits at the start
+    barrier); a consumer that arrives later gets the whole epoch
+    (pkg/tests/test_producer_consumer.py:290-298)."""
+    producer, pt = run_producer(SeqLoader(5), endpoints, 1)
+    time.sleep(0.5)
+    assert producer.stats["announced"] == 0
+    out = {}
+    consume(endpoints, 1, 1, out)
+    pt.join(30)
+    assert out["seq"] == expected(1, 5)
+    producer.close()
+
+
+def test_all_consumers_evicted_producer_pauses(endpoints):
+    """The only consumer stops heartbeating and is evicted: the producer then
+    announces nothing more until someone is admitted again
+    (pkg/tests/test_producer_consumer.py:336-365)."""
+    producer, pt = run_producer(SeqLoader(200), endpoints, 1, ring_slots=4,
+                                heartbeat_timeout_s=0.4)
+    victim = {}
+    consume(endpoints, 1, 1, victim, stop_after=2, heartbeat_interval_s=0.1)
+    victim["loader"].finished = True  # heartbeats stop ("hung")
+    deadline = time.time() + 10
+    while producer.stats["evictions"] < 1 and time.time() < deadline:
+        time.sleep(0.01)
+    assert producer.stats["evictions"] == 1
+    time.sleep(0.3)
+    a = producer.stats["announced"]
+    time.sleep(0.5)
+    assert producer.stats["announced"] == a < 200  # paused with no consumers
+    producer.join(0.0)
+    pt.join(30)
+    producer.close()
+
+
+def test_version_mismatch_drops_connection(endpoints):
+    """A Join with an unknown protocol version is closed without a Welcome;
+    the producer keeps serving (pkg/tests/test_producer_consumer.py:418-434)."""
+    import socket
+
+    from paper_2409_18749_b200.transport import dial
+    from paper_2409_18749_b200.wire import Heartbeat, encode
+
+    producer, pt = run_producer(SeqLoader(5), endpoints, 1)
+    b, a = endpoints
+    bs = dial(b, 5)
+    bs.sendall(encode(Heartbeat(9, 0)))
+    ag = dial(a, 5)
+    ag.sendall(bytes.fromhex("0b000000" "01" "0900000000000000" "6300"))  # Join(9, version 99)
+    ag.settimeout(10)
+    assert ag.recv(4096) == b""
+    bs.close()
+    ag.close()
+    out = {}
+    consume(endpoints, 1, 1, out)
+    pt.join(30)
+    assert out["seq"] == expected(1, 5)
+    assert 9 not in [d[0] for d in producer.drops]  # never admitted
+    producer.close()

@@ -112,3 +112,15 @@ def test_descriptor_exchange_gloo_world2():
         p.join(30)
     want = [(0, 0, 0, 2), (1, 1, 1, 2)]
     assert res == {0: want, 1: want}
+
+
+def test_connect_error_when_no_producer(tmp_path):
+    """No producer at the endpoints: the consumer fails with StreamError after
+    its connect timeout (pkg/tests/test_producer_consumer.py:436-445)."""
+    from paper_2409_18749_b200 import SharedLoader
+    from paper_2409_18749_b200.errors import StreamError
+
+    ld = SharedLoader(f"unix:{tmp_path}/nope-b.sock", f"unix:{tmp_path}/nope-a.sock",
+                      consumer_id=1, connect_timeout_s=0.3)
+    with pytest.raises(StreamError):
+        next(iter(ld))
