@@ -124,3 +124,54 @@ def test_connect_error_when_no_producer(tmp_path):
                       consumer_id=1, connect_timeout_s=0.3)
     with pytest.raises(StreamError):
         next(iter(ld))
+
+
+def test_consumer_heartbeat_cadence(tmp_path):
+    """A scripted producer (raw sockets, the wire codec) admits one
+    SharedLoader and times its Heartbeats on the aggregate channel: ~10 in
+    1.1 s at a 100 ms interval, no gap above 2x the interval plus slack
+    (pkg/tests/test_producer_consumer.py:518-556)."""
+    import socket
+    import threading
+    import time
+
+    from paper_2409_18749_b200 import SharedLoader
+    from paper_2409_18749_b200.transport import listen
+    from paper_2409_18749_b200.wire import FrameDecoder, Heartbeat, Join, Welcome, encode
+
+    b_ep, a_ep = f"unix:{tmp_path}/fb.sock", f"unix:{tmp_path}/fa.sock"
+    lb, la = listen(b_ep), listen(a_ep)
+    box = {}
+
+    def client():
+        ld = SharedLoader(b_ep, a_ep, consumer_id=6, heartbeat_interval_s=0.1, device=0)
+        ld._connect()
+        box["ld"] = ld
+        time.sleep(1.1)
+        ld.finished = True
+
+    t = threading.Thread(target=client)
+    t.start()
+    bs, _ = lb.accept()
+    bs.recv(4096)  # identification heartbeat
+    ag, _ = la.accept()
+    dec = FrameDecoder()
+    while not any(isinstance(m, Join) for m in dec.feed(ag.recv(4096))):
+        pass
+    ag.sendall(encode(Welcome(6, 0, 10, 0, 2, 2)))
+    ag.settimeout(3.0)
+    arrivals = []
+    deadline = time.monotonic() + 1.2
+    while time.monotonic() < deadline:
+        try:
+            data = ag.recv(4096)
+        except socket.timeout:
+            break
+        if not data:
+            break
+        arrivals += [time.monotonic() for m in dec.feed(data) if isinstance(m, Heartbeat)]
+    t.join(10)
+    for s in (bs, ag, lb, la):
+        s.close()
+    assert len(arrivals) >= 8
+    assert max(b - a for a, b in zip(arrivals, arrivals[1:])) < 0.25
