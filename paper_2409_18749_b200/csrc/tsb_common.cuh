@@ -79,7 +79,7 @@ __host__ __device__ __forceinline__ void derive_aug_host(uint64_t aug_mixed, uin
 struct IngestCrop {
     uint64_t aug_mixed;  // mix64(aug_seed ^ AUG_DOMAIN)
     uint64_t epoch;
-    int h, row_bytes, pad, flip;
+    int h, w, row_bytes, pad, flip;
 };
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

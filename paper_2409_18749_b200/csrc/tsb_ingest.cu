@@ -61,6 +61,9 @@ void preload_ingest() { touch_kernel(iota_kernel); }
 // reads source row y + oy - pad, so rows [max(0, oy-pad), min(h, h+oy-pad))
 // of each sample (on average 8.2 of 224 rows fewer at pad 16).  The collate
 // kernel loads exactly those rows of a staged sample, never the others.
+// (Columns too would save another 3.7%, but 2D copies -- cudaMemcpy3DBatchAsync,
+// one op per sample -- run ~10x slower on the copy engine: e2e 154 k vs 1.49 M
+// samples/s; profiles/r1/ingest_2d_ab.txt.)
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
                  void *dst, void *stream, int *k_out, bool after_stream, const IngestCrop *crop) {
     TSB_CHECK(g && host_store && h_idx && k_out, "null argument");
@@ -85,7 +88,8 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     const size_t sb = (size_t)g->sample_bytes;
     int32_t *hp = g->h_params + (size_t)k * g->max_batch * 3;
     size_t nbytes = 0;
-    for (int64_t i = 0; i < b; ++i) {
+    bool done = false;
+    for (int64_t i = 0; i < b && !done; ++i) {
         size_t off = 0, len = sb;
         if (crop) {
             int oy = 0, ox = 0, fl = 0;
@@ -106,8 +110,7 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         g->sizes[i] = len;
         nbytes += g->sizes[i];
     }
-    bool done = false;
-    if (g->batch_api) {
+    if (!done && g->batch_api) {
         cudaMemcpyAttributes attr{};
         attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
         attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
@@ -123,7 +126,7 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     }
     if (!done)
         for (int64_t i = 0; i < b; ++i)
-            TSB_CUDA(cudaMemcpyAsync(g->dsts[i], g->srcs[i], sb, cudaMemcpyHostToDevice,
+            TSB_CUDA(cudaMemcpyAsync(g->dsts[i], g->srcs[i], g->sizes[i], cudaMemcpyHostToDevice,
                                      g->stream));
     TSB_CUDA(cudaMemcpyAsync(g->d_idx + (size_t)k * g->max_batch, hk, sizeof(int64_t) * (size_t)b,
                              cudaMemcpyHostToDevice, g->stream));

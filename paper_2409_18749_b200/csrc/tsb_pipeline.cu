@@ -160,7 +160,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                     if (staged) {  // copy-engine ingest into HBM staging, then collate it
                         // crop-aware: only the rows the crop reads cross PCIe, and the
                         // param table is derived on the host and uploaded with the indices
-                        const IngestCrop crop{mix64(a->seed ^ AUG_DOMAIN), a->epoch, a->h,
+                        const IngestCrop crop{mix64(a->seed ^ AUG_DOMAIN), a->epoch, a->h, a->w,
                                               a->w * a->c, a->pad, a->flip};
                         int k = 0;
                         if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, nullptr,
