@@ -89,7 +89,7 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     int32_t *hp = g->h_params + (size_t)k * g->max_batch * 3;
     size_t nbytes = 0;
     bool done = false;
-    for (int64_t i = 0; i < b && !done; ++i) {
+    for (int64_t i = 0; i < b; ++i) {
         size_t off = 0, len = sb;
         if (crop) {
             int oy = 0, ox = 0, fl = 0;
