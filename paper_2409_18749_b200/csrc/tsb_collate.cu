@@ -192,7 +192,14 @@ struct Epi {
     int pdl;                 // launch as a programmatic dependent of the previous batch
     int sys_fence;           // destinations on other devices: order stores at system scope
     const int64_t *tgt_idx;  // sample indices written as the target (nullptr = the gather indices)
+    int fence_all;           // A/B (TSB_FENCE_ALL=1): every thread fences before the CTA barrier
 };
+
+// Publish ordering knob, read once per process.
+int fence_all_knob() {
+    static const int v = getenv("TSB_FENCE_ALL") ? atoi(getenv("TSB_FENCE_ALL")) : 0;
+    return v;
+}
 
 __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -206,20 +213,31 @@ __device__ __forceinline__ void write_targets(const Epi &ep, const int64_t *__re
             for (int i = tid; i < b; i += nthreads) ep.tgt[d][i] = src[i];
 }
 
-// Last CTA to finish publishes the slot: every thread orders its stores
-// (gpu scope, or system scope when peers are among the destinations), the
-// CTA's `nthreads` participating threads meet on named barrier 1, one thread
-// bumps the completion counter and the last CTA release-stores each
-// destination's ready word at system scope (host-shared control words and
-// peer devices both observe it).
+// Last CTA to finish publishes the slot.  The CTA's `nthreads` participating
+// threads meet on named barrier 1 (CTA-scope ordering of all their stores
+// before thread 0), then thread 0 alone fences -- gpu scope, or system scope
+// when peers are among the destinations; the fence is cumulative over the
+// stores the barrier ordered before it, the CUTLASS semaphore pattern -- and
+// bumps the completion counter.  The last CTA fences again (acquire side) and
+// release-stores each destination's ready word at system scope (host-shared
+// control words and peer devices both observe it).  A per-thread fence before
+// the barrier (TSB_FENCE_ALL=1, the earlier scheme) stalls every warp on
+// its own store acknowledgements (21% of the passthrough kernel's stalls,
+// profiles/r1/ncu_full_passthrough_v3.txt).
 __device__ __forceinline__ void publish_epilogue(const Epi &ep, int tid, int nthreads) {
     if (!ep.counter) return;
-    if (ep.sys_fence)
-        __threadfence_system();
-    else
-        __threadfence();
+    if (ep.fence_all) {
+        if (ep.sys_fence)
+            __threadfence_system();
+        else
+            __threadfence();
+    }
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
     if (tid == 0) {
+        if (ep.sys_fence)
+            __threadfence_system();
+        else
+            __threadfence();
         const unsigned int prev = atomicAdd(ep.counter, 1u);
         if (prev == gridDim.x - 1) {  // last CTA: every store of the batch is visible
             *ep.counter = 0u;
@@ -1172,6 +1190,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     ep.counter = counter;
     ep.pdl = pdl;
     ep.tgt_idx = tgt_idx;
+    ep.fence_all = fence_all_knob();
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
                           out_kind, d_params, d, stream, ep);
 }
@@ -1198,6 +1217,7 @@ int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int 
     ep.counter = counter;
     ep.pdl = pdl;
     ep.sys_fence = sys_fence;
+    ep.fence_all = fence_all_knob();
     if (mode == TSB_SRC_AUGMENT)
         return launch_collate(src, idx, b, h, w, c, pad, flip, seed, epoch, scale, bias, out_kind,
                               nullptr, d, stream, ep);
