@@ -1137,10 +1137,11 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
                 if (k < v1) st_v4(o + 16 * k, v[u]);
             }
         }
-        // batch i done by this CTA: the last CTA publishes the slot
-        __threadfence();
+        // batch i done by this CTA: the last CTA publishes the slot (barrier,
+        // then one cumulative fence -- as publish_epilogue)
         __syncthreads();
         if (tid == 0) {
+            __threadfence();
             const unsigned int prev = atomicAdd(a.counters + slot, 1u);
             if (prev == gridDim.x - 1) {
                 a.counters[slot] = 0u;
