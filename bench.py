@@ -462,9 +462,9 @@ def run_ours(args):
                            "bs/cli.py:252-258)"},
         "roofline": roofline,
         "e2e": e2e,
-        # per step: the collate (N=1, outputs fan-out); the row gather + param
-        # table + collate (two-stage)
-        "gpu_launches": K if fanout != "inputs" else 3 * K,
+        # per step: the collate (N=1, outputs fan-out); the row gather + the
+        # collate (two-stage)
+        "gpu_launches": K if fanout != "inputs" else 2 * K,
         "clocks": clk,
         "extra": {"producer_ms": round(ms, 3),
                   "consumer_rates_samples_s": {str(k): round(v, 1) for k, v in consumer_rates.items()},

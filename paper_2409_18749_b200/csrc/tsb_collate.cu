@@ -282,8 +282,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return r;
 }
 
+// Item parameters.  `idx` locates the sample's source rows; the augment key
+// is the real sample index `kidx` -- the same array unless the rows were
+// staged (staged ingest, two-stage all-gather), where idx is the identity
+// and kidx the batch's target indices (Epi::tgt_idx).
 __device__ __forceinline__ ItemPar item_par(const CaGeom &g, int item,
                                             const int64_t *__restrict__ idx,
+                                            const int64_t *__restrict__ kidx,
                                             const int32_t *__restrict__ params,
                                             uint64_t aug_mixed, uint64_t epoch, int flip_en) {
     ItemPar p;
@@ -294,7 +299,7 @@ __device__ __forceinline__ ItemPar item_par(const CaGeom &g, int item,
         p.ox = params[3 * p.s + 1];
         p.fl = params[3 * p.s + 2];
     } else {
-        derive_aug(aug_mixed, epoch, idx[p.s], g.pad, flip_en, p.oy, p.ox, p.fl);
+        derive_aug(aug_mixed, epoch, kidx[p.s], g.pad, flip_en, p.oy, p.ox, p.fl);
     }
     return p;
 }
@@ -439,6 +444,7 @@ __global__ void __launch_bounds__(NT + 32)
     ItemPar *par = reinterpret_cast<ItemPar *>(empty + g.nstage);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const int64_t *kidx = ep.tgt_idx ? ep.tgt_idx : idx;  // augment keys (see item_par)
     // this CTA's items: item(k) = i0 + k * istep
     int nk, i0, istep;
     if (g.blocked) {
@@ -460,7 +466,7 @@ __global__ void __launch_bounds__(NT + 32)
     }
     // crop/flip params + source offsets of this CTA's items, derived in parallel
     for (int k = tid; k < min(nk, META_CAP); k += blockDim.x)
-        par[k] = item_par(g, i0 + k * istep, idx, params, aug_mixed, epoch, flip_en);
+        par[k] = item_par(g, i0 + k * istep, idx, kidx, params, aug_mixed, epoch, flip_en);
     if (tid == 0) {
         for (int i = 0; i < g.nstage; ++i) {
             mbar_init(&full[i], g.use_tma ? 1 : 32);
@@ -472,7 +478,8 @@ __global__ void __launch_bounds__(NT + 32)
 
     auto get_par = [&](int k) -> ItemPar {
         return k < META_CAP ? par[k]
-                            : item_par(g, i0 + k * istep, idx, params, aug_mixed, epoch, flip_en);
+                            : item_par(g, i0 + k * istep, idx, kidx, params, aug_mixed, epoch,
+                                       flip_en);
     };
 
     if (warp == NCW) {
@@ -636,7 +643,8 @@ __global__ void __launch_bounds__(DC_THREADS)
             p.ox = params[3 * s + 1];
             p.fl = params[3 * s + 2];
         } else {
-            derive_aug(aug_mixed, epoch, idx[s], g.pad, flip_en, p.oy, p.ox, p.fl);
+            derive_aug(aug_mixed, epoch, (ep.tgt_idx ? ep.tgt_idx : idx)[s], g.pad, flip_en,
+                       p.oy, p.ox, p.fl);
         }
         p.src_off = idx[s] * g.sample_bytes;
         par[s] = p;
@@ -1179,7 +1187,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
                             int pdl, void *stream, const int32_t *d_params,
-                            const int64_t *tgt_idx) {
+                            const int64_t *tgt_idx, uint64_t *release) {
     Dsts d{};
     d.p[0] = out;
     d.n = 1;
@@ -1187,6 +1195,10 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     ep.tgt[0] = tgt;
     ep.ready[0] = ready;
     ep.n = 1;
+    if (release) {  // a second word the last CTA sets to `seq`: the input slot's release
+        ep.ready[1] = release;
+        ep.n = 2;
+    }
     ep.seq = seq;
     ep.counter = counter;
     ep.pdl = pdl;

@@ -30,7 +30,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
                             int pdl, void *stream, const int32_t *d_params,
-                            const int64_t *tgt_idx);
+                            const int64_t *tgt_idx, uint64_t *release = nullptr);
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
                  void *dst, void *stream, int *k_out, bool after_stream,
                  const IngestCrop *crop = nullptr);
@@ -408,6 +408,11 @@ int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
               (long long)b);
     const size_t out_bytes = (size_t)a->input_bytes + (a->with_target ? 8 * (size_t)b : 0);
     TSB_CHECK(out_stride >= out_bytes, "output slot too small");
+    uint8_t *in_base = nullptr;
+    int64_t in_sstride = 0;
+    uint64_t *in_ready = nullptr, *in_cursors = nullptr;
+    unsigned int *in_counters = nullptr;
+    ring_internals(in_ring, &in_base, &in_sstride, &in_ready, &in_cursors, &in_counters);
     for (int i = 0; i < n; ++i) {
         const uint64_t q = seq0 + (uint64_t)i;
         const int islot = (int)((q - 1) % (uint64_t)in_slots);
@@ -420,22 +425,22 @@ int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
         if (int rc = tsb_ring_slot_ptr(in_ring, islot, &in)) return rc;
         if (int rc = tsb_ring_slot_ptr(out_ring, oslot, &out)) return rc;
         const int64_t *ridx = reinterpret_cast<const int64_t *>(static_cast<uint8_t *>(in) + b * sb);
-        int32_t *params = ingest_params(a->ingest, 0);
-        if (int rc = tsb_aug_params(a->seed, a->epoch, ridx, b, a->pad, a->flip, params, stream))
-            return rc;
         uint64_t *ready = nullptr;
         unsigned int *counter = nullptr;
         if (int rc = ring_publish_ptrs(out_ring, oslot, 0, &ready, &counter)) return rc;
         int64_t *tgt = a->with_target
                            ? reinterpret_cast<int64_t *>(static_cast<uint8_t *>(out) + a->input_bytes)
                            : nullptr;
+        // crop/flip keys are the staged target indices (the kernel derives the
+        // params itself, no table kernel); the last CTA publishes the output slot
+        // and releases the input slot (its cursor := q) once every CTA has read
+        // its rows -- so the stream carries only these kernels, PDL-chained
         if (int rc = collate_augment_publish(in, ingest_identity(a->ingest), b, a->h, a->w, a->c,
                                              a->pad, a->flip, a->seed, a->epoch, a->scale, a->bias,
-                                             a->out_kind, out, tgt, ready, q, counter, 0, stream,
-                                             params, ridx))
+                                             a->out_kind, out, tgt, ready, q, counter,
+                                             (i > 0 || a->chain) ? 1 : 0, stream, nullptr, ridx,
+                                             in_cursors + in_consumer))
             return rc;
-        // the kernel has read the staged rows: release the input slot (stream-ordered)
-        if (int rc = tsb_ring_ack(in_ring, in_consumer, q, stream)) return rc;
     }
     return TSB_OK;
 }
