@@ -253,8 +253,6 @@ def test_all_consumers_evicted_producer_pauses(endpoints):
 def test_version_mismatch_drops_connection(endpoints):
     """A Join with an unknown protocol version is closed without a Welcome;
     the producer keeps serving (pkg/tests/test_producer_consumer.py:418-434)."""
-    import socket
-
     from paper_2409_18749_b200.transport import dial
     from paper_2409_18749_b200.wire import Heartbeat, encode
 
