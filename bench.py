@@ -506,9 +506,12 @@ def run_e2e(args, ctx, dev, rank, world):
         store = StoreSource.synthetic(0, N_SAMPLES, (H, W, C), location="pinned")
         ds = DatasetSpec(store, N_SAMPLES, B, shuffle_seed=0)
         loader = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="float32"))
+        # N > 1: the same fan-out design as the device-timed value (two-stage
+        # input all-gather by default, TSB_BENCH_FANOUT=outputs for the fused one)
+        fan = "inputs" if os.environ.get("TSB_BENCH_FANOUT", "inputs") == "inputs" else "sharded"
         producer = TensorProducer(loader, bcast, agg, min_consumers=N_CONSUMERS * world,
                                   ring_slots=RING_SLOTS, heartbeat_timeout_s=60.0,
-                                  devices=devs if world > 1 else None)
+                                  devices=devs if world > 1 else None, fanout=fan)
         producer._start()  # listeners up before any rank's consumers dial
     if world > 1:
         torch.distributed.barrier()
@@ -557,9 +560,11 @@ def run_e2e(args, ctx, dev, rank, world):
             "engine, with the host-derived crop/flip table; consumers .item() one element per "
             "batch")
     if world > 1:
-        path = (f"one TensorProducer(devices={world} GPUs, sharded ingest: each GPU reads its "
-                "1/N rows of every batch from pinned host memory, fused all-gather into every "
-                "ring) -> 4 SharedLoader(device=g) processes per GPU; consumers .item() per batch")
+        path = (f"one TensorProducer(devices={world} GPUs, fanout="
+                f"{'inputs' if os.environ.get('TSB_BENCH_FANOUT', 'inputs') == 'inputs' else 'sharded'}"
+                ": each GPU reads its 1/N rows of every batch from pinned host memory and stores "
+                "them into every GPU's ring) -> 4 SharedLoader(device=g) processes per GPU; "
+                "consumers .item() per batch")
     return {"value": round(value, 1), "unit": "samples/s",
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * N_CONSUMERS * world,

@@ -38,8 +38,11 @@ consumer maps the ring of its own GPU (``SharedLoader(device=...)``, Join v2).
 ``fanout="sharded"`` (default): every device collates its 1/G rows of each
 batch and the kernel stores them into the same slot of every device's ring
 (P2P stores over NVLink/NVSwitch -- the all-gather fused into the producing
-kernel, ``tsb_produce_group``); ``fanout="star"``: the first device produces
-the whole batch into every ring (the literal single-producer fan-out).
+kernel, ``tsb_produce_group``); ``fanout="inputs"`` (two-stage): every
+device gathers its 1/G compact u8 rows into every device's input ring, then
+each device collates the whole batch locally (a quarter of the NVLink bytes
+at f32); ``fanout="star"``: the first device produces the
+whole batch into every ring (the literal single-producer fan-out).
 
 Heterogeneous consumers (``SharedLoader(batch_size=b)``): each receives
 exactly the reference's batches for its own batch size -- samples
@@ -64,7 +67,7 @@ from .errors import ProducerClosed
 from .ledger import (ConsumerRecord, Ledger, admission_code, rebatch_epoch_len, retention_window,
                      seq_of, window_slots)
 from ._lib import GATE_HOST
-from .ring import DeviceRing, produce_group_multi, produce_range
+from .ring import DeviceRing, produce_group_multi, produce_range, restage_collate
 from .hub import Hub
 from .transport import HANDOFF, Conn, endpoints_from_env, listen
 from .wire import (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT, SUPPORTED_VERSIONS, Ack,
@@ -112,12 +115,24 @@ class TensorProducer:
         if not 1 <= len(self._devices) <= 8:
             raise ValueError("1..8 devices")
         self.device = self._devices[0]
-        if fanout not in ("sharded", "star"):
-            raise ValueError("fanout must be 'sharded' or 'star'")
+        if fanout not in ("sharded", "star", "inputs"):
+            raise ValueError("fanout must be 'sharded', 'star' or 'inputs'")
         self._multi = len(self._devices) > 1
         if self._multi and control != "host":
             raise ValueError("multi-GPU rings need control='host' (host-shared control words)")
         self._sharded = self._multi and fanout == "sharded"
+        # two-stage: every device gathers its 1/G u8 rows of each
+        # batch into every device's input ring, then each device collates the
+        # whole staged batch into its own ring
+        self._two_stage = self._multi and fanout == "inputs"
+        if self._two_stage and not (getattr(data_loader, "augment", None) is not None and
+                                    hasattr(data_loader, "dataset")):
+            raise ValueError("fanout='inputs' needs a CollateLoader with an AugmentSpec")
+        self._in_rings: dict[int, DeviceRing] = {}
+        self._streams2: dict = {}
+        self._tables: dict = {}
+        self._gather_loader = None
+        self._chain2_ok = False
         self._rings: dict[int, DeviceRing] = {}
         self._streams: dict = {}
         self._descriptors: dict[int, sg.RingDescriptor] = {}
@@ -190,7 +205,7 @@ class TensorProducer:
                         if not dp.can_access_peer(a, b):
                             raise ValueError(f"GPU {a} cannot access GPU {b} (no P2P)")
                         dp.enable_peer(a, b)
-        writers = len(self._devices) if self._sharded else 1
+        writers = len(self._devices) if self._sharded else 1  # two-stage: one writer per ring
         for k, d in enumerate(self._devices):
             with torch.cuda.device(d):
                 # cursor index max_consumers is the producer's retention cursor
@@ -201,6 +216,19 @@ class TensorProducer:
                 rid = self.ring_id if k == 0 else (self.ring_id ^ (k << 44))
                 self._ring_ids[k] = rid
                 _RINGS[rid] = ring
+        if self._two_stage:
+            from .collate import CollateLoader, _Ingest
+
+            ds = self._loader.dataset
+            self._gather_loader = CollateLoader(ds)  # u8 rows + target indices (stage 1)
+            for k, d in enumerate(self._devices):
+                with torch.cuda.device(d):
+                    r = DeviceRing(4, self._gather_loader.batch_nbytes, 1, device=d,
+                                   control="host", writers=len(self._devices))
+                    r.set_cursor(0, 0)
+                    self._in_rings[k] = r
+                    self._streams2[k] = torch.cuda.Stream(device=d)
+                    self._tables[k] = _Ingest(d, ds.batch_size, ds.source.sample_nbytes)
         self._ring = self._rings[0]
         self._stream = self._streams[0]
         with torch.cuda.device(self.device):
@@ -664,7 +692,9 @@ class TensorProducer:
             # park on a device wait, so no stream of this process (in-process
             # consumers included) can be blocked behind one
             self._host_gate(q, live_by_ring)
-        if self._multi and self._device_loader and not self._checksum:
+        if self._two_stage and not self._checksum:
+            self._publish_two_stage(q, index)
+        elif self._multi and self._device_loader and not self._checksum:
             self._publish_group(q, index)
         elif self._device_loader and host_gated and not self._checksum:
             a = self._loader.produce_args(self._epoch)  # fused collate + target + publish
@@ -779,6 +809,48 @@ class TensorProducer:
                             [[] for _ in range(G)])  # gated on the host already (_host_gate)
         self._chain_ok = True
 
+    def _publish_two_stage(self, q: int, index: int) -> None:
+        """Multi-GPU, two-stage: stage 1 -- every device gathers its 1/G rows of
+        batch q (u8 + target indices) into slot q of every device's input ring
+        (tsb_produce_group_multi, gated on the input rings' single cursor);
+        stage 2 -- each device collates the whole staged batch into its own
+        ring on a second stream (tsb_restage_collate: the kernel publishes the
+        output slot and releases the input slot).  The output rings were gated
+        on the host already (_host_gate)."""
+        from ._lib import ProduceArgs
+
+        G = len(self._devices)
+        key = (self._epoch, "inputs")
+        if getattr(self, "_group_cache", (None,))[0] != key:
+            gbase = self._gather_loader.produce_args(self._epoch)
+            abase = self._loader.produce_args(self._epoch)
+            gargs, aargs = [], []
+            for k in range(G):
+                a = ProduceArgs.from_buffer_copy(gbase)
+                a.d_order = self._order_on(self._devices[k], self._epoch).data_ptr()
+                a.gate = GATE_HOST
+                gargs.append(a)
+                a2 = ProduceArgs.from_buffer_copy(abase)
+                a2.ingest = self._tables[k].handle
+                a2.gate = GATE_HOST
+                aargs.append(a2)
+            self._group_cache = (key, (gargs, aargs))
+        gargs, aargs = self._group_cache[1]
+        for a in gargs:
+            a.chain = int(self._chain_ok)
+        produce_group_multi([self._in_rings[k] for k in range(G)], gargs, list(range(G)),
+                            self._devices, [self._streams[k] for k in range(G)], q, index, 1,
+                            [[0] for _ in range(G)])
+        self._chain_ok = True
+        import torch
+
+        for k, d in enumerate(self._devices):
+            aargs[k].chain = int(self._chain2_ok)
+            with torch.cuda.device(d):
+                restage_collate(self._in_rings[k], 0, self._rings[k], aargs[k], q, 1, [],
+                                stream=self._streams2[k])
+        self._chain2_ok = True
+
     def _send_announces(self, anns: dict) -> None:
         """Announce a batch: each consumer gets the slot name of its own GPU's ring."""
         data = {d: encode(a) for d, a in anns.items()}
@@ -836,7 +908,7 @@ class TensorProducer:
     def close(self) -> None:
         """Release the device ring (after join()).  Consumers must be gone."""
         self.join(0.0)
-        for st in self._streams.values():
+        for st in list(self._streams.values()) + list(self._streams2.values()):
             st.synchronize()
         with self._lock:  # the sweeper drains the hub under the same lock
             self._hub.close()
@@ -844,6 +916,10 @@ class TensorProducer:
             _RINGS.pop(self._ring_ids[d], None)
             ring.close()
         self._rings.clear()
+        for ring in self._in_rings.values():
+            ring.close()
+        self._in_rings.clear()
+        self._tables.clear()
         self._ring = None
 
     def __del__(self):

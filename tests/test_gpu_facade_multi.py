@@ -90,7 +90,7 @@ def _run(endpoints, ld, consumers_kw, epochs, **pkw):
     return producer, outs
 
 
-@pytest.mark.parametrize("fanout", ["sharded", "star"])
+@pytest.mark.parametrize("fanout", ["sharded", "star", "inputs"])
 @pytest.mark.parametrize("out_dtype,kind", [("float32", 1), ("bfloat16", 2)])
 def test_multi_ring_producer_every_consumer_gets_every_batch(endpoints, oracle, fanout,
                                                              out_dtype, kind):
