@@ -73,6 +73,18 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def reduce_over_ranks(x: float, op: str, backend: str) -> float:
+    """max (device time of the slowest rank) or sum (whole-job throughput)
+    of a per-rank number, on the process group's device."""
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64,
+                     device="cuda" if backend == "nccl" else "cpu")
+    torch.distributed.all_reduce(t, op=(torch.distributed.ReduceOp.MAX if op == "max" else
+                                        torch.distributed.ReduceOp.SUM))
+    return float(t.item())
+
+
 class Clocks:
     """SM clock + throttle-reason sampling during the timed region
     (B200_PROFILING.md clocks line).  NVML in a thread at 5 ms (the timed
@@ -390,9 +402,7 @@ def run_ours(args):
     # kernel's average launch duration is the timed region / K
     avg_launch_ms = ms / K
     if world > 1:
-        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_max = float(t.item())
+        ms_max = reduce_over_ranks(ms, "max", backend)
         torch.distributed.barrier()  # peers are done writing into our ring
     else:
         ms_max = ms
@@ -551,10 +561,7 @@ def run_e2e(args, ctx, dev, rank, world):
     wall = time.monotonic() - t_start
     value = sum(rates.values())
     if world > 1:
-        t = torch.tensor([value], device="cuda" if os.environ.get("TSB_BENCH_BACKEND", "nccl")
-                         == "nccl" else "cpu")
-        torch.distributed.all_reduce(t)
-        value = float(t.item())
+        value = reduce_over_ranks(value, "sum", os.environ.get("TSB_BENCH_BACKEND", "nccl"))
     path = ("TensorProducer(CollateLoader(pinned-host StoreSource)) -> 4 SharedLoader processes "
             "(CUDA IPC); each batch's sample rows that the crop reads cross PCIe by the copy "
             "engine, with the host-derived crop/flip table; consumers .item() one element per "

@@ -32,3 +32,42 @@ def test_warmup_floor_enforced():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--warmup", "2"],
                          capture_output=True, text=True, timeout=120, cwd=ROOT)
     assert out.returncode != 0 and "warmup" in out.stderr
+
+
+def _reduce_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import bench
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, w, lr = bench.dist_env()
+        ms = [3.5, 7.25][rank]  # per-rank device time of the timed region
+        q.put((rank, (r, w, lr), bench.reduce_over_ranks(ms, "max", "gloo"),
+               bench.reduce_over_ranks(1000.0 * (rank + 1), "sum", "gloo")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_multi_rank_timing_is_max_over_ranks_gloo_world2():
+    """bench.py at N > 1: every rank reads its rank from the env, the timed
+    region is the max over ranks, e2e throughput is summed over ranks."""
+    import multiprocessing as mp
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_reduce_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {m[0]: m[1:] for m in (q.get(timeout=120) for _ in ps)}
+    for p in ps:
+        p.join(30)
+    for r in (0, 1):
+        assert res[r] == ((r, 2, r), 7.25, 3000.0)
