@@ -152,7 +152,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=512)
     ap.add_argument("--warmup", type=int, default=16)
-    ap.add_argument("--only", default="c1,c2bf16,c5video,c5llm,c4")
+    ap.add_argument("--only", default="c1,c2bf16,c5video,c5llm,c4native,c4")
     ap.add_argument("--persistent", action="store_true",
                     help="passthrough configs (C1, C5) as one persistent launch per range")
     args = ap.parse_args()
@@ -225,6 +225,18 @@ def main():
                         % (sum(map(len, files)) // len(files) // 1024,
                            src.decoder(0, 256).backend))
         print(json.dumps(r), flush=True)
+    if "c4native" in which:
+        # the data plane under C4: one B=512 bf16 producer, 8 map-and-ack consumers.
+        # A consumer with b in {64,128,256,512} reads b-sample zero-copy windows of
+        # the slot (ledger.rebatch_window_plan) and releases the slot after its last
+        # window there, so per slot it receives the same 512 samples.
+        store = StoreSource.synthetic(0, N, (224, 224, 3), location="hbm")
+        ld = CollateLoader(DatasetSpec(store, N, 512), AugmentSpec(out_dtype="bfloat16"))
+        r = device_run(ld, 8, K, Wm)
+        r.update(config="C4 data plane (one GPU): B=512 bf16 slots, 8 map-and-ack consumers "
+                        "(b=64..512 read zero-copy windows of each slot)")
+        print(json.dumps(r), flush=True)
+        del store, ld
     if "c4" in which:
         r = c4()
         r.update(config="C4 (one GPU): consumers with b=64/128/256/512 (2 each) on one producer "
