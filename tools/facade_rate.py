@@ -58,7 +58,14 @@ def main():
     tmp = f"/tmp/tsb-fr-{os.getpid()}"
     os.makedirs(tmp, exist_ok=True)
     b, a = f"unix:{tmp}/b.sock", f"unix:{tmp}/a.sock"
-    prod = TensorProducer(ld, b, a, min_consumers=K, ring_slots=8, heartbeat_timeout_s=60)
+    # TSB_FR_DEVICES="0,0" + TSB_FR_FANOUT=inputs|sharded|star: the multi-ring
+    # producer (one GPU here: every ring on device 0, consumers spread over them)
+    devs = os.environ.get("TSB_FR_DEVICES")
+    kw = {}
+    if devs:
+        kw = dict(devices=[int(d) for d in devs.split(",")],
+                  fanout=os.environ.get("TSB_FR_FANOUT", "inputs"))
+    prod = TensorProducer(ld, b, a, min_consumers=K, ring_slots=8, heartbeat_timeout_s=60, **kw)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     ps = [ctx.Process(target=consumer, args=(b, a, 100 + k, n, q, sync)) for k in range(K)]
@@ -91,7 +98,8 @@ def main():
     print(json.dumps({"consumer_batches_per_s": [round(r, 1) for r in rates],
                       "delivered_samples_per_s": round(sum(rates) * B, 1),
                       "producer_loop_batches_per_s": round((n - n // 4) / (t1 - t0), 1),
-                      "sync": sync, "consumers": K}))
+                      "sync": sync, "consumers": K, **({"devices": devs, "fanout": kw["fanout"]}
+                                                       if devs else {})}))
 
 
 if __name__ == "__main__":
