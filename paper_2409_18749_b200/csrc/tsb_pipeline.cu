@@ -3,6 +3,8 @@
 // a few driver calls instead of a Python round trip.
 #include <stdlib.h>
 
+#include <cstdlib>
+
 #include "tsb_common.cuh"
 
 using namespace tsb;
@@ -417,8 +419,12 @@ int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
         const uint64_t q = seq0 + (uint64_t)i;
         const int islot = (int)((q - 1) % (uint64_t)in_slots);
         const int oslot = (int)((q - 1) % (uint64_t)out_slots);
-        // every writer's shard of batch q is in the input slot (host-side wait)
-        if (int rc = tsb_ring_host_wait_ready(in_ring, islot, q, -1)) return rc;
+        // every writer's shard of batch q is in the input slot (host-side wait,
+        // bounded like the flow gate: TSB_GATE_TIMEOUT_S, default 600 s)
+        static const int64_t wait_us =
+            (int64_t)(1e6 * (getenv("TSB_GATE_TIMEOUT_S") ? atof(getenv("TSB_GATE_TIMEOUT_S"))
+                                                          : 600.0));
+        if (int rc = tsb_ring_host_wait_ready(in_ring, islot, q, wait_us)) return rc;
         if (q > (uint64_t)out_slots)
             if (int rc = ring_host_gate(out_ring, live, n_live, q - (uint64_t)out_slots)) return rc;
         void *in = nullptr, *out = nullptr;
