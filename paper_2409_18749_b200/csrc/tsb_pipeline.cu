@@ -3,8 +3,6 @@
 // a few driver calls instead of a Python round trip.
 #include <stdlib.h>
 
-#include <cstdlib>
-
 #include "tsb_common.cuh"
 
 using namespace tsb;
