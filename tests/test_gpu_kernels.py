@@ -274,3 +274,33 @@ def test_directory_source_files_and_batches_match_reference(golden, tmp_path):
     (tmp_path / "sample-00000003.bin").write_bytes(b"short")
     with pytest.raises(ValueError, match="expected"):
         StoreSource.from_directory(str(tmp_path), (d["sample_bytes"],))
+
+
+@pytest.mark.parametrize("mean,std", [
+    ((0.485, 0.456, 0.406), (0.229, 0.224, 0.225)),        # one-FMA bf16 path is exact here
+    ((0.8041, 0.7499, 0.6343), (0.4834, 0.4703, 0.3993)),  # ... and not here (channel 0)
+])
+def test_bf16_fma_path_selection_is_bit_exact(oracle, mean, std):
+    """The bf16 kernel takes one FFMA2 per pair only when, for the batch's
+    scale/bias, the single rounding gives the oracle's bf16 for all 256 byte
+    values of every channel (checked on the host); otherwise it keeps the two
+    roundings.  Either way the output is the oracle's, bit for bit."""
+    h, w, c, b, pad = 32, 64, 3, 16, 4
+    store = oracle.make_store(3, 64, h * w * c)
+    idx = oracle.epoch_order(64, 0, 1)[:b]
+    scale, bias = oracle.norm_consts(mean, std)
+    u = np.arange(256, dtype=np.float32)
+    two = ((u[:, None] * scale).astype(np.float32) + bias).astype(np.float32)
+    fma = (u[:, None].astype(np.float64) * scale.astype(np.float64) + bias).astype(np.float32)
+
+    def rne(x):
+        bits = x.view(np.uint32).astype(np.uint64)
+        return (bits + 0x7FFF + ((bits >> 16) & 1)) >> 16
+
+    exact_fma = np.array_equal(rne(two), rne(fma))
+    assert exact_fma == (mean[0] == 0.485)  # the two cases really differ
+    want = oracle.collate_augment(store, idx, h, w, c, pad, True, 5, 1, 2, scale, bias)
+    out = torch.empty((b, c, h, w), dtype=torch.int16, device="cuda")
+    dp.collate_augment(dev(store), dev(idx), b, h, w, c, pad, True, 5, 1, 2, out,
+                       scale=scale, bias=bias)
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16), want)

@@ -2,9 +2,10 @@
 
 The knobs (TSB_CA_R rows per item, TSB_CA_STAGES pipeline depth,
 TSB_CA_ORDER item order, TSB_CA_OCC grid cap, TSB_CA_GRID absolute grid,
-TSB_CA_RESIDENT resident CTAs per SM, TSB_CA_NOTMA cooperative staging, TSB_CA_IMPL=direct staging-free
-kernel, TSB_CA_ST / TSB_CA_LDHINT cache hints) are read once per process, so
-each configuration runs in a child process that prints the CRC-32 of the
+TSB_CA_RESIDENT resident CTAs per SM, TSB_CA_NOTMA cooperative staging,
+TSB_CA_IMPL=direct staging-free kernel, TSB_CA_ST / TSB_CA_LDHINT cache
+hints, TSB_BF16_FMA=0 two-rounding bf16) are read once per process, so each
+configuration runs in a child process that prints the CRC-32 of the
 collated batch; the parent checks it against the oracle's bytes."""
 
 import json
@@ -52,6 +53,7 @@ KNOBS = [
     {"TSB_CA_NOTMA": "1"},
     {"TSB_CA_IMPL": "direct"},
     {"TSB_CA_ST": "plain", "TSB_CA_LDHINT": "0"},
+    {"TSB_BF16_FMA": "0"},
 ]
 
 
