@@ -397,22 +397,23 @@ __device__ __forceinline__ uint4 make_vec(const uint32_t *wv, float sc, float bi
             }
             return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
-        }
-#pragma unroll
-        for (int i = 0; i < P; i += 2) {
-            uint64_t u = pack_f32x2(__uint_as_float(bits[i]), __uint_as_float(bits[i + 1]));
-            u = mul_rn_f32x2(add_rn_f32x2(u, k23), sc2);
-            float m0, m1;
-            unpack_f32x2(u, m0, m1);
-            f[i] = __fadd_rn(m0, bi);  // scalar .rn add: keeps the product's rounding
-            f[i + 1] = __fadd_rn(m1, bi);
-        }
-        if constexpr (OUT_KIND == TSB_OUT_F32) {
-            return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
-                              __float_as_uint(f[3]));
         } else {
-            return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
-                              pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+#pragma unroll
+            for (int i = 0; i < P; i += 2) {
+                uint64_t u = pack_f32x2(__uint_as_float(bits[i]), __uint_as_float(bits[i + 1]));
+                u = mul_rn_f32x2(add_rn_f32x2(u, k23), sc2);
+                float m0, m1;
+                unpack_f32x2(u, m0, m1);
+                f[i] = __fadd_rn(m0, bi);  // scalar .rn add: keeps the product's rounding
+                f[i + 1] = __fadd_rn(m1, bi);
+            }
+            if constexpr (OUT_KIND == TSB_OUT_F32) {
+                return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                                  __float_as_uint(f[2]), __float_as_uint(f[3]));
+            } else {
+                return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                  pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+            }
         }
     }
 }
@@ -1053,7 +1054,10 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
 // local ring and peer rings over NVLink.  Work items = (sample, 16 KB chunk),
 // strided over a persistent grid; 4 independent 16 B loads per thread.
 constexpr int PT_THREADS = 256;
-constexpr int PT_CHUNK = 16384;
+#ifndef TSB_PT_CHUNK
+#define TSB_PT_CHUNK 16384
+#endif
+constexpr int PT_CHUNK = TSB_PT_CHUNK;  // bytes per passthrough work item
 
 template <bool SYNTH, bool MULTI>
 __global__ void __launch_bounds__(PT_THREADS)
