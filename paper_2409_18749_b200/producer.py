@@ -35,7 +35,9 @@ missing barrier is the start race noted in SURVEY.md §4), ``checksum``
 
 Multi-GPU (``devices=[0, 1, ...]``): one ring per device, each
 consumer maps the ring of its own GPU (``SharedLoader(device=...)``, Join v2).
-``fanout="sharded"`` (default): every device collates its 1/G rows of each
+``fanout="auto"`` (default) picks ``"inputs"`` for an augmenting
+``CollateLoader`` and ``"sharded"`` otherwise.  ``fanout="sharded"``: every
+device collates its 1/G rows of each
 batch and the kernel stores them into the same slot of every device's ring
 (P2P stores over NVLink/NVSwitch -- the all-gather fused into the producing
 kernel, ``tsb_produce_group``); ``fanout="inputs"`` (two-stage): every
@@ -89,7 +91,7 @@ class TensorProducer:
                  min_consumers: int = 1, checksum: bool = False,
                  rubberband_fraction: float = 0.0, max_consumers: int = 64,
                  device: int | None = None, control: str = "host", devices=None,
-                 fanout: str = "sharded"):
+                 fanout: str = "auto"):
         import torch
 
         if not hasattr(data_loader, "__len__"):
@@ -115,8 +117,12 @@ class TensorProducer:
         if not 1 <= len(self._devices) <= 8:
             raise ValueError("1..8 devices")
         self.device = self._devices[0]
-        if fanout not in ("sharded", "star", "inputs"):
-            raise ValueError("fanout must be 'sharded', 'star' or 'inputs'")
+        if fanout not in ("auto", "sharded", "star", "inputs"):
+            raise ValueError("fanout must be 'auto', 'sharded', 'star' or 'inputs'")
+        if fanout == "auto":  # two-stage where a collate follows the gather, else sharded
+            fanout = "inputs" if (getattr(data_loader, "augment", None) is not None and
+                                  hasattr(data_loader, "dataset")) else "sharded"
+        self.fanout = fanout
         self._multi = len(self._devices) > 1
         if self._multi and control != "host":
             raise ValueError("multi-GPU rings need control='host' (host-shared control words)")
