@@ -84,6 +84,16 @@ struct IngestCrop {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Restores the calling thread's current device on scope exit: an entry point
+// that works on a given device leaves the caller's device as it found it.
+struct CurrentDeviceGuard {
+    int prev = -1;
+    CurrentDeviceGuard() { cudaGetDevice(&prev); }
+    ~CurrentDeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 inline int sm_count() {
     static int cached[64] = {0};
     int dev = 0;

@@ -165,6 +165,7 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
                       tsb_ingest **out) {
     TSB_CHECK(out && max_batch >= 1 && sample_bytes >= 1 && depth >= 1 && depth <= 8,
               "bad ingest geometry");
+    CurrentDeviceGuard device_guard;
     TSB_CUDA(cudaSetDevice(dev));
     tsb_ingest *g = new tsb_ingest{};
     g->dev = dev;

@@ -160,6 +160,7 @@ int tsb_jpeg_create(int dev, int64_t max_batch, int h, int w, int backend, tsb_j
         set_error("libnvjpeg.so.12 not found: the JPEG source needs nvJPEG");
         return TSB_ERR_UNSUPPORTED;
     }
+    CurrentDeviceGuard device_guard;
     TSB_CUDA(cudaSetDevice(dev));
     tsb_jpeg *j = new tsb_jpeg{};
     j->dev = dev;

@@ -114,24 +114,34 @@ __global__ void wait_kernel(WaitSet set, uint64_t value) {
 }
 
 // Driver-API stream memops need a current context on the calling thread;
-// runtime calls create it lazily, so bind the ring's device first.
-int bind_ctx(int dev) {
-    static thread_local int bound_dev = -1;
+// runtime calls create it lazily, so bind the ring's device first -- and give
+// the caller's current device back afterwards (a multi-GPU producer thread
+// must not find its current device switched under it by a ring operation).
+struct DeviceGuard {
+    int prev = -1;
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+int bind_ctx(int dev, DeviceGuard &guard) {
+    static thread_local uint64_t ready_mask = 0;  // devices whose context this thread made current
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) {
         TSB_CUDA(cudaSetDevice(dev));
-        bound_dev = -1;
+        guard.prev = cur;
     }
-    if (bound_dev != dev) {
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+    if (!(ready_mask & bit)) {
         TSB_CUDA(cudaFree(nullptr));  // no-op that makes the primary context current
-        bound_dev = dev;
+        ready_mask |= bit;
     }
     return TSB_OK;
 }
 
 int dev_write(tsb_ring *r, uint64_t *addr, uint64_t v, void *stream) {
     if (resolve_mode() == 1) {
-        if (int rc = bind_ctx(r->dev)) return rc;
+        DeviceGuard guard;
+        if (int rc = bind_ctx(r->dev, guard)) return rc;
         CUresult e = g_write64((CUstream)stream, (CUdeviceptr)addr, v, 0);
         if (e != CUDA_SUCCESS) {
             set_error("cuStreamWriteValue64 failed (%d)", (int)e);
@@ -148,7 +158,8 @@ int dev_write(tsb_ring *r, uint64_t *addr, uint64_t v, void *stream) {
 int dev_wait(tsb_ring *r, const uint64_t *const *addrs, int n, uint64_t v, void *stream) {
     if (n <= 0) return TSB_OK;
     if (resolve_mode() == 1) {
-        if (int rc = bind_ctx(r->dev)) return rc;
+        DeviceGuard guard;
+        if (int rc = bind_ctx(r->dev, guard)) return rc;
         for (int i = 0; i < n; ++i) {
             CUresult e = g_wait64((CUstream)stream, (CUdeviceptr)addrs[i], v,
                                   CU_STREAM_WAIT_VALUE_GEQ);
@@ -300,6 +311,7 @@ int tsb_ring_create_ex(int dev, int slots, size_t slot_bytes, int max_consumers,
     TSB_CHECK(slots >= 1 && max_consumers >= 1 && max_consumers <= 4096,
               "bad ring geometry slots=%d consumers=%d", slots, max_consumers);
     TSB_CHECK(writers >= 1 && writers <= TSB_MAX_WRITERS, "writers must be 1..%d", TSB_MAX_WRITERS);
+    CurrentDeviceGuard device_guard;
     TSB_CUDA(cudaSetDevice(dev));
     tsb_ring *r = new tsb_ring{};
     r->dev = dev;
@@ -390,6 +402,7 @@ int tsb_ring_attach_host_control(tsb_ring *r, void *host_ctl, size_t bytes, int 
     TSB_CHECK(bytes >= need && ((uintptr_t)host_ctl & 7) == 0,
               "host control block too small or misaligned (%zu < %zu)", bytes, need);
     if (init) memset(host_ctl, 0, need);
+    CurrentDeviceGuard device_guard;
     TSB_CUDA(cudaSetDevice(r->dev));
     TSB_CUDA(cudaHostRegister(host_ctl, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
     void *dptr = nullptr;

@@ -302,3 +302,18 @@ def test_persistent_producer_matches_reference(golden, mode):
     np.testing.assert_array_equal(crcs[1][1], cases[(0, 0)]["indices"])
     a.persistent = 0
     ring.close()
+
+
+def test_ring_operations_leave_the_current_device_alone():
+    """Entry points that work on a ring's device (creation, host-control
+    attach, stream memops) give the caller's current device back (on a
+    one-GPU box this checks the plumbing; the guard matters with several)."""
+    torch.cuda.set_device(0)
+    before = torch.cuda.current_device()
+    ring = DeviceRing(2, 4096, 1, device=0, control="host")
+    s = torch.cuda.Stream()
+    ring.publish(0, 1, s)
+    ring.ack(0, 1, s)
+    s.synchronize()
+    assert torch.cuda.current_device() == before
+    ring.close()
