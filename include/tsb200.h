@@ -324,11 +324,13 @@ int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_
  * compact u8 rows cross NVLink: 1x the input instead of the 2-4x larger
  * f32/bf16 outputs), target = the real sample indices.  Stage 2, per GPU,
  * for each batch q: host-wait until every writer's shard is in in_ring,
- * host-gate out_ring's slot on its live consumers, collate/augment the
- * staged rows into out_ring's slot (params keyed by the staged indices) with
- * the fused publish, then release the input slot from the stream
- * (in_ring cursor in_consumer := q).  a: augment geometry of the OUTPUT and
- * a->ingest for the param / identity tables. */
+ * host-gate out_ring's slot on its live consumers, then one PDL-chained
+ * kernel collates/augments the staged rows into out_ring's slot (crop/flip
+ * keyed by the staged target indices, derived in-kernel); its last CTA
+ * publishes the output slot and releases the input slot (in_ring cursor
+ * in_consumer := q).  a: augment geometry of the OUTPUT, a->ingest for the
+ * identity table, a->chain = the stream's previous op was this call's
+ * kernel. */
 int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
                         const tsb_produce_args *a, uint64_t seq0, int n, const int *live,
                         int n_live, void *stream);
