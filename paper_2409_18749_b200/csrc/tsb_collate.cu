@@ -196,11 +196,18 @@ struct Epi {
     int sys_fence;           // destinations on other devices: order stores at system scope
     const int64_t *tgt_idx;  // sample indices written as the target (nullptr = the gather indices)
     int fence_all;           // A/B (TSB_FENCE_ALL=1): every thread fences before the CTA barrier
+    int early_pdl;           // passthrough: let the next batch launch at this kernel's start
 };
 
 // Publish ordering knob, read once per process.
 int fence_all_knob() {
     static const int v = getenv("TSB_FENCE_ALL") ? atoi(getenv("TSB_FENCE_ALL")) : 0;
+    return v;
+}
+// Passthrough batches trigger their dependent launch at kernel start
+// (TSB_PT_EARLY=0: at the end, as the collate does).
+int early_pdl_knob() {
+    static const int v = getenv("TSB_PT_EARLY") ? atoi(getenv("TSB_PT_EARLY")) : 1;
     return v;
 }
 
@@ -1064,6 +1071,10 @@ __global__ void __launch_bounds__(PT_THREADS)
     passthrough_multi_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx,
                              int64_t sb, int b, uint64_t seed, uint64_t epoch, Dsts dsts, Epi ep) {
     const int tid = threadIdx.x;
+    // the next batch writes another slot and was gated on the host: nothing it
+    // does depends on this grid, so a latency-bound small batch can let it
+    // start right away and the two overlap (PDL; no griddepcontrol.wait)
+    if (ep.early_pdl) pdl_launch_dependents();
     if (blockIdx.x == 0) write_targets(ep, idx, b, tid, PT_THREADS);
     const int chunks = (int)((sb + PT_CHUNK - 1) / PT_CHUNK);
     const int items = b * chunks;
@@ -1306,6 +1317,7 @@ int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int 
     ep.pdl = pdl;
     ep.sys_fence = sys_fence;
     ep.fence_all = fence_all_knob();
+    ep.early_pdl = early_pdl_knob();
     if (mode == TSB_SRC_AUGMENT)
         return launch_collate(src, idx, b, h, w, c, pad, flip, seed, epoch, scale, bias, out_kind,
                               nullptr, d, stream, ep);
