@@ -1001,15 +1001,17 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
                    (g.sample_bytes % 4 == 0) && (((uintptr_t)src & 3) == 0) && b <= DC_MAX_B &&
                    b * (int64_t)h * (w / vec) < (1ll << 31);
     // Rows per item (measured on B200, B=256 224x224x3, inside the PDL-chained
-    // producer loop; profiles/r1/collate_rows_sweep.txt): items of ~45 rows --
-    // each sample split into ceil(h/45) nearly equal row blocks, 5 for 224 --
-    // with 2 stages (73 KB of shared memory, 3 CTAs per SM).  Long items keep
-    // each CTA's write streams long (R rows x w per channel plane) between its
-    // read bursts; f32 32.2 us (0.91 of the HBM peak), bf16 22.3, u8 18.4 per
-    // batch, against 36.9 / 24.4 / 19.8 at the earlier power-of-two R.
+    // producer loop with the start-of-kernel trigger; profiles/r1/
+    // collate_rows_sweep_v2.txt): items of ~32 rows -- each sample split into
+    // ceil(h/32) nearly equal row blocks, 7 of 32 for 224 -- with 2 stages
+    // (52 KB of shared memory, 4 CTAs per SM).  Long items keep each CTA's
+    // write streams long (R rows x w per channel plane) between its read
+    // bursts: f32 29.5 us (the measured copy peak), bf16 19.0, u8 14.8 per
+    // batch (45-row items: 30.0 / 19.4 / 15.7; 4-row items: 36.9 / 24.4 / 19.8
+    // before the trigger change).
     int R;
     {
-        const int nb = (h + 44) / 45;
+        const int nb = (h + 31) / 32;
         R = (h + nb - 1) / nb;
     }
     const int nt = out_kind == TSB_OUT_F32 ? CA_THREADS_F32 : CA_THREADS;
@@ -1034,8 +1036,8 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     size_t smem = (size_t)(nstage * R + 1) * g.rs + 2 * nstage * sizeof(uint64_t) +
                   META_CAP * sizeof(ItemPar);
     // Resident CTAs per SM (A/B knob TSB_CA_RESIDENT): reserve shared memory so
-    // at most `resident` CTAs fit on an SM.  With 45-row items the natural 3
-    // per SM wins (2: 35.0 us; profiles/r1/collate_rows_sweep.txt).
+    // at most `resident` CTAs fit on an SM (the natural count wins;
+    // profiles/r1/collate_rows_sweep.txt).
     int resident = 0;
     if (kn.resident >= 0) resident = kn.resident;
     if (resident > 0) {
