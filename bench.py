@@ -423,6 +423,9 @@ def run_ours(args):
         achieved = B * ALG_BYTES_PER_SAMPLE / (avg_launch_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
+                    # the measured peak is a best-of-10 torch copy; the HGX spec figure
+                    # (B200_PROFILING.md) for comparison
+                    "spec_peak_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4),
                     "kernel": "collate_augment_kernel<f32,C=3>",
                     "alg_bytes_per_launch": B * ALG_BYTES_PER_SAMPLE,
                     "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src}
