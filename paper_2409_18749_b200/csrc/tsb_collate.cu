@@ -134,11 +134,11 @@ __global__ void aug_params_kernel(uint64_t aug_mixed, uint64_t epoch,
 // in parallel by warp 0 in the prologue (or read from a param table).
 // Sources TMA cannot address (pinned host memory, unaligned rows) use the
 // same loop with cooperative 16-byte LDG staging instead.
-// Consumer threads per CTA (+1 producer warp): 128 for f32 (31.8 vs 32.3 us
-// per B=256 batch), 256 for bf16/u8 (22.2 vs 23.5 us at 128);
-// profiles/r1/collate_threads_ab.txt.
+// Consumer threads per CTA (+1 producer warp): 128 for every output kind at
+// the final item size (f32 31.8 vs 32.3 us per B=256 batch at 256; bf16 18.9
+// vs 19.1, u8 14.8 vs 14.9 with 32-row items; profiles/r1/collate_threads_ab.txt).
 #ifndef TSB_CA_THREADS
-#define TSB_CA_THREADS 256
+#define TSB_CA_THREADS 128
 #endif
 #ifndef TSB_CA_THREADS_F32
 #define TSB_CA_THREADS_F32 128
