@@ -57,6 +57,10 @@ OUT_BYTES = C * H * W * 4          # f32 NCHW per sample
 ALG_BYTES_PER_SAMPLE = SAMPLE_BYTES + OUT_BYTES  # 752,640 B read + write (collate)
 METRIC = "delivered samples/sec (all consumers)"
 REF_BUDGET_S = 90.0  # reference arm: total CPU seconds the timed + warm-up steps may take
+E2E_BATCHES = 4096  # e2e API leg: fixed window of batches, independent of --steps
+E2E_WARMUP = 64     # e2e batches before the window (consumer start-up skew)
+E2E_BUFFER_DEPTH = RING_SLOTS - 2  # flow gate of the e2e producer (reference default is 2)
+HOLD_S = 0.004      # value leg: the stream is held while the first batches are enqueued
 NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
 WORKLOAD = ("C2: 1 producer + 4 same-GPU consumers via CUDA IPC zero copy, 224x224x3 u8 store "
             "-> ResNet-50-shaped f32 NCHW (crop pad16 + hflip from the reference RNG + ImageNet "
@@ -239,7 +243,8 @@ def host_consumer(dev, handle, control, slots, slot_bytes, max_consumers, cursor
 
 def api_consumer(dev, bcast, agg, cid, warmup, steps, q):
     """e2e consumer through the public API: SharedLoader over CUDA IPC; reads
-    one element per batch back to the host (the step result)."""
+    one element per batch back to the host (the step result).  Reports the
+    fetch time of every batch after the warm-up."""
     import torch
 
     torch.cuda.set_device(dev)
@@ -260,7 +265,23 @@ def api_consumer(dev, bcast, agg, cid, warmup, steps, q):
             break
     loader.close()
     rate = (len(times) - 1) / (times[-1] - times[0]) * B if len(times) > 1 else 0.0
-    q.put(("done", cid, rate, n))
+    q.put(("done", cid, rate, n, times))
+
+
+def common_window_rate(stamps: dict) -> tuple[float, float, int]:
+    """Aggregate delivered samples/s over the window every consumer was
+    streaming in: [latest first fetch, earliest last fetch]; each consumer's
+    fetches inside it, by the reference formula's spirit (bs/cli.py:220-236:
+    batches x batch / elapsed), summed (bs/harness.py:574).  Returns (rate,
+    window seconds, batches counted)."""
+    lo = max(t[0] for t in stamps.values())
+    hi = min(t[-1] for t in stamps.values())
+    if hi <= lo:
+        return 0.0, 0.0, 0
+    n = 0
+    for t in stamps.values():
+        n += sum(1 for x in t if lo < x <= hi)
+    return n * B / (hi - lo), hi - lo, n
 
 
 # --------------------------------------------------------------- ours ------
@@ -382,15 +403,27 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0, t1 = dp.DeviceEvent(), dp.DeviceEvent()
+    # The stream is held on a host-released word while the host enqueues the
+    # first batches (up to the ring depth, then the slot gate blocks it), so
+    # t0 marks the device starting batch Wm+1, not the host's launch latency;
+    # after the release the host keeps enqueueing ahead of the device.
+    hold = DeviceRing(1, 64, 1, device=dev, control="host")
+    hold.wait_free([0], 1, stream)
+    t0.record(stream)
+    release = threading.Timer(HOLD_S, hold.host_ack, args=(0, 1))
     clocks = Clocks(dev)
     clocks.start()
-    t0.record(stream)
+    release.start()
     produce(Wm + 1, K)
     t1.record(stream)
     stream.synchronize()
     clk = clocks.stop()
+    release.join()
     torch.cuda.synchronize()
     ms = t0.elapsed_ms(t1)
+    hold.close()
+    parity = check_ring_parity(ring, loader, Wm + K, dp) if world == 1 else None
+    bf16 = bf16_line(dev, store, ds, K, Wm) if world == 1 else None
     consumer_rates = {}
     for _ in procs:
         msg = q.get(timeout=300)
@@ -414,6 +447,8 @@ def run_ours(args):
         in_ring.close()
     ring.close()
     del store, loader
+    if parity is not None and not parity["ok"]:
+        log("PARITY FAILURE:", json.dumps(parity))
 
     # ---- e2e through the public API (pinned host store, PCIe ingest) ----
     e2e = run_e2e(args, ctx, dev, rank, world)
@@ -481,7 +516,12 @@ def run_ours(args):
         "clocks": clk,
         "extra": {"producer_ms": round(ms, 3),
                   "consumer_rates_samples_s": {str(k): round(v, 1) for k, v in consumer_rates.items()},
-                  "produced_samples_per_s": round(B * K / (ms_max / 1e3), 1)},
+                  "produced_samples_per_s": round(B * K / (ms_max / 1e3), 1),
+                  "timing": f"device events on the producer stream; the stream is held for "
+                            f"{HOLD_S * 1e3:.0f} ms on a host-released word while the first "
+                            f"batches are enqueued (t0 = device start of batch {Wm + 1})",
+                  **({"parity": parity} if parity is not None else {}),
+                  **({"bf16": bf16} if bf16 is not None else {})},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
@@ -490,6 +530,112 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def oracle_batch_crc(o, epoch: int, bi: int, out_kind: int, nthreads: int) -> int:
+    """CRC-32 the reference path gives batch (epoch, bi) of the C2 stream:
+    oracle collate+augment of the samples order[bi*B:(bi+1)*B] (a store
+    sample i = fill(derive_key(0, 0, i)), pipeline.py:139-155), followed by
+    the int64 target indices (the pair payload, sl/abi.py:291-308)."""
+    import numpy as np
+
+    order = o.epoch_order(N_SAMPLES, 0, epoch)
+    idx = np.ascontiguousarray(order[bi * B:(bi + 1) * B])
+    mini = o.prepare_synthetic(0, 0, idx, SAMPLE_BYTES, nthreads)  # just those samples
+    params = o.aug_params(0, epoch, idx, PAD)
+    scale, bias = o.norm_consts()
+    out = o.collate_augment(mini, np.arange(B, dtype=np.int64), H, W, C, PAD, True, 0, epoch,
+                            out_kind, scale, bias, params=params, nthreads=nthreads)
+    return o.crc32(idx.astype(np.int64), o.crc32(out))
+
+
+def check_ring_parity(ring, loader, last_seq: int, dp) -> dict:
+    """After the timed region: the device CRC-32 of every batch still in the
+    ring (the last `slots` produced) against the oracle's CRC of the same
+    batch (a CRC gate on every run)."""
+    import torch
+
+    from oracle import oracle as o
+
+    nthreads = os.cpu_count() or 1
+    L = len(loader)
+    crc = torch.zeros(1, dtype=torch.int32, device=f"cuda:{ring.device}")
+    rows, ok = [], True
+    for q in range(max(1, last_seq - ring.slots + 1), last_seq + 1):
+        slot = ring.slot_of(q)
+        epoch, bi = divmod(q - 1, L)
+        dp.crc32(ring.slot_ptr(slot), loader.batch_nbytes, crc)
+        torch.cuda.synchronize()
+        got = int(crc.item()) & 0xFFFFFFFF
+        want = oracle_batch_crc(o, epoch, bi, o.OUT_F32, nthreads)
+        ready = ring.read_ready(slot)
+        ok = ok and got == want and ready == q
+        rows.append({"seq": q, "epoch": epoch, "batch": bi, "crc": f"{got:#010x}",
+                     "oracle": f"{want:#010x}"})
+    return {"ok": ok, "batches_checked": len(rows), "bytes_per_batch": loader.batch_nbytes,
+            "how": "device CRC-32 (tsb_crc32) of each resident ring slot = f32 NCHW input + "
+                   "int64 targets, vs the oracle's collate+augment of the same batch",
+            "batches": rows}
+
+
+def bf16_line(dev, store, ds, K: int, Wm: int) -> dict:
+    """C2/C3's bf16 output through the same native loop (no consumers: the
+    collate alone, PDL-chained, device-timed), plus its parity on the last batch."""
+    import torch
+
+    from oracle import oracle as o
+    from paper_2409_18749_b200 import AugmentSpec, CollateLoader
+    from paper_2409_18749_b200 import dataplane as dp
+    from paper_2409_18749_b200._lib import GATE_HOST
+    from paper_2409_18749_b200.ring import DeviceRing, produce_range
+
+    ld = CollateLoader(ds, AugmentSpec(pad=PAD, flip=True, out_dtype="bfloat16"))
+    ring = DeviceRing(RING_SLOTS, ld.batch_nbytes, 1, device=dev, control="host")
+    st = torch.cuda.Stream()
+    L = len(ld)
+
+    def run(seq0, n):
+        done = 0
+        while done < n:
+            q0 = seq0 + done
+            epoch, bi = divmod(q0 - 1, L)
+            m = min(n - done, L - bi)
+            a = ld.produce_args(epoch)
+            a.gate = GATE_HOST
+            produce_range(ring, a, q0, bi, m, [], stream=st)
+            done += m
+
+    run(1, Wm)
+    st.synchronize()
+    hold = DeviceRing(1, 64, 1, device=dev, control="host")
+    hold.wait_free([0], 1, st)
+    e0, e1 = dp.DeviceEvent(), dp.DeviceEvent()
+    e0.record(st)
+    rel = threading.Timer(HOLD_S, hold.host_ack, args=(0, 1))
+    rel.start()
+    run(Wm + 1, K)
+    e1.record(st)
+    st.synchronize()
+    rel.join()
+    ms = e0.elapsed_ms(e1)
+    hold.close()
+    last = Wm + K
+    epoch, bi = divmod(last - 1, L)
+    crc = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+    dp.crc32(ring.slot_ptr(ring.slot_of(last)), ld.batch_nbytes, crc, st)
+    st.synchronize()
+    got = int(crc.item()) & 0xFFFFFFFF
+    want = oracle_batch_crc(o, epoch, bi, o.OUT_BF16, os.cpu_count() or 1)
+    ring.close()
+    alg = B * (SAMPLE_BYTES + C * H * W * 2)
+    peak, _ = measured_hbm_peak()
+    achieved = alg / (ms / K / 1e3) / 1e9
+    return {"kernel": "collate_augment_kernel<bf16,C=3>", "avg_launch_ms": round(ms / K, 5),
+            "delivered_samples_s": round(N_CONSUMERS * B * K / (ms / 1e3), 1),
+            "achieved_gbs": round(achieved, 1), "frac": round(achieved / peak, 4),
+            "alg_bytes_per_launch": alg,
+            "parity": {"ok": got == want, "crc": f"{got:#010x}", "oracle": f"{want:#010x}",
+                       "seq": last}}
 
 
 def run_e2e(args, ctx, dev, rank, world):
@@ -522,13 +668,17 @@ def run_e2e(args, ctx, dev, rank, world):
         # N > 1: the same fan-out design as the device-timed value (two-stage
         # input all-gather by default, TSB_BENCH_FANOUT=outputs for the fused one)
         fan = "inputs" if os.environ.get("TSB_BENCH_FANOUT", "inputs") == "inputs" else "sharded"
-        producer = TensorProducer(loader, bcast, agg, min_consumers=N_CONSUMERS * world,
+        producer = TensorProducer(loader, bcast, agg, buffer_depth=E2E_BUFFER_DEPTH,
+                                  min_consumers=N_CONSUMERS * world,
                                   ring_slots=RING_SLOTS, heartbeat_timeout_s=60.0,
                                   devices=devs if world > 1 else None, fanout=fan)
         producer._start()  # listeners up before any rank's consumers dial
     if world > 1:
         torch.distributed.barrier()
     q = ctx.Queue()
+    # a fixed window independent of --steps (start-up skew of a few batches
+    # must not decide the number)
+    Wm, K = E2E_WARMUP, max(K, E2E_BATCHES)
     procs = [ctx.Process(target=api_consumer,
                          args=(dev, bcast, agg, 1000 + 100 * rank + k, Wm, K, q))
              for k in range(N_CONSUMERS)]
@@ -549,22 +699,27 @@ def run_e2e(args, ctx, dev, rank, world):
         # copy-engine ingest counts what it enqueued: the rows the crop reads,
         # plus the index and parameter uploads
         h2d = int(round(loader._ingest.bytes_enqueued() / produced))
-    rates = {}
+    rates, stamps = {}, {}
     for _ in procs:
         msg = q.get(timeout=600)
         while msg[0] != "done":
             msg = q.get(timeout=600)
         rates[msg[1]] = msg[2]
+        stamps[msg[1]] = msg[4]
     for p in procs:
         p.join(60)
     if world > 1:
         torch.distributed.barrier()  # every consumer is done before the rings go
+    drift = None
     if producer is not None:
+        drift = producer._ledger.drift_max
         producer.close()
     wall = time.monotonic() - t_start
-    value = sum(rates.values())
+    value, window_s, counted = common_window_rate(stamps)
     if world > 1:
         value = reduce_over_ranks(value, "sum", os.environ.get("TSB_BENCH_BACKEND", "nccl"))
+    per = list(rates.values())
+    spread = (max(per) - min(per)) / max(per) if per and max(per) > 0 else None
     path = ("TensorProducer(CollateLoader(pinned-host StoreSource)) -> 4 SharedLoader processes "
             "(CUDA IPC); each batch's sample rows that the crop reads cross PCIe by the copy "
             "engine, with the host-derived crop/flip table; consumers .item() one element per "
@@ -579,7 +734,14 @@ def run_e2e(args, ctx, dev, rank, world):
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4 * N_CONSUMERS * world,
             "path": path,
+            "window": {"batches_per_consumer": K, "warmup_batches": Wm,
+                       "seconds": round(window_s, 3), "batches_counted": counted,
+                       "how": "aggregate over the interval every consumer was fetching in "
+                              "(latest first fetch to earliest last fetch)"},
             "per_consumer": {str(k): round(v, 1) for k, v in rates.items()},
+            "per_consumer_spread": None if spread is None else round(spread, 4),
+            "sum_per_consumer": round(sum(per), 1),
+            "buffer_depth": E2E_BUFFER_DEPTH, "ledger_drift_max": drift,
             "wall_s": round(wall, 2), "batches_produced": produced}
 
 
@@ -593,11 +755,36 @@ def cpu_reference_step(o, store, order, bi, nthreads, out, scale, bias):
     return o.crc32(out)
 
 
+def reference_unmodified(timeout_s: float = 300.0):
+    """The UNMODIFIED reference (baseline/_ref, batchsocket run_scenario in
+    shared mode, tools/ref_cpu_bench.py) at C2's shape: 4 consumers, B=256,
+    224x224x3 u8 -- it has no augment, so its batch is the collated u8 bytes
+    (SURVEY.md §8a A6).  None when the install is absent."""
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "ref_cpu_bench.py"), "--only", "c2",
+           "--epoch-len", "30"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)
+        line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
+        d = json.loads(line)
+    except (subprocess.SubprocessError, IndexError, ValueError, OSError) as exc:
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+    if "unavailable" in d:
+        return d
+    return {"value": d["aggregate_samples_s"], "unit": "samples/s", "cores": d["workers"],
+            "kind": "reference",
+            "sample": f"unmodified reference (baseline/_ref) run_scenario shared mode: "
+                      f"{d['consumers']} consumers, B={d['batch_size']}, 224x224x3 u8 (no "
+                      f"augment exists in the reference), {d['epochs']} epochs x "
+                      f"{d['epoch_len']} batches, workers={d['workers']}, "
+                      f"wall {d['wall_s']} s",
+            "per_consumer": d["per_consumer_samples_s"], "cpu_model": d.get("cpu")}
+
+
 def cpu_baseline(seconds: float = 15.0):
     from oracle import oracle as o
 
     nthreads = os.cpu_count() or 1
-    n_store = 2048
+    n_store = N_SAMPLES
     store = o.make_store(0, n_store, SAMPLE_BYTES, nthreads=nthreads)
     order = o.epoch_order(n_store, 0, 0)
     scale, bias = o.norm_consts()
@@ -627,7 +814,9 @@ def cpu_baseline(seconds: float = 15.0):
             "sample": f"{n} batches x {B} samples ({dt:.1f} s): oracle C/OpenMP collate+augment "
                       f"f32 NCHW + CRC-32 per batch, {nthreads} threads; delivered = "
                       f"{N_CONSUMERS} zero-copy consumers x produced",
-            "produced_samples_per_s": round(produced, 1), "cpu_model": _cpu_model()}
+            "produced_samples_per_s": round(produced, 1), "cpu_model": _cpu_model(),
+            "same_config": True, "samples_per_epoch": n_store,
+            "reference": reference_unmodified()}
 
 
 def _cpu_model():
@@ -649,7 +838,7 @@ def run_reference(args):
     import numpy as np
 
     nthreads = os.cpu_count() or 1
-    n_store = 2048
+    n_store = N_SAMPLES  # the same store as the GPU arm (same_config)
     store = o.make_store(0, n_store, SAMPLE_BYTES, nthreads=nthreads)
     order = o.epoch_order(n_store, 0, 0)
     scale, bias = o.norm_consts()
@@ -685,7 +874,8 @@ def run_reference(args):
         "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (same store/order/augment as ours)",
-        "config": {"workload": WORKLOAD, "global_batch": B, "samples_per_epoch": n_store},
+        "config": {"workload": WORKLOAD, "global_batch": B, "samples_per_epoch": n_store,
+                   "consumers_per_gpu": N_CONSUMERS, "same_config": True},
         "cpu_baseline": {"value": round(value, 1), "unit": "samples/s", "cores": nthreads,
                          "kind": "port",
                          "sample": f"{args.steps} steps x {b} samples (of a {B}-sample batch): "

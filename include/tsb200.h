@@ -408,6 +408,18 @@ int tsb_hub_drain(tsb_hub *h, tsb_hub_event *out, int cap, int *n);
 /* Blocking sends of one frame to fds[0..n); failed[i] = 1 on error (peer gone). */
 int tsb_hub_broadcast(const int *fds, int n, const uint8_t *frame, size_t len, int *failed);
 int tsb_hub_destroy(tsb_hub *h);
+/* The reference's flow gate on received wire Acks (bs/producer.py:230-238,
+ * sl/producer.py:291-294: announce while fewer than buffer_depth batches await
+ * acks).  The hub keeps, per consumer id, the highest acked 1-based global
+ * seq (epoch * epoch_len + batch_index + 1) of every Ack it decodes.
+ * set_acked assigns (admission baseline, or a sentinel >= 2^61 on drop);
+ * wait_acked blocks until every listed consumer acked >= need: TSB_OK, or
+ * TSB_ERR_STALE after timeout_us (< 0: no timeout).  read_acked: 0 if unknown. */
+int tsb_hub_set_epoch_len(tsb_hub *h, uint64_t epoch_len);
+int tsb_hub_set_acked(tsb_hub *h, uint64_t consumer_id, uint64_t seq);
+int tsb_hub_read_acked(tsb_hub *h, uint64_t consumer_id, uint64_t *seq);
+int tsb_hub_wait_acked(tsb_hub *h, const uint64_t *consumer_ids, int n, uint64_t need,
+                       int64_t timeout_us);
 
 #ifdef __cplusplus
 }

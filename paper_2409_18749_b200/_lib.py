@@ -175,6 +175,10 @@ SIGNATURES["tsb_hub_remove"] = (i32, [vp, i32])
 SIGNATURES["tsb_hub_drain"] = (i32, [vp, ctypes.POINTER(HubEvent), i32, ctypes.POINTER(i32)])
 SIGNATURES["tsb_hub_broadcast"] = (i32, [ctypes.POINTER(i32), i32, vp, sz, ctypes.POINTER(i32)])
 SIGNATURES["tsb_hub_destroy"] = (i32, [vp])
+SIGNATURES["tsb_hub_set_epoch_len"] = (i32, [vp, u64])
+SIGNATURES["tsb_hub_set_acked"] = (i32, [vp, u64, u64])
+SIGNATURES["tsb_hub_read_acked"] = (i32, [vp, u64, ctypes.POINTER(u64)])
+SIGNATURES["tsb_hub_wait_acked"] = (i32, [vp, ctypes.POINTER(u64), i32, u64, i64])
 SIGNATURES["tsb_wire_encode"] = (i32, [ctypes.POINTER(Msg), vp, sz, ctypes.POINTER(sz)])
 SIGNATURES["tsb_wire_decode"] = (i32, [vp, sz, ctypes.POINTER(Msg), ctypes.POINTER(sz)])
 SIGNATURES["tsb_produce_group"] = (i32, [pp, i32, i32, ctypes.POINTER(ProduceArgs), i32, i32, u64,

@@ -22,6 +22,8 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -51,9 +53,20 @@ struct tsb_hub {
     int wake = -1;
     std::thread th;
     std::atomic<bool> stop{false};
-    std::mutex mu;                      // guards conns and events
+    std::mutex mu;                      // guards conns, events and acked
+    std::condition_variable cv;         // an Ack raised some consumer's acked seq
     std::unordered_map<int, HubConn> conns;
     std::vector<tsb_hub_event> events;
+    uint64_t epoch_len = 0;             // 0: acked seqs are not tracked
+    std::unordered_map<uint64_t, uint64_t> acked;  // consumer id -> highest acked seq
+
+    bool all_acked(const uint64_t *ids, int n, uint64_t need) const {  // caller holds mu
+        for (int i = 0; i < n; ++i) {
+            auto it = acked.find(ids[i]);
+            if (it == acked.end() || it->second < need) return false;
+        }
+        return true;
+    }
 
     void push(uint8_t kind, uint64_t cid, uint32_t epoch, uint64_t bi, int fd) {
         tsb_hub_event e{};
@@ -87,6 +100,15 @@ struct tsb_hub {
             if (tsb_wire_decode(c.buf.data() + off, 4 + body, &m, &eo) != TSB_OK) return false;
             if (m.kind == TSB_MSG_ACK || m.kind == TSB_MSG_HEARTBEAT || m.kind == TSB_MSG_BYE)
                 push(m.kind, m.consumer_id, m.epoch, m.batch_index, fd);
+            if (m.kind == TSB_MSG_ACK && epoch_len) {
+                // max-monotone, as the reference's ack cursor (bs/producer.py:251)
+                const uint64_t seq = (uint64_t)m.epoch * epoch_len + m.batch_index + 1;
+                auto it = acked.find(m.consumer_id);
+                if (it != acked.end() && seq > it->second) {
+                    it->second = seq;
+                    cv.notify_all();
+                }
+            }
             off += 4 + body;
         }
         c.buf.erase(c.buf.begin(), c.buf.begin() + off);
@@ -199,6 +221,42 @@ int tsb_hub_broadcast(const int *fds, int n, const uint8_t *frame, size_t len, i
         if (failed) failed[i] = bad;
     }
     return TSB_OK;
+}
+
+int tsb_hub_set_epoch_len(tsb_hub *h, uint64_t epoch_len) {
+    if (!h) return TSB_ERR_INVALID;
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->epoch_len = epoch_len;
+    return TSB_OK;
+}
+
+int tsb_hub_set_acked(tsb_hub *h, uint64_t consumer_id, uint64_t seq) {
+    if (!h) return TSB_ERR_INVALID;
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->acked[consumer_id] = seq;
+    h->cv.notify_all();
+    return TSB_OK;
+}
+
+int tsb_hub_read_acked(tsb_hub *h, uint64_t consumer_id, uint64_t *seq) {
+    if (!h || !seq) return TSB_ERR_INVALID;
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->acked.find(consumer_id);
+    *seq = it == h->acked.end() ? 0 : it->second;
+    return TSB_OK;
+}
+
+int tsb_hub_wait_acked(tsb_hub *h, const uint64_t *consumer_ids, int n, uint64_t need,
+                       int64_t timeout_us) {
+    if (!h || (n && !consumer_ids) || n < 0) return TSB_ERR_INVALID;
+    std::unique_lock<std::mutex> lk(h->mu);
+    auto ok = [&] { return h->all_acked(consumer_ids, n, need); };
+    if (timeout_us < 0) {
+        h->cv.wait(lk, ok);
+        return TSB_OK;
+    }
+    return h->cv.wait_for(lk, std::chrono::microseconds(timeout_us), ok) ? TSB_OK
+                                                                        : TSB_ERR_STALE;
 }
 
 int tsb_hub_destroy(tsb_hub *h) {

@@ -321,17 +321,28 @@ int tsb_ring_create_ex(int dev, int slots, size_t slot_bytes, int max_consumers,
     r->writers = writers;
     r->phys_dev = dev;
     layout(r);
-    cudaError_t e = cudaMalloc(&r->base, r->total);
+    const size_t total = r->total;
+    cudaError_t e = cudaMalloc(&r->base, total);
     if (e != cudaSuccess) {
+        r->base = nullptr;
         delete r;
-        set_error("ring allocation of %zu bytes failed: %s", r->total, cudaGetErrorString(e));
+        set_error("ring allocation of %zu bytes failed: %s", total, cudaGetErrorString(e));
         return TSB_ERR_CUDA;
     }
     bind(r);
-    TSB_CUDA(cudaStreamCreateWithFlags(&r->host_stream, cudaStreamNonBlocking));
-    TSB_CUDA(cudaMemsetAsync(r->ready, 0, r->total - r->slot_stride * (size_t)r->slots,
-                             r->host_stream));
-    TSB_CUDA(cudaStreamSynchronize(r->host_stream));
+    // control words start zeroed; on any failure release everything made so far
+    e = cudaStreamCreateWithFlags(&r->host_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(r->ready, 0, total - r->slot_stride * (size_t)r->slots,
+                            r->host_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(r->host_stream);
+    if (e != cudaSuccess) {
+        if (r->host_stream) cudaStreamDestroy(r->host_stream);
+        cudaFree(r->base);
+        delete r;
+        set_error("ring control-word init failed: %s", cudaGetErrorString(e));
+        return TSB_ERR_CUDA;
+    }
     resolve_mode();
     *out = r;
     return TSB_OK;

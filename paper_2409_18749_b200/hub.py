@@ -47,6 +47,33 @@ class Hub:
                 return out
         return out
 
+    # -- the reference's flow gate on received wire Acks (bs/producer.py:230-238)
+    def set_epoch_len(self, epoch_len: int) -> None:
+        _lib.call("tsb_hub_set_epoch_len", self._h, epoch_len)
+
+    def set_acked(self, consumer_id: int, seq: int) -> None:
+        """Assign a consumer's acked seq (admission baseline; a sentinel on drop)."""
+        if self._h:
+            _lib.call("tsb_hub_set_acked", self._h, consumer_id, seq)
+
+    def read_acked(self, consumer_id: int) -> int:
+        v = ctypes.c_uint64()
+        _lib.call("tsb_hub_read_acked", self._h, consumer_id, ctypes.byref(v))
+        return v.value
+
+    def wait_acked(self, consumer_ids, need: int, timeout_s: float = -1.0) -> bool:
+        """Block until every listed consumer acked seq >= need; False on timeout."""
+        ids = list(consumer_ids)
+        if not ids or need <= 0:
+            return True
+        arr = (ctypes.c_uint64 * len(ids))(*ids)
+        rc = self._L.tsb_hub_wait_acked(self._h, arr, len(ids), need,
+                                        -1 if timeout_s < 0 else int(timeout_s * 1e6))
+        if rc == _lib.TSB_ERR_STALE:
+            return False
+        _lib.check(rc, "tsb_hub_wait_acked")
+        return True
+
     @staticmethod
     def broadcast(fds, frame: bytes) -> list:
         """Send `frame` to every fd; returns the fds whose send failed."""

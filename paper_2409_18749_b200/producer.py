@@ -77,6 +77,7 @@ from .wire import (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND, ADMIT_WAIT, SUPPORTED_VERS
                    dtype_of, encode)
 
 MONITOR_ID = 0  # bs/producer.py:52-54: passive broadcast observers
+SENTINEL_MIN = 1 << 61  # cursors at or above this are evicted / unused words
 _RINGS: dict[int, DeviceRing] = {}  # ring_id -> ring, for same-process consumers
 
 
@@ -172,7 +173,11 @@ class TensorProducer:
         self._retained: dict[int, dict] = {}  # seq -> {device: announce} (rubberband prefix)
         self._retention_active = False
         self.ring_id = (os.getpid() << 20) ^ (id(self) & 0xFFFFF)
-        self.stats = {"announced": 0, "acks": 0, "evictions": 0}
+        self.stats = {"announced": 0, "acks": 0, "evictions": 0, "live_max": 0,
+                      "live_max_window": 0}
+        # (epoch, batch_index, checksum) of every announced batch, the
+        # reference's RunReport.batches (bs/producer.py:528) for exactly-once checks
+        self.batches: list[tuple[int, int, int]] = []
         self.drops: list[tuple[int, str, float]] = []  # (consumer_id, reason, time) event log
         self._chain_ok = False  # PDL across produce calls (previous op = our fused kernel)
         # wire Acks are queued by the reader threads without taking the lock and
@@ -301,6 +306,7 @@ class TensorProducer:
         if self._started:
             return
         self._started = True
+        self._hub.set_epoch_len(max(1, len(self._loader)))
         hint = self._batch_nbytes_hint()
         if hint is not None:
             with self._lock:
@@ -369,7 +375,15 @@ class TensorProducer:
 
             def on_handoff(pending, conn=conn, state=state):
                 with self._lock:
+                    # the consumer may have been dropped (failed send, rejoin)
+                    # between admission and this handoff: its fd is then closed
+                    # or already reused, and must not be handed to the hub
+                    rec = self._consumers.get(state["cid"])
+                    if rec is None or rec.conn is not conn or conn.closed:
+                        return
                     fd = conn.sock.fileno()
+                    if fd < 0:
+                        return
                     self._hub_fds[fd] = state["cid"]
                     self._hub.add(fd, state["cid"], pending)
 
@@ -507,6 +521,8 @@ class TensorProducer:
         if code in (ADMIT_IMMEDIATE, ADMIT_RUBBERBAND):
             rec.admitted = True
             self._rings[k].set_cursor(rec.cursor, q0 - 1)
+            rec.ack_seq = q0 - 1  # ack cursor baseline (bs/producer.py:626-634)
+            self._hub.set_acked(cid, q0 - 1)
             welcome = Welcome(cid, self._epoch, L, progress if code == ADMIT_RUBBERBAND else 0,
                               self._depth, code)
         else:
@@ -549,6 +565,7 @@ class TensorProducer:
             return
         now = time.monotonic()
         self.drops.append((cid, reason, now))
+        self._hub.set_acked(cid, SENTINEL_MIN)  # no flow-gate wait on a departed consumer
         if rec.ring in self._rings:
             self._rings[rec.ring].evict(rec.cursor)  # unblocks every wait on this consumer
         if reason != "timeout":
@@ -645,6 +662,8 @@ class TensorProducer:
                 if rec.waiting_for_epoch == self._epoch:
                     rec.waiting_for_epoch = None
                     rec.admitted = True
+                    rec.ack_seq = q0 - 1
+                    self._hub.set_acked(rec.consumer_id, q0 - 1)
                     if rec.ring in self._rings:
                         self._rings[rec.ring].set_cursor(rec.cursor, q0 - 1)
             self._epoch_started = True
@@ -685,6 +704,13 @@ class TensorProducer:
             self._ensure_ring(nbytes)
             self._lock.wait_for(lambda: self._admitted() or self._closed)
             admitted = self._admitted()
+            # the reference's flow gate (bs/producer.py:230-238, sl/producer.py:
+            # 291-294): announce only while fewer than buffer_depth batches await
+            # acks, counted on the wire Acks the native hub has received (so the
+            # ledger's drift series obeys the same bound).  Consumers with their
+            # own batch size and the rubberband retention cursor only gate slot
+            # reuse (retained-but-acked batches do not count, :182-184)
+            depth_ids = [r.consumer_id for r in admitted if not r.batch_size]
             live_by_ring = {k: [r.cursor for r in admitted if r.ring == k]
                             for k in range(len(self._devices))}
             if self._retention_active:
@@ -693,11 +719,13 @@ class TensorProducer:
         ring, stream = self._ring, self._stream
         slot = ring.slot_of(q)
         host_gated = all(r.host_control for r in self._rings.values())
+        self._ack_gate(q, depth_ids)
         if host_gated:
-            # flow gate on the host-shared cursors: the producer's streams never
-            # park on a device wait, so no stream of this process (in-process
-            # consumers included) can be blocked behind one
+            # slot-reuse gate on the host-shared cursors: the producer's streams
+            # never park on a device wait, so no stream of this process
+            # (in-process consumers included) can be blocked behind one
             self._host_gate(q, live_by_ring)
+            self._sample_live(q, live_by_ring)
         if self._two_stage and not self._checksum:
             self._publish_two_stage(q, index)
         elif self._multi and self._device_loader and not self._checksum:
@@ -752,6 +780,7 @@ class TensorProducer:
             self._drain_acks()
             self._ledger.add(q, [r.consumer_id for r in self._admitted()])
             self._send_announces(anns)
+            self.batches.append((self._epoch, index, crc))
             self._announced_in_epoch = index + 1
             self.stats["announced"] += 1
             window = retention_window(self._fraction, L)
@@ -772,8 +801,21 @@ class TensorProducer:
             self._orders[key] = torch.from_numpy(host).to(f"cuda:{dev}")
         return self._orders[key]
 
+    def _ack_gate(self, q: int, ids) -> None:
+        """The reference's flow gate (bs/producer.py:230-238): batch q is
+        announced only once every consumer acked q - buffer_depth on the wire,
+        i.e. fewer than buffer_depth announced batches await acks.  The native
+        hub counts the Acks as it decodes them (no interpreter on the wait)."""
+        need = q - self._depth
+        while not self._hub.wait_acked(ids, need, timeout_s=0.1):
+            if self._closed:
+                raise ProducerClosed("producer closed while waiting for consumers")
+            with self._lock:  # evicted / departed consumers leave the gate
+                ids = [i for i in ids if i in self._consumers]
+
     def _host_gate(self, q: int, live_by_ring) -> None:
-        """Block until every live consumer of every ring released batch q-S."""
+        """Block until every live cursor of every ring released batch q-S
+        (slot reuse)."""
         need = q - self._ring.slots
         if need <= 0:
             return
@@ -784,6 +826,24 @@ class TensorProducer:
             while not ring.host_gate(live, need, timeout_s=0.1):
                 if self._closed:
                     raise ProducerClosed("producer closed while waiting for consumers")
+
+    def _sample_live(self, q: int, live_by_ring) -> None:
+        """Live slots when batch q is published: batches announced but not yet
+        released by every live cursor (SPEC.md:528 memory bound: <= N+1 outside
+        the rubberband window)."""
+        low = None
+        for k, ring in self._rings.items():
+            cur = ring.cursor_words
+            for c in live_by_ring[k]:
+                v = int(cur[c])
+                if v < SENTINEL_MIN and (low is None or v < low):
+                    low = v
+        if low is None:
+            return
+        live = q - low
+        key = "live_max_window" if self._retention_active else "live_max"
+        if live > self.stats[key]:
+            self.stats[key] = live
 
     def _publish_group(self, q: int, index: int) -> None:
         """Multi-GPU: every device produces its shard of the batch straight into

@@ -71,3 +71,22 @@ def test_multi_rank_timing_is_max_over_ranks_gloo_world2():
         p.join(30)
     for r in (0, 1):
         assert res[r] == ((r, 2, r), 7.25, 3000.0)
+
+
+def test_common_window_rate():
+    """e2e aggregate over the window every consumer was fetching in: a
+    consumer that started late does not inflate the others' count, and a
+    consumer's own start-up skew is cut off (bench.common_window_rate)."""
+    import bench
+
+    B = bench.B
+    stamps = {
+        1: [0.0 + 0.01 * i for i in range(101)],   # 0.00 .. 1.00
+        2: [0.5 + 0.01 * i for i in range(101)],   # 0.50 .. 1.50 (late start)
+    }
+    rate, window, n = bench.common_window_rate(stamps)
+    assert abs(window - 0.5) < 1e-9
+    # window (0.5, 1.0]: 50 fetches each
+    assert n == 100
+    assert abs(rate - 100 * B / 0.5) < 1e-6 * rate
+    assert bench.common_window_rate({1: [0.0, 1.0], 2: [2.0, 3.0]}) == (0.0, 0.0, 0)

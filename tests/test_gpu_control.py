@@ -84,18 +84,88 @@ def consume(endpoints, cid, epochs, out, delay_s=0.0, stop_after=None, **kw):
 
 
 def test_slow_consumer_backpressure(endpoints):
-    """Drift bound (criterion 4): the producer runs at most ring_slots batches
-    ahead of the slowest consumer's releases."""
-    producer, pt = run_producer(SeqLoader(12), endpoints, 1, buffer_depth=2, ring_slots=4)
+    """Flow gate (bs/producer.py:230-238, sl/producer.py:291-294): the producer
+    announces only while fewer than buffer_depth batches await the slowest
+    consumer's ack -- extra ring slots serve retention and rebatching, not
+    run-ahead (pkg/tests/test_producer_consumer.py:273-288)."""
+    producer, pt = run_producer(SeqLoader(12), endpoints, 1, buffer_depth=2, ring_slots=8)
     out = {}
     w = threading.Thread(target=consume, args=(endpoints, 1, 1, out), kwargs={"delay_s": 0.05})
     w.start()
-    time.sleep(0.3)
-    announced, fetched = producer.stats["announced"], len(out.get("seq", []))
-    assert announced <= fetched + 4
+    for _ in range(6):
+        time.sleep(0.07)
+        announced = producer.stats["announced"]
+        fetched = out["loader"].fetched if "loader" in out else 0
+        assert announced <= fetched + 2
     w.join(30)
     pt.join(30)
     assert out["seq"] == expected(1, 12)
+    producer.close()
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_drift_bound_mixed_speeds(endpoints, depth):
+    """SPEC.md:524 criterion 4: over the whole run, max - min wire-ack cursor
+    across admitted consumers stays <= buffer_depth (ledger drift series), for
+    consumers of very different speeds; and SPEC.md:528 criterion 8: at most
+    N+1 slots are live (announced, not yet released by every consumer) when
+    no rubberband window is open."""
+    E, n = 2, 24
+    producer, pt = run_producer(SeqLoader(n), endpoints, E, buffer_depth=depth, ring_slots=8,
+                                min_consumers=3)
+    outs = [{} for _ in range(3)]
+    ts = [threading.Thread(target=consume, args=(endpoints, 20 + k, E, outs[k]),
+                           kwargs={"delay_s": d}) for k, d in enumerate((0.0, 0.004, 0.02))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    pt.join(60)
+    for o in outs:
+        assert o["seq"] == expected(E, n)
+    assert producer._ledger.drift_series, "no drift samples"
+    assert producer._ledger.drift_max <= depth, producer._ledger.drift_series
+    assert 1 <= producer.stats["live_max"] <= depth + 1
+    producer.close()
+
+
+def test_checksum_exactly_once_three_consumers(endpoints):
+    """SPEC.md:525 criterion 5 with checksums on (bs/harness.py:636-671): each
+    consumer's (epoch, index, checksum) sequence equals the producer's records,
+    zero duplicates; every announced checksum is the zlib CRC-32 of the bytes
+    the consumer actually read (input bytes + target bytes, the pair ABI);
+    one consumer also verifies on the device (verify_checksum)."""
+    import zlib
+
+    E, n = 2, 10
+    producer, pt = run_producer(SeqLoader(n), endpoints, E, min_consumers=3, checksum=True)
+    outs = [{} for _ in range(3)]
+
+    def run(k):
+        o = outs[k]
+        loader = SharedLoader(*endpoints, consumer_id=40 + k, verify_checksum=(k == 0))
+        recs = o.setdefault("recs", [])
+        with torch.cuda.stream(torch.cuda.Stream()):
+            for _ in range(E):
+                for inp, tgt in loader:
+                    a = loader.last_announce
+                    raw = inp.cpu().numpy().tobytes() + tgt.cpu().numpy().tobytes()
+                    assert zlib.crc32(raw) == a.checksum
+                    recs.append((a.epoch, a.batch_index, a.checksum))
+                if loader.finished:
+                    break
+        loader.close()
+
+    ts = [threading.Thread(target=run, args=(k,)) for k in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    pt.join(60)
+    assert len(producer.batches) == E * n
+    assert all(c != 0 for _, _, c in producer.batches)
+    for o in outs:
+        assert o["recs"] == producer.batches
     producer.close()
 
 
@@ -139,6 +209,57 @@ def test_eviction_unblocks_survivors(endpoints):
     assert survivor["seq"] == expected(1, 40)
     assert victim["seq"] == expected(1, 40)[:3]
     producer.close()
+
+
+def test_rubberband_replay_race_no_delays(endpoints):
+    """A rubberband joiner whose broadcast announces overtake its private
+    replay (no loader or consumer delays) still gets the whole epoch in order:
+    overtaking announces wait for the replayed prefix instead of being dropped
+    (bs/producer.py:599-685 halts; here the flow gate holds the producer on the
+    joiner's cursor and the consumer buffers the overtakers)."""
+    for trial in range(3):
+        b, a = endpoints
+        eps = (b + f".{trial}", a + f".{trial}")
+        producer, pt = run_producer(SeqLoader(32), eps, 2, rubberband_fraction=0.25,
+                                    ring_slots=16, buffer_depth=2)
+        base, joiner = {}, {}
+        gate = threading.Event()
+
+        def run_base():
+            loader = SharedLoader(*eps, consumer_id=1)
+            base["loader"] = loader
+            seq = base.setdefault("seq", [])
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for _ in range(2):
+                    for inp, tgt in loader:
+                        t = tgt.cpu().numpy()
+                        seq.append((int(t[0]), int(t[1])))
+                        if len(seq) == 1:
+                            gate.wait(30)  # hold the producer inside the window
+                    if loader.finished:
+                        break
+            loader.close()
+
+        bt = threading.Thread(target=run_base)
+        bt.start()
+        deadline = time.time() + 30
+        while producer.stats["announced"] < 2 and time.time() < deadline:
+            time.sleep(0.001)
+        jt = threading.Thread(target=consume, args=(eps, 2, 2, joiner))
+        jt.start()
+        deadline = time.time() + 30
+        while "loader" not in joiner and time.time() < deadline:
+            time.sleep(0.001)
+        while joiner["loader"].welcome is None and time.time() < deadline:
+            time.sleep(0.001)
+        gate.set()
+        jt.join(60)
+        bt.join(60)
+        pt.join(60)
+        assert joiner["loader"].welcome.admitted == 1  # ADMIT_RUBBERBAND
+        assert base["seq"] == expected(2, 32)
+        assert joiner["seq"] == expected(2, 32)
+        producer.close()
 
 
 def test_rubberband_join_gets_full_epoch(endpoints):
