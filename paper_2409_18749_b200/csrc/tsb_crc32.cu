@@ -16,6 +16,21 @@
 // runs are XOR-reduced (XOR is associative/commutative) with one atomicXor
 // per warp.  Multiplication by a constant x^k mod P uses 4-bit
 // tables (8 nibbles x 16 entries).  One read of the data.
+//
+// crc_tile_kernel (the default for 16-byte-aligned buffers) reaches the
+// shared-memory bound of a table CRC (1 lookup per byte):
+//   * one CTA of 8 warps per SM; each warp owns a contiguous run of 4.5 KB
+//     tiles and streams them with TMA bulk copies (cp.async.bulk, 2 stages per
+//     warp, mbarrier complete_tx) -- one coalesced request per tile;
+//   * lane l reads its 144 contiguous bytes of a tile with 9 LDS.128 (144 B =
+//     9 x 16 B, an odd count: conflict-free) and runs two slice-by-4 chains
+//     of 72 B, each carried to its next tile by one constant multiply;
+//   * the slice tables are replicated per lane in two 64 KB-aligned regions
+//     (entry i of T_even/T_odd at i*256 (+128) + lane*4), so ONE PRMT builds
+//     the full shared address of a lookup from the data byte and a per-lane
+//     constant: 11 instructions and 4 conflict-free LDS per 4 data bytes.
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "tsb_common.cuh"
@@ -37,6 +52,21 @@ __device__ uint32_t g_tree_tab[TREE_LEVELS * NT];
 __device__ uint32_t g_half_tab[NT];
 __device__ uint32_t g_gap_tab[NT];
 __device__ uint32_t g_shift_tab[SHIFT_BITS * NT];
+
+// ---- tile kernel geometry and its shift tables ----
+constexpr int T_WARPS = 8;
+constexpr int T_THREADS = 32 * T_WARPS;
+constexpr int T_LANE = 144;                // bytes per lane and tile: 9 x 16 B
+constexpr int T_WORDS = T_LANE / 4;        // 36
+constexpr int T_TILE = 32 * T_LANE;        // 4608 B per warp tile
+constexpr int T_CHAIN = T_LANE / 2;        // two chains of 72 B (18 words)
+constexpr int T_STAGES = 2;
+constexpr int T_SMEM = 232448;             // the 227 KB opt-in maximum
+constexpr uint32_t T_TAB_BYTES = 131072;   // 4 tables x 256 entries x 32 lanes x 4 B
+__device__ uint32_t g_t_tree[TREE_LEVELS * NT];   // x^(8 * T_LANE * 2^k)
+__device__ uint32_t g_t_gap[NT];                  // x^(8 * (T_TILE - T_CHAIN))
+__device__ uint32_t g_t_half[NT];                 // x^(8 * T_CHAIN)
+__device__ uint32_t g_t_shift[SHIFT_BITS * NT];   // x^(8 * T_TILE * 2^k)
 
 uint32_t h_multmodp(uint32_t a, uint32_t b) {
     uint32_t m = 1u << 31, p = 0;
@@ -91,6 +121,16 @@ int ensure_tables() {
     TSB_CUDA(cudaMemcpyToSymbol(g_half_tab, ht, sizeof(ht)));
     TSB_CUDA(cudaMemcpyToSymbol(g_gap_tab, gt, sizeof(gt)));
     TSB_CUDA(cudaMemcpyToSymbol(g_shift_tab, st, sizeof(st)));
+    static uint32_t t_tree[TREE_LEVELS * NT], t_gap[NT], t_half[NT], t_shift[SHIFT_BITS * NT];
+    for (int k = 0; k < TREE_LEVELS; ++k)
+        h_nibble_table(h_x8n((uint64_t)T_LANE << k), t_tree + k * NT);
+    h_nibble_table(h_x8n(T_TILE - T_CHAIN), t_gap);
+    h_nibble_table(h_x8n(T_CHAIN), t_half);
+    for (int k = 0; k < SHIFT_BITS; ++k) h_nibble_table(h_x8n((uint64_t)T_TILE << k), t_shift + k * NT);
+    TSB_CUDA(cudaMemcpyToSymbol(g_t_tree, t_tree, sizeof(t_tree)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_t_gap, t_gap, sizeof(t_gap)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_t_half, t_half, sizeof(t_half)));
+    TSB_CUDA(cudaMemcpyToSymbol(g_t_shift, t_shift, sizeof(t_shift)));
     if (dev < 64) g_ready[dev] = true;
     return TSB_OK;
 }
@@ -214,6 +254,219 @@ __global__ void __launch_bounds__(CRC_THREADS)
     }
 }
 
+// ---------------------------------------------------------------------------
+// crc_tile_kernel
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds_even(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_odd(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1+128];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// slice-by-4 step of the raw reflected CRC: x = c ^ w;
+//   c' = T3[x.b0] ^ T2[x.b1] ^ T1[x.b2] ^ T0[x.b3]
+// b_lo / b_hi = (region base & 0xFFFF0000) | lane*4 of the T0/T1 and T2/T3
+// regions: prmt keeps their bytes 0, 2, 3 and puts data byte k in byte 1
+__device__ __forceinline__ uint32_t tile_step(uint32_t c, uint32_t w, uint32_t b_lo,
+                                              uint32_t b_hi) {
+    const uint32_t x = c ^ w;
+    return lds_odd(prmt(x, b_hi, 0x7604u)) ^ lds_even(prmt(x, b_hi, 0x7614u)) ^
+           lds_odd(prmt(x, b_lo, 0x7624u)) ^ lds_even(prmt(x, b_lo, 0x7634u));
+}
+
+struct TileLayout {  // shared addresses (u32), identical in every CTA; this warp's buffers
+    uint32_t tab0, gap, stage0, stage1, bar0, bar1, bar_first;
+};
+
+// First-fit of the buffers around the two 64 KB-aligned table regions.
+__device__ __forceinline__ bool tile_layout(uint32_t base, int wib, TileLayout &L) {
+    const uint32_t end = base + T_SMEM;
+    L.tab0 = (base + 65535u) & ~65535u;
+    uint32_t lo = base, lo_end = L.tab0, hi = L.tab0 + T_TAB_BYTES;
+    if (hi > end) return false;
+    auto take = [&](uint32_t bytes, uint32_t align, uint32_t &out) {
+        uint32_t a = (lo + align - 1) & ~(align - 1);
+        if (a + bytes <= lo_end) { out = a; lo = a + bytes; return true; }
+        a = (hi + align - 1) & ~(align - 1);
+        if (a + bytes <= end) { out = a; hi = a + bytes; return true; }
+        return false;
+    };
+    bool ok = take(NT * 32 * 4, 128, L.gap);
+#pragma unroll
+    for (int w = 0; w < T_WARPS; ++w)
+#pragma unroll
+        for (int s = 0; s < T_STAGES; ++s) {
+            uint32_t a = 0;
+            ok = ok && take(T_TILE, 128, a);
+            if (w == wib) (s ? L.stage1 : L.stage0) = a;
+        }
+#pragma unroll
+    for (int w = 0; w < T_WARPS; ++w)
+#pragma unroll
+        for (int s = 0; s < T_STAGES; ++s) {
+            uint32_t a = 0;
+            ok = ok && take(8, 8, a);
+            if (w == 0 && s == 0) L.bar_first = a;
+            if (w == wib) (s ? L.bar1 : L.bar0) = a;
+        }
+    return ok;
+}
+
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(addr)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void tile_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TW_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tile_load(uint32_t dst, const void *src, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((uint32_t)T_TILE)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst),
+        "l"(src), "r"((uint32_t)T_TILE), "r"(bar)
+        : "memory");
+}
+// product with a lane-replicated nibble table at shared address t (+ lane*4)
+__device__ __forceinline__ uint32_t mul_nib_rep_s(uint32_t v, uint32_t t) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r ^= lds_even(t + ((uint32_t)(j * 16 + ((v >> (4 * j)) & 15u)) << 7));
+    return r;
+}
+
+// Virtual message = z zero bytes || data (n + z = n_tiles * T_TILE); tile t
+// holds data bytes [t*T_TILE - z, (t+1)*T_TILE - z).  Tile 0 (the only one
+// with virtual zeros) is filled by its warp; every other tile is one TMA
+// bulk copy, so (data - z) must be 16-byte aligned.
+__global__ void __launch_bounds__(T_THREADS, 1)
+    crc_tile_kernel(const uint8_t *__restrict__ data, uint64_t n, uint64_t z, uint64_t n_tiles,
+                    uint32_t *out) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const uint32_t base = smem_u32(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    TileLayout L;
+    if (!tile_layout(base, wib, L)) __trap();
+    // lane-replicated slice tables: region r holds T_{2r} (even slot) and T_{2r+1} (odd)
+    for (int e = tid; e < 4 * 256; e += T_THREADS) {
+        const uint32_t v = g_slice_tab[e];
+        const int t = e >> 8, i = e & 255;
+        const uint32_t row = L.tab0 + (uint32_t)(t >> 1) * 65536u + (uint32_t)i * 256u +
+                             (uint32_t)(t & 1) * 128u;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) sts_u32(row + (uint32_t)(((l + e) & 31) << 2), v);
+    }
+    for (int e = tid; e < NT; e += T_THREADS) {
+        const uint32_t v = g_t_gap[e];
+        for (int l = 0; l < 32; ++l) sts_u32(L.gap + (uint32_t)e * 128u + (uint32_t)(((l + e) & 31) << 2), v);
+    }
+    if (tid < T_WARPS * T_STAGES) {  // the barriers are allocated contiguously, 8 B each
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(L.bar_first + 8u * tid)
+                     : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    const uint64_t warp = (uint64_t)blockIdx.x * T_WARPS + wib;
+    const uint64_t nwarps = (uint64_t)gridDim.x * T_WARPS;
+    const uint64_t per = (n_tiles + nwarps - 1) / nwarps;
+    const uint64_t t0 = warp * per, t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
+    if (t0 >= t1) return;
+    const uint32_t b_lo = (L.tab0 & 0xFFFF0000u) | ((uint32_t)lane << 2);
+    const uint32_t b_hi = ((L.tab0 + 65536u) & 0xFFFF0000u) | ((uint32_t)lane << 2);
+    const uint32_t gap = L.gap + ((uint32_t)lane << 2);
+    const uint8_t *src0 = data - z;  // virtual byte 0 (never dereferenced below z)
+
+    auto issue = [&](uint64_t t, int s) {
+        if (t == 0 && z) {  // virtual zeros || data head: filled by this warp
+            const uint32_t dst = s ? L.stage1 : L.stage0;
+            for (uint32_t i = (uint32_t)lane; i < (uint32_t)T_TILE; i += 32) {
+                const uint32_t v = i >= z && (uint64_t)i - z < n ? data[i - z] : 0u;
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + i), "r"(v) : "memory");
+            }
+            __syncwarp();
+            if (lane == 0)  // complete the stage's phase with no transfer
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s ? L.bar1 : L.bar0)
+                             : "memory");
+        } else if (lane == 0) {
+            tile_load(s ? L.stage1 : L.stage0, src0 + t * (uint64_t)T_TILE, s ? L.bar1 : L.bar0);
+        }
+    };
+    issue(t0, 0);
+    if (t0 + 1 < t1) issue(t0 + 1, 1);
+    uint32_t cA = 0, cB = 0, phase = 0;  // phase bit s: parity to wait for on stage s
+    for (uint64_t t = t0; t < t1; ++t) {
+        const int s = (int)((t - t0) & 1);
+        tile_wait(s ? L.bar1 : L.bar0, (phase >> s) & 1u);
+        phase ^= 1u << s;
+        uint32_t wv[T_WORDS];
+        const uint32_t row = (s ? L.stage1 : L.stage0) + (uint32_t)lane * T_LANE;
+#pragma unroll
+        for (int k = 0; k < T_WORDS / 4; ++k) {
+            const uint4 q = lds_v4(row + 16u * k);
+            wv[4 * k] = q.x;
+            wv[4 * k + 1] = q.y;
+            wv[4 * k + 2] = q.z;
+            wv[4 * k + 3] = q.w;
+        }
+        __syncwarp();
+        if (t + 2 < t1) issue(t + 2, s);  // the stage is free: every lane holds its words
+        if (t != t0) {
+            cA = mul_nib_rep_s(cA, gap);
+            cB = mul_nib_rep_s(cB, gap);
+        }
+#pragma unroll
+        for (int j = 0; j < T_WORDS / 2; ++j) {
+            cA = tile_step(cA, wv[j], b_lo, b_hi);
+            cB = tile_step(cB, wv[T_WORDS / 2 + j], b_lo, b_hi);
+        }
+    }
+    uint32_t c = mul_nib(cA, g_t_half) ^ cB;  // the lane's bytes, relative to its chunk end
+#pragma unroll
+    for (int k = 0; k < TREE_LEVELS; ++k) {
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, c, 1 << k);
+        if (lane & (1 << k))
+            c = mul_nib(other, g_t_tree + k * NT) ^ c;
+        else
+            c = mul_nib(c, g_t_tree + k * NT) ^ other;
+    }
+    if (lane == 0) {
+        uint64_t q = n_tiles - t1;  // the tiles after this warp's run
+        int k = 0;
+        while (q) {
+            if (q & 1) c = mul_nib(c, g_t_shift + k * NT);
+            q >>= 1;
+            ++k;
+        }
+        if (c) atomicXor(out, c);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -232,6 +485,29 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
     crc_init_kernel<<<1, 1, 0, s>>>(d_out, init);
     TSB_LAUNCH_CHECK();
     if (n == 0) return TSB_OK;
+    static const int force_old = getenv("TSB_CRC_IMPL") && !strcmp(getenv("TSB_CRC_IMPL"), "v1");
+    {
+        const uint64_t zt = (T_TILE - n % T_TILE) % T_TILE;
+        const uint64_t n_tiles = (n + zt) / T_TILE;
+        if (!force_old && n >= (uint64_t)T_TILE * 64 && ((((uintptr_t)data) - zt) & 15) == 0 &&
+            n_tiles < (1ull << SHIFT_BITS)) {
+            static bool t_attr[64] = {false};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 64 && !t_attr[dev]) {
+                TSB_CUDA(cudaFuncSetAttribute(crc_tile_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM));
+                t_attr[dev] = true;
+            }
+            uint64_t blocks = (n_tiles + T_WARPS - 1) / T_WARPS;
+            const uint64_t cap = (uint64_t)sm_count();  // one CTA per SM
+            if (blocks > cap) blocks = cap;
+            crc_tile_kernel<<<(unsigned)blocks, T_THREADS, T_SMEM, s>>>(
+                static_cast<const uint8_t *>(data), n, zt, n_tiles, d_out);
+            TSB_LAUNCH_CHECK();
+            return TSB_OK;
+        }
+    }
     const uint64_t z = (UNIT - n % UNIT) % UNIT;
     const uint64_t n_units = (n + z) / UNIT;
     TSB_CHECK(n_units < (1ull << SHIFT_BITS), "buffer too large for CRC shift tables");
@@ -261,5 +537,6 @@ namespace tsb {
 void preload_crc32() {
     touch_kernel(crc_init_kernel);
     touch_kernel(crc_kernel);
+    touch_kernel(crc_tile_kernel);
 }
 }  // namespace tsb

@@ -166,6 +166,22 @@ def test_crc32_device(n, offset):
     assert int(out.item()) & 0xFFFFFFFF == zlib.crc32(data[offset:].tobytes())
 
 
+@pytest.mark.parametrize("n", [4608 * 64, 4608 * 64 + 16, 4608 * 1000 + 16, 4608 * 777 + 4592,
+                               4608 * 5000 - 48, 154142720])
+@pytest.mark.parametrize("offset", [0, 16, 48])
+def test_crc32_tile_kernel_sizes(n, offset):
+    """The TMA tile CRC kernel (16 B-aligned buffers of >= 64 tiles): exact
+    multiples of the 4,608-byte tile, a front-padded first tile (z = 16 ..
+    4,592 virtual zeros), many warps' runs, and a whole f32 C2 batch."""
+    rng = np.random.default_rng(n % 9973 + offset)
+    data = rng.integers(0, 256, n + offset, dtype=np.uint8)
+    t = dev(data)
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dp.crc32(t.data_ptr() + offset, n, out)
+    torch.cuda.synchronize()
+    assert int(out.item()) & 0xFFFFFFFF == zlib.crc32(data[offset:].tobytes())
+
+
 def test_crc32_known_answers(golden):
     out = torch.zeros(1, dtype=torch.int32, device="cuda")
     for hexdata, want in golden["crc32"]:
