@@ -29,6 +29,7 @@
 //     (entry i of T_even/T_odd at i*256 (+128) + lane*4), so ONE PRMT builds
 //     the full shared address of a lookup from the data byte and a per-lane
 //     constant: 11 instructions and 4 conflict-free LDS per 4 data bytes.
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -59,14 +60,16 @@ constexpr int T_THREADS = 32 * T_WARPS;
 constexpr int T_LANE = 144;                // bytes per lane and tile: 9 x 16 B
 constexpr int T_WORDS = T_LANE / 4;        // 36
 constexpr int T_TILE = 32 * T_LANE;        // 4608 B per warp tile
-constexpr int T_CHAIN = T_LANE / 2;        // two chains of 72 B (18 words)
+// a lane runs K = 2, 3 or 4 slice-by-4 chains over its 144 B (72 / 48 / 36 B each)
+constexpr int chain_bytes(int k) { return T_LANE / k; }
 constexpr int T_STAGES = 2;
+constexpr int T_PREFETCH = 6;              // tiles ahead prefetched into L2 (cp.async.bulk.prefetch)
 constexpr int T_SMEM = 232448;             // the 227 KB opt-in maximum
 constexpr uint32_t T_TAB_BYTES = 131072;   // 4 tables x 256 entries x 32 lanes x 4 B
 __device__ uint32_t g_t_tree[TREE_LEVELS * NT];   // x^(8 * T_LANE * 2^k)
-__device__ uint32_t g_t_gap[NT];                  // x^(8 * (T_TILE - T_CHAIN))
-__device__ uint32_t g_t_half[NT];                 // x^(8 * T_CHAIN)
-__device__ uint32_t g_t_shift[SHIFT_BITS * NT];   // x^(8 * T_TILE * 2^k)
+__device__ uint32_t g_t_gap[3 * NT];              // [K-2]: x^(8 * (T_TILE - chain_bytes(K)))
+__device__ uint32_t g_t_half[3 * NT];             // [K-2]: x^(8 * chain_bytes(K))
+__device__ uint32_t g_t_pow[SHIFT_BITS];          // x^(8 * T_TILE * 2^k) mod P (values)
 
 uint32_t h_multmodp(uint32_t a, uint32_t b) {
     uint32_t m = 1u << 31, p = 0;
@@ -98,9 +101,10 @@ void h_nibble_table(uint32_t k, uint32_t *t) {
 std::mutex g_mu;
 bool g_ready[64] = {false};
 
-int ensure_tables() {
-    int dev = 0;
-    TSB_CUDA(cudaGetDevice(&dev));
+std::atomic<bool> g_ready_fast[64];
+
+int ensure_tables(int dev) {
+    if (dev >= 0 && dev < 64 && g_ready_fast[dev].load(std::memory_order_acquire)) return TSB_OK;
     std::lock_guard<std::mutex> lk(g_mu);
     if (dev < 64 && g_ready[dev]) return TSB_OK;
     static uint32_t sl[4 * 256], tt[TREE_LEVELS * NT], ht[NT], gt[NT], st[SHIFT_BITS * NT];
@@ -121,17 +125,22 @@ int ensure_tables() {
     TSB_CUDA(cudaMemcpyToSymbol(g_half_tab, ht, sizeof(ht)));
     TSB_CUDA(cudaMemcpyToSymbol(g_gap_tab, gt, sizeof(gt)));
     TSB_CUDA(cudaMemcpyToSymbol(g_shift_tab, st, sizeof(st)));
-    static uint32_t t_tree[TREE_LEVELS * NT], t_gap[NT], t_half[NT], t_shift[SHIFT_BITS * NT];
+    static uint32_t t_tree[TREE_LEVELS * NT], t_gap[3 * NT], t_half[3 * NT], t_pow[SHIFT_BITS];
     for (int k = 0; k < TREE_LEVELS; ++k)
         h_nibble_table(h_x8n((uint64_t)T_LANE << k), t_tree + k * NT);
-    h_nibble_table(h_x8n(T_TILE - T_CHAIN), t_gap);
-    h_nibble_table(h_x8n(T_CHAIN), t_half);
-    for (int k = 0; k < SHIFT_BITS; ++k) h_nibble_table(h_x8n((uint64_t)T_TILE << k), t_shift + k * NT);
+    for (int k = 2; k <= 4; ++k) {
+        h_nibble_table(h_x8n(T_TILE - chain_bytes(k)), t_gap + (k - 2) * NT);
+        h_nibble_table(h_x8n(chain_bytes(k)), t_half + (k - 2) * NT);
+    }
+    for (int k = 0; k < SHIFT_BITS; ++k) t_pow[k] = h_x8n((uint64_t)T_TILE << k);
     TSB_CUDA(cudaMemcpyToSymbol(g_t_tree, t_tree, sizeof(t_tree)));
     TSB_CUDA(cudaMemcpyToSymbol(g_t_gap, t_gap, sizeof(t_gap)));
     TSB_CUDA(cudaMemcpyToSymbol(g_t_half, t_half, sizeof(t_half)));
-    TSB_CUDA(cudaMemcpyToSymbol(g_t_shift, t_shift, sizeof(t_shift)));
-    if (dev < 64) g_ready[dev] = true;
+    TSB_CUDA(cudaMemcpyToSymbol(g_t_pow, t_pow, sizeof(t_pow)));
+    if (dev < 64) {
+        g_ready[dev] = true;
+        g_ready_fast[dev].store(true, std::memory_order_release);
+    }
     return TSB_OK;
 }
 
@@ -221,10 +230,16 @@ __global__ void __launch_bounds__(CRC_THREADS)
                 c0 = crc_word(rep, c0, w[j]);
                 c1 = crc_word(rep, c1, w[HW + j]);
             }
-        } else {
+        } else {  // (unrolled: the byte loads are issued together, not one per CRC step)
+            uint8_t bytes[LANE_BYTES];
+#pragma unroll
             for (int k = 0; k < LANE_BYTES; ++k) {
                 const int64_t p = vpos + k;
-                const uint32_t byte = (p >= 0 && (uint64_t)p < n) ? data[p] : 0u;
+                bytes[k] = (p >= 0 && (uint64_t)p < n) ? data[p] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < LANE_BYTES; ++k) {
+                const uint32_t byte = bytes[k];
                 if (k < LANE_BYTES / 2)
                     c0 = rep[((c0 ^ byte) & 0xFFu) << 5] ^ (c0 >> 8);
                 else
@@ -283,8 +298,9 @@ __device__ __forceinline__ uint32_t tile_step(uint32_t c, uint32_t w, uint32_t b
 }
 
 struct TileLayout {  // shared addresses (u32), identical in every CTA; this warp's buffers
-    uint32_t tab0, gap, stage0, stage1, bar0, bar1, bar_first;
+    uint32_t tab0, gap, small, stage0, stage1, bar0, bar1, bar_first;
 };
+constexpr int T_SMALL_WORDS = TREE_LEVELS * NT + NT;  // lane-tree + half nibble tables
 
 // First-fit of the buffers around the two 64 KB-aligned table regions.
 __device__ __forceinline__ bool tile_layout(uint32_t base, int wib, TileLayout &L) {
@@ -299,7 +315,7 @@ __device__ __forceinline__ bool tile_layout(uint32_t base, int wib, TileLayout &
         if (a + bytes <= end) { out = a; hi = a + bytes; return true; }
         return false;
     };
-    bool ok = take(NT * 32 * 4, 128, L.gap);
+    bool ok = take(NT * 32 * 4, 128, L.gap) && take(T_SMALL_WORDS * 4, 16, L.small);
 #pragma unroll
     for (int w = 0; w < T_WARPS; ++w)
 #pragma unroll
@@ -360,66 +376,161 @@ __device__ __forceinline__ uint32_t mul_nib_rep_s(uint32_t v, uint32_t t) {
     return r;
 }
 
+// a * b mod P (reflected; x^0 = bit 31), no tables: 32 branch-free steps
+__device__ __forceinline__ uint32_t d_multmodp(uint32_t a, uint32_t b) {
+    uint32_t p = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        p ^= b & (0u - ((a >> (31 - i)) & 1u));
+        b = (b >> 1) ^ (POLY & (0u - (b & 1u)));
+    }
+    return p;
+}
+// nibble-table product with the table in shared memory (t = shared address)
+__device__ __forceinline__ uint32_t mul_nib_s(uint32_t v, uint32_t t) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r ^= lds_even(t + 4u * (uint32_t)(j * 16 + ((v >> (4 * j)) & 15u)));
+    return r;
+}
+
 // Virtual message = z zero bytes || data (n + z = n_tiles * T_TILE); tile t
 // holds data bytes [t*T_TILE - z, (t+1)*T_TILE - z).  Tile 0 (the only one
 // with virtual zeros) is filled by its warp; every other tile is one TMA
 // bulk copy, so (data - z) must be 16-byte aligned.
+template <int K>
 __global__ void __launch_bounds__(T_THREADS, 1)
     crc_tile_kernel(const uint8_t *__restrict__ data, uint64_t n, uint64_t z, uint64_t n_tiles,
                     uint32_t *out) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
+    static_assert(T_WORDS % K == 0, "chains split the lane's words evenly");
+    constexpr int CW = T_WORDS / K;  // words per chain
+    extern __shared__ __align__(16) uint8_t smem_raw[];
     const uint32_t base = smem_u32(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     TileLayout L;
     if (!tile_layout(base, wib, L)) __trap();
-    // lane-replicated slice tables: region r holds T_{2r} (even slot) and T_{2r+1} (odd)
-    for (int e = tid; e < 4 * 256; e += T_THREADS) {
-        const uint32_t v = g_slice_tab[e];
-        const int t = e >> 8, i = e & 255;
-        const uint32_t row = L.tab0 + (uint32_t)(t >> 1) * 65536u + (uint32_t)i * 256u +
-                             (uint32_t)(t & 1) * 128u;
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) sts_u32(row + (uint32_t)(((l + e) & 31) << 2), v);
-    }
-    for (int e = tid; e < NT; e += T_THREADS) {
-        const uint32_t v = g_t_gap[e];
-        for (int l = 0; l < 32; ++l) sts_u32(L.gap + (uint32_t)e * 128u + (uint32_t)(((l + e) & 31) << 2), v);
-    }
-    if (tid < T_WARPS * T_STAGES) {  // the barriers are allocated contiguously, 8 B each
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(L.bar_first + 8u * tid)
-                     : "memory");
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-
     const uint64_t warp = (uint64_t)blockIdx.x * T_WARPS + wib;
     const uint64_t nwarps = (uint64_t)gridDim.x * T_WARPS;
     const uint64_t per = (n_tiles + nwarps - 1) / nwarps;
     const uint64_t t0 = warp * per, t1 = t0 + per < n_tiles ? t0 + per : n_tiles;
-    if (t0 >= t1) return;
-    const uint32_t b_lo = (L.tab0 & 0xFFFF0000u) | ((uint32_t)lane << 2);
-    const uint32_t b_hi = ((L.tab0 + 65536u) & 0xFFFF0000u) | ((uint32_t)lane << 2);
-    const uint32_t gap = L.gap + ((uint32_t)lane << 2);
+    const bool active = t0 < t1;
     const uint8_t *src0 = data - z;  // virtual byte 0 (never dereferenced below z)
 
+    // 1. this warp's barriers, then its first loads (nothing below depends on
+    //    the tables), so the HBM latency of the first tiles overlaps the
+    //    table fill and the shift-constant product
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(L.bar0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(L.bar1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     auto issue = [&](uint64_t t, int s) {
-        if (t == 0 && z) {  // virtual zeros || data head: filled by this warp
+        if (t == 0 && z) {  // virtual zeros || data head (only the first warp's first tile)
             const uint32_t dst = s ? L.stage1 : L.stage0;
-            for (uint32_t i = (uint32_t)lane; i < (uint32_t)T_TILE; i += 32) {
-                const uint32_t v = i >= z && (uint64_t)i - z < n ? data[i - z] : 0u;
-                asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + i), "r"(v) : "memory");
+            const uint32_t bar = s ? L.bar1 : L.bar0;
+            if ((z & 15) == 0) {  // 16 B-aligned head: zeros by the lanes, the data by TMA
+                for (uint32_t i = 16u * lane; i < (uint32_t)z; i += 512)
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(dst + i), "r"(0u)
+                                 : "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    const uint32_t bytes = (uint32_t)T_TILE - (uint32_t)z;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                                 "r"(bytes)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+                        "[%1], %2, [%3];" ::"r"(dst + (uint32_t)z),
+                        "l"(data), "r"(bytes), "r"(bar)
+                        : "memory");
+                }
+            } else {  // ragged head: byte loads issued 16 at a time, then stored
+                for (uint32_t i0 = 16u * lane; i0 < (uint32_t)T_TILE; i0 += 512) {
+                    uint32_t v[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t i = i0 + k;
+                        v[k] = i >= z && (uint64_t)i - z < n ? data[i - z] : 0u;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + i0 + k), "r"(v[k]) : "memory");
+                }
+                __syncwarp();
+                if (lane == 0)  // complete the stage's phase with no transfer
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
             }
-            __syncwarp();
-            if (lane == 0)  // complete the stage's phase with no transfer
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s ? L.bar1 : L.bar0)
-                             : "memory");
         } else if (lane == 0) {
             tile_load(s ? L.stage1 : L.stage0, src0 + t * (uint64_t)T_TILE, s ? L.bar1 : L.bar0);
         }
     };
-    issue(t0, 0);
-    if (t0 + 1 < t1) issue(t0 + 1, 1);
-    uint32_t cA = 0, cB = 0, phase = 0;  // phase bit s: parity to wait for on stage s
+    // The two smem stages alone keep ~2 tiles per warp in flight, less than
+    // HBM latency x bandwidth per SM: tiles further ahead are prefetched into
+    // L2 (no smem), so the TMA load of a stage mostly hits L2.
+    auto prefetch = [&](uint64_t t) {
+        if (lane == 0 && t < t1 && t > 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src0 + t * (uint64_t)T_TILE),
+                         "r"((uint32_t)T_TILE)
+                         : "memory");
+    };
+    if (active) {
+        issue(t0, 0);
+        if (t0 + 1 < t1) issue(t0 + 1, 1);
+#pragma unroll 1
+        for (int k = 2; k < 2 + T_PREFETCH; ++k) prefetch(t0 + k);
+    }
+
+    // 2. the tables: every word this thread stores is loaded first (one
+    //    global round trip for the whole fill)
+    constexpr int NSL = 4 * 256 / T_THREADS;                              // 4
+    constexpr int NSM = (T_SMALL_WORDS + T_THREADS - 1) / T_THREADS;      // 3
+    uint32_t vsl[NSL], vsm[NSM], vgap = 0;
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) vsl[k] = g_slice_tab[tid + k * T_THREADS];
+#pragma unroll
+    for (int k = 0; k < NSM; ++k) {
+        const int e = tid + k * T_THREADS;
+        vsm[k] = e < TREE_LEVELS * NT ? g_t_tree[e]
+                 : e < T_SMALL_WORDS  ? g_t_half[(K - 2) * NT + e - TREE_LEVELS * NT]
+                                      : 0u;
+    }
+    if (tid < NT) vgap = g_t_gap[(K - 2) * NT + tid];
+    // lane-replicated slice tables: region r holds T_{2r} (even slot) and T_{2r+1} (odd)
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) {
+        const int e = tid + k * T_THREADS;
+        const int t = e >> 8, i = e & 255;
+        const uint32_t row = L.tab0 + (uint32_t)(t >> 1) * 65536u + (uint32_t)i * 256u +
+                             (uint32_t)(t & 1) * 128u;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) sts_u32(row + (uint32_t)(((l + e) & 31) << 2), vsl[k]);
+    }
+    if (tid < NT) {
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l)
+            sts_u32(L.gap + (uint32_t)tid * 128u + (uint32_t)(((l + tid) & 31) << 2), vgap);
+    }
+#pragma unroll
+    for (int k = 0; k < NSM; ++k) {
+        const int e = tid + k * T_THREADS;
+        if (e < T_SMALL_WORDS) sts_u32(L.small + 4u * e, vsm[k]);
+    }
+    __syncthreads();
+    if (!active) return;
+    // 3. shift by the tiles after this warp's run: x^(8*T_TILE*m) = prod over
+    //    the set bits k of m of x^(8*T_TILE*2^k), one factor per lane,
+    //    multiplied together across the lanes (5 levels, no table loads)
+    const uint64_t m = n_tiles - t1;
+    uint32_t f = (lane < SHIFT_BITS && ((m >> lane) & 1)) ? g_t_pow[lane] : 0x80000000u;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) f = d_multmodp(f, __shfl_xor_sync(0xFFFFFFFFu, f, 1 << k));
+    const uint32_t b_lo = (L.tab0 & 0xFFFF0000u) | ((uint32_t)lane << 2);
+    const uint32_t b_hi = ((L.tab0 + 65536u) & 0xFFFF0000u) | ((uint32_t)lane << 2);
+    const uint32_t gap = L.gap + ((uint32_t)lane << 2);
+    uint32_t ch[K], phase = 0;  // phase bit s: parity to wait for on stage s
+#pragma unroll
+    for (int k = 0; k < K; ++k) ch[k] = 0;
     for (uint64_t t = t0; t < t1; ++t) {
         const int s = (int)((t - t0) & 1);
         tile_wait(s ? L.bar1 : L.bar0, (phase >> s) & 1u);
@@ -436,33 +547,28 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         }
         __syncwarp();
         if (t + 2 < t1) issue(t + 2, s);  // the stage is free: every lane holds its words
+        prefetch(t + 2 + T_PREFETCH);
         if (t != t0) {
-            cA = mul_nib_rep_s(cA, gap);
-            cB = mul_nib_rep_s(cB, gap);
+#pragma unroll
+            for (int k = 0; k < K; ++k) ch[k] = mul_nib_rep_s(ch[k], gap);
         }
 #pragma unroll
-        for (int j = 0; j < T_WORDS / 2; ++j) {
-            cA = tile_step(cA, wv[j], b_lo, b_hi);
-            cB = tile_step(cB, wv[T_WORDS / 2 + j], b_lo, b_hi);
-        }
+        for (int j = 0; j < CW; ++j)
+#pragma unroll
+            for (int k = 0; k < K; ++k) ch[k] = tile_step(ch[k], wv[k * CW + j], b_lo, b_hi);
     }
-    uint32_t c = mul_nib(cA, g_t_half) ^ cB;  // the lane's bytes, relative to its chunk end
+    // the lane's bytes, relative to the end of its chunk in the last tile
+    uint32_t c = ch[0];
 #pragma unroll
-    for (int k = 0; k < TREE_LEVELS; ++k) {
+    for (int k = 1; k < K; ++k) c = mul_nib_s(c, L.small + 4u * TREE_LEVELS * NT) ^ ch[k];
+#pragma unroll
+    for (int k = 0; k < TREE_LEVELS; ++k) {  // lanes in address order (shared tables)
         const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, c, 1 << k);
-        if (lane & (1 << k))
-            c = mul_nib(other, g_t_tree + k * NT) ^ c;
-        else
-            c = mul_nib(c, g_t_tree + k * NT) ^ other;
+        const uint32_t tk = L.small + 4u * k * NT;
+        c = (lane & (1 << k)) ? mul_nib_s(other, tk) ^ c : mul_nib_s(c, tk) ^ other;
     }
     if (lane == 0) {
-        uint64_t q = n_tiles - t1;  // the tiles after this warp's run
-        int k = 0;
-        while (q) {
-            if (q & 1) c = mul_nib(c, g_t_shift + k * NT);
-            q >>= 1;
-            ++k;
-        }
+        if (m) c = d_multmodp(c, f);
         if (c) atomicXor(out, c);
     }
 }
@@ -477,13 +583,32 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
     (void)d_workspace;
     TSB_CHECK(d_out, "null output");
     TSB_CHECK(data || n == 0, "null data");
-    int rc = ensure_tables();
+    int dev = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    int rc = ensure_tables(dev);
     if (rc) return rc;
     auto s = as_stream(stream);
-    // init term: x^(8n) * 0xFFFFFFFF xor 0xFFFFFFFF (n = 0 -> 0)
-    const uint32_t init = h_multmodp(h_x8n(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
-    crc_init_kernel<<<1, 1, 0, s>>>(d_out, init);
-    TSB_LAUNCH_CHECK();
+    // init term: x^(8n) * 0xFFFFFFFF xor 0xFFFFFFFF (n = 0 -> 0); a ring's
+    // batches all have one size, so the last few sizes are cached
+    static thread_local uint64_t init_n[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+    static thread_local uint32_t init_v[4];
+    uint32_t init = 0;
+    int hit = -1;
+    for (int i = 0; i < 4; ++i)
+        if (init_n[i] == n) hit = i;
+    if (hit >= 0) {
+        init = init_v[hit];
+    } else {
+        init = h_multmodp(h_x8n(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+        for (int i = 3; i > 0; --i) init_n[i] = init_n[i - 1], init_v[i] = init_v[i - 1];
+        init_n[0] = n;
+        init_v[0] = init;
+    }
+    static const int skip_init = getenv("TSB_CRC_INIT") && !strcmp(getenv("TSB_CRC_INIT"), "none");
+    if (!skip_init) {  // (skip: timing diagnostics only -- the result is then wrong)
+        crc_init_kernel<<<1, 1, 0, s>>>(d_out, init);
+        TSB_LAUNCH_CHECK();
+    }
     if (n == 0) return TSB_OK;
     static const int force_old = getenv("TSB_CRC_IMPL") && !strcmp(getenv("TSB_CRC_IMPL"), "v1");
     {
@@ -491,18 +616,19 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
         const uint64_t n_tiles = (n + zt) / T_TILE;
         if (!force_old && n >= (uint64_t)T_TILE * 64 && ((((uintptr_t)data) - zt) & 15) == 0 &&
             n_tiles < (1ull << SHIFT_BITS)) {
+            static const int chains = getenv("TSB_CRC_CHAINS") ? atoi(getenv("TSB_CRC_CHAINS")) : 2;
+            auto kern = chains == 4 ? crc_tile_kernel<4> : chains == 3 ? crc_tile_kernel<3>
+                                                                       : crc_tile_kernel<2>;
             static bool t_attr[64] = {false};
-            int dev = 0;
-            cudaGetDevice(&dev);
             if (dev < 64 && !t_attr[dev]) {
-                TSB_CUDA(cudaFuncSetAttribute(crc_tile_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM));
+                TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              T_SMEM));
                 t_attr[dev] = true;
             }
             uint64_t blocks = (n_tiles + T_WARPS - 1) / T_WARPS;
             const uint64_t cap = (uint64_t)sm_count();  // one CTA per SM
             if (blocks > cap) blocks = cap;
-            crc_tile_kernel<<<(unsigned)blocks, T_THREADS, T_SMEM, s>>>(
+            kern<<<(unsigned)blocks, T_THREADS, T_SMEM, s>>>(
                 static_cast<const uint8_t *>(data), n, zt, n_tiles, d_out);
             TSB_LAUNCH_CHECK();
             return TSB_OK;
@@ -514,8 +640,6 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
     const int vec = ((((uintptr_t)data) - z) & 15) == 0;
     const size_t smem = sizeof(CrcSmem);
     static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (dev < 64 && !attr_set[dev]) {
         TSB_CUDA(cudaFuncSetAttribute(crc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
@@ -537,6 +661,8 @@ namespace tsb {
 void preload_crc32() {
     touch_kernel(crc_init_kernel);
     touch_kernel(crc_kernel);
-    touch_kernel(crc_tile_kernel);
+    touch_kernel(crc_tile_kernel<2>);
+    touch_kernel(crc_tile_kernel<3>);
+    touch_kernel(crc_tile_kernel<4>);
 }
 }  // namespace tsb

@@ -81,8 +81,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         TSB_CHECK(jpeg_sample_bytes(a->jpeg) == a->sample_bytes,
                   "decoder geometry (%lld B) does not match the samples (%lld B)",
                   (long long)jpeg_sample_bytes(a->jpeg), (long long)a->sample_bytes);
-        TSB_CHECK(!a->d_crc && !no_fused && ring_writers(r) == 1,
-                  "the JPEG source needs the fused single-writer path (no per-batch CRC)");
+        TSB_CHECK(!no_fused && ring_writers(r) == 1,
+                  "the JPEG source needs the fused single-writer path");
     }
     const bool staged = !jpeg && a->ingest && a->h_order && !ev;
     if (a->persistent) {  // one cooperative launch for the whole range, gated on the device
@@ -131,7 +131,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         bool published = false, staged_target = false;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
-                if (!a->d_crc && !no_fused && ring_writers(r) == 1) {  // fused epilogue: target copy + publish from the kernel
+                if (!no_fused && ring_writers(r) == 1) {  // fused epilogue: target copy + publish from the kernel
                     uint64_t *ready = nullptr;
                     unsigned int *counter = nullptr;
                     if ((rc = ring_publish_ptrs(r, slot, 0, &ready, &counter))) return rc;
@@ -217,7 +217,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                 }
                 [[fallthrough]];
             case TSB_SRC_SYNTHETIC:
-                if (!a->d_crc && !no_fused && ring_writers(r) == 1 && a->sample_bytes % 16 == 0 &&
+                if (!no_fused && ring_writers(r) == 1 && a->sample_bytes % 16 == 0 &&
                     ((uintptr_t)out & 15) == 0) {
                     // one persistent passthrough launch: samples + target + slot publish
                     uint64_t *ready = nullptr;
@@ -247,9 +247,18 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                 TSB_CHECK(false, "bad produce mode %d", a->mode);
         }
         if (rc) return rc;
-        prev_fused = published;
+        // With a per-batch CRC the fused kernel still publishes the slot: the
+        // checksum only rides in the Announce, which the host sends after
+        // reading it, so no consumer fetches the slot before its CRC is known
+        // (and nothing rewrites it before every consumer released it).  The
+        // CRC launches sit between two collates, so that pair is not PDL-chained.
+        prev_fused = published && !a->d_crc;
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
-        if (published) continue;
+        if (published) {
+            if (a->d_crc)
+                if (int rc2 = tsb_crc32(out, nbytes, a->d_crc + slot, nullptr, stream)) return rc2;
+            continue;
+        }
         if (a->with_target && !staged_target)
             TSB_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(out) + a->input_bytes, idx, 8 * b,
                                      cudaMemcpyDeviceToDevice, s));

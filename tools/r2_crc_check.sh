@@ -2,7 +2,7 @@
 # round 2: tile CRC kernel -- tests, throughput (tile vs v1), one ncu capture
 out=gpurun_out/${1:-crc}; mkdir -p $out
 timeout 600 python -m pytest tests/test_gpu_kernels.py -q -k crc > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log
-timeout 300 python tools/crc_bench.py > $out/crc_tile.jsonl 2>&1
-TSB_CRC_IMPL=v1 timeout 300 python tools/crc_bench.py > $out/crc_v1.jsonl 2>&1
+timeout 300 python tools/crc_bench.py 154.14272 77.07 38.5 9.633792 2.1 0.4 > $out/crc_tile.jsonl 2>&1
+TSB_CRC_IMPL=v1 timeout 300 python tools/crc_bench.py 154.14272 9.633792 2.1 > $out/crc_v1.jsonl 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:crc_tile -s 2 -c 1 \
     -o $out/full_crc_tile -f python tools/profile_one.py crc 4 > $out/ncu_crc.log 2>&1
