@@ -742,6 +742,8 @@ def run_e2e(args, ctx, dev, rank, world):
             "per_consumer_spread": None if spread is None else round(spread, 4),
             "sum_per_consumer": round(sum(per), 1),
             "buffer_depth": E2E_BUFFER_DEPTH, "ledger_drift_max": drift,
+            "checksum": "device CRC-32 of every batch in its Announce (TensorProducer default, "
+                        "as the reference's create_segment, bs/payload.py:218)",
             "wall_s": round(wall, 2), "batches_produced": produced}
 
 

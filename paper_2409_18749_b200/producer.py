@@ -29,7 +29,8 @@ Keyword-only extensions: ``ring_slots`` (device ring depth; bounds drift),
 shm block -- evictions and map-and-ack consumers never touch a GPU channel;
 "device": words in HBM), ``min_consumers`` (start barrier, bs/producer.py:73-76 -- the facade's
 missing barrier is the start race noted in SURVEY.md §4), ``checksum``
-(device CRC-32 of every batch into Announce.checksum), ``rubberband_fraction``
+(device CRC-32 of every batch into Announce.checksum; default on for one GPU,
+as the reference checksums every segment), ``rubberband_fraction``
 (late-join replay window, bs/producer.py:119-135; 0 = facade behaviour),
 ``device``; ``devices`` + ``fanout`` (multi-GPU, below).
 
@@ -89,7 +90,7 @@ class TensorProducer:
     def __init__(self, data_loader, broadcast: str | None = None, aggregate: str | None = None,
                  buffer_depth: int = 2, heartbeat_timeout_s: float = 5.0,
                  pause_poll_s: float = 0.05, *, ring_slots: int | None = None,
-                 min_consumers: int = 1, checksum: bool = False,
+                 min_consumers: int = 1, checksum: bool | None = None,
                  rubberband_fraction: float = 0.0, max_consumers: int = 64,
                  device: int | None = None, control: str = "host", devices=None,
                  fanout: str = "auto"):
@@ -108,7 +109,7 @@ class TensorProducer:
         self._hb_timeout = heartbeat_timeout_s
         self._poll = pause_poll_s
         self._min_consumers = min_consumers
-        self._checksum = checksum
+        self._checksum_arg = checksum
         self._fraction = rubberband_fraction
         self._max_consumers = max_consumers
         self._ring_slots = ring_slots
@@ -125,6 +126,11 @@ class TensorProducer:
                                   hasattr(data_loader, "dataset")) else "sharded"
         self.fanout = fanout
         self._multi = len(self._devices) > 1
+        # every batch's CRC-32 rides in its Announce, as the reference's
+        # create_segment computes it (bs/payload.py:218, sl/producer.py:313):
+        # the default on one GPU; the fused multi-GPU fan-out paths announce 0
+        # (no checksum) unless checksum=True selects the per-device path
+        self._checksum = (not self._multi) if checksum is None else bool(checksum)
         if self._multi and control != "host":
             raise ValueError("multi-GPU rings need control='host' (host-shared control words)")
         self._sharded = self._multi and fanout == "sharded"
@@ -190,6 +196,10 @@ class TensorProducer:
         self._hub_fds: dict[int, int] = {}  # fd -> consumer id
         self._hdr_key = None
         self._hdr_reserved = b""
+        # checksum=True: a batch is announced once its CRC-32 reached the host,
+        # which is after the NEXT batch was enqueued (the copy engine / collate
+        # of batch q+1 never waits for batch q's checksum)
+        self._pending_ann = None
 
     # -- ring -------------------------------------------------------------
     def _batch_nbytes_hint(self) -> int | None:
@@ -639,6 +649,7 @@ class TensorProducer:
                 self._start_epoch(L)
             self._publish(index, batch)
             yield None
+        self._flush_pending()
         with self._lock:
             self._send_all(EpochEnd(self._epoch))
             self._drop_retention()
@@ -719,6 +730,8 @@ class TensorProducer:
         ring, stream = self._ring, self._stream
         slot = ring.slot_of(q)
         host_gated = all(r.host_control for r in self._rings.values())
+        if self._pending_ann is not None and self._pending_ann[0] <= q - self._depth:
+            self._flush_pending()  # (buffer_depth 1: the gate waits for that batch's acks)
         self._ack_gate(q, depth_ids)
         if host_gated:
             # slot-reuse gate on the host-shared cursors: the producer's streams
@@ -730,13 +743,21 @@ class TensorProducer:
             self._publish_two_stage(q, index)
         elif self._multi and self._device_loader and not self._checksum:
             self._publish_group(q, index)
-        elif self._device_loader and host_gated and not self._checksum:
-            a = self._loader.produce_args(self._epoch)  # fused collate + target + publish
+        elif self._device_loader and host_gated and not self._multi:
+            # fused collate + target + publish; with checksum=True the device
+            # CRC-32 of the slot follows on the same stream (tsb_produce_range)
+            a = self._loader.produce_args(self._epoch,
+                                          with_crc=self._crc if self._checksum else None)
             a.gate = GATE_HOST
             a.chain = int(self._chain_ok)  # the stream's previous op was our fused kernel
             with torch.cuda.device(self.device):
                 produce_range(ring, a, q, index, 1, [], stream=stream)
-            self._chain_ok = True
+                if self._checksum:
+                    with torch.cuda.stream(stream):
+                        self._crc_host[slot:slot + 1].copy_(self._crc[slot:slot + 1],
+                                                            non_blocking=True)
+                    self._events[slot].record(stream)
+            self._chain_ok = not self._checksum
         else:
             if not host_gated and q > ring.slots:
                 # bound host run-ahead: batch q-S (same slot) must have been published
@@ -763,24 +784,45 @@ class TensorProducer:
                     r.publish(slot, q, st)
                     if k == 0:
                         self._events[slot].record(st)
-        crc = 0
-        if self._checksum:
-            self._events[slot].synchronize()
-            crc = int(self._crc_host[slot]) & 0xFFFFFFFF
         hkey = (int(in_dt), in_shape, int(tg_dt), tg_shape, in_bytes, nbytes)
         if self._hdr_key != hkey:  # the pair layout is fixed for a loader: pack it once
             self._hdr_key = hkey
             self._hdr_reserved = sg.pack_pair_reserved(int(in_dt), len(in_shape), int(tg_dt),
                                                        len(tg_shape), in_bytes)
-        header = sg.pack_header(self._epoch, index, DType.U8, (nbytes,), nbytes, crc,
-                                reserved=self._hdr_reserved, extra_slots=(*in_shape, *tg_shape))
-        anns = {k: Announce(self._epoch, index, sg.slot_name(self._ring_ids[k], slot, header),
+        cur = (q, index, slot, nbytes, (*in_shape, *tg_shape), self._epoch)
+        if not self._checksum:
+            self._announce(cur, 0)
+            return
+        prev, self._pending_ann = self._pending_ann, cur
+        if prev is not None:
+            self._announce_crc(prev)
+
+    def _announce_crc(self, p) -> None:
+        """Announce a batch whose device CRC-32 was enqueued (waits for it)."""
+        slot = p[2]
+        self._events[slot].synchronize()
+        self._announce(p, int(self._crc_host[slot]) & 0xFFFFFFFF)
+
+    def _flush_pending(self) -> None:
+        p, self._pending_ann = self._pending_ann, None
+        if p is not None:
+            self._announce_crc(p)
+
+    def _announce(self, p, crc: int) -> None:
+        """Announce (q, index, slot, nbytes, extra shape slots, epoch) with its
+        checksum to every consumer: the 80-byte segment header rides in the
+        slot name (bs/producer.py:506-534)."""
+        q, index, slot, nbytes, extra, epoch = p
+        header = sg.pack_header(epoch, index, DType.U8, (nbytes,), nbytes, crc,
+                                reserved=self._hdr_reserved, extra_slots=extra)
+        anns = {k: Announce(epoch, index, sg.slot_name(self._ring_ids[k], slot, header),
                             nbytes, DType.U8, (nbytes,), crc) for k in self._rings}
+        L = len(self._loader)
         with self._lock:
             self._drain_acks()
             self._ledger.add(q, [r.consumer_id for r in self._admitted()])
             self._send_announces(anns)
-            self.batches.append((self._epoch, index, crc))
+            self.batches.append((epoch, index, crc))
             self._announced_in_epoch = index + 1
             self.stats["announced"] += 1
             window = retention_window(self._fraction, L)
@@ -940,6 +982,7 @@ class TensorProducer:
         """Wait for outstanding acks, broadcast Shutdown, release the ring."""
         if self._closed:
             return
+        self._flush_pending()
         deadline = time.monotonic() + drain_timeout_s
         with self._lock:
             while time.monotonic() < deadline:
