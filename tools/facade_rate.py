@@ -65,6 +65,8 @@ def main():
     if devs:
         kw = dict(devices=[int(d) for d in devs.split(",")],
                   fanout=os.environ.get("TSB_FR_FANOUT", "inputs"))
+    kw["checksum"] = os.environ.get("TSB_FR_CHECKSUM", "0") == "1"
+    kw["buffer_depth"] = int(os.environ.get("TSB_FR_DEPTH", 6))
     prod = TensorProducer(ld, b, a, min_consumers=K, ring_slots=8, heartbeat_timeout_s=60, **kw)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -98,8 +100,9 @@ def main():
     print(json.dumps({"consumer_batches_per_s": [round(r, 1) for r in rates],
                       "delivered_samples_per_s": round(sum(rates) * B, 1),
                       "producer_loop_batches_per_s": round((n - n // 4) / (t1 - t0), 1),
-                      "sync": sync, "consumers": K, **({"devices": devs, "fanout": kw["fanout"]}
-                                                       if devs else {})}))
+                      "sync": sync, "consumers": K, "checksum": kw["checksum"],
+                      "buffer_depth": kw["buffer_depth"],
+                      **({"devices": devs, "fanout": kw["fanout"]} if devs else {})}))
 
 
 if __name__ == "__main__":
