@@ -420,6 +420,32 @@ int tsb_hub_set_acked(tsb_hub *h, uint64_t consumer_id, uint64_t seq);
 int tsb_hub_read_acked(tsb_hub *h, uint64_t consumer_id, uint64_t *seq);
 int tsb_hub_wait_acked(tsb_hub *h, const uint64_t *consumer_ids, int n, uint64_t need,
                        int64_t timeout_us);
+/* Largest max - min acked seq seen over the registered consumers (those given
+ * a baseline by set_acked, sentinel entries excluded) at any Ack: the
+ * reference's drift statistic, sampled at every Ack. */
+int tsb_hub_drift_max(tsb_hub *h, uint64_t *drift);
+
+/* ---- the facade producer's per-batch host path (sl/producer.py:279-316) ----
+ * For one GPU and a device loader: tsb_facade_produce = the flow gate on the
+ * hub's acked seqs (>= seq - depth, TSB_ERR_STALE after timeout_us) +
+ * tsb_produce_range(ring, args, seq, index, 1, live) (+ the batch CRC's
+ * read-back into h_crc[slot] and events[slot] when d_crc is set);
+ * tsb_facade_announce = (wait for the CRC) + the 80-byte segment header with
+ * epoch / crc / index patched into `header80`, base64 in the slot name
+ * "tsb1:<ring_id hex>:<slot>:<b64>", one Announce frame written to every fd
+ * (failed[i] = 1 for a socket that failed). */
+typedef struct tsb_facade tsb_facade;
+int tsb_facade_create(tsb_facade **out);
+int tsb_facade_destroy(tsb_facade *f);
+int tsb_facade_set_batch(tsb_facade *f, tsb_hub *hub, tsb_ring *ring, const tsb_produce_args *a,
+                         void *stream, int depth, uint64_t ring_id, const uint8_t *header80,
+                         uint64_t nbytes, uint32_t *d_crc, uint32_t *h_crc, void *const *events,
+                         int slots);
+int tsb_facade_set_consumers(tsb_facade *f, const uint64_t *ack_ids, int n_ack, const int *live,
+                             int n_live, const int *fds, int n_fds);
+int tsb_facade_produce(tsb_facade *f, uint64_t seq, int64_t index, int chain, int64_t timeout_us);
+int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t index,
+                        int with_crc, uint32_t *crc_out, int *failed);
 
 #ifdef __cplusplus
 }

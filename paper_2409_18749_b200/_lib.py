@@ -179,6 +179,16 @@ SIGNATURES["tsb_hub_set_epoch_len"] = (i32, [vp, u64])
 SIGNATURES["tsb_hub_set_acked"] = (i32, [vp, u64, u64])
 SIGNATURES["tsb_hub_read_acked"] = (i32, [vp, u64, ctypes.POINTER(u64)])
 SIGNATURES["tsb_hub_wait_acked"] = (i32, [vp, ctypes.POINTER(u64), i32, u64, i64])
+SIGNATURES["tsb_hub_drift_max"] = (i32, [vp, ctypes.POINTER(u64)])
+SIGNATURES["tsb_facade_create"] = (i32, [pp])
+SIGNATURES["tsb_facade_destroy"] = (i32, [vp])
+SIGNATURES["tsb_facade_set_batch"] = (i32, [vp, vp, vp, ctypes.POINTER(ProduceArgs), vp, i32, u64,
+                                            ctypes.c_char_p, u64, vp, vp, pp, i32])
+SIGNATURES["tsb_facade_set_consumers"] = (i32, [vp, ctypes.POINTER(u64), i32, ctypes.POINTER(i32),
+                                                i32, ctypes.POINTER(i32), i32])
+SIGNATURES["tsb_facade_produce"] = (i32, [vp, u64, i64, i32, i64])
+SIGNATURES["tsb_facade_announce"] = (i32, [vp, u64, ctypes.c_uint32, u64, i32,
+                                           ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(i32)])
 SIGNATURES["tsb_wire_encode"] = (i32, [ctypes.POINTER(Msg), vp, sz, ctypes.POINTER(sz)])
 SIGNATURES["tsb_wire_decode"] = (i32, [vp, sz, ctypes.POINTER(Msg), ctypes.POINTER(sz)])
 SIGNATURES["tsb_produce_group"] = (i32, [pp, i32, i32, ctypes.POINTER(ProduceArgs), i32, i32, u64,

@@ -59,6 +59,17 @@ struct tsb_hub {
     std::vector<tsb_hub_event> events;
     uint64_t epoch_len = 0;             // 0: acked seqs are not tracked
     std::unordered_map<uint64_t, uint64_t> acked;  // consumer id -> highest acked seq
+    uint64_t drift_max = 0;             // max - min acked over registered consumers, any Ack
+
+    void sample_drift() {  // caller holds mu
+        uint64_t lo = ~0ull, hi = 0;
+        for (const auto &kv : acked) {
+            if (kv.second >= (1ull << 61)) continue;  // departed (sentinel)
+            if (kv.second < lo) lo = kv.second;
+            if (kv.second > hi) hi = kv.second;
+        }
+        if (hi >= lo && hi - lo > drift_max) drift_max = hi - lo;
+    }
 
     bool all_acked(const uint64_t *ids, int n, uint64_t need) const {  // caller holds mu
         for (int i = 0; i < n; ++i) {
@@ -106,6 +117,7 @@ struct tsb_hub {
                 auto it = acked.find(m.consumer_id);
                 if (it != acked.end() && seq > it->second) {
                     it->second = seq;
+                    sample_drift();
                     cv.notify_all();
                 }
             }
@@ -257,6 +269,13 @@ int tsb_hub_wait_acked(tsb_hub *h, const uint64_t *consumer_ids, int n, uint64_t
     }
     return h->cv.wait_for(lk, std::chrono::microseconds(timeout_us), ok) ? TSB_OK
                                                                         : TSB_ERR_STALE;
+}
+
+int tsb_hub_drift_max(tsb_hub *h, uint64_t *drift) {
+    if (!h || !drift) return TSB_ERR_INVALID;
+    std::lock_guard<std::mutex> lk(h->mu);
+    *drift = h->drift_max;
+    return TSB_OK;
 }
 
 int tsb_hub_destroy(tsb_hub *h) {

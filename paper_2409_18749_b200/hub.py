@@ -74,6 +74,14 @@ class Hub:
         _lib.check(rc, "tsb_hub_wait_acked")
         return True
 
+    def drift_max(self) -> int:
+        """Largest acked-seq spread over registered consumers seen at any Ack."""
+        if not self._h:
+            return 0
+        v = ctypes.c_uint64()
+        _lib.call("tsb_hub_drift_max", self._h, ctypes.byref(v))
+        return v.value
+
     @staticmethod
     def broadcast(fds, frame: bytes) -> list:
         """Send `frame` to every fd; returns the fds whose send failed."""
@@ -89,6 +97,68 @@ class Hub:
         h, self._h = self._h, None
         if h:
             self._L.tsb_hub_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Facade:
+    """tsb_facade: the per-batch producer path (flow gate, fused launch,
+    checksum read-back, Announce encode + broadcast) in two native calls."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        _lib.call("tsb_facade_create", ctypes.byref(h))
+        self._h = h.value
+        self._L = _lib.load()
+        self._keep = []
+        self._failed = (ctypes.c_int * 1)()
+        self._crc = ctypes.c_uint32(0)
+        self.fds: list = []
+
+    def set_batch(self, hub: Hub, ring, args, stream, depth: int, ring_id: int, header: bytes,
+                  nbytes: int, d_crc=None, h_crc=None, events=None) -> None:
+        evs = None
+        if d_crc is not None:
+            evs = (ctypes.c_void_p * ring.slots)(*[int(e.cuda_event) for e in events])
+        self._keep = [args, evs, header]
+        _lib.call("tsb_facade_set_batch", self._h, hub._h, ring._h, ctypes.byref(args),
+                  _lib.stream_handle(stream), depth, ring_id, header, nbytes,
+                  None if d_crc is None else d_crc.data_ptr(),
+                  None if h_crc is None else h_crc.data_ptr(), evs, ring.slots)
+
+    def set_consumers(self, ack_ids, live, fds) -> None:
+        n1, n2, n3 = len(ack_ids), len(live), len(fds)
+        a = (ctypes.c_uint64 * max(1, n1))(*ack_ids)
+        b = (ctypes.c_int * max(1, n2))(*live)
+        c = (ctypes.c_int * max(1, n3))(*fds)
+        self._failed = (ctypes.c_int * max(1, n3))()
+        self.fds = list(fds)
+        _lib.call("tsb_facade_set_consumers", self._h, a, n1, b, n2, c, n3)
+
+    def produce(self, seq: int, index: int, chain: bool, timeout_s: float) -> bool:
+        """False when the flow gate timed out (the caller re-checks shutdown)."""
+        rc = self._L.tsb_facade_produce(self._h, seq, index, int(chain), int(timeout_s * 1e6))
+        if rc == _lib.TSB_ERR_STALE:
+            return False
+        _lib.check(rc, "tsb_facade_produce")
+        return True
+
+    def announce(self, seq: int, epoch: int, index: int, with_crc: bool):
+        """-> (crc, [fds whose send failed])."""
+        _lib.check(self._L.tsb_facade_announce(self._h, seq, epoch, index, int(with_crc),
+                                               ctypes.byref(self._crc), self._failed),
+                   "tsb_facade_announce")
+        failed = [fd for i, fd in enumerate(self.fds) if self._failed[i]] if self.fds else []
+        return self._crc.value, failed
+
+    def close(self) -> None:
+        h, self._h = self._h, None
+        if h:
+            self._L.tsb_facade_destroy(h)
 
     def __del__(self):
         try:

@@ -200,6 +200,14 @@ class TensorProducer:
         # which is after the NEXT batch was enqueued (the copy engine / collate
         # of batch q+1 never waits for batch q's checksum)
         self._pending_ann = None
+        # the one-GPU device-loader fast path (hub.Facade): consumer lists are
+        # pushed to it when _cver (bumped on every membership change) moves
+        self._cver = 0
+        self._facade = None
+        self._facade_ver = -1
+        self._facade_epoch = None
+        self._facade_fds: dict = {}
+        self._since_drain = 0
 
     # -- ring -------------------------------------------------------------
     def _batch_nbytes_hint(self) -> int | None:
@@ -254,6 +262,8 @@ class TensorProducer:
         self._stream = self._streams[0]
         with torch.cuda.device(self.device):
             self._events = [torch.cuda.Event() for _ in range(slots)]
+            for e in self._events:  # materialise the CUDA events (native code records them)
+                e.record(self._stream)
             self._crc = torch.zeros(slots, dtype=torch.int32, device=f"cuda:{self.device}")
             self._crc_host = torch.zeros(slots, dtype=torch.int32).pin_memory()
         self._lock.notify_all()
@@ -352,6 +362,7 @@ class TensorProducer:
                             self._consumers[m.consumer_id].bcast = conn
                         else:
                             self._bcast_pending[m.consumer_id] = conn
+                        self._cver += 1
                         self._lock.notify_all()
 
             def on_close(conn=conn, state=state):
@@ -359,6 +370,7 @@ class TensorProducer:
                     cid = state["cid"]
                     if cid == MONITOR_ID and conn in self._monitors:
                         self._monitors.remove(conn)
+                        self._cver += 1
                     elif cid is not None and cid in self._consumers and \
                             self._consumers[cid].bcast is conn:
                         self._drop(cid, "disconnect")
@@ -552,6 +564,7 @@ class TensorProducer:
                         conn.send(anns[k])
         except OSError:
             self._drop(cid, "disconnect")
+        self._cver += 1
         self._lock.notify_all()
         return cid
 
@@ -590,6 +603,7 @@ class TensorProducer:
         for c in (rec.conn, rec.bcast if close_bcast else None):
             if c is not None:
                 c.close()
+        self._cver += 1
         self._lock.notify_all()
 
     def _sweep_loop(self) -> None:
@@ -616,6 +630,7 @@ class TensorProducer:
                 c.send_raw(data)
             except OSError:
                 self._monitors.remove(c)
+                self._cver += 1
 
     def _admitted(self):
         return [r for r in self._consumers.values() if r.admitted]
@@ -680,6 +695,7 @@ class TensorProducer:
             self._epoch_started = True
             self._announced_in_epoch = 0
             self._retained.clear()
+            self._cver += 1
             window = retention_window(self._fraction, L)
             if window > 0 and self._rings:
                 for ring in self._rings.values():
@@ -691,11 +707,131 @@ class TensorProducer:
         if self._retention_active:
             for ring in self._rings.values():
                 ring.evict(self._retention_cursor)
+            self._cver += 1
         self._retention_active = False
+
+    # -- the one-GPU device-loader fast path ------------------------------------
+    def _fast_ok(self) -> bool:
+        return (self._device_loader and not self._multi and self._ring is not None and
+                self._ring.host_control)
+
+    def _fast_refresh(self) -> None:
+        """Push the consumer lists to the native path (caller holds the lock)."""
+        admitted = self._admitted()
+        ack_ids = [r.consumer_id for r in admitted if not r.batch_size]
+        live = [r.cursor for r in admitted]
+        if self._retention_active:
+            live.append(self._retention_cursor)
+        fds, owner = [], {}
+        for r in self._consumers.values():
+            if r.bcast is not None and not r.bcast.closed:
+                fd = r.bcast.sock.fileno()
+                if fd >= 0:
+                    fds.append(fd)
+                    owner[fd] = r.consumer_id
+        for c in self._monitors:
+            fd = c.sock.fileno()
+            if fd >= 0:
+                fds.append(fd)
+                owner[fd] = c
+        self._facade.set_consumers(ack_ids, live, fds)
+        self._facade_fds = owner
+        self._fast_ids = [r.consumer_id for r in admitted]
+        self._fast_live = live
+        self._facade_ver = self._cver
+
+    def _publish_fast(self, index: int) -> None:
+        """_publish for one GPU and a CollateLoader-style device loader: the flow
+        gate, the fused launch (+ CRC) and the Announce of each batch run in
+        native code (hub.Facade); Python keeps the ledger and admission."""
+        import torch
+
+        from .hub import Facade
+
+        ld, ring = self._loader, self._ring
+        L = len(ld)
+        q = seq_of(self._epoch, index, L)
+        with self._lock:
+            self._lock.wait_for(lambda: self._admitted() or self._closed)
+            if self._closed:
+                raise ProducerClosed("producer closed")
+            if self._facade is None:
+                self._facade = Facade()
+            if self._facade_epoch != self._epoch:
+                a = ld.produce_args(self._epoch, with_crc=self._crc if self._checksum else None)
+                a.gate = GATE_HOST
+                in_dt, in_shape = ld.input_dtype, tuple(ld.input_shape)
+                tg_dt, tg_shape = ld.target_dtype, tuple(ld.target_shape)
+                in_bytes, nbytes = ld.input_nbytes, ld.batch_nbytes
+                self._hdr_reserved = sg.pack_pair_reserved(int(in_dt), len(in_shape), int(tg_dt),
+                                                           len(tg_shape), in_bytes)
+                self._hdr_key = (int(in_dt), in_shape, int(tg_dt), tg_shape, in_bytes, nbytes)
+                self._fast_meta = (nbytes, (*in_shape, *tg_shape))
+                header = sg.pack_header(self._epoch, 0, DType.U8, (nbytes,), nbytes, 0,
+                                        reserved=self._hdr_reserved,
+                                        extra_slots=(*in_shape, *tg_shape))
+                self._facade.set_batch(self._hub, ring, a, self._stream, self._depth,
+                                       self._ring_ids[0], header, nbytes,
+                                       self._crc if self._checksum else None,
+                                       self._crc_host if self._checksum else None,
+                                       self._events)
+                self._facade_epoch = self._epoch
+            if self._facade_ver != self._cver:
+                self._fast_refresh()
+        if self._pending_ann is not None and self._pending_ann[0] <= q - self._depth:
+            self._flush_pending()  # (buffer_depth 1: the gate waits for that batch's acks)
+        with torch.cuda.device(self.device):
+            while not self._facade.produce(q, index, self._chain_ok, 0.1):
+                if self._closed:
+                    raise ProducerClosed("producer closed while waiting for consumers")
+                with self._lock:  # evicted / departed consumers leave the gate
+                    if self._facade_ver != self._cver:
+                        self._fast_refresh()
+        self._chain_ok = not self._checksum
+        self._sample_live(q, {0: self._fast_live})
+        cur = (q, index, ring.slot_of(q), self._epoch)
+        if not self._checksum:
+            self._announce_fast(cur, False)
+            return
+        prev, self._pending_ann = self._pending_ann, cur
+        if prev is not None:
+            self._announce_fast(prev, True)
+
+    def _announce_fast(self, p, with_crc: bool) -> None:
+        q, index, slot, epoch = p
+        crc, failed = self._facade.announce(q, epoch, index, with_crc)
+        L = len(self._loader)
+        with self._lock:
+            for fd in failed:
+                who = self._facade_fds.get(fd)
+                if isinstance(who, int):
+                    self._drop(who, "disconnect")
+                elif who in self._monitors:
+                    self._monitors.remove(who)
+                    self._cver += 1
+            self._ledger.add(q, self._fast_ids)
+            self.batches.append((epoch, index, crc))
+            self._announced_in_epoch = index + 1
+            self.stats["announced"] += 1
+            if self._retention_active:  # replayable announces for rubberband joiners
+                nbytes, extra = self._fast_meta
+                header = sg.pack_header(epoch, index, DType.U8, (nbytes,), nbytes, crc,
+                                        reserved=self._hdr_reserved, extra_slots=extra)
+                self._retained[q] = {0: Announce(epoch, index,
+                                                 sg.slot_name(self._ring_ids[0], slot, header),
+                                                 nbytes, DType.U8, (nbytes,), crc)}
+                if self._announced_in_epoch >= retention_window(self._fraction, L):
+                    self._drop_retention()
+            self._since_drain += 1
+            if self._since_drain >= 16:  # wire Acks fold into the ledger in bulk
+                self._since_drain = 0
+                self._drain_acks()
 
     def _publish(self, index: int, batch) -> None:
         import torch
 
+        if self._fast_ok():
+            return self._publish_fast(index)
         L = len(self._loader)
         q = seq_of(self._epoch, index, L)
         if self._device_loader:
@@ -799,6 +935,9 @@ class TensorProducer:
 
     def _announce_crc(self, p) -> None:
         """Announce a batch whose device CRC-32 was enqueued (waits for it)."""
+        if len(p) == 4:  # enqueued by the native fast path
+            self._announce_fast(p, True)
+            return
         slot = p[2]
         self._events[slot].synchronize()
         self._announce(p, int(self._crc_host[slot]) & 0xFFFFFFFF)
@@ -976,6 +1115,7 @@ class TensorProducer:
                 c.send_raw(data[0])
             except OSError:
                 self._monitors.remove(c)
+                self._cver += 1
 
     # -- shutdown ---------------------------------------------------------------
     def join(self, drain_timeout_s: float = 10.0) -> None:
@@ -1014,6 +1154,12 @@ class TensorProducer:
                 c.close()
             self._lock.notify_all()
 
+    @property
+    def drift_max(self) -> int:
+        """Largest wire-ack spread between admitted consumers seen so far
+        (SPEC.md:524): the hub samples it at every Ack, the ledger at every drain."""
+        return max(self._ledger.drift_max, self._hub.drift_max())
+
     def close(self) -> None:
         """Release the device ring (after join()).  Consumers must be gone."""
         self.join(0.0)
@@ -1021,6 +1167,9 @@ class TensorProducer:
             st.synchronize()
         with self._lock:  # the sweeper drains the hub under the same lock
             self._hub.close()
+            if self._facade is not None:
+                self._facade.close()
+                self._facade = None
         for d, ring in self._rings.items():
             _RINGS.pop(self._ring_ids[d], None)
             ring.close()
