@@ -446,6 +446,10 @@ int tsb_facade_set_consumers(tsb_facade *f, const uint64_t *ack_ids, int n_ack, 
 int tsb_facade_produce(tsb_facade *f, uint64_t seq, int64_t index, int chain, int64_t timeout_us);
 int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t index,
                         int with_crc, uint32_t *crc_out, int *failed);
+/* produce(seq) then, if ann_seq != 0, announce(ann_seq): one call per batch. */
+int tsb_facade_step(tsb_facade *f, uint64_t seq, int64_t index, int chain, int64_t timeout_us,
+                    uint64_t ann_seq, uint32_t ann_epoch, uint64_t ann_index, int ann_with_crc,
+                    uint32_t *crc_out, int *failed);
 
 #ifdef __cplusplus
 }

@@ -187,6 +187,8 @@ SIGNATURES["tsb_facade_set_batch"] = (i32, [vp, vp, vp, ctypes.POINTER(ProduceAr
 SIGNATURES["tsb_facade_set_consumers"] = (i32, [vp, ctypes.POINTER(u64), i32, ctypes.POINTER(i32),
                                                 i32, ctypes.POINTER(i32), i32])
 SIGNATURES["tsb_facade_produce"] = (i32, [vp, u64, i64, i32, i64])
+SIGNATURES["tsb_facade_step"] = (i32, [vp, u64, i64, i32, i64, u64, ctypes.c_uint32, u64, i32,
+                                       ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(i32)])
 SIGNATURES["tsb_facade_announce"] = (i32, [vp, u64, ctypes.c_uint32, u64, i32,
                                            ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(i32)])
 SIGNATURES["tsb_wire_encode"] = (i32, [ctypes.POINTER(Msg), vp, sz, ctypes.POINTER(sz)])

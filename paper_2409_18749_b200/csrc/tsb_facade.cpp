@@ -184,4 +184,12 @@ int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t in
     return TSB_OK;
 }
 
+int tsb_facade_step(tsb_facade *f, uint64_t seq, int64_t index, int chain, int64_t timeout_us,
+                    uint64_t ann_seq, uint32_t ann_epoch, uint64_t ann_index, int ann_with_crc,
+                    uint32_t *crc_out, int *failed) {
+    if (int rc = tsb_facade_produce(f, seq, index, chain, timeout_us)) return rc;
+    if (!ann_seq) return TSB_OK;
+    return tsb_facade_announce(f, ann_seq, ann_epoch, ann_index, ann_with_crc, crc_out, failed);
+}
+
 }  // extern "C"

@@ -137,6 +137,11 @@ def collate_augment_fanout(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoc
          arr, len(dsts), current_stream(stream))
 
 
+def stream_sync(handle: int) -> None:
+    """cudaStreamSynchronize on a raw stream handle (no torch objects)."""
+    call("tsb_stream_sync", ctypes.c_void_p(handle))
+
+
 def crc32(data, nbytes: int, d_out, stream=None) -> None:
     """CRC-32/IEEE of device bytes into a device uint32 (wire.py:170-172)."""
     call("tsb_crc32", ptr(data), nbytes, ptr(d_out), None, current_stream(stream))
@@ -163,7 +168,7 @@ def rebatch_gather(ring_base, ring_samples: int, sample_bytes: int, first: int, 
 
 
 __all__ = [
-    "OUT_U8", "OUT_F32", "OUT_BF16", "ptr", "mix64", "derive_key", "permutation",
+    "OUT_U8", "OUT_F32", "OUT_BF16", "stream_sync", "ptr", "mix64", "derive_key", "permutation",
     "epoch_order", "norm_consts", "fill_synthetic", "make_store", "gather", "aug_params",
     "collate_augment", "collate_augment_fanout", "crc32", "fanout", "rebatch_gather",
     "rebatch_window",

@@ -147,6 +147,22 @@ class Facade:
         _lib.check(rc, "tsb_facade_produce")
         return True
 
+    def step(self, seq: int, index: int, chain: bool, timeout_s: float, ann=None,
+             with_crc: bool = False):
+        """produce(seq) + announce(ann = (seq, epoch, index)) in one call:
+        None when the flow gate timed out (nothing was produced), else
+        (crc, failed fds) of the announce (or (0, []) with no announce)."""
+        aq, ae, ai = ann if ann is not None else (0, 0, 0)
+        rc = self._L.tsb_facade_step(self._h, seq, index, int(chain), int(timeout_s * 1e6), aq, ae,
+                                     ai, int(with_crc), ctypes.byref(self._crc), self._failed)
+        if rc == _lib.TSB_ERR_STALE:
+            return None
+        _lib.check(rc, "tsb_facade_step")
+        if ann is None:
+            return 0, []
+        failed = [fd for i, fd in enumerate(self.fds) if self._failed[i]] if self.fds else []
+        return self._crc.value, failed
+
     def announce(self, seq: int, epoch: int, index: int, with_crc: bool):
         """-> (crc, [fds whose send failed])."""
         _lib.check(self._L.tsb_facade_announce(self._h, seq, epoch, index, int(with_crc),

@@ -780,26 +780,39 @@ class TensorProducer:
                 self._fast_refresh()
         if self._pending_ann is not None and self._pending_ann[0] <= q - self._depth:
             self._flush_pending()  # (buffer_depth 1: the gate waits for that batch's acks)
-        with torch.cuda.device(self.device):
-            while not self._facade.produce(q, index, self._chain_ok, 0.1):
-                if self._closed:
-                    raise ProducerClosed("producer closed while waiting for consumers")
-                with self._lock:  # evicted / departed consumers leave the gate
-                    if self._facade_ver != self._cver:
-                        self._fast_refresh()
+        cur = (q, index, ring.slot_of(q), self._epoch)
+        # announce in the same native call: this batch (no checksum), or the
+        # previous one, whose CRC was enqueued before this batch's launch
+        ann = cur if not self._checksum else self._pending_ann
+        import contextlib
+
+        here = torch.cuda.current_device() == self.device  # (the usual case: no switch)
+        while True:
+            with contextlib.nullcontext() if here else torch.cuda.device(self.device):
+                res = self._facade.step(q, index, self._chain_ok, 0.1,
+                                        None if ann is None else (ann[0], ann[3], ann[1]),
+                                        self._checksum)
+            if res is not None:
+                break
+            if self._closed:
+                raise ProducerClosed("producer closed while waiting for consumers")
+            with self._lock:  # evicted / departed consumers leave the gate
+                if self._facade_ver != self._cver:
+                    self._fast_refresh()
         self._chain_ok = not self._checksum
         self._sample_live(q, {0: self._fast_live})
-        cur = (q, index, ring.slot_of(q), self._epoch)
-        if not self._checksum:
-            self._announce_fast(cur, False)
-            return
-        prev, self._pending_ann = self._pending_ann, cur
-        if prev is not None:
-            self._announce_fast(prev, True)
+        if self._checksum:
+            self._pending_ann = cur
+        if ann is not None:
+            self._announced_fast(ann, *res)
 
     def _announce_fast(self, p, with_crc: bool) -> None:
         q, index, slot, epoch = p
-        crc, failed = self._facade.announce(q, epoch, index, with_crc)
+        self._announced_fast(p, *self._facade.announce(q, epoch, index, with_crc))
+
+    def _announced_fast(self, p, crc: int, failed) -> None:
+        """Bookkeeping of an Announce the native path sent."""
+        q, index, slot, epoch = p
         L = len(self._loader)
         with self._lock:
             for fd in failed:
