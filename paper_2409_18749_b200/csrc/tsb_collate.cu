@@ -1172,91 +1172,127 @@ __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t *p) {
     return v;
 }
 
+// min over the live release cursors (host-shared, PCIe reads), wrap-around order
+__device__ __forceinline__ uint64_t min_live_cursor(const PersistArgs &a, uint64_t need) {
+    uint64_t lo = need + (1ull << 61);
+    for (int j = 0; j < a.n_live; ++j) {
+        const uint64_t c = ld_acquire_sys_u64(a.cursors + a.live[j]);
+        if ((int64_t)(c - lo) < 0) lo = c;
+    }
+    return lo;
+}
+
+// The range is one stream of work items (batch i, 16 KB chunk c), i-major,
+// strided over the grid: CTAs do not wait for each other at batch boundaries,
+// so small batches (C5 LLM: 128 items of 2 MB per batch on 296 CTAs) from
+// consecutive slots are copied concurrently and the range runs at copy
+// speed.  Per item: the slot gate (a shared cached level; CTA thread 0 polls
+// the gate word / the host-shared cursors only when the level is behind),
+// the copy, a barrier, then ONE thread -- rotating over the warps, so no warp
+// carries it every item -- fences (cumulative over the barrier-ordered
+// stores) and counts the item; the item that completes a batch publishes the
+// slot (st.release.sys of the ready word).  The next item's copy overlaps
+// that fence + atomic.
 template <bool SYNTH>
 __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(PersistArgs a) {
     const int tid = threadIdx.x;
     const int chunks = (int)((a.sb + PT_CHUNK - 1) / PT_CHUNK);
-    const int items = (int)a.b * chunks;
+    const int ipb = (int)a.b * chunks;  // items per batch
+    const int64_t total = (int64_t)ipb * a.n;
     const int64_t nvec = a.sb >> 4;
     constexpr int U = PT_CHUNK / 16 / PT_THREADS;
-    uint64_t known = 0;  // thread 0: every live cursor is known to have released `known`
-    for (int i = 0; i < a.n; ++i) {
+    __shared__ uint64_t s_known;  // every live cursor is known to have released this level
+    if (tid == 0) s_known = 0;
+    __syncthreads();
+    int turn = 0;
+    for (int64_t g = blockIdx.x; g < total; g += gridDim.x, ++turn) {
+        const int i = (int)(g / ipb);
+        const int it = (int)(g - (int64_t)i * ipb);
         const uint64_t q = a.seq0 + (uint64_t)i;
         const int slot = (int)((q - 1) % (uint64_t)a.slots);
-        if (tid == 0 && q > (uint64_t)a.slots) {
-            // CTA 0 alone reads the host-shared cursors (a PCIe round trip) and
-            // publishes the verified release level in a device word; the other
-            // CTAs wait on that word in L2 -- no flood of host reads
-            const uint64_t need = q - (uint64_t)a.slots;
-            while ((int64_t)(known - need) < 0) {
-                if (blockIdx.x == 0) {
-                    uint64_t lo = need + (1ull << 61);
-                    for (int j = 0; j < a.n_live; ++j) {
-                        const uint64_t c = ld_acquire_sys_u64(a.cursors + a.live[j]);
-                        if ((int64_t)(c - lo) < 0) lo = c;  // min under wrap-around order
-                    }
-                    if ((int64_t)(lo - need) >= 0) {
-                        atomicMax(a.gate, (unsigned long long)lo);
-                        known = lo;
-                    } else {
-                        __nanosleep(500);
-                    }
-                } else {
-                    uint64_t g;
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(g) : "l"(a.gate)
+        if (q > (uint64_t)a.slots && (int64_t)(s_known - (q - (uint64_t)a.slots)) < 0) {
+            // (uniform: s_known only changes between these two barriers)
+            __syncthreads();
+            if (tid == 0) {
+                const uint64_t need = q - (uint64_t)a.slots;
+                uint64_t known = s_known;
+                while ((int64_t)(known - need) < 0) {
+                    uint64_t gw;  // the level CTA 0 verified (an L2 read)
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw) : "l"(a.gate)
                                  : "memory");
-                    known = g;
-                    if ((int64_t)(known - need) < 0) __nanosleep(100);
+                    if ((int64_t)(gw - known) > 0) known = gw;
+                    if ((int64_t)(known - need) >= 0) break;
+                    if (blockIdx.x == 0) {  // CTA 0 alone reads the host-shared cursors (PCIe)
+                        const uint64_t lo = min_live_cursor(a, need);
+                        if ((int64_t)(lo - known) > 0) {
+                            known = lo;
+                            atomicMax(a.gate, (unsigned long long)lo);
+                        }
+                    }
+                    if ((int64_t)(known - need) < 0) __nanosleep(blockIdx.x == 0 ? 200 : 100);
                 }
+                s_known = known;
             }
+            __syncthreads();
         }
-        __syncthreads();  // the slot is free for this CTA's stores
         const int64_t *idx = a.order + (a.batch0 + i) * a.b;
         uint8_t *out = a.ring_base + (int64_t)slot * a.slot_stride;
-        if (blockIdx.x == 0 && a.with_target) {
+        if (it == 0 && a.with_target) {
             int64_t *tgt = reinterpret_cast<int64_t *>(out + a.input_bytes);
             for (int k = tid; k < a.b; k += PT_THREADS) tgt[k] = idx[k];
         }
-        for (int it = blockIdx.x; it < items; it += gridDim.x) {
-            const int sidx = it / chunks, c = it - sidx * chunks;
-            const int64_t v0 = (int64_t)c * (PT_CHUNK / 16);
-            const int64_t v1 = min(v0 + PT_CHUNK / 16, nvec);
-            const uint64_t key = SYNTH ? derive_key(a.seed, a.epoch, (uint64_t)idx[sidx]) : 0;
-            const uint8_t *in = SYNTH ? nullptr : a.src + idx[sidx] * a.sb;
-            uint8_t *o = out + (int64_t)sidx * a.sb;
-            uint4 v[U];
+        const int sidx = it / chunks, c = it - sidx * chunks;
+        const int64_t v0 = (int64_t)c * (PT_CHUNK / 16);
+        const int64_t v1 = min(v0 + PT_CHUNK / 16, nvec);
+        const uint64_t key = SYNTH ? derive_key(a.seed, a.epoch, (uint64_t)idx[sidx]) : 0;
+        const uint8_t *in = SYNTH ? nullptr : a.src + idx[sidx] * a.sb;
+        uint8_t *o = out + (int64_t)sidx * a.sb;
+        uint4 v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t k = v0 + tid + u * PT_THREADS;
-                if (k < v1) {
-                    if constexpr (SYNTH) {
-                        const uint64_t w0 = mix64(key + (uint64_t)(2 * k + 1) * GAMMA);
-                        const uint64_t w1 = mix64(key + (uint64_t)(2 * k + 2) * GAMMA);
-                        v[u] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1,
-                                          (uint32_t)(w1 >> 32));
-                    } else {
-                        v[u] = ld_nc_v4(in + 16 * k);
-                    }
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = v0 + tid + u * PT_THREADS;
+            if (k < v1) {
+                if constexpr (SYNTH) {
+                    const uint64_t w0 = mix64(key + (uint64_t)(2 * k + 1) * GAMMA);
+                    const uint64_t w1 = mix64(key + (uint64_t)(2 * k + 2) * GAMMA);
+                    v[u] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1,
+                                      (uint32_t)(w1 >> 32));
+                } else {
+                    v[u] = ld_nc_v4(in + 16 * k);
                 }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t k = v0 + tid + u * PT_THREADS;
-                if (k < v1) st_v4(o + 16 * k, v[u]);
-            }
         }
-        // batch i done by this CTA: the last CTA publishes the slot (barrier,
-        // then one cumulative fence -- as publish_epilogue)
-        __syncthreads();
-        if (tid == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = v0 + tid + u * PT_THREADS;
+            if (k < v1) st_v4(o + 16 * k, v[u]);
+        }
+        __syncthreads();  // this item's stores are issued by every thread
+        if (tid == 32 * (turn % (PT_THREADS / 32))) {
             __threadfence();
             const unsigned int prev = atomicAdd(a.counters + slot, 1u);
-            if (prev == gridDim.x - 1) {
+            if (prev == (unsigned int)ipb - 1) {  // the batch's last item: publish the slot
                 a.counters[slot] = 0u;
                 __threadfence_system();
                 asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.ready + slot), "l"(q)
                              : "memory");
             }
+        }
+    }
+    // CTA 0 keeps the gate level moving until the range's last batch is out:
+    // other CTAs may still wait on it after CTA 0 ran out of items
+    if (blockIdx.x == 0 && tid == 0 && a.n > 0) {
+        const uint64_t q_last = a.seq0 + (uint64_t)a.n - 1;
+        const int last_slot = (int)((q_last - 1) % (uint64_t)a.slots);
+        uint64_t known = s_known;
+        while (ld_acquire_sys_u64(a.ready + last_slot) != q_last) {
+            const uint64_t need = q_last > (uint64_t)a.slots ? q_last - (uint64_t)a.slots : 0;
+            const uint64_t lo = min_live_cursor(a, need);
+            if ((int64_t)(lo - known) > 0) {
+                known = lo;
+                atomicMax(a.gate, (unsigned long long)lo);
+            }
+            __nanosleep(500);
         }
     }
 }

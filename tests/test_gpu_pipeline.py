@@ -317,3 +317,48 @@ def test_ring_operations_leave_the_current_device_alone():
     s.synchronize()
     assert torch.cuda.current_device() == before
     ring.close()
+
+
+def test_persistent_producer_pipelines_small_batches(oracle):
+    """C5 LLM shape through the persistent producer: many small batches whose
+    work items run concurrently across slots (no grid-wide batch boundary);
+    with only 4 slots every reuse is gated on the host consumer's release.
+    Each batch is checked (CRC of the slot before releasing it) against the
+    oracle's synthetic fill of the same indices (bs/pipeline.py:183-189)."""
+    import threading
+    import zlib
+
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    N, B, n = 1 << 14, 256, 48
+    ld = CollateLoader(DatasetSpec(SyntheticSource(3, (2048,), DType.I32), N, B, shuffle_seed=4))
+    ring = DeviceRing(4, ld.batch_nbytes, 1, control="host")
+    ring.set_cursor(0, 0)
+    got = {}
+
+    def consumer():
+        for q in range(1, n + 1):
+            s = ring.slot_of(q)
+            ring.host_wait_ready(s, q, timeout_s=60)
+            v = ring.view(s, (ld.batch_nbytes,), torch.uint8).cpu().numpy()
+            got[q] = (zlib.crc32(v[:ld.input_nbytes].tobytes()),
+                      v[ld.input_nbytes:].view(np.int64).copy())
+            ring.host_ack(0, q)
+
+    t = threading.Thread(target=consumer)
+    t.start()
+    a = ld.produce_args(1)
+    a.gate = GATE_HOST
+    a.persistent = 1
+    ps = torch.cuda.Stream()
+    produce_range(ring, a, 1, 0, n, [0], stream=ps)
+    ps.synchronize()
+    t.join(60)
+    assert not t.is_alive() and len(got) == n
+    order = oracle.epoch_order(N, 4, 1)
+    for q in range(1, n + 1):
+        idx = order[(q - 1) * B:q * B]
+        np.testing.assert_array_equal(got[q][1], idx)
+        assert got[q][0] == oracle.crc32(oracle.prepare_synthetic(3, 1, idx, 2048 * 4)), q
+    a.persistent = 0
+    ring.close()

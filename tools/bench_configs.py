@@ -24,10 +24,30 @@ sys.path.insert(0, ROOT)
 
 from bench import host_consumer  # noqa: E402
 
-REF = {  # reference CPU path, shared mode, aggregate delivered samples/s
-    "c1": 8941, "c2_shape_u8": 18629, "c3_shape_u8_k8": 37493, "c5_llm_k8": 422972,
-    "c5_video_k8": 8928,
-}
+# the UNMODIFIED reference (baseline/_ref, run_scenario shared mode) on the GPU
+# box's 16 host cores, aggregate delivered samples/s (profiles/r1/ref_cpu_gpu_host.jsonl)
+REF = {"c1": 19050.7, "c2_shape_u8": 35139.1, "c5_llm_k8": 938897.3, "c5_video_k8": 18014.0}
+REF_SOURCE = "profiles/r1/ref_cpu_gpu_host.jsonl (unmodified reference, 16 host cores)"
+L2_BYTES = 126 * 2**20
+
+
+def hbm_line(r: dict, sample_bytes: int, slots: int, slot_bytes: int, rw: int = 2) -> dict:
+    """Passthrough roofline: each produced sample is read once and written
+    once (rw = 2 x sample_bytes; rw = 1 for the synthetic source, generated
+    in the kernel); the ring must exceed L2 for the writes to reach HBM."""
+    import json as _j
+    import os as _o
+
+    peak = 6532.2
+    try:
+        with open(_o.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = float(_j.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        pass
+    produced = r["value"] / r["consumers"]
+    gbs = produced * rw * sample_bytes / 1e9
+    return {"hbm_alg_gbs": round(gbs, 1), "alg_bytes_per_sample": rw * sample_bytes, "hbm_frac": round(gbs / peak, 4), "hbm_peak_gbs": peak,
+            "ring_bytes": slots * slot_bytes, "ring_exceeds_l2": slots * slot_bytes > L2_BYTES}
 
 
 def device_run(loader, n_consumers, steps, warmup, slots=8, persistent=False):
@@ -153,6 +173,8 @@ def main():
     ap.add_argument("--steps", type=int, default=512)
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--only", default="c1,c2bf16,c5video,c5llm,c4native,c4")
+    ap.add_argument("--slots", type=int, default=8,
+                    help="ring slots for the passthrough configs (C1, C5); > L2 for HBM fractions")
     ap.add_argument("--persistent", action="store_true",
                     help="passthrough configs (C1, C5) as one persistent launch per range")
     args = ap.parse_args()
@@ -169,10 +191,11 @@ def main():
     if "c1" in which:
         store = StoreSource.synthetic(0, N, (224, 224, 3), location="hbm")
         ld = CollateLoader(DatasetSpec(store, N, 64))
-        r = device_run(ld, 2, K, Wm, persistent=args.persistent)
+        r = device_run(ld, 2, K, Wm, slots=args.slots, persistent=args.persistent)
         r.update(config="C1: 224x224x3 u8 passthrough (DirectorySource gather), B=64, 2 consumers"
                  + (" [persistent]" if args.persistent else ""),
-                 reference_cpu=REF["c1"])
+                 reference_cpu=REF["c1"], reference_source=REF_SOURCE,
+                 **hbm_line(r, 150528, args.slots, ld.batch_nbytes))
         print(json.dumps(r), flush=True)
         del store, ld
     if "c2bf16" in which:
@@ -186,16 +209,20 @@ def main():
     if "c5video" in which:
         ld = CollateLoader(DatasetSpec(StoreSource.synthetic(0, 4096, (16, 3, 112, 112)), 4096,
                                        16))
-        r = device_run(ld, 8, K, Wm, persistent=args.persistent)
-        r.update(config="C5 video: (16,3,112,112) u8 clips, B=16, 8 consumers (one GPU)",
-                 reference_cpu=REF["c5_video_k8"])
+        r = device_run(ld, 8, K, Wm, slots=args.slots, persistent=args.persistent)
+        r.update(config="C5 video: (16,3,112,112) u8 clips, B=16, 8 consumers (one GPU)"
+                 + (" [persistent]" if args.persistent else ""),
+                 reference_cpu=REF["c5_video_k8"], reference_source=REF_SOURCE,
+                 **hbm_line(r, 602112, args.slots, ld.batch_nbytes))
         print(json.dumps(r), flush=True)
         del ld
     if "c5llm" in which:
         ld = CollateLoader(DatasetSpec(SyntheticSource(0, (2048,), DType.I32), N, 256))
-        r = device_run(ld, 8, K, Wm, persistent=args.persistent)
+        r = device_run(ld, 8, K, Wm, slots=args.slots, persistent=args.persistent)
         r.update(config="C5 LLM: (2048,) int32 tokens (SyntheticSource on device), B=256, "
-                        "8 consumers (one GPU)", reference_cpu=REF["c5_llm_k8"])
+                        "8 consumers (one GPU)" + (" [persistent]" if args.persistent else ""),
+                 reference_cpu=REF["c5_llm_k8"], reference_source=REF_SOURCE,
+                 **hbm_line(r, 8192, args.slots, ld.batch_nbytes, rw=1))
         print(json.dumps(r), flush=True)
         del ld
     if "jpeg" in which:
