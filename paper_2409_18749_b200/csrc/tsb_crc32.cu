@@ -30,6 +30,8 @@
 //     the full shared address of a lookup from the data byte and a per-lane
 //     constant: 11 instructions and 4 conflict-free LDS per 4 data bytes.
 #include <atomic>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -70,6 +72,7 @@ __device__ uint32_t g_t_tree[TREE_LEVELS * NT];   // x^(8 * T_LANE * 2^k)
 __device__ uint32_t g_t_gap[3 * NT];              // [K-2]: x^(8 * (T_TILE - chain_bytes(K)))
 __device__ uint32_t g_t_half[3 * NT];             // [K-2]: x^(8 * chain_bytes(K))
 __device__ uint32_t g_t_pow[SHIFT_BITS];          // x^(8 * T_TILE * 2^k) mod P (values)
+__device__ uint32_t g_pow8[SHIFT_BITS];           // x^(8 * 2^k) mod P (values): any byte shift
 
 uint32_t h_multmodp(uint32_t a, uint32_t b) {
     uint32_t m = 1u << 31, p = 0;
@@ -133,6 +136,9 @@ int ensure_tables(int dev) {
         h_nibble_table(h_x8n(chain_bytes(k)), t_half + (k - 2) * NT);
     }
     for (int k = 0; k < SHIFT_BITS; ++k) t_pow[k] = h_x8n((uint64_t)T_TILE << k);
+    static uint32_t pow8[SHIFT_BITS];
+    for (int k = 0; k < SHIFT_BITS; ++k) pow8[k] = h_x8n(1ull << k);
+    TSB_CUDA(cudaMemcpyToSymbol(g_pow8, pow8, sizeof(pow8)));
     TSB_CUDA(cudaMemcpyToSymbol(g_t_tree, t_tree, sizeof(t_tree)));
     TSB_CUDA(cudaMemcpyToSymbol(g_t_gap, t_gap, sizeof(t_gap)));
     TSB_CUDA(cudaMemcpyToSymbol(g_t_half, t_half, sizeof(t_half)));
@@ -573,6 +579,198 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// crc_rows_kernel: the message viewed as rows of C bytes (C a multiple of
+// 48), read column tile by column tile with ONE 2D TMA box per warp and
+// stage (96 rows x 48 B): lane l runs three slice-by-4 chains, one per row
+// l, l+32, l+64 of its warp's 96 rows, each over a whole contiguous row --
+// no gap multiplies, three independent chains per lane.
+//   message = head (H < C bytes) || body (R_b rows of C bytes); virtual row
+//   vb0-1 is the head, front-padded with zeros (leading zeros do not change
+//   a raw CRC), rows below it are all-zero, and the body's rows are vb0..;
+//   TMA zero-fills the rows above the tensor (negative coordinates), the
+//   head row comes from a shared copy loaded up front.
+// Shift constants depend on C: x^(8*C*2^k) (k = 0..4: nibble tables built in
+// shared memory at kernel start, for the lane tree; k = 5, 6: the chain
+// combine) and the warp's shift by the bytes after its rows (a lane-parallel
+// product over the set bits of the byte count).
+constexpr int R_ROWS = 96;         // rows per warp (3 chains x 32 lanes)
+constexpr int R_COLS = 48;         // bytes per row per column tile: 3 x 16 B, conflict-free LDS.128
+constexpr int R_BOX = R_ROWS * R_COLS;  // 4608 B per TMA box
+constexpr int R_HEAD_MAX = 16384;  // head row buffer (C <= 16 KB)
+constexpr int R_KTAB = 5;          // lane-tree nibble tables x^(8*C*2^k)
+
+struct RowsLayout {
+    uint32_t tab0, head, ktab, stage0, stage1, bar0, bar1;
+};
+
+__device__ __forceinline__ bool rows_layout(uint32_t base, int wib, RowsLayout &L) {
+    const uint32_t end = base + T_SMEM;
+    L.tab0 = (base + 65535u) & ~65535u;
+    uint32_t lo = base, lo_end = L.tab0, hi = L.tab0 + T_TAB_BYTES;
+    if (hi > end) return false;
+    auto take = [&](uint32_t bytes, uint32_t align, uint32_t &out) {
+        uint32_t a = (lo + align - 1) & ~(align - 1);
+        if (a + bytes <= lo_end) { out = a; lo = a + bytes; return true; }
+        a = (hi + align - 1) & ~(align - 1);
+        if (a + bytes <= end) { out = a; hi = a + bytes; return true; }
+        return false;
+    };
+    bool ok = take(R_HEAD_MAX, 128, L.head) && take(R_KTAB * NT * 4, 16, L.ktab);
+#pragma unroll
+    for (int w = 0; w < T_WARPS; ++w)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            uint32_t a = 0;
+            ok = ok && take(R_BOX, 128, a);
+            if (w == wib) (s ? L.stage1 : L.stage0) = a;
+        }
+#pragma unroll
+    for (int w = 0; w < T_WARPS; ++w)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            uint32_t a = 0;
+            ok = ok && take(8, 8, a);
+            if (w == wib) (s ? L.bar1 : L.bar0) = a;
+        }
+    return ok;
+}
+
+// x^(8*m) mod P by a lane-parallel product over the set bits of m (m < 2^32 lanes' worth)
+__device__ __forceinline__ uint32_t warp_x8m(uint64_t m, int lane) {
+    uint32_t f = (lane < SHIFT_BITS && ((m >> lane) & 1)) ? g_pow8[lane] : 0x80000000u;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) f = d_multmodp(f, __shfl_xor_sync(0xFFFFFFFFu, f, 1 << k));
+    return f;
+}
+
+__global__ void __launch_bounds__(T_THREADS, 1)
+    crc_rows_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t *__restrict__ data,
+                    uint32_t C, uint32_t H, uint32_t vb0, uint32_t rows_virtual, uint32_t *out) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t base = smem_u32(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    RowsLayout L;
+    if (!rows_layout(base, wib, L)) __trap();
+    const uint32_t w = blockIdx.x * T_WARPS + wib;
+    const uint32_t r0 = w * R_ROWS;                       // this warp's first virtual row
+    const bool active = r0 + R_ROWS > (vb0 ? vb0 - 1 : 0);  // holds a non-zero row
+    const int ncol = (int)(C / R_COLS);
+    const int32_t y0 = (int32_t)r0 - (int32_t)vb0;       // tensor row of virtual row r0
+
+    // 1. barriers and the first two boxes
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(L.bar0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(L.bar1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int j, int s) {
+        if (lane == 0) {
+            const uint32_t bar = s ? L.bar1 : L.bar0;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"((uint32_t)R_BOX)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(s ? L.stage1 : L.stage0),
+                "l"(&tmap), "r"(j * R_COLS), "r"(y0), "r"(bar)
+                : "memory");
+        }
+    };
+    if (active) {
+        issue(0, 0);
+        if (ncol > 1) issue(1, 1);
+    }
+    // 2. the head row (virtual row vb0-1), zero-padded at the front, if this warp holds it
+    const bool has_head = H && vb0 >= 1 && vb0 - 1 >= r0 && vb0 - 1 < r0 + R_ROWS;
+    if (has_head) {
+        for (uint32_t p = 16u * lane; p < C; p += 512) {
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (p >= C - H) v = *reinterpret_cast<const uint4 *>(data + (p - (C - H)));
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(L.head + p), "r"(v.x),
+                         "r"(v.y), "r"(v.z), "r"(v.w)
+                         : "memory");
+        }
+    }
+    // 3. slice tables (lane-replicated) + the lane-tree tables x^(8*C*2^k)
+    constexpr int NSL = 4 * 256 / T_THREADS;
+    uint32_t vsl[NSL];
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) vsl[k] = g_slice_tab[tid + k * T_THREADS];
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) {
+        const int e = tid + k * T_THREADS;
+        const int t = e >> 8, i = e & 255;
+        const uint32_t row = L.tab0 + (uint32_t)(t >> 1) * 65536u + (uint32_t)i * 256u +
+                             (uint32_t)(t & 1) * 128u;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) sts_u32(row + (uint32_t)(((l + e) & 31) << 2), vsl[k]);
+    }
+    if (wib == 0) {  // K_k = x^(8*C*2^k): warp 0 builds the 5 nibble tables
+        uint32_t K = warp_x8m(C, lane);
+        for (int k = 0; k < R_KTAB; ++k) {
+            for (int e = lane; e < NT; e += 32)
+                sts_u32(L.ktab + 4u * (k * NT + e), d_multmodp(K, (uint32_t)(e & 15) << (4 * (e >> 4))));
+            K = d_multmodp(K, K);
+        }
+    }
+    __syncthreads();
+    if (!active) return;
+    // 4. constants of the combine: x^(8*C*32), x^(8*C*64), and the shift of
+    //    this warp's rows by the rows after them
+    const uint32_t k32 = warp_x8m((uint64_t)C * 32, lane);
+    const uint32_t k64 = d_multmodp(k32, k32);
+    const uint32_t fw = warp_x8m((uint64_t)C * (rows_virtual - r0 - R_ROWS), lane);
+    const uint32_t b_lo = (L.tab0 & 0xFFFF0000u) | ((uint32_t)lane << 2);
+    const uint32_t b_hi = ((L.tab0 + 65536u) & 0xFFFF0000u) | ((uint32_t)lane << 2);
+    uint32_t ch[3] = {0, 0, 0}, phase = 0;
+    // a chain whose row is the head reads the shared head copy instead of the box
+    const int head_chain = has_head && (int)((vb0 - 1 - r0) & 31) == lane ? (int)((vb0 - 1 - r0) >> 5) : -1;
+    for (int j = 0; j < ncol; ++j) {
+        const int s = j & 1;
+        tile_wait(s ? L.bar1 : L.bar0, (phase >> s) & 1u);
+        phase ^= 1u << s;
+        uint32_t wv[3][12];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t row = (c == head_chain) ? L.head + (uint32_t)(j * R_COLS)
+                                                   : (s ? L.stage1 : L.stage0) +
+                                                         (uint32_t)((32 * c + lane) * R_COLS);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const uint4 q = lds_v4(row + 16u * k);
+                wv[c][4 * k] = q.x;
+                wv[c][4 * k + 1] = q.y;
+                wv[c][4 * k + 2] = q.z;
+                wv[c][4 * k + 3] = q.w;
+            }
+        }
+        __syncwarp();
+        if (j + 2 < ncol) issue(j + 2, s);  // the stage is free: every lane holds its words
+#pragma unroll
+        for (int i = 0; i < 12; ++i)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ch[c] = tile_step(ch[c], wv[c][i], b_lo, b_hi);
+    }
+    // lanes of each chain in row order (row l+1 follows row l: shift by C)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int k = 0; k < TREE_LEVELS; ++k) {
+            const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, ch[c], 1 << k);
+            const uint32_t tk = L.ktab + 4u * k * NT;
+            ch[c] = (lane & (1 << k)) ? mul_nib_s(other, tk) ^ ch[c] : mul_nib_s(ch[c], tk) ^ other;
+        }
+    }
+    if (lane == 0) {
+        // chains: rows 0-31, 32-63, 64-95 of the warp, then the rows after the warp
+        uint32_t c = d_multmodp(ch[0], k64) ^ d_multmodp(ch[1], k32) ^ ch[2];
+        if (r0 + R_ROWS < rows_virtual) c = d_multmodp(c, fw);
+        if (c) atomicXor(out, c);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -610,7 +808,58 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
         TSB_LAUNCH_CHECK();
     }
     if (n == 0) return TSB_OK;
-    static const int force_old = getenv("TSB_CRC_IMPL") && !strcmp(getenv("TSB_CRC_IMPL"), "v1");
+    static const char *impl_env = getenv("TSB_CRC_IMPL");
+    static const int force_old = impl_env && !strcmp(impl_env, "v1");
+    static const int force_tile = impl_env && !strcmp(impl_env, "tile");
+    if (!force_old && !force_tile && n >= (uint64_t)T_TILE * 64 && n % 16 == 0 &&
+        ((uintptr_t)data & 15) == 0 && n < (1ull << 32)) {
+        // rows layout: grid sized so each warp gets >= 4 column tiles
+        const uint64_t per_cta_min = (uint64_t)T_WARPS * R_ROWS * R_COLS * 4;
+        uint64_t grid = (n + per_cta_min - 1) / per_cta_min;
+        if (grid > (uint64_t)sm_count()) grid = (uint64_t)sm_count();
+        if (grid < 1) grid = 1;
+        const uint64_t rows_virtual = grid * T_WARPS * R_ROWS;
+        const uint64_t C = ((n + rows_virtual * R_COLS - 1) / (rows_virtual * R_COLS)) * R_COLS;
+        const uint64_t R_b = n / C, H = n - R_b * C;
+        if (C <= (uint64_t)R_HEAD_MAX && R_b >= 1 && R_b + (H ? 1 : 0) <= rows_virtual) {
+            static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+            if (!encode) {
+                cudaDriverEntryPointQueryResult q;
+                void *fn = nullptr;
+                if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                        cudaSuccess ||
+                    q != cudaDriverEntryPointSuccess) {
+                    cudaGetLastError();
+                    fn = nullptr;
+                }
+                encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+            }
+            CUtensorMap tm;
+            const cuuint64_t dims[2] = {C, R_b};
+            const cuuint64_t strides[1] = {C};
+            const cuuint32_t box[2] = {(cuuint32_t)R_COLS, (cuuint32_t)R_ROWS};
+            const cuuint32_t estr[2] = {1, 1};
+            if (encode &&
+                encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                       const_cast<uint8_t *>(static_cast<const uint8_t *>(data)) + H, dims, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+                static bool r_attr[64] = {false};
+                if (dev < 64 && !r_attr[dev]) {
+                    TSB_CUDA(cudaFuncSetAttribute(crc_rows_kernel,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  T_SMEM));
+                    r_attr[dev] = true;
+                }
+                crc_rows_kernel<<<(unsigned)grid, T_THREADS, T_SMEM, s>>>(
+                    tm, static_cast<const uint8_t *>(data), (uint32_t)C, (uint32_t)H,
+                    (uint32_t)(rows_virtual - R_b), (uint32_t)rows_virtual, d_out);
+                TSB_LAUNCH_CHECK();
+                return TSB_OK;
+            }
+        }
+    }
     {
         const uint64_t zt = (T_TILE - n % T_TILE) % T_TILE;
         const uint64_t n_tiles = (n + zt) / T_TILE;
@@ -661,6 +910,7 @@ namespace tsb {
 void preload_crc32() {
     touch_kernel(crc_init_kernel);
     touch_kernel(crc_kernel);
+    touch_kernel(crc_rows_kernel);
     touch_kernel(crc_tile_kernel<2>);
     touch_kernel(crc_tile_kernel<3>);
     touch_kernel(crc_tile_kernel<4>);
