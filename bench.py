@@ -57,7 +57,9 @@ OUT_BYTES = C * H * W * 4          # f32 NCHW per sample
 ALG_BYTES_PER_SAMPLE = SAMPLE_BYTES + OUT_BYTES  # 752,640 B read + write (collate)
 METRIC = "delivered samples/sec (all consumers)"
 REF_BUDGET_S = 90.0  # reference arm: total CPU seconds the timed + warm-up steps may take
-E2E_BATCHES = 4096  # e2e API leg: fixed window of batches, independent of --steps
+# e2e API leg: a fixed window of batches, independent of --steps
+# (TSB_BENCH_E2E_BATCHES shortens it for profiler runs only)
+E2E_BATCHES = int(os.environ.get("TSB_BENCH_E2E_BATCHES", 4096))
 E2E_WARMUP = 64     # e2e batches before the window (consumer start-up skew)
 E2E_BUFFER_DEPTH = RING_SLOTS - 2  # flow gate of the e2e producer (reference default is 2)
 HOLD_S = 0.004      # value leg: the stream is held while the first batches are enqueued

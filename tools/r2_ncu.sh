@@ -1,21 +1,19 @@
 #!/bin/bash
-# round 2: one ncu --set full capture per kernel of the data plane, plus the bench launch list
+# round 2: one ncu --set full capture per kernel of the data plane (summarised
+# on the box: gpurun copies back <= 64 MiB), plus the bench launch list
 out=gpurun_out/${1:-ncu_r2}; mkdir -p $out
-cap() {  # name regex what n skip
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -s $5 -c 1 \
-      -o $out/full_$1 -f python tools/profile_r2.py $3 $4 > $out/$1.log 2>&1
-}
-cap f32 collate_augment f32 6 2
-cap bf16 collate_augment bf16 6 2
-cap u8 collate_augment u8 6 2
-cap passthrough passthrough_multi passthrough 6 2
-cap llm passthrough_multi llm 6 2
-cap llm_persistent persistent_passthrough llm_persistent 64 0
-cap video passthrough_multi video 6 2
-cap rebatch rebatch_window rebatch 4 1
-cap fanout fanout_v16 fanout 4 1
-cap twostage_gather passthrough_multi twostage 6 2
-cap twostage_collate collate_augment twostage 6 2
-cap crc crc_tile crc 4 1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-    --log-file $out/launches_bench.csv python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $out/bench_under_ncu.log 2>&1
+shift
+targets=${@:-"f32 bf16 u8 passthrough llm llm_persistent video rebatch fanout twostage_gather twostage_collate crc"}
+declare -A K=( [f32]=collate_augment [bf16]=collate_augment [u8]=collate_augment [passthrough]=passthrough_multi
+  [llm]=passthrough_multi [llm_persistent]=persistent_passthrough [video]=passthrough_multi [rebatch]=rebatch_window
+  [fanout]=fanout_v16 [twostage_gather]=passthrough_multi [twostage_collate]=collate_augment [crc]=crc_ )
+declare -A W=( [twostage_gather]=twostage [twostage_collate]=twostage )
+declare -A N=( [llm_persistent]="64 0" [rebatch]="4 1" [fanout]="4 1" [crc]="4 1" )
+for t in $targets; do
+  what=${W[$t]:-$t}; ns=${N[$t]:-"6 2"}; n=${ns% *}; skip=${ns#* }
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:${K[$t]} -s $skip -c 1 \
+      -o /tmp/full_$t -f python tools/profile_r2.py $what $n > $out/$t.log 2>&1
+  python tools/ncu_summary.py /tmp/full_$t.ncu-rep 20 > $out/ncu_full_$t.txt 2>&1
+  ncu -i /tmp/full_$t.ncu-rep --page raw --csv > $out/raw_$t.csv 2>/dev/null
+  rm -f /tmp/full_$t.ncu-rep
+done
