@@ -810,8 +810,11 @@ int tsb_crc32(const void *data, size_t n, uint32_t *d_out, void *d_workspace, vo
     if (n == 0) return TSB_OK;
     static const char *impl_env = getenv("TSB_CRC_IMPL");
     static const int force_old = impl_env && !strcmp(impl_env, "v1");
-    static const int force_tile = impl_env && !strcmp(impl_env, "tile");
-    if (!force_old && !force_tile && n >= (uint64_t)T_TILE * 64 && n % 16 == 0 &&
+    // the row-layout kernel is an A/B candidate (TSB_CRC_IMPL=rows): its 48-byte
+    // column boxes read each row in short strided pieces (12% DRAM over-fetch,
+    // 49.8 us vs the tile kernel's 42.8 us for 154 MB: profiles/r2/crc_impl_ab.jsonl)
+    static const int use_rows = impl_env && !strcmp(impl_env, "rows");
+    if (use_rows && n >= (uint64_t)T_TILE * 64 && n % 16 == 0 &&
         ((uintptr_t)data & 15) == 0 && n < (1ull << 32)) {
         // rows layout: grid sized so each warp gets >= 4 column tiles
         const uint64_t per_cta_min = (uint64_t)T_WARPS * R_ROWS * R_COLS * 4;
