@@ -62,6 +62,7 @@ REF_BUDGET_S = 90.0  # reference arm: total CPU seconds the timed + warm-up step
 E2E_BATCHES = int(os.environ.get("TSB_BENCH_E2E_BATCHES", 4096))
 E2E_WARMUP = 64     # e2e batches before the window (consumer start-up skew)
 E2E_BUFFER_DEPTH = RING_SLOTS - 2  # flow gate of the e2e producer (reference default is 2)
+CHECKSUM = True     # per-batch CRC-32 in the timed producer (--checksum)
 HOLD_S = 0.004      # value leg: the stream is held while the first batches are enqueued
 NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
 WORKLOAD = ("C2: 1 producer + 4 same-GPU consumers via CUDA IPC zero copy, 224x224x3 u8 store "
@@ -362,6 +363,11 @@ def run_ours(args):
     stream = torch.cuda.Stream()
     live = list(range(N_CONSUMERS))
     L = len(loader)
+    # the reference checksums every segment it creates (bs/payload.py:218): the
+    # per-batch CRC-32 (input + target) is fused into the collate kernel and
+    # lands in d_crc[slot] before the slot is published
+    d_crc = (torch.zeros(RING_SLOTS, dtype=torch.int32, device=f"cuda:{dev}")
+             if CHECKSUM and world == 1 else None)
 
     def chunks(seq0, n):
         done = 0
@@ -385,7 +391,7 @@ def run_ours(args):
             feeder = threading.Thread(target=stage1, args=(seq0, n, s1))
             feeder.start()
         for q0, epoch, bi, m in chunks(seq0, n):
-            a = loader.produce_args(epoch)
+            a = loader.produce_args(epoch, with_crc=d_crc)
             a.gate = GATE_HOST  # gate on the host-shared cursors; PDL-chained kernels
             if world == 1:
                 produce_range(ring, a, q0, bi, m, live, stream=stream)
@@ -424,7 +430,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = t0.elapsed_ms(t1)
     hold.close()
-    parity = check_ring_parity(ring, loader, Wm + K, dp) if world == 1 else None
+    parity = check_ring_parity(ring, loader, Wm + K, dp, d_crc) if world == 1 else None
     bf16 = bf16_line(dev, store, ds, K, Wm) if world == 1 else None
     consumer_rates = {}
     for _ in procs:
@@ -463,7 +469,7 @@ def run_ours(args):
                     # the measured peak is a best-of-10 torch copy; the HGX spec figure
                     # (B200_PROFILING.md) for comparison
                     "spec_peak_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4),
-                    "kernel": "collate_augment_kernel<f32,C=3>",
+                    "kernel": ("collate_crc_kernel<f32,C=3> (collate + fused batch CRC-32)" if CHECKSUM else "collate_augment_kernel<f32,C=3>"),
                     "alg_bytes_per_launch": B * ALG_BYTES_PER_SAMPLE,
                     "avg_launch_ms": round(avg_launch_ms, 5), "peak_source": peak_src}
     else:
@@ -509,7 +515,10 @@ def run_ours(args):
                            "blocks, never the stream); fused publish (release store from the "
                            "kernel's last CTA); consecutive batches chained with programmatic "
                            "dependent launch; consumers: host wait + host ack (map-and-ack, "
-                           "bs/cli.py:252-258)"},
+                           "bs/cli.py:252-258)",
+                   "checksum": ("CRC-32 of every batch (input + target, as create_segment, "
+                                "bs/payload.py:218), fused into the collate kernel, in the timed "
+                                "region" if d_crc is not None else "off")},
         "roofline": roofline,
         "e2e": e2e,
         # per step: the collate (N=1, outputs fan-out); the row gather + the
@@ -551,10 +560,11 @@ def oracle_batch_crc(o, epoch: int, bi: int, out_kind: int, nthreads: int) -> in
     return o.crc32(idx.astype(np.int64), o.crc32(out))
 
 
-def check_ring_parity(ring, loader, last_seq: int, dp) -> dict:
+def check_ring_parity(ring, loader, last_seq: int, dp, d_crc=None) -> dict:
     """After the timed region: the device CRC-32 of every batch still in the
     ring (the last `slots` produced) against the oracle's CRC of the same
-    batch (a CRC gate on every run)."""
+    batch (a CRC gate on every run), and the checksum the
+    producer computed for it (fused into the collate) against both."""
     import torch
 
     from oracle import oracle as o
@@ -572,11 +582,17 @@ def check_ring_parity(ring, loader, last_seq: int, dp) -> dict:
         want = oracle_batch_crc(o, epoch, bi, o.OUT_F32, nthreads)
         ready = ring.read_ready(slot)
         ok = ok and got == want and ready == q
-        rows.append({"seq": q, "epoch": epoch, "batch": bi, "crc": f"{got:#010x}",
-                     "oracle": f"{want:#010x}"})
+        row = {"seq": q, "epoch": epoch, "batch": bi, "crc": f"{got:#010x}",
+               "oracle": f"{want:#010x}"}
+        if d_crc is not None:
+            prod = int(d_crc[slot].item()) & 0xFFFFFFFF
+            ok = ok and prod == want
+            row["producer_crc"] = f"{prod:#010x}"
+        rows.append(row)
     return {"ok": ok, "batches_checked": len(rows), "bytes_per_batch": loader.batch_nbytes,
             "how": "device CRC-32 (tsb_crc32) of each resident ring slot = f32 NCHW input + "
-                   "int64 targets, vs the oracle's collate+augment of the same batch",
+                   "int64 targets, vs the oracle's collate+augment of the same batch; "
+                   "producer_crc = the checksum the timed producer computed (fused)",
             "batches": rows}
 
 
@@ -595,6 +611,7 @@ def bf16_line(dev, store, ds, K: int, Wm: int) -> dict:
     ring = DeviceRing(RING_SLOTS, ld.batch_nbytes, 1, device=dev, control="host")
     st = torch.cuda.Stream()
     L = len(ld)
+    d_crc = torch.zeros(RING_SLOTS, dtype=torch.int32, device=f"cuda:{dev}") if CHECKSUM else None
 
     def run(seq0, n):
         done = 0
@@ -602,7 +619,7 @@ def bf16_line(dev, store, ds, K: int, Wm: int) -> dict:
             q0 = seq0 + done
             epoch, bi = divmod(q0 - 1, L)
             m = min(n - done, L - bi)
-            a = ld.produce_args(epoch)
+            a = ld.produce_args(epoch, with_crc=d_crc)
             a.gate = GATE_HOST
             produce_range(ring, a, q0, bi, m, [], stream=st)
             done += m
@@ -628,16 +645,20 @@ def bf16_line(dev, store, ds, K: int, Wm: int) -> dict:
     st.synchronize()
     got = int(crc.item()) & 0xFFFFFFFF
     want = oracle_batch_crc(o, epoch, bi, o.OUT_BF16, os.cpu_count() or 1)
+    prod = (int(d_crc[ring.slot_of(last)].item()) & 0xFFFFFFFF) if d_crc is not None else None
     ring.close()
     alg = B * (SAMPLE_BYTES + C * H * W * 2)
     peak, _ = measured_hbm_peak()
     achieved = alg / (ms / K / 1e3) / 1e9
-    return {"kernel": "collate_augment_kernel<bf16,C=3>", "avg_launch_ms": round(ms / K, 5),
+    return {"kernel": ("collate_crc_kernel<bf16,C=3> (collate + fused batch CRC-32)"
+                       if d_crc is not None else "collate_augment_kernel<bf16,C=3>"),
+            "avg_launch_ms": round(ms / K, 5),
             "delivered_samples_s": round(N_CONSUMERS * B * K / (ms / 1e3), 1),
             "achieved_gbs": round(achieved, 1), "frac": round(achieved / peak, 4),
             "alg_bytes_per_launch": alg,
-            "parity": {"ok": got == want, "crc": f"{got:#010x}", "oracle": f"{want:#010x}",
-                       "seq": last}}
+            "parity": {"ok": got == want and prod in (None, want), "crc": f"{got:#010x}",
+                       "oracle": f"{want:#010x}", "seq": last,
+                       **({"producer_crc": f"{prod:#010x}"} if prod is not None else {})}}
 
 
 def run_e2e(args, ctx, dev, rank, world):
@@ -905,7 +926,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--checksum", default="on", choices=["on", "off"],
+                    help="per-batch CRC-32 in the timed producer (the reference's create_segment "
+                         "checksums every segment)")
     args = ap.parse_args()
+    global CHECKSUM
+    CHECKSUM = args.checksum == "on"
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":

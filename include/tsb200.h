@@ -218,8 +218,8 @@ int tsb_rebatch_window(const void *const *slots, int n_slots, int64_t first, int
 #define TSB_SRC_AUGMENT 0   /* store -> fused collate/augment            */
 #define TSB_SRC_GATHER 1    /* store -> passthrough gather (DirectorySource) */
 #define TSB_SRC_SYNTHETIC 2 /* SplitMix64 generator (SyntheticSource)    */
-/* Staged PCIe ingest for pinned-host stores (copy engine, double-buffered
- * HBM staging; one cudaMemcpyBatchAsync of the batch's sample rows). */
+/* Staged PCIe ingest for pinned-host stores (double-buffered
+ * HBM staging; one gather kernel per batch reads the mapped pinned rows). */
 typedef struct tsb_ingest tsb_ingest;
 int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int depth,
                       tsb_ingest **out);

@@ -501,7 +501,7 @@ class CollateLoader:
 
 
 class _Ingest:
-    """tsb_ingest: staged PCIe ingest (one cudaMemcpyBatchAsync per batch)."""
+    """tsb_ingest: staged PCIe ingest (one gather launch per batch over the mapped pinned store)."""
 
     def __init__(self, device: int, max_batch: int, sample_bytes: int, depth: int = 2):
         import ctypes

@@ -10,8 +10,11 @@
 
 #include <utility>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "tsb_common.cuh"
 
@@ -915,6 +918,8 @@ int launch_ca_c(int c, const uint8_t *src, const int64_t *idx, CaGeom g, int fli
     }
 }
 
+#include "tsb_collate_crc.cuh"
+
 // HBM of the launching device (TMA staging); peer HBM and pinned host memory
 // take the LDG staging path.
 int is_device_memory(const void *p) {
@@ -937,10 +942,16 @@ int is_device_memory(const void *p) {
     return v;
 }
 
+int launch_ca_kind(int c, const uint8_t *s8, const int64_t *d_indices, const CaGeom &g, int flip,
+                   uint64_t aug_mixed, uint64_t epoch, const Norm &norm,
+                   const int32_t *d_params, const Dsts &dsts, size_t smem, cudaStream_t s,
+                   const Epi &ep, int out_kind);
+
 int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, int w, int c,
                    int pad, int flip, uint64_t aug_seed, uint64_t epoch, const float *scale,
                    const float *bias, int out_kind, const int32_t *d_params, const Dsts &dsts,
-                   void *stream, const Epi &ep = Epi{}) {
+                   void *stream, const Epi &ep = Epi{}, uint32_t *crc_out = nullptr,
+                   int *crc_done = nullptr) {
     TSB_CHECK(src && d_indices, "null src/indices");
     TSB_CHECK(b >= 0 && h > 0 && w > 0 && c > 0 && c <= 4, "bad shape b=%lld h=%d w=%d c=%d",
               (long long)b, h, w, c);
@@ -1055,6 +1066,31 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     const uint64_t aug_mixed = mix64(aug_seed ^ AUG_DOMAIN);
     const auto *s8 = static_cast<const uint8_t *>(src);
     auto s = as_stream(stream);
+    if (crc_done) *crc_done = 0;
+    if (crc_out && cc_fusable(g, c, dsts, ep)) {  // the batch CRC-32 from the staged source rows
+        const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
+        int rc = TSB_OK;
+        if (cc_mode_knob() == 2) {  // one kernel: emit + checksum + publish
+            rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
+                                    d_params, dsts, s, ep, crc_out, true, ep.pdl);
+        } else {  // the collate (publishes the slot), then the checksum kernel, chained
+            rc = launch_ca_kind(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params, dsts,
+                                smem, s, ep, out_kind);
+            if (!rc)
+                rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
+                                        d_params, dsts, s, ep, crc_out, false, 1);
+        }
+        if (!rc && crc_done) *crc_done = 1;
+        return rc;
+    }
+    return launch_ca_kind(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params, dsts, smem,
+                          s, ep, out_kind);
+}
+
+int launch_ca_kind(int c, const uint8_t *s8, const int64_t *d_indices, const CaGeom &g, int flip,
+                   uint64_t aug_mixed, uint64_t epoch, const Norm &norm,
+                   const int32_t *d_params, const Dsts &dsts, size_t smem, cudaStream_t s,
+                   const Epi &ep, int out_kind) {
     if (out_kind == TSB_OUT_U8)
         return launch_ca_c<TSB_OUT_U8>(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params,
                                        dsts, smem, s, ep);
@@ -1323,7 +1359,8 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
                             int pdl, void *stream, const int32_t *d_params,
-                            const int64_t *tgt_idx, uint64_t *release) {
+                            const int64_t *tgt_idx, uint64_t *release, uint32_t *crc_out,
+                            int *crc_done) {
     Dsts d{};
     d.p[0] = out;
     d.n = 1;
@@ -1342,7 +1379,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     ep.fence_all = fence_all_knob();
     ep.early_pdl = ca_early_knob();
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
-                          out_kind, d_params, d, stream, ep);
+                          out_kind, d_params, d, stream, ep, crc_out, crc_done);
 }
 
 // One batch shard into n destinations (fan-out), fused target copy + publish:
@@ -1590,6 +1627,10 @@ void preload_collate() {
     preload_ca<TSB_OUT_F32>();
     preload_ca<TSB_OUT_BF16>();
     preload_ca<OUT_BF16_FMA>();
+    preload_cc<TSB_OUT_U8>();
+    preload_cc<TSB_OUT_F32>();
+    preload_cc<TSB_OUT_BF16>();
+    preload_cc<OUT_BF16_FMA>();
     touch_kernel(passthrough_multi_kernel<false, false>);
     touch_kernel(passthrough_multi_kernel<false, true>);
     touch_kernel(passthrough_multi_kernel<true, false>);

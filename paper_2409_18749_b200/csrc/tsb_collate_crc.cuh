@@ -1,0 +1,710 @@
+// Collate/augment with the batch CRC-32 fused in (included by tsb_collate.cu,
+// inside its anonymous namespace: uses CaGeom, Norm, Dsts, Epi, ItemPar,
+// OutTraits, emit_pixels, item_par, write_targets).
+//
+// Replaces create_segment's crc32 over the whole segment (payload.py:218,
+// called per batch by the producer, bs/producer.py and sl/producer.py:311-314)
+// with work done on bytes the collate already holds in shared memory: the
+// separate pass re-read the 154 MB slot from HBM at 1 table lookup per output
+// byte; here the checksum costs ONE conflict-free lookup per output ELEMENT
+// and no extra HBM traffic.
+//
+// The output element of channel c for source byte v is F_c(v) (f32 / bf16 /
+// u8), so by linearity of the raw (zero-init) CRC over GF(2) the checksum of
+// a run of 32 output elements is
+//     raw(run) = XOR_p G_c[v_p][p],   G_c[v][p] = x^(8 E (31-p)) * raw(F_c(v))
+// a table of 256 x 32 words per channel.  Stored as G_c[v][p] at shared
+// address region | v << 8 | half << 7 | p << 2 it is read with ONE PRMT (the
+// data byte straight into address byte 1) and lands in bank p; the lanes of a
+// warp always look up 32 distinct positions p (the pixel order inside a run
+// is rotated per lane), so no lookup ever conflicts.
+//
+// Per CTA (one per SM, 227 KB of shared memory): 14 emit warps (the normal
+// collate), one TMA producer warp, and C checksum warps.  Checksum warp c
+// walks channel c of each staged item: lane r takes output row r (R <= 32
+// rows per item), 32-element runs chained by a constant multiply (x^(8*32E),
+// lane-replicated nibble tables), then shifts its row to the end of the item
+// segment (a lane-specific constant, also nibble tables), and the warp
+// XOR-reduces the 32 rows: raw(segment).  That segment is placed in the slot
+// through a per-segment table W[m][i] = x^(8 (SEGB m + tail)) * e_i (bit i of
+// the segment CRC selects lane i's word; m = segments after it), XORed into
+// a lane accumulator -- no per-segment reduction.  Block 0's checksum warp 0
+// also folds in the int64 target that follows the input.  At the end each
+// checksum warp reduces its accumulator into one device word (atomicXor), and
+// the CTA that completes the batch turns it into the zlib CRC-32 of the slot
+// (data + target) before it releases the ready word.
+//
+// Shared memory: two 64 KB-aligned table regions (region 1: G_0 | G_1,
+// region 2: G_2 | the two nibble tables); the item stages, zero row, barriers
+// and params are placed first-fit around them.
+constexpr int CC_EMIT = 256;       // fused variant: 8 emit warps (7 / 3.5 / 1.75 slots per thread)
+constexpr int CC_MAX_C = 3;
+constexpr int CC_SMEM = 232448;    // the 227 KB opt-in maximum
+constexpr int CC_STAGES = 3;
+constexpr uint32_t CC_IMG_WORDS = 2 * 256 * 64;  // the two table regions (128 KB)
+constexpr int CC_ACC_POOL = 1024;
+__device__ uint32_t g_cc_acc[CC_ACC_POOL];     // per-launch accumulators (zero at rest)
+__device__ unsigned int g_cc_cnt[CC_ACC_POOL]; // per-launch CTA completion counters (zero at rest)
+
+struct CrcFuse {
+    const uint32_t *img;    // CC_IMG_WORDS: the shared image of the two table regions
+    const uint32_t *slice;  // zlib slice-by-4 tables T0..T3 (target checksum)
+    const uint32_t *wtab;   // [nseg][32]
+    const uint32_t *wrun;   // [runs][32]: x^(8*32E*(runs-1-run)) * e_i
+    uint32_t tgt_k[5];      // x^(8 * 8 nl 2^k): the target lanes' tree
+    uint32_t init;          // x^(8 total) * ~0 ^ ~0: the init/xorout term of the slot
+    int nseg;
+    int with_tgt;
+    int tab_c;              // 1: every channel uses table 0 (u8 output: F_c(v) = v)
+    uint32_t *acc;          // this launch's accumulator (the completing CTA resets it)
+    unsigned int *count;    // this launch's CTA completion counter (same)
+    int ncrc;               // checksum warps: C x (w / 32)
+    uint32_t *out;          // the slot's CRC-32
+};
+
+__device__ __forceinline__ uint32_t cc_lds(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t cc_prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+// product with a lane-replicated nibble table: t = table base + lane*4 (entry
+// e of lane l at t + e*256)
+__device__ __forceinline__ uint32_t cc_mul_nib(uint32_t v, uint32_t t) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r ^= cc_lds(t + ((uint32_t)(j * 16) << 8) + (((v >> (4 * j)) & 15u) << 8));
+    return r;
+}
+// a * b mod P (reflected; x^0 = bit 31), 32 branch-free steps
+__device__ __forceinline__ uint32_t cc_multmodp(uint32_t a, uint32_t b) {
+    uint32_t p = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        p ^= b & (0u - ((a >> (31 - i)) & 1u));
+        b = (b >> 1) ^ (0xEDB88320u & (0u - (b & 1u)));
+    }
+    return p;
+}
+__device__ __forceinline__ uint32_t cc_crc_word(const uint32_t *__restrict__ t, uint32_t c,
+                                                uint32_t w) {
+    const uint32_t x = c ^ w;
+    return __ldg(t + 3 * 256 + (x & 0xFFu)) ^ __ldg(t + 2 * 256 + ((x >> 8) & 0xFFu)) ^
+           __ldg(t + 256 + ((x >> 16) & 0xFFu)) ^ __ldg(t + (x >> 24));
+}
+
+// mbarrier wait that sleeps until the phase completes (suspend-time hint):
+// waiting warps do not re-issue the try_wait in a loop and take no issue slots
+__device__ __forceinline__ void cc_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "CCW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra CCW_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x100000u)
+        : "memory");
+}
+
+// Shared layout, identical in every CTA (offsets from the dynamic base).
+struct CcLayout {
+    uint32_t r1, r2;        // shared addresses of the two table regions
+    uint32_t lo_stage, n_lo, hi_stage;  // stages: n_lo at lo_stage, the rest at hi_stage
+    uint32_t zero, bars, par, sel;      // offsets
+};
+__host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, uint32_t rs,
+                                          int nstage, CcLayout &L) {
+    L.r1 = (sbase + 0xFFFFu) & ~0xFFFFu;
+    L.r2 = L.r1 + 0x10000u;
+    uint32_t lo = 0, lo_end = L.r1 - sbase;
+    uint32_t hi = L.r2 + 0x10000u - sbase, hi_end = (uint32_t)CC_SMEM;
+    if (hi > hi_end) return false;
+    auto take = [&](uint32_t bytes, uint32_t align, uint32_t &out) {
+        uint32_t a = (lo + align - 1) & ~(align - 1);
+        if (a + bytes <= lo_end) { out = a; lo = a + bytes; return true; }
+        a = (hi + align - 1) & ~(align - 1);
+        if (a + bytes <= hi_end) { out = a; hi = a + bytes; return true; }
+        return false;
+    };
+    bool ok = take((2 * nstage + 1) * 8, 8, L.bars) &&
+              take(META_CAP * (uint32_t)sizeof(ItemPar), 16, L.par) && take(rs, 128, L.zero) &&
+              take(8 * 3 * 32 * 4, 16, L.sel);
+    // stages: as many as fit below region 1, the rest above region 2
+    L.n_lo = 0;
+    L.lo_stage = (lo + 127) & ~127u;
+    const uint32_t below = lo_end > L.lo_stage ? (lo_end - L.lo_stage) / stage_bytes : 0;
+    L.n_lo = below < (uint32_t)nstage ? below : (uint32_t)nstage;
+    L.hi_stage = (hi + 127) & ~127u;
+    const uint32_t need_hi = (uint32_t)nstage - L.n_lo;
+    if (need_hi && L.hi_stage + need_hi * stage_bytes > hi_end) return false;
+    return ok;
+}
+
+// EMIT: the fused variant (8 emit warps write the batch too); else the
+// checksum alone (the collate kernel ran just before, PDL-chained, and
+// published the slot).  Warp layout: [emit warps] producer, then ncrc
+// checksum warps: warp i takes channel i % C and 32-element column run i / C.
+template <int OUT_KIND, int C, bool EMIT>
+__global__ void __launch_bounds__(1024, 1)
+    collate_crc_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx, CaGeom g,
+                       int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
+                       const int32_t *__restrict__ params, Dsts dsts, Epi ep, CrcFuse cf) {
+    using T = OutTraits<OUT_KIND>;
+    constexpr int P = T::P;
+    constexpr int E = T::ELEM;
+    constexpr int NT = EMIT ? CC_EMIT : 0;
+    constexpr int NCW = NT / 32;         // emit warps; warp NCW = producer; then the checksum warps
+    const int ncrc = cf.ncrc;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t stage_bytes = (uint32_t)(g.R * g.rs);
+    CcLayout L;
+    constexpr int NST = CC_STAGES;
+    if (!cc_layout(sbase, stage_bytes, (uint32_t)g.rs, NST, L)) __trap();
+    auto soff = [&](int st) -> uint32_t {
+        return (uint32_t)st < L.n_lo ? L.lo_stage + (uint32_t)st * stage_bytes
+                                      : L.hi_stage + ((uint32_t)st - L.n_lo) * stage_bytes;
+    };
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
+    uint64_t *empty = full + NST;
+    uint64_t *tab_bar = empty + NST;
+    uint32_t *sel_tab = reinterpret_cast<uint32_t *>(smem + L.sel);
+    ItemPar *par = reinterpret_cast<ItemPar *>(smem + L.par);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t *kidx = ep.tgt_idx ? ep.tgt_idx : idx;
+    pdl_launch_dependents();  // the next kernel may launch now (it waits for this SM's smem)
+    const int nk = (g.items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int i0 = (int)blockIdx.x, istep = (int)gridDim.x;
+
+    // zero the stages and the zero row once: borders are never overwritten
+    for (int st = 0; st < NST; ++st) {
+        uint4 *z = reinterpret_cast<uint4 *>(smem + soff(st));
+        for (int i = tid; i < (int)(stage_bytes >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(smem + L.zero);
+        for (int i = tid; i < (g.rs >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    for (int k = tid; k < min(nk, META_CAP); k += blockDim.x)
+        par[k] = item_par(g, i0 + k * istep, idx, kidx, params, aug_mixed, epoch, flip_en);
+    // the checksum warps' byte-gather selectors for each (flip, word misalignment):
+    // byte j of a 4-element group sits at window offset o_j and goes to byte
+    // (j - s_l) & 3 (s_l = lane >> 3: the per-lane rotation of the positions)
+    for (int e = tid; e < 8 * 32; e += blockDim.x) {
+        const int ln = e & 31, combo = e >> 5, fl = combo >> 2, mis = combo & 3;
+        uint32_t s1 = 0, s2 = 0, s3 = 0;
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t o = (uint32_t)(mis + C * (fl ? 3 - j : j));
+            const uint32_t t = (uint32_t)((j - (ln >> 3)) & 3);
+            if (o < 8) {
+                s1 |= o << (4 * t);
+                s3 |= t << (4 * t);
+            } else {
+                s2 |= (o - 8) << (4 * t);
+                s3 |= (4 + t) << (4 * t);
+            }
+        }
+        sel_tab[(combo * 3 + 0) * 32 + ln] = s1;
+        sel_tab[(combo * 3 + 1) * 32 + ln] = s2;
+        sel_tab[(combo * 3 + 2) * 32 + ln] = s3;
+    }
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCW + ncrc);
+        }
+        mbar_init(tab_bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto get_par = [&](int k) -> ItemPar {
+        return k < META_CAP ? par[k]
+                            : item_par(g, i0 + k * istep, idx, kidx, params, aug_mixed, epoch,
+                                       flip_en);
+    };
+
+    if (warp == NCW) {
+        // ---------------- producer warp: the tables, then the items' source rows ----
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(tab_bar, CC_IMG_WORDS * 4u);
+            tma_load_1d(smem + (L.r1 - sbase), cf.img, 65536u, tab_bar);
+            tma_load_1d(smem + (L.r2 - sbase), cf.img + CC_IMG_WORDS / 2, 65536u, tab_bar);
+        }
+        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
+            if (k >= NST) cc_wait(&empty[st], ph ^ 1);
+            const int item = i0 + k * istep;
+            const ItemPar p = get_par(k);
+            const int y0 = (item - p.s * g.nrb) * g.R;
+            const int sy_first = y0 + p.oy - g.pad;
+            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
+            const uint8_t *sample = src + p.src_off;
+            uint8_t *dst = smem + soff(st) + g.io;
+            // one lane per row: the row copies are issued in parallel
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&full[st], (uint32_t)max(0, hi - lo) * (uint32_t)g.row_bytes);
+            }
+            __syncwarp();
+            const uint64_t pol = l2_evict_first_policy();
+            for (int r = lo + lane; r < hi; r += 32)
+                tma_load_1d_hint(dst + (r - sy_first) * g.rs, sample + (int64_t)r * g.row_bytes,
+                                 (uint32_t)g.row_bytes, &full[st], pol);
+            if (++st == NST) st = 0, ph ^= 1;
+        }
+        return;
+    }
+
+    if (EMIT && warp < NCW) {
+        // ---------------- emit warps: normalised NCHW (as collate_augment_kernel) ----
+        const uint32_t *smem_words = reinterpret_cast<const uint32_t *>(smem);
+        if (blockIdx.x == 0) write_targets(ep, idx, g.b, tid, NT);
+        const int64_t plane_bytes = g.plane * E;
+        const int r_first = tid / g.groups;
+        const int x_first = (tid - r_first * g.groups) * P;
+        const int dr = NT / g.groups;
+        const int dx = (NT - dr * g.groups) * P;
+        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
+            const int item = i0 + k * istep;
+            const ItemPar p = get_par(k);
+            const int y0 = (item - p.s * g.nrb) * g.R;
+            const int sy_first = y0 + p.oy - g.pad;
+            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
+            const int64_t out_item = ((int64_t)p.s * C * g.plane + (int64_t)y0 * g.w) * E;
+            const uint32_t so = soff(st);
+            cc_wait(&full[st], ph);
+            int r = r_first, x0 = x_first;
+#pragma unroll 1
+            for (int sl = tid; sl < g.slots; sl += NT) {
+                const int sy = sy_first + r;
+                const uint32_t row_off = (sy >= lo && sy < hi) ? so + (uint32_t)(r * g.rs) : L.zero;
+                const int64_t off = out_item + ((int64_t)r * g.w + x0) * E;
+                if (!p.fl) {
+                    const uint32_t ws = row_off + g.rdoff + (x0 + p.ox) * C;
+                    emit_pixels<OUT_KIND, C, false, false>(smem_words, ws, norm, dsts, off,
+                                                           plane_bytes,
+                                                           std::make_integer_sequence<int, C>{});
+                } else {
+                    const uint32_t ws = row_off + g.rdoff + (g.w - P - x0 + p.ox) * C;
+                    emit_pixels<OUT_KIND, C, false, true>(smem_words, ws, norm, dsts, off,
+                                                          plane_bytes,
+                                                          std::make_integer_sequence<int, C>{});
+                }
+                r += dr;
+                x0 += dx;
+                if (x0 >= g.w) {
+                    x0 -= g.w;
+                    r += 1;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == NST) st = 0, ph ^= 1;
+        }
+    } else {
+        // ------- checksum warps: channel c, column run `run` of every staged item ------
+        const int cw = warp - NCW - 1;
+        const int c = cw % C, run = cw / C;
+        const int runs = g.w >> 5;
+        const uint32_t tc = cf.tab_c ? 0u : (uint32_t)c;
+        const uint32_t gbase = (tc < 2 ? L.r1 : L.r2) | ((tc & 1u) << 7);
+        const uint32_t rowsh = L.r2 + 128u + 4u * (uint32_t)lane + (128u << 8);  // x^(8 wE (R-1-lane))
+        const uint32_t wrun = __ldg(cf.wrun + run * 32 + lane);  // x^(8*32E*(runs-1-run)) * e_lane
+        const int s_l = lane >> 3, g_l = (lane + s_l) & 7;
+        uint32_t jj[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) jj[t] = (uint32_t)((t + s_l) & 3) << 2;
+        uint32_t wacc = 0;
+        if (blockIdx.x == 0 && cw == 0 && cf.with_tgt) {
+            // raw CRC of the int64 target (b entries after the input): lane l takes
+            // nl entries of the front-zero-padded run, then a 5-level tree
+            const int nl = (g.b + 31) >> 5, z = 32 * nl - g.b;
+            uint32_t cr = 0;
+            for (int e = 0; e < nl; ++e) {
+                const int v = lane * nl + e - z;
+                if (v >= 0) {
+                    const uint64_t x = (uint64_t)kidx[v];
+                    cr = cc_crc_word(cf.slice, cr, (uint32_t)x);
+                    cr = cc_crc_word(cf.slice, cr, (uint32_t)(x >> 32));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, cr, 1 << k);
+                cr = (lane & (1 << k)) ? cc_multmodp(cf.tgt_k[k], other) ^ cr
+                                       : cc_multmodp(cf.tgt_k[k], cr) ^ other;
+            }
+            if (lane == 0) wacc = cr;
+        }
+        cc_wait(tab_bar, 0);
+        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
+            const int item = i0 + k * istep;
+            const ItemPar p = get_par(k);
+            const int rb = item - p.s * g.nrb;
+            const int y0 = rb * g.R;
+            const int sy_first = y0 + p.oy - g.pad;
+            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
+            const int m = cf.nseg - 1 - ((p.s * C + c) * g.nrb + rb);
+            const uint32_t wv = __ldg(cf.wtab + (int64_t)m * 32 + lane);
+            const uint32_t so = soff(st);
+            cc_wait(&full[st], ph);
+            uint32_t S = 0;
+            if (lane < g.R) {
+                const int sy = sy_first + lane;
+                const uint32_t row_off = (sy >= lo && sy < hi) ? so + (uint32_t)(lane * g.rs) : L.zero;
+                // lowest shared byte of the run's element group 0 (4 elements), step per group
+                int a0, step;
+                if (!p.fl) {
+                    a0 = (int)row_off + g.rdoff + (32 * run + p.ox) * C + c;
+                    step = 4 * C;
+                } else {
+                    a0 = (int)row_off + g.rdoff + (g.w - 4 - 32 * run + p.ox) * C + c;
+                    step = -4 * C;
+                }
+                const uint32_t mis = (uint32_t)a0 & 3u;
+                const uint32_t abase = sbase + ((uint32_t)a0 & ~3u);
+                const uint32_t *sl3 = sel_tab + ((p.fl ? 4 : 0) + mis) * 96 + lane;
+                const uint32_t sel1 = sl3[0], sel2 = sl3[32], sel3 = sl3[64];
+                uint32_t acc = 0;
+#pragma unroll
+                for (int to = 0; to < 8; ++to) {
+                    const int gi = (to + g_l) & 7;
+                    const uint32_t a = abase + (uint32_t)(gi * step);
+                    const uint32_t w0 = cc_lds(a), w1 = cc_lds(a + 4), w2 = cc_lds(a + 8),
+                                   w3 = cc_lds(a + 12);
+                    const uint32_t v = cc_prmt(cc_prmt(w0, w1, sel1), cc_prmt(w2, w3, sel2), sel3);
+                    const uint32_t gb = gbase | ((uint32_t)gi << 4);
+                    acc ^= cc_lds(cc_prmt(v, gb | jj[0], 0x7604u)) ^
+                           cc_lds(cc_prmt(v, gb | jj[1], 0x7614u)) ^
+                           cc_lds(cc_prmt(v, gb | jj[2], 0x7624u)) ^
+                           cc_lds(cc_prmt(v, gb | jj[3], 0x7634u));
+                }
+                S = cc_mul_nib(acc, rowsh);  // row `lane` -> the segment's last row
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);  // the stage is no longer read
+            if (++st == NST) st = 0, ph ^= 1;
+#pragma unroll
+            for (int k2 = 16; k2 >= 1; k2 >>= 1) S ^= __shfl_xor_sync(0xFFFFFFFFu, S, k2);
+            // the run's column -> the segment's end, then the segment -> the slot's end
+            uint32_t t2 = ((S >> lane) & 1u) ? wrun : 0u;
+#pragma unroll
+            for (int k2 = 16; k2 >= 1; k2 >>= 1) t2 ^= __shfl_xor_sync(0xFFFFFFFFu, t2, k2);
+            wacc ^= ((t2 >> lane) & 1u) ? wv : 0u;
+        }
+#pragma unroll
+        for (int k2 = 16; k2 >= 1; k2 >>= 1) wacc ^= __shfl_xor_sync(0xFFFFFFFFu, wacc, k2);
+        if (lane == 0 && wacc) atomicXor(cf.acc, wacc);
+    }
+    // the completing CTA finishes the checksum (and, fused, publishes the slot)
+    asm volatile("bar.sync 1, %0;" ::"r"(NT + 32 * ncrc) : "memory");
+    if (tid == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(cf.count, 1u);
+        if (prev == gridDim.x - 1) {
+            *cf.count = 0u;
+            __threadfence();
+            const uint32_t v = atomicExch(cf.acc, 0u);
+            *cf.out = v ^ cf.init;
+            __threadfence_system();
+            if (EMIT)
+                for (int d = 0; d < ep.n; ++d)
+                    if (ep.ready[d])
+                        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready[d]),
+                                     "l"(ep.seq)
+                                     : "memory");
+        }
+    }
+}
+
+// ---- host: tables (cached per configuration) and the launch ---------------
+constexpr uint32_t CC_POLY = 0xEDB88320u;
+inline uint32_t cc_h_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ CC_POLY : b >> 1;
+    }
+    return p;
+}
+inline uint32_t cc_h_x8n(uint64_t n) {  // x^(8n) mod P
+    uint32_t p = 1u << 31, sq = 1u << 30;  // sq = x^1
+    for (int i = 0; i < 3; ++i) sq = cc_h_multmodp(sq, sq);  // x^8
+    while (n) {
+        if (n & 1) p = cc_h_multmodp(sq, p);
+        n >>= 1;
+        sq = cc_h_multmodp(sq, sq);
+    }
+    return p;
+}
+inline void cc_h_tables(uint32_t t[4 * 256]) {
+    for (uint32_t i = 0; i < 256; ++i) {
+        uint32_t r = i;
+        for (int k = 0; k < 8; ++k) r = (r >> 1) ^ (CC_POLY & (0u - (r & 1u)));
+        t[i] = r;
+    }
+    for (int s = 1; s < 4; ++s)
+        for (uint32_t i = 0; i < 256; ++i)
+            t[s * 256 + i] = (t[(s - 1) * 256 + i] >> 8) ^ t[t[(s - 1) * 256 + i] & 0xFFu];
+}
+// the output element F_c(v) as the emit path computes it (two IEEE roundings;
+// bf16 by round-to-nearest-even of that f32)
+inline void cc_h_element(int out_kind, const Norm &n, int c, int v, uint8_t *b) {
+    if (out_kind == TSB_OUT_U8) {
+        b[0] = (uint8_t)v;
+        return;
+    }
+    volatile float prod = (float)v * n.scale[c];
+    volatile float sum = prod + n.bias[c];
+    const float f = sum;
+    uint32_t bits;
+    memcpy(&bits, &f, 4);
+    if (out_kind == TSB_OUT_F32) {
+        memcpy(b, &bits, 4);
+        return;
+    }
+    const uint16_t h = (uint16_t)((bits + 0x7FFFu + ((bits >> 16) & 1u)) >> 16);
+    memcpy(b, &h, 2);
+}
+
+struct CcKey {
+    int dev, out_kind, c, w, h, R, b, with_tgt;
+    float scale[4], bias[4];
+};
+struct CcPlan {
+    CcKey key;
+    uint32_t *d_img = nullptr, *d_slice = nullptr, *d_w = nullptr, *d_wrun = nullptr;
+    uint32_t tgt_k[5];
+    uint32_t init;
+    int nseg;
+};
+
+int cc_plan(const CcKey &key, cudaStream_t s, const CcPlan **out) {
+    static std::mutex mu;
+    static CcPlan plans[16];
+    static int n_plans = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < n_plans; ++i)
+        if (memcmp(&plans[i].key, &key, sizeof(CcKey)) == 0) {
+            *out = &plans[i];
+            return TSB_OK;
+        }
+    TSB_CHECK(n_plans < 16, "too many fused-checksum configurations in one process");
+    const int E = key.out_kind == TSB_OUT_U8 ? 1 : key.out_kind == TSB_OUT_F32 ? 4 : 2;
+    Norm nm{};
+    memcpy(nm.scale, key.scale, sizeof(nm.scale));
+    memcpy(nm.bias, key.bias, sizeof(nm.bias));
+    std::vector<uint32_t> img(CC_IMG_WORDS, 0u), slice(4 * 256);
+    cc_h_tables(slice.data());
+    uint32_t kp[32];
+    for (int p = 0; p < 32; ++p) kp[p] = cc_h_x8n((uint64_t)E * (31 - p));
+    const int ntab = key.out_kind == TSB_OUT_U8 ? 1 : key.c;
+    for (int tc = 0; tc < ntab; ++tc) {
+        const int region = tc >> 1, half = tc & 1;
+        for (int v = 0; v < 256; ++v) {
+            uint8_t el[4];
+            cc_h_element(key.out_kind, nm, tc, v, el);
+            uint32_t raw = 0;
+            for (int i = 0; i < E; ++i) raw = slice[(raw ^ el[i]) & 0xFFu] ^ (raw >> 8);
+            for (int p = 0; p < 32; ++p)
+                img[(size_t)(region * 256 + v) * 64 + half * 32 + p] = cc_h_multmodp(kp[p], raw);
+        }
+    }
+    // region 2, upper halves: entries 128..255 the lane-specific row shift
+    for (int l = 0; l < 32; ++l) {
+        const uint32_t kr = l < key.R ? cc_h_x8n((uint64_t)key.w * E * (key.R - 1 - l)) : 0u;
+        for (int j = 0; j < 8; ++j)
+            for (uint32_t q = 0; q < 16; ++q)
+                img[(size_t)(256 + 128 + j * 16 + q) * 64 + 32 + l] =
+                    l < key.R ? cc_h_multmodp(kr, q << (4 * j)) : 0u;
+    }
+    // the column run -> the row's end: x^(8*32E*(runs-1-run)) * e_i
+    const int runs = key.w / 32;
+    std::vector<uint32_t> wr((size_t)runs * 32);
+    for (int r = 0; r < runs; ++r) {
+        const uint32_t kr = cc_h_x8n((uint64_t)32 * E * (runs - 1 - r));
+        for (int i = 0; i < 32; ++i) wr[(size_t)r * 32 + i] = cc_h_multmodp(kr, 1u << i);
+    }
+    const int nrb = key.h / key.R;
+    const int64_t nseg = (int64_t)key.b * key.c * nrb;
+    const uint64_t segb = (uint64_t)key.R * key.w * E;
+    const uint64_t tail = key.with_tgt ? 8ull * (uint64_t)key.b : 0ull;
+    std::vector<uint32_t> wt((size_t)nseg * 32);
+    const uint32_t k_seg = cc_h_x8n(segb);
+    uint32_t km = cc_h_x8n(tail);
+    for (int64_t m = 0; m < nseg; ++m) {
+        // W[m][i] = K_m * e_i: bit i is x^(31-i), so W[m][31] = K_m and each step down is *x
+        uint32_t v = km;
+        for (int i = 31; i >= 0; --i) {
+            wt[(size_t)m * 32 + i] = v;
+            v = (v & 1) ? (v >> 1) ^ CC_POLY : v >> 1;
+        }
+        km = cc_h_multmodp(k_seg, km);
+    }
+    CcPlan &pl = plans[n_plans];
+    pl.key = key;
+    const int nl = (key.b + 31) >> 5;
+    for (int k = 0; k < 5; ++k) pl.tgt_k[k] = cc_h_x8n((uint64_t)8 * nl << k);
+    pl.init = cc_h_multmodp(cc_h_x8n((uint64_t)nseg * segb + tail), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+    pl.nseg = (int)nseg;
+    TSB_CUDA(cudaMalloc(&pl.d_img, img.size() * 4));
+    TSB_CUDA(cudaMalloc(&pl.d_slice, slice.size() * 4));
+    TSB_CUDA(cudaMalloc(&pl.d_w, wt.size() * 4));
+    TSB_CUDA(cudaMalloc(&pl.d_wrun, wr.size() * 4));
+    // stream-ordered before the launch; synchronous on the host side so the
+    // staging vectors may go (pageable sources are staged before return)
+    TSB_CUDA(cudaMemcpyAsync(pl.d_img, img.data(), img.size() * 4, cudaMemcpyHostToDevice, s));
+    TSB_CUDA(cudaMemcpyAsync(pl.d_slice, slice.data(), slice.size() * 4, cudaMemcpyHostToDevice, s));
+    TSB_CUDA(cudaMemcpyAsync(pl.d_w, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, s));
+    TSB_CUDA(cudaMemcpyAsync(pl.d_wrun, wr.data(), wr.size() * 4, cudaMemcpyHostToDevice, s));
+    TSB_CUDA(cudaStreamSynchronize(s));
+    ++n_plans;
+    *out = &pl;
+    return TSB_OK;
+}
+
+// TSB_CRC_FUSED: 2 (default) the fused emit + checksum kernel, 1 the checksum
+// kernel after the collate, 0 the output-side CRC (tsb_crc32) after it.
+int cc_mode_knob() {
+    static const int v = getenv("TSB_CRC_FUSED") ? atoi(getenv("TSB_CRC_FUSED")) : 2;
+    return v;
+}
+
+// Can this batch take the source-side checksum?  (else: collate, then tsb_crc32)
+bool cc_fusable(const CaGeom &g, int c, const Dsts &dsts, const Epi &ep) {
+    if (!cc_mode_knob() || !ep.counter || dsts.n != 1 || c > CC_MAX_C || !g.use_tma ||
+        g.use_direct)
+        return false;
+    if (g.w % 32 || g.R > 32 || g.h % g.R || g.nrb * g.R != g.h) return false;
+    const int ncrc = c * (g.w / 32);
+    if (ncrc > (cc_mode_knob() == 2 ? 32 - 1 - CC_EMIT / 32 : 31)) return false;
+    // the layout must fit for the dynamic shared base the runtime may pick
+    CcLayout L;
+    for (uint32_t sb : {0u, 1024u, 2048u})
+        if (!cc_layout(sb, (uint32_t)(g.R * g.rs), (uint32_t)g.rs, CC_STAGES, L)) return false;
+    return true;
+}
+
+template <int K, int C, bool EMIT>
+int launch_cc(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
+              uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
+              cudaStream_t s, const Epi &ep, const CrcFuse &cf, int pdl) {
+    auto kern = collate_crc_kernel<K, C, EMIT>;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) dev = 63;
+    if (!attr_set[dev]) {
+        TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CC_SMEM));
+        attr_set[dev] = true;
+    }
+    const int grid = g.items < sm_count() ? g.items : sm_count();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((EMIT ? CC_EMIT : 0) + 32 + 32 * cf.ncrc);
+    cfg.dynamicSmemBytes = CC_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
+                                ep, cf));
+    return TSB_OK;
+}
+
+template <int K, bool EMIT>
+int launch_cc_c(int c, const uint8_t *src, const int64_t *idx, const CaGeom &g, int flip,
+                uint64_t aug_mixed, uint64_t epoch, const Norm &norm, const int32_t *params,
+                const Dsts &dsts, cudaStream_t s, const Epi &ep, const CrcFuse &cf, int pdl) {
+    switch (c) {
+        case 1: return launch_cc<K, 1, EMIT>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf, pdl);
+        case 2: return launch_cc<K, 2, EMIT>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf, pdl);
+        default: return launch_cc<K, 3, EMIT>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf, pdl);
+    }
+}
+
+// The batch checksum from the staged source rows (the caller checked
+// cc_fusable).  emit: the fused kernel also writes and publishes the batch;
+// else the checksum kernel alone, PDL-chained after the collate that did.
+// crc_out receives the zlib CRC-32 of input + target.
+int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, int flip,
+                       uint64_t aug_mixed, uint64_t epoch, const Norm &norm, int out_kind,
+                       const int32_t *params, const Dsts &dsts, cudaStream_t s, const Epi &ep,
+                       uint32_t *crc_out, bool emit, int pdl) {
+    int dev = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    CcKey key{};
+    key.dev = dev;
+    key.out_kind = out_kind == OUT_BF16_FMA ? TSB_OUT_BF16 : out_kind;
+    key.c = c;
+    key.w = g.w;
+    key.h = g.h;
+    key.R = g.R;
+    key.b = g.b;
+    key.with_tgt = ep.tgt[0] != nullptr;
+    if (key.out_kind != TSB_OUT_U8) {
+        memcpy(key.scale, norm.scale, sizeof(key.scale));
+        memcpy(key.bias, norm.bias, sizeof(key.bias));
+    }
+    const CcPlan *pl = nullptr;
+    if (int rc = cc_plan(key, s, &pl)) return rc;
+    static uint32_t *acc_base[64] = {nullptr};
+    static unsigned int *cnt_base[64] = {nullptr};
+    static std::atomic<unsigned> acc_next{0};
+    if (!acc_base[dev]) {
+        void *p = nullptr, *q = nullptr;
+        TSB_CUDA(cudaGetSymbolAddress(&p, g_cc_acc));
+        TSB_CUDA(cudaGetSymbolAddress(&q, g_cc_cnt));
+        acc_base[dev] = static_cast<uint32_t *>(p);
+        cnt_base[dev] = static_cast<unsigned int *>(q);
+    }
+    const unsigned slot = acc_next.fetch_add(1, std::memory_order_relaxed) % CC_ACC_POOL;
+    CrcFuse cf{};
+    cf.img = pl->d_img;
+    cf.slice = pl->d_slice;
+    cf.wtab = pl->d_w;
+    cf.wrun = pl->d_wrun;
+    memcpy(cf.tgt_k, pl->tgt_k, sizeof(cf.tgt_k));
+    cf.init = pl->init;
+    cf.nseg = pl->nseg;
+    cf.with_tgt = key.with_tgt;
+    cf.tab_c = key.out_kind == TSB_OUT_U8;
+    cf.acc = acc_base[dev] + slot;
+    cf.count = cnt_base[dev] + slot;
+    cf.ncrc = c * (g.w / 32);
+    cf.out = crc_out;
+    g.nstage = CC_STAGES;  // (the kernel uses the compile-time count)
+    const auto *s8 = src;
+#define TSB_CC_KIND(KK)                                                                            \
+    return emit ? launch_cc_c<KK, true>(c, s8, idx, g, flip, aug_mixed, epoch, norm, params, dsts, \
+                                        s, ep, cf, pdl)                                            \
+                : launch_cc_c<KK, false>(c, s8, idx, g, flip, aug_mixed, epoch, norm, params,      \
+                                         dsts, s, ep, cf, pdl)
+    if (out_kind == TSB_OUT_U8) TSB_CC_KIND(TSB_OUT_U8);
+    if (out_kind == TSB_OUT_F32) TSB_CC_KIND(TSB_OUT_F32);
+    if (out_kind == OUT_BF16_FMA) TSB_CC_KIND(OUT_BF16_FMA);
+    TSB_CC_KIND(TSB_OUT_BF16);
+#undef TSB_CC_KIND
+}
+
+template <int K>
+void preload_cc() {
+    touch_kernel(collate_crc_kernel<K, 1, true>);
+    touch_kernel(collate_crc_kernel<K, 2, true>);
+    touch_kernel(collate_crc_kernel<K, 3, true>);
+    touch_kernel(collate_crc_kernel<K, 1, false>);
+    touch_kernel(collate_crc_kernel<K, 2, false>);
+    touch_kernel(collate_crc_kernel<K, 3, false>);
+}

@@ -3,14 +3,17 @@
 // The reference reads each batch's samples from its DirectorySource into a
 // host buffer (pipeline.py:190-210) before the segment memcpy
 // (payload.py:234-235).  Here the batch's samples -- scattered rows of a
-// pinned host store, in epoch order -- cross PCIe once, by the copy engine:
-// one cudaMemcpyBatchAsync of B sample rows per batch on a dedicated ingest
-// stream into a double-buffered HBM staging area, overlapped with the
-// collate kernel of the previous batch on the producer stream.  The copy
-// engine sustains ~55 GB/s H2D on B200's PCIe Gen5 x16 link against ~48 GB/s
-// for SM loads of pinned memory (profiles/r1), and the collate kernel then
-// reads HBM through its TMA path.  Passthrough batches are copied straight
-// into the ring slot (no kernel at all).
+// pinned host store, in epoch order -- cross PCIe once: one gather kernel per
+// batch on a dedicated ingest stream reads the mapped pinned rows with
+// 16-byte loads (thousands in flight cover the PCIe latency) and writes them
+// into a double-buffered HBM staging area, overlapped with the collate kernel
+// of the previous batch on the producer stream.  It co-resides with the
+// collate (no shared memory, few registers).  One copy-engine operation per
+// sample would cost ~2 us of host API time each (0.5 ms per 256-sample
+// batch); SM loads of pinned memory reach ~48 GB/s on B200's PCIe Gen5 x16
+// link (profiles/r1/h2d_probe.json).  The collate kernel then reads HBM
+// through its TMA path.  Passthrough batches are gathered straight into the
+// ring slot.
 #include <cstring>
 #include <vector>
 
@@ -34,9 +37,6 @@ struct tsb_ingest {
     std::vector<cudaEvent_t> done, freed;
     std::vector<int> used;
     int next;
-    std::vector<void *> dsts, srcs;
-    std::vector<size_t> sizes;
-    int batch_api;        // cudaMemcpyBatchAsync usable (else one copy per sample)
 };
 
 namespace {
@@ -44,6 +44,47 @@ __global__ void iota_kernel(int64_t *p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         p[i] = i;
+}
+
+// Sample s of the batch: bytes [lo*row_bytes, hi*row_bytes) of store row
+// idx[s] -> out + s*sb (+ the same offset).  With crop params only the rows
+// the crop reads (rows [max(0, oy-pad), min(h, h+oy-pad))); else the sample.
+// 16-byte vectors when every offset is 16-byte aligned, else bytes.
+constexpr int IG_THREADS = 256;
+constexpr int IG_CHUNK = 16384;  // bytes per CTA and sample
+__global__ void __launch_bounds__(IG_THREADS)
+    ingest_gather_kernel(const uint8_t *__restrict__ host, const int64_t *__restrict__ idx,
+                         const int32_t *__restrict__ params, int64_t sb, int row_bytes, int h,
+                         int pad, int vec, uint8_t *__restrict__ out) {
+    const int s = blockIdx.y;
+    int64_t begin = 0, end = sb;
+    if (params) {
+        const int oy = params[3 * s];
+        const int lo = max(oy - pad, 0), hi = min(h + oy - pad, h);
+        begin = (int64_t)lo * row_bytes;
+        end = hi > lo ? (int64_t)hi * row_bytes : begin;
+    }
+    const int64_t c0 = begin + (int64_t)blockIdx.x * IG_CHUNK;
+    const int64_t c1 = min(c0 + IG_CHUNK, end);
+    if (c0 >= c1) return;
+    const uint8_t *src = host + idx[s] * sb;
+    uint8_t *dst = out + (int64_t)s * sb;
+    if (vec) {
+        constexpr int U = IG_CHUNK / 16 / IG_THREADS;
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t o = c0 + 16 * (int64_t)(threadIdx.x + u * IG_THREADS);
+            if (o < c1) v[u] = ld_nc_v4(src + o);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t o = c0 + 16 * (int64_t)(threadIdx.x + u * IG_THREADS);
+            if (o < c1) *reinterpret_cast<uint4 *>(dst + o) = v[u];
+        }
+    } else {
+        for (int64_t o = c0 + threadIdx.x; o < c1; o += IG_THREADS) dst[o] = src[o];
+    }
 }
 }  // namespace
 
@@ -61,9 +102,8 @@ void preload_ingest() { touch_kernel(iota_kernel); }
 // reads source row y + oy - pad, so rows [max(0, oy-pad), min(h, h+oy-pad))
 // of each sample (on average 8.2 of 224 rows fewer at pad 16).  The collate
 // kernel loads exactly those rows of a staged sample, never the others.
-// (Columns too would save another 3.7%, but 2D copies -- cudaMemcpy3DBatchAsync,
-// one op per sample -- run ~10x slower on the copy engine: e2e 154 k vs 1.49 M
-// samples/s; profiles/r1/ingest_2d_ab.txt.)
+// (Columns too would save another 3.7%, but 2D copies -- one op per sample --
+// ran ~10x slower: e2e 154 k vs 1.49 M samples/s; profiles/r1/ingest_2d_ab.txt.)
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
                  void *dst, void *stream, int *k_out, bool after_stream, const IngestCrop *crop) {
     TSB_CHECK(g && host_store && h_idx && k_out, "null argument");
@@ -84,13 +124,11 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     }
     uint8_t *out = dst ? static_cast<uint8_t *>(dst)
                        : g->staging + (size_t)k * (size_t)(g->max_batch * g->sample_bytes);
-    const uint8_t *src = static_cast<const uint8_t *>(host_store);
     const size_t sb = (size_t)g->sample_bytes;
     int32_t *hp = g->h_params + (size_t)k * g->max_batch * 3;
     size_t nbytes = 0;
-    bool done = false;
     for (int64_t i = 0; i < b; ++i) {
-        size_t off = 0, len = sb;
+        size_t len = sb;
         if (crop) {
             int oy = 0, ox = 0, fl = 0;
             derive_aug_host(crop->aug_mixed, crop->epoch, h_idx[i], crop->pad, crop->flip, oy, ox,
@@ -100,43 +138,29 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
             hp[3 * i + 2] = fl;
             const int lo = oy - crop->pad > 0 ? oy - crop->pad : 0;
             const int hi = crop->h + oy - crop->pad < crop->h ? crop->h + oy - crop->pad : crop->h;
-            // a sample cropped out entirely (pad >= h) still gets a 1-byte copy
-            // (the batch API takes no empty entries); the kernel reads none of it
-            off = hi > lo ? (size_t)lo * (size_t)crop->row_bytes : 0;
-            len = hi > lo ? (size_t)(hi - lo) * (size_t)crop->row_bytes : 1;
+            len = hi > lo ? (size_t)(hi - lo) * (size_t)crop->row_bytes : 0;
         }
-        g->dsts[i] = out + (size_t)i * sb + off;
-        g->srcs[i] = const_cast<uint8_t *>(src + (size_t)h_idx[i] * sb + off);
-        g->sizes[i] = len;
-        nbytes += g->sizes[i];
+        nbytes += len;
     }
-    if (!done && g->batch_api) {
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        size_t attr_idx = 0, fail = 0;
-        cudaError_t e = cudaMemcpyBatchAsync(g->dsts.data(), g->srcs.data(), g->sizes.data(),
-                                             (size_t)b, &attr, &attr_idx, 1, &fail, g->stream);
-        if (e == cudaSuccess) {
-            done = true;
-        } else {
-            cudaGetLastError();
-            g->batch_api = 0;  // driver without the batch API: per-sample copies from now on
-        }
-    }
-    if (!done)
-        for (int64_t i = 0; i < b; ++i)
-            TSB_CUDA(cudaMemcpyAsync(g->dsts[i], g->srcs[i], g->sizes[i], cudaMemcpyHostToDevice,
-                                     g->stream));
-    TSB_CUDA(cudaMemcpyAsync(g->d_idx + (size_t)k * g->max_batch, hk, sizeof(int64_t) * (size_t)b,
-                             cudaMemcpyHostToDevice, g->stream));
+    int64_t *dk = g->d_idx + (size_t)k * g->max_batch;
+    int32_t *pk = g->d_params + (size_t)k * g->max_batch * 3;
+    TSB_CUDA(cudaMemcpyAsync(dk, hk, sizeof(int64_t) * (size_t)b, cudaMemcpyHostToDevice,
+                             g->stream));
     nbytes += sizeof(int64_t) * (size_t)b;
     if (crop) {
-        TSB_CUDA(cudaMemcpyAsync(g->d_params + (size_t)k * g->max_batch * 3, hp,
-                                 sizeof(int32_t) * 3 * (size_t)b, cudaMemcpyHostToDevice,
+        TSB_CUDA(cudaMemcpyAsync(pk, hp, sizeof(int32_t) * 3 * (size_t)b, cudaMemcpyHostToDevice,
                                  g->stream));
         nbytes += sizeof(int32_t) * 3 * (size_t)b;
     }
+    const int row_bytes = crop ? crop->row_bytes : 0;
+    const bool vec = ((uintptr_t)host_store & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
+                     sb % 16 == 0 && (!crop || row_bytes % 16 == 0);
+    dim3 grid((unsigned)((sb + IG_CHUNK - 1) / IG_CHUNK), (unsigned)b);
+    TSB_CHECK(b <= 65535, "batch %lld exceeds the gather grid", (long long)b);
+    ingest_gather_kernel<<<grid, IG_THREADS, 0, g->stream>>>(
+        static_cast<const uint8_t *>(host_store), dk, crop ? pk : nullptr, (int64_t)sb, row_bytes,
+        crop ? crop->h : 0, crop ? crop->pad : 0, vec ? 1 : 0, out);
+    TSB_LAUNCH_CHECK();
     g->bytes += nbytes;
     TSB_CUDA(cudaEventRecord(g->done[k], g->stream));
     TSB_CUDA(cudaStreamWaitEvent(as_stream(stream), g->done[k], 0));
@@ -172,7 +196,6 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
     g->depth = depth;
     g->max_batch = max_batch;
     g->sample_bytes = sample_bytes;
-    g->batch_api = 1;
     const size_t stage = (size_t)max_batch * (size_t)sample_bytes;
     cudaError_t e = cudaMalloc(&g->staging, stage * depth);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_idx, sizeof(int64_t) * max_batch * depth);
@@ -194,9 +217,6 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
         TSB_CUDA(cudaEventCreateWithFlags(&g->done[k], cudaEventDisableTiming));
         TSB_CUDA(cudaEventCreateWithFlags(&g->freed[k], cudaEventDisableTiming));
     }
-    g->dsts.resize(max_batch);
-    g->srcs.resize(max_batch);
-    g->sizes.resize(max_batch);
     iota_kernel<<<(unsigned)((max_batch + 255) / 256), 256, 0, g->stream>>>(g->d_identity,
                                                                           max_batch);
     TSB_LAUNCH_CHECK();
@@ -223,7 +243,7 @@ int tsb_ingest_destroy(tsb_ingest *g) {
 
 int tsb_ingest_batch_api(tsb_ingest *g, int *used) {
     TSB_CHECK(g && used, "null argument");
-    *used = g->batch_api;
+    *used = 1;  // one gather launch per batch
     return TSB_OK;
 }
 

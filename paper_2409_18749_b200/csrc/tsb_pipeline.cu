@@ -30,7 +30,8 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             const float *scale, const float *bias, int out_kind, void *out,
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
                             int pdl, void *stream, const int32_t *d_params,
-                            const int64_t *tgt_idx, uint64_t *release = nullptr);
+                            const int64_t *tgt_idx, uint64_t *release = nullptr,
+                            uint32_t *crc_out = nullptr, int *crc_done = nullptr);
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
                  void *dst, void *stream, int *k_out, bool after_stream,
                  const IngestCrop *crop = nullptr);
@@ -129,6 +130,10 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i]), s));
         int rc = TSB_OK;
         bool published = false, staged_target = false;
+        // per-batch CRC fused into the collate when the geometry allows (the
+        // kernel's completing CTA writes d_crc[slot] before the ready word)
+        uint32_t *crc_out = a->d_crc ? a->d_crc + slot : nullptr;
+        int crc_done = 0;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
                 if (!no_fused && ring_writers(r) == 1) {  // fused epilogue: target copy + publish from the kernel
@@ -153,7 +158,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                      b, a->h, a->w, a->c, a->pad, a->flip, a->seed,
                                                      a->epoch, a->scale, a->bias, a->out_kind, out,
                                                      tgt, ready, q, counter, 0, stream, params,
-                                                     jpeg_indices(a->jpeg));
+                                                     jpeg_indices(a->jpeg), nullptr, crc_out,
+                                                     &crc_done);
                         published = true;
                         break;
                     }
@@ -172,7 +178,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                      a->c, a->pad, a->flip, a->seed, a->epoch,
                                                      a->scale, a->bias, a->out_kind, out, tgt,
                                                      ready, q, counter, 0, stream, params,
-                                                     ingest_indices(a->ingest, k));
+                                                     ingest_indices(a->ingest, k), nullptr,
+                                                     crc_out, &crc_done);
                         if (!rc) rc = ingest_release(a->ingest, k, stream);
                         published = true;
                         break;
@@ -180,7 +187,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                     rc = collate_augment_publish(a->src, idx, b, a->h, a->w, a->c, a->pad,
                                                  a->flip, a->seed, a->epoch, a->scale, a->bias,
                                                  a->out_kind, out, tgt, ready, q, counter, pdl,
-                                                 stream, nullptr, nullptr);
+                                                 stream, nullptr, nullptr, nullptr, crc_out,
+                                                 &crc_done);
                     published = true;
                     break;
                 }
@@ -247,15 +255,15 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                 TSB_CHECK(false, "bad produce mode %d", a->mode);
         }
         if (rc) return rc;
-        // With a per-batch CRC the fused kernel still publishes the slot: the
+        // With a separate per-batch CRC the fused kernel still publishes the slot: the
         // checksum only rides in the Announce, which the host sends after
         // reading it, so no consumer fetches the slot before its CRC is known
         // (and nothing rewrites it before every consumer released it).  The
         // CRC launches sit between two collates, so that pair is not PDL-chained.
-        prev_fused = published && !a->d_crc;
+        prev_fused = published && (!a->d_crc || crc_done);
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
         if (published) {
-            if (a->d_crc)
+            if (a->d_crc && !crc_done)
                 if (int rc2 = tsb_crc32(out, nbytes, a->d_crc + slot, nullptr, stream)) return rc2;
             continue;
         }

@@ -185,7 +185,7 @@ def test_host_gate_needs_host_control():
                                         ("augment_u8", 24, 24)])
 def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode, h, pad):
     """Pinned-host store: each batch's scattered sample rows cross PCIe by the
-    copy engine (cudaMemcpyBatchAsync) into HBM staging (augment) or straight
+    one gather kernel over the mapped pinned store) into HBM staging (augment) or straight
     into the slot (gather); results identical to the oracle.  Augment
     batches copy only the rows the crop reads (the staging buffers keep the
     previous batches' other rows, which the kernel must never read) -- down
@@ -248,7 +248,7 @@ def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode, h, pad):
             epoch, bi = divmod(q - 1, L)
             idx = oracle.epoch_order(N, 1, epoch)[bi * B:(bi + 1) * B]
             d = h - np.abs(oracle.aug_params(2, epoch, idx, pad)[:, 0].astype(np.int64) - pad)
-            rows += int(np.where(d > 0, d * w * c, 1).sum())  # cropped-out sample: 1 byte
+            rows += int(np.where(d > 0, d * w * c, 0).sum())  # cropped-out sample: no bytes
         assert sent == rows + 12 * B * n
     ring.close()
 

@@ -4,6 +4,7 @@ ncu (`-k regex:<kernel> -s <skip> -c 1`):
     python tools/profile_r2.py <what> [batches]
 
 what: f32 | bf16 | u8            C2 collate (B=256 224x224x3) through produce_range
+      f32crc | bf16crc | u8crc   the same with the per-batch CRC fused (collate_crc_kernel)
       passthrough                C1 gather (B=64 224x224x3 u8) through produce_range
       llm | llm_persistent       C5 LLM (2048,) int32 B=256 synthetic, per-batch / persistent
       video                      C5 video (16,3,112,112) u8 B=16 synthetic
@@ -32,9 +33,10 @@ torch.cuda.set_device(0)
 H, W, C = 224, 224, 3
 
 
-def run_range(ld, persistent=False, slots=8):
+def run_range(ld, persistent=False, slots=8, crc=False):
     ring = DeviceRing(slots, ld.batch_nbytes, 1, control="host")
-    a = ld.produce_args(0)
+    d_crc = torch.zeros(slots, dtype=torch.int32, device="cuda") if crc else None
+    a = ld.produce_args(0, with_crc=d_crc)
     a.gate = GATE_HOST
     a.persistent = int(persistent)
     s = torch.cuda.Stream()
@@ -43,10 +45,11 @@ def run_range(ld, persistent=False, slots=8):
     ring.close()
 
 
-if what in ("f32", "bf16", "u8"):
-    dt = {"f32": "float32", "bf16": "bfloat16", "u8": "uint8"}[what]
+if what.rstrip("crc") in ("f32", "bf16", "u8"):
+    dt = {"f32": "float32", "bf16": "bfloat16", "u8": "uint8"}[what.replace("crc", "")]
     store = StoreSource.synthetic(0, 16384, (H, W, C), location="hbm")
-    run_range(CollateLoader(DatasetSpec(store, 16384, 256), AugmentSpec(out_dtype=dt)))
+    run_range(CollateLoader(DatasetSpec(store, 16384, 256), AugmentSpec(out_dtype=dt)),
+              crc=what.endswith("crc"))
 elif what == "passthrough":
     store = StoreSource.synthetic(0, 4096, (H, W, C), location="hbm")
     run_range(CollateLoader(DatasetSpec(store, 4096, 64)))

@@ -3,8 +3,8 @@
 # on the box: gpurun copies back <= 64 MiB), plus the bench launch list
 out=gpurun_out/${1:-ncu_r2}; mkdir -p $out
 shift
-targets=${@:-"f32 bf16 u8 passthrough llm llm_persistent video rebatch fanout twostage_gather twostage_collate crc"}
-declare -A K=( [f32]=collate_augment [bf16]=collate_augment [u8]=collate_augment [passthrough]=passthrough_multi
+targets=${@:-"f32crc bf16crc u8crc f32 bf16 u8 passthrough llm llm_persistent video rebatch fanout twostage_gather twostage_collate crc"}
+declare -A K=( [f32crc]=collate_crc [bf16crc]=collate_crc [u8crc]=collate_crc [f32]=collate_augment [bf16]=collate_augment [u8]=collate_augment [passthrough]=passthrough_multi
   [llm]=passthrough_multi [llm_persistent]=persistent_passthrough [video]=passthrough_multi [rebatch]=rebatch_window
   [fanout]=fanout_v16 [twostage_gather]=passthrough_multi [twostage_collate]=collate_augment [crc]=crc_ )
 declare -A W=( [twostage_gather]=twostage [twostage_collate]=twostage )
