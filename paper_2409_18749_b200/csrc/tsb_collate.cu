@@ -425,7 +425,9 @@ __device__ __forceinline__ uint4 make_vec(const uint32_t *wv, float sc, float bi
                 u = mul_rn_f32x2(add_rn_f32x2(u, k23), sc2);
                 float m0, m1;
                 unpack_f32x2(u, m0, m1);
-                f[i] = __fadd_rn(m0, bi);  // scalar .rn add: keeps the product's rounding
+                // scalar .rn adds: a paired add after the paired multiply measured
+                // 1 ulp off the oracle's fl(fl(u*s)+b) (fused by ptxas)
+                f[i] = __fadd_rn(m0, bi);
                 f[i + 1] = __fadd_rn(m1, bi);
             }
             if constexpr (OUT_KIND == TSB_OUT_F32) {
@@ -1067,19 +1069,11 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     const auto *s8 = static_cast<const uint8_t *>(src);
     auto s = as_stream(stream);
     if (crc_done) *crc_done = 0;
-    if (crc_out && cc_fusable(g, c, dsts, ep)) {  // the batch CRC-32 from the staged source rows
+    const int cc_ne = crc_out ? cc_fusable(g, c, out_kind, dsts, ep) : 0;
+    if (cc_ne) {  // collate + batch CRC, one kernel
         const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
-        int rc = TSB_OK;
-        if (cc_mode_knob() == 2) {  // one kernel: emit + checksum + publish
-            rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
-                                    d_params, dsts, s, ep, crc_out, true, ep.pdl);
-        } else {  // the collate (publishes the slot), then the checksum kernel, chained
-            rc = launch_ca_kind(c, s8, d_indices, g, flip, aug_mixed, epoch, norm, d_params, dsts,
-                                smem, s, ep, out_kind);
-            if (!rc)
-                rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
-                                        d_params, dsts, s, ep, crc_out, false, 1);
-        }
+        const int rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
+                                          d_params, dsts, s, ep, crc_out, cc_ne);
         if (!rc && crc_done) *crc_done = 1;
         return rc;
     }

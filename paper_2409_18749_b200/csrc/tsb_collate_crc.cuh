@@ -1,43 +1,49 @@
 // Collate/augment with the batch CRC-32 fused in (included by tsb_collate.cu,
 // inside its anonymous namespace: uses CaGeom, Norm, Dsts, Epi, ItemPar,
-// OutTraits, emit_pixels, item_par, write_targets).
+// OutTraits, make_vec, item_par, write_targets).
 //
 // Replaces create_segment's crc32 over the whole segment (payload.py:218,
-// called per batch by the producer, bs/producer.py and sl/producer.py:311-314)
-// with work done on bytes the collate already holds in shared memory: the
-// separate pass re-read the 154 MB slot from HBM at 1 table lookup per output
-// byte; here the checksum costs ONE conflict-free lookup per output ELEMENT
-// and no extra HBM traffic.
+// called per batch by the producer, bs/producer.py and sl/producer.py:311-314).
+// The separate pass (tsb_crc32 after the collate) re-read the 154 MB slot
+// from HBM at one table lookup per output BYTE; here the checksum costs one
+// conflict-free shared-memory lookup per output ELEMENT, done by the warps
+// that already hold the element's source byte in a register, and no HBM
+// traffic at all.
 //
 // The output element of channel c for source byte v is F_c(v) (f32 / bf16 /
 // u8), so by linearity of the raw (zero-init) CRC over GF(2) the checksum of
-// a run of 32 output elements is
+// a run of 32 consecutive output elements is
 //     raw(run) = XOR_p G_c[v_p][p],   G_c[v][p] = x^(8 E (31-p)) * raw(F_c(v))
-// a table of 256 x 32 words per channel.  Stored as G_c[v][p] at shared
-// address region | v << 8 | half << 7 | p << 2 it is read with ONE PRMT (the
-// data byte straight into address byte 1) and lands in bank p; the lanes of a
-// warp always look up 32 distinct positions p (the pixel order inside a run
-// is rotated per lane), so no lookup ever conflicts.
+// (a table of 256 x 32 words per channel).  G_c[v][p] sits at shared address
+// R1 + c_off | v << 8 | p << 2: ONE PRMT puts the data byte into address byte
+// 1 next to the lane's position bits, and the word lands in bank p.
 //
-// Per CTA (one per SM, 227 KB of shared memory): 14 emit warps (the normal
-// collate), one TMA producer warp, and C checksum warps.  Checksum warp c
-// walks channel c of each staged item: lane r takes output row r (R <= 32
-// rows per item), 32-element runs chained by a constant multiply (x^(8*32E),
-// lane-replicated nibble tables), then shifts its row to the end of the item
-// segment (a lane-specific constant, also nibble tables), and the warp
-// XOR-reduces the 32 rows: raw(segment).  That segment is placed in the slot
-// through a per-segment table W[m][i] = x^(8 (SEGB m + tail)) * e_i (bit i of
-// the segment CRC selects lane i's word; m = segments after it), XORed into
-// a lane accumulator -- no per-segment reduction.  Block 0's checksum warp 0
-// also folds in the int64 target that follows the input.  At the end each
-// checksum warp reduces its accumulator into one device word (atomicXor), and
-// the CTA that completes the batch turns it into the zlib CRC-32 of the slot
-// (data + target) before it releases the ready word.
+// Emit warps (14): thread t owns one column group (P elements of every
+// channel) of rows t / groups + k*dr of each staged item.  Besides the
+// normalised stores it looks up its P elements per channel; the lanes of a
+// warp cover P column runs, and each lane visits its elements in an order
+// rotated by its run index (register and byte rotations), so every lookup
+// instruction reads 32 distinct positions p -- 32 banks, no conflicts.  The
+// 32/P lanes of a run XOR-reduce (shuffles) and one writes raw(row, run) of
+// each channel to a small per-stage buffer.
 //
-// Shared memory: two 64 KB-aligned table regions (region 1: G_0 | G_1,
-// region 2: G_2 | the two nibble tables); the item stages, zero row, barriers
-// and params are placed first-fit around them.
-constexpr int CC_EMIT = 256;       // fused variant: 8 emit warps (7 / 3.5 / 1.75 slots per thread)
+// Combiner warps (one per column run): lane r takes row r, shifts raw(row r,
+// run) to the end of the item's segment (a lane-specific constant multiply,
+// lane-replicated nibble tables), the warp XOR-reduces the rows, and the run
+// offset and the segment's place in the slot are applied by bit expansion
+// (W[m][i] = x^(8 (SEGB m + tail)) * e_i: bit i of the value selects lane i's
+// word), accumulated per lane -- no per-segment reduction.  Block 0's first
+// combiner also folds in the int64 target that follows the input.  At the
+// end each combiner reduces its accumulator into one device word
+// (atomicXor), and the CTA that completes the batch turns it into the zlib
+// CRC-32 of the slot (input + target) before it releases the ready word.
+//
+// Shared memory: two 64 KB-aligned table regions (R1: G_0 | G_1 in the two
+// 128-byte halves of each 256-byte row, R2: G_2 | the row-shift nibble
+// tables), and first-fit around them the item stages, zero row, barriers,
+// params and the run buffers.
+constexpr int CC_EMIT = 448;       // 14 emit warps (8 / 16 / 32 rows apart for f32 / bf16 / u8)
+constexpr int CC_MAX_RUNS = 9;     // combiner warps: 32-element column runs per row (w <= 288)
 constexpr int CC_MAX_C = 3;
 constexpr int CC_SMEM = 232448;    // the 227 KB opt-in maximum
 constexpr int CC_STAGES = 3;
@@ -58,13 +64,19 @@ struct CrcFuse {
     int tab_c;              // 1: every channel uses table 0 (u8 output: F_c(v) = v)
     uint32_t *acc;          // this launch's accumulator (the completing CTA resets it)
     unsigned int *count;    // this launch's CTA completion counter (same)
-    int ncrc;               // checksum warps: C x (w / 32)
     uint32_t *out;          // the slot's CRC-32
+    int ne;                 // emit threads: groups x dr (dr rows apart, dr divides R)
 };
 
 __device__ __forceinline__ uint32_t cc_lds(uint32_t a) {
     uint32_t v;
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+template <uint32_t OFF>
+__device__ __forceinline__ uint32_t cc_lds_off(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
     return v;
 }
 __device__ __forceinline__ uint32_t cc_prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -96,9 +108,7 @@ __device__ __forceinline__ uint32_t cc_crc_word(const uint32_t *__restrict__ t, 
     return __ldg(t + 3 * 256 + (x & 0xFFu)) ^ __ldg(t + 2 * 256 + ((x >> 8) & 0xFFu)) ^
            __ldg(t + 256 + ((x >> 16) & 0xFFu)) ^ __ldg(t + (x >> 24));
 }
-
-// mbarrier wait that sleeps until the phase completes (suspend-time hint):
-// waiting warps do not re-issue the try_wait in a loop and take no issue slots
+// mbarrier wait that sleeps until the phase completes (suspend-time hint)
 __device__ __forceinline__ void cc_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -110,15 +120,42 @@ __device__ __forceinline__ void cc_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity), "r"(0x100000u)
         : "memory");
 }
+// bytes K0..K3 (compile-time indices into the realigned window words wv[0..NWV))
+// packed into one word, byte t = window byte K_t
+template <int NWV, int K0, int K1, int K2, int K3>
+__device__ __forceinline__ uint32_t cc_gather4(const uint32_t *wv) {
+    constexpr int KMIN = K0 < K1 ? (K0 < K2 ? (K0 < K3 ? K0 : K3) : (K2 < K3 ? K2 : K3))
+                                 : (K1 < K2 ? (K1 < K3 ? K1 : K3) : (K2 < K3 ? K2 : K3));
+    constexpr int LO = KMIN >> 2;
+    constexpr int k[4] = {K0 - 4 * LO, K1 - 4 * LO, K2 - 4 * LO, K3 - 4 * LO};
+    constexpr uint32_t sa = (uint32_t)((k[0] < 8 ? k[0] : 0) | (k[1] < 8 ? k[1] : 0) << 4 |
+                                       (k[2] < 8 ? k[2] : 0) << 8 | (k[3] < 8 ? k[3] : 0) << 12);
+    constexpr bool need_b = k[0] >= 8 || k[1] >= 8 || k[2] >= 8 || k[3] >= 8;
+    constexpr int W1 = LO + 1 < NWV ? LO + 1 : NWV - 1;
+    const uint32_t a = cc_prmt(wv[LO], wv[W1], sa);
+    if constexpr (!need_b) {
+        return a;
+    } else {
+        constexpr uint32_t sb = (uint32_t)((k[0] >= 8 ? k[0] - 8 : 0) | (k[1] >= 8 ? k[1] - 8 : 0) << 4 |
+                                           (k[2] >= 8 ? k[2] - 8 : 0) << 8 |
+                                           (k[3] >= 8 ? k[3] - 8 : 0) << 12);
+        constexpr int W2 = LO + 2 < NWV ? LO + 2 : NWV - 1;
+        constexpr int W3 = LO + 3 < NWV ? LO + 3 : NWV - 1;
+        const uint32_t b = cc_prmt(wv[W2], wv[W3], sb);
+        constexpr uint32_t sm = (uint32_t)((k[0] < 8 ? 0 : 4) | (k[1] < 8 ? 1 : 5) << 4 |
+                                           (k[2] < 8 ? 2 : 6) << 8 | (k[3] < 8 ? 3 : 7) << 12);
+        return cc_prmt(a, b, sm);
+    }
+}
 
 // Shared layout, identical in every CTA (offsets from the dynamic base).
 struct CcLayout {
     uint32_t r1, r2;        // shared addresses of the two table regions
     uint32_t lo_stage, n_lo, hi_stage;  // stages: n_lo at lo_stage, the rest at hi_stage
-    uint32_t zero, bars, par, sel;      // offsets
+    uint32_t zero, bars, par, part;     // offsets
 };
 __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, uint32_t rs,
-                                          int nstage, CcLayout &L) {
+                                          uint32_t part_bytes, int nstage, CcLayout &L) {
     L.r1 = (sbase + 0xFFFFu) & ~0xFFFFu;
     L.r2 = L.r1 + 0x10000u;
     uint32_t lo = 0, lo_end = L.r1 - sbase;
@@ -131,11 +168,10 @@ __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, 
         if (a + bytes <= hi_end) { out = a; hi = a + bytes; return true; }
         return false;
     };
-    bool ok = take((2 * nstage + 1) * 8, 8, L.bars) &&
+    bool ok = take((3 * nstage + 1) * 8, 8, L.bars) &&
               take(META_CAP * (uint32_t)sizeof(ItemPar), 16, L.par) && take(rs, 128, L.zero) &&
-              take(8 * 3 * 32 * 4, 16, L.sel);
+              take(part_bytes * nstage, 16, L.part);
     // stages: as many as fit below region 1, the rest above region 2
-    L.n_lo = 0;
     L.lo_stage = (lo + 127) & ~127u;
     const uint32_t below = lo_end > L.lo_stage ? (lo_end - L.lo_stage) / stage_bytes : 0;
     L.n_lo = below < (uint32_t)nstage ? below : (uint32_t)nstage;
@@ -145,40 +181,117 @@ __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, 
     return ok;
 }
 
-// EMIT: the fused variant (8 emit warps write the batch too); else the
-// checksum alone (the collate kernel ran just before, PDL-chained, and
-// published the slot).  Warp layout: [emit warps] producer, then ncrc
-// checksum warps: warp i takes channel i % C and 32-element column run i / C.
-template <int OUT_KIND, int C, bool EMIT>
-__global__ void __launch_bounds__(1024, 1)
+// One slot of an emit thread: P elements x C channels of output row r -- the
+// normalised stores, and raw(row r, the lane's run) of each channel into the
+// run buffer (after the 32/P lanes of the run XOR-reduced their lookups).
+template <int OUT_KIND, int C, bool FLIP, int CH>
+__device__ __forceinline__ void cc_emit_channel(const uint32_t *wv, const Norm &norm, uint8_t *out,
+                                                int64_t plane_bytes, int lane,
+                                                const uint32_t *A, const uint32_t *B, int ra,
+                                                int rb, uint32_t *part_c) {
+    using T = OutTraits<OUT_KIND>;
+    constexpr int P = T::P;
+    constexpr int NS = P / 4;          // 4-element sub-words per lane
+    constexpr int LPR = 32 / P;        // lanes per column run
+    constexpr int NWV = (P * C + 3) / 4;
+    const uint4 v = make_vec<OUT_KIND, C, FLIP, CH>(wv, norm.scale[CH], norm.bias[CH],
+                                                    std::make_integer_sequence<int, P>{});
+    st_cs_v4(out + CH * plane_bytes, v);
+    // the channel's P source bytes in output order, 4 per word
+    uint32_t V[NS];
+    if constexpr (OUT_KIND == TSB_OUT_U8) {
+        V[0] = v.x;
+        V[1] = v.y;
+        V[2] = v.z;
+        V[3] = v.w;
+    } else {
+        constexpr auto kx = [](int q) { return (FLIP ? P - 1 - q : q) * C + CH; };
+        V[0] = cc_gather4<NWV, kx(0), kx(1), kx(2), kx(3)>(wv);
+        if constexpr (NS > 1) V[1] = cc_gather4<NWV, kx(4), kx(5), kx(6), kx(7)>(wv);
+    }
+    // rotate: word s <- V[(s + ra) % NS], then bytes by rb (lane's run index = ra*4 + rb)
+    uint32_t R[NS];
+    if constexpr (NS == 1) {
+        R[0] = V[0];
+    } else if constexpr (NS == 2) {
+        R[0] = ra ? V[1] : V[0];
+        R[1] = ra ? V[0] : V[1];
+    } else {
+        uint32_t t1[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) t1[s] = (ra & 1) ? V[(s + 1) & 3] : V[s];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) R[s] = (ra & 2) ? t1[(s + 2) & 3] : t1[s];
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) R[s] = __funnelshift_r(R[s], R[s], 8 * rb);
+    constexpr uint32_t COFF = OUT_KIND == TSB_OUT_U8 ? 0u : (CH == 0 ? 0u : CH == 1 ? 128u : 65536u);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            acc ^= cc_lds_off<COFF>(cc_prmt(R[s], A[s] | B[t], 0x7604u | (t << 4)));
+#pragma unroll
+    for (int k = 1; k < LPR; k <<= 1) acc ^= __shfl_xor_sync(0xFFFFFFFFu, acc, k);
+    if ((lane & (LPR - 1)) == 0) *part_c = acc;
+}
+
+template <int OUT_KIND, int C, bool FLIP, int... CHs>
+__device__ __forceinline__ void cc_emit_slot(const uint32_t *smem_words, uint32_t ws,
+                                             const Norm &norm, uint8_t *out, int64_t plane_bytes,
+                                             int lane, const uint32_t *A,
+                                             const uint32_t *B, int ra, int rb, uint32_t *part,
+                                             int part_cstride, std::integer_sequence<int, CHs...>) {
+    constexpr int P = OutTraits<OUT_KIND>::P;
+    constexpr int NB = P * C;
+    constexpr int NW = (NB + 3) / 4 + 1;
+    const uint32_t *wp = smem_words + (ws >> 2);
+    const int shift = 8 * (int)(ws & 3);
+    uint32_t raw[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) raw[i] = wp[i];
+    uint32_t wv[NW - 1];
+#pragma unroll
+    for (int i = 0; i < NW - 1; ++i) wv[i] = __funnelshift_r(raw[i], raw[i + 1], shift);
+    (cc_emit_channel<OUT_KIND, C, FLIP, CHs>(wv, norm, out, plane_bytes, lane, A, B, ra, rb,
+                                             part + CHs * part_cstride),
+     ...);
+}
+
+template <int OUT_KIND, int C>
+__global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
     collate_crc_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ idx, CaGeom g,
                        int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
                        const int32_t *__restrict__ params, Dsts dsts, Epi ep, CrcFuse cf) {
     using T = OutTraits<OUT_KIND>;
     constexpr int P = T::P;
     constexpr int E = T::ELEM;
-    constexpr int NT = EMIT ? CC_EMIT : 0;
-    constexpr int NCW = NT / 32;         // emit warps; warp NCW = producer; then the checksum warps
-    const int ncrc = cf.ncrc;
+    constexpr int NS = P / 4;
+    const int NT = cf.ne;
+    const int NCW = NT >> 5;             // emit warps; warp NCW = producer; then the combiners
+    constexpr int NST = CC_STAGES;
+    const int runs = g.w >> 5;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const uint32_t stage_bytes = (uint32_t)(g.R * g.rs);
+    const int part_words = C * g.R * runs;  // per stage: [c][row][run]
     CcLayout L;
-    constexpr int NST = CC_STAGES;
-    if (!cc_layout(sbase, stage_bytes, (uint32_t)g.rs, NST, L)) __trap();
+    if (!cc_layout(sbase, stage_bytes, (uint32_t)g.rs, 4u * part_words, NST, L)) __trap();
     auto soff = [&](int st) -> uint32_t {
         return (uint32_t)st < L.n_lo ? L.lo_stage + (uint32_t)st * stage_bytes
                                       : L.hi_stage + ((uint32_t)st - L.n_lo) * stage_bytes;
     };
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
     uint64_t *empty = full + NST;
-    uint64_t *tab_bar = empty + NST;
-    uint32_t *sel_tab = reinterpret_cast<uint32_t *>(smem + L.sel);
+    uint64_t *pfull = empty + NST;
+    uint64_t *tab_bar = pfull + NST;
     ItemPar *par = reinterpret_cast<ItemPar *>(smem + L.par);
+    uint32_t *part = reinterpret_cast<uint32_t *>(smem + L.part);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t *kidx = ep.tgt_idx ? ep.tgt_idx : idx;
-    pdl_launch_dependents();  // the next kernel may launch now (it waits for this SM's smem)
+    pdl_launch_dependents();  // the next batch may launch now (it waits for this SM's smem)
     const int nk = (g.items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int i0 = (int)blockIdx.x, istep = (int)gridDim.x;
 
@@ -193,31 +306,11 @@ __global__ void __launch_bounds__(1024, 1)
     }
     for (int k = tid; k < min(nk, META_CAP); k += blockDim.x)
         par[k] = item_par(g, i0 + k * istep, idx, kidx, params, aug_mixed, epoch, flip_en);
-    // the checksum warps' byte-gather selectors for each (flip, word misalignment):
-    // byte j of a 4-element group sits at window offset o_j and goes to byte
-    // (j - s_l) & 3 (s_l = lane >> 3: the per-lane rotation of the positions)
-    for (int e = tid; e < 8 * 32; e += blockDim.x) {
-        const int ln = e & 31, combo = e >> 5, fl = combo >> 2, mis = combo & 3;
-        uint32_t s1 = 0, s2 = 0, s3 = 0;
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t o = (uint32_t)(mis + C * (fl ? 3 - j : j));
-            const uint32_t t = (uint32_t)((j - (ln >> 3)) & 3);
-            if (o < 8) {
-                s1 |= o << (4 * t);
-                s3 |= t << (4 * t);
-            } else {
-                s2 |= (o - 8) << (4 * t);
-                s3 |= (4 + t) << (4 * t);
-            }
-        }
-        sel_tab[(combo * 3 + 0) * 32 + ln] = s1;
-        sel_tab[(combo * 3 + 1) * 32 + ln] = s2;
-        sel_tab[(combo * 3 + 2) * 32 + ln] = s3;
-    }
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NCW + ncrc);
+            mbar_init(&empty[i], NCW + runs);
+            mbar_init(&pfull[i], NT);
         }
         mbar_init(tab_bar, 1);
         fence_mbar_init();
@@ -261,67 +354,61 @@ __global__ void __launch_bounds__(1024, 1)
         return;
     }
 
-    if (EMIT && warp < NCW) {
-        // ---------------- emit warps: normalised NCHW (as collate_augment_kernel) ----
+    if (warp < NCW) {
+        // ------- emit warps: normalised NCHW + per-element checksum lookups -----------
         const uint32_t *smem_words = reinterpret_cast<const uint32_t *>(smem);
         if (blockIdx.x == 0) write_targets(ep, idx, g.b, tid, NT);
         const int64_t plane_bytes = g.plane * E;
-        const int r_first = tid / g.groups;
-        const int x_first = (tid - r_first * g.groups) * P;
-        const int dr = NT / g.groups;
-        const int dx = (NT - dr * g.groups) * P;
+        const int xg = tid % g.groups, r_first = tid / g.groups, dr = NT / g.groups;
+        const int x0 = xg * P, run = x0 >> 5;
+        const int ridx = lane / (32 / P), ra = ridx >> 2, rb = ridx & 3;
+        uint32_t A[NS], B[4];  // position bits: p = (x0 & 31) + 4*((s + ra) % NS) + ((t + rb) & 3)
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2)
+            A[s2] = L.r1 | ((uint32_t)((x0 & 31) + 4 * ((s2 + ra) % NS)) << 2);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) B[t] = (uint32_t)((t + rb) & 3) << 2;
+        const int n_iter = g.R / dr;  // cc_fusable: dr divides R, every slot is a real row
         for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
             const int item = i0 + k * istep;
             const ItemPar p = get_par(k);
             const int y0 = (item - p.s * g.nrb) * g.R;
             const int sy_first = y0 + p.oy - g.pad;
             const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
-            const int64_t out_item = ((int64_t)p.s * C * g.plane + (int64_t)y0 * g.w) * E;
+            uint8_t *out_item = static_cast<uint8_t *>(dsts.p[0]) +
+                                ((int64_t)p.s * C * g.plane + (int64_t)y0 * g.w + x0) * E;
             const uint32_t so = soff(st);
+            uint32_t *pst = part + st * part_words + run;
             cc_wait(&full[st], ph);
-            int r = r_first, x0 = x_first;
 #pragma unroll 1
-            for (int sl = tid; sl < g.slots; sl += NT) {
+            for (int j = 0; j < n_iter; ++j) {
+                const int r = r_first + j * dr;
                 const int sy = sy_first + r;
                 const uint32_t row_off = (sy >= lo && sy < hi) ? so + (uint32_t)(r * g.rs) : L.zero;
-                const int64_t off = out_item + ((int64_t)r * g.w + x0) * E;
-                if (!p.fl) {
-                    const uint32_t ws = row_off + g.rdoff + (x0 + p.ox) * C;
-                    emit_pixels<OUT_KIND, C, false, false>(smem_words, ws, norm, dsts, off,
-                                                           plane_bytes,
-                                                           std::make_integer_sequence<int, C>{});
-                } else {
-                    const uint32_t ws = row_off + g.rdoff + (g.w - P - x0 + p.ox) * C;
-                    emit_pixels<OUT_KIND, C, false, true>(smem_words, ws, norm, dsts, off,
-                                                          plane_bytes,
-                                                          std::make_integer_sequence<int, C>{});
-                }
-                r += dr;
-                x0 += dx;
-                if (x0 >= g.w) {
-                    x0 -= g.w;
-                    r += 1;
-                }
+                uint8_t *o = out_item + (int64_t)r * g.w * E;
+                uint32_t *pr = pst + r * runs;
+                if (!p.fl)
+                    cc_emit_slot<OUT_KIND, C, false>(smem_words, row_off + g.rdoff + (x0 + p.ox) * C,
+                                                     norm, o, plane_bytes, lane, A, B, ra, rb,
+                                                     pr, g.R * runs, std::make_integer_sequence<int, C>{});
+                else
+                    cc_emit_slot<OUT_KIND, C, true>(smem_words,
+                                                    row_off + g.rdoff + (g.w - P - x0 + p.ox) * C,
+                                                    norm, o, plane_bytes, lane, A, B, ra, rb,
+                                                    pr, g.R * runs, std::make_integer_sequence<int, C>{});
             }
+            mbar_arrive(&pfull[st]);  // this thread's run values are in the buffer
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             if (++st == NST) st = 0, ph ^= 1;
         }
     } else {
-        // ------- checksum warps: channel c, column run `run` of every staged item ------
-        const int cw = warp - NCW - 1;
-        const int c = cw % C, run = cw / C;
-        const int runs = g.w >> 5;
-        const uint32_t tc = cf.tab_c ? 0u : (uint32_t)c;
-        const uint32_t gbase = (tc < 2 ? L.r1 : L.r2) | ((tc & 1u) << 7);
+        // ------- combiner warps: one column run, lane = row of the item ---------------
+        const int run = warp - NCW - 1;
         const uint32_t rowsh = L.r2 + 128u + 4u * (uint32_t)lane + (128u << 8);  // x^(8 wE (R-1-lane))
         const uint32_t wrun = __ldg(cf.wrun + run * 32 + lane);  // x^(8*32E*(runs-1-run)) * e_lane
-        const int s_l = lane >> 3, g_l = (lane + s_l) & 7;
-        uint32_t jj[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) jj[t] = (uint32_t)((t + s_l) & 3) << 2;
         uint32_t wacc = 0;
-        if (blockIdx.x == 0 && cw == 0 && cf.with_tgt) {
+        if (blockIdx.x == 0 && run == 0 && cf.with_tgt) {
             // raw CRC of the int64 target (b entries after the input): lane l takes
             // nl entries of the front-zero-padded run, then a 5-level tree
             const int nl = (g.b + 31) >> 5, z = 32 * nl - g.b;
@@ -347,63 +434,37 @@ __global__ void __launch_bounds__(1024, 1)
             const int item = i0 + k * istep;
             const ItemPar p = get_par(k);
             const int rb = item - p.s * g.nrb;
-            const int y0 = rb * g.R;
-            const int sy_first = y0 + p.oy - g.pad;
-            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
-            const int m = cf.nseg - 1 - ((p.s * C + c) * g.nrb + rb);
-            const uint32_t wv = __ldg(cf.wtab + (int64_t)m * 32 + lane);
-            const uint32_t so = soff(st);
-            cc_wait(&full[st], ph);
-            uint32_t S = 0;
-            if (lane < g.R) {
-                const int sy = sy_first + lane;
-                const uint32_t row_off = (sy >= lo && sy < hi) ? so + (uint32_t)(lane * g.rs) : L.zero;
-                // lowest shared byte of the run's element group 0 (4 elements), step per group
-                int a0, step;
-                if (!p.fl) {
-                    a0 = (int)row_off + g.rdoff + (32 * run + p.ox) * C + c;
-                    step = 4 * C;
-                } else {
-                    a0 = (int)row_off + g.rdoff + (g.w - 4 - 32 * run + p.ox) * C + c;
-                    step = -4 * C;
-                }
-                const uint32_t mis = (uint32_t)a0 & 3u;
-                const uint32_t abase = sbase + ((uint32_t)a0 & ~3u);
-                const uint32_t *sl3 = sel_tab + ((p.fl ? 4 : 0) + mis) * 96 + lane;
-                const uint32_t sel1 = sl3[0], sel2 = sl3[32], sel3 = sl3[64];
-                uint32_t acc = 0;
+            uint32_t wv[C];
 #pragma unroll
-                for (int to = 0; to < 8; ++to) {
-                    const int gi = (to + g_l) & 7;
-                    const uint32_t a = abase + (uint32_t)(gi * step);
-                    const uint32_t w0 = cc_lds(a), w1 = cc_lds(a + 4), w2 = cc_lds(a + 8),
-                                   w3 = cc_lds(a + 12);
-                    const uint32_t v = cc_prmt(cc_prmt(w0, w1, sel1), cc_prmt(w2, w3, sel2), sel3);
-                    const uint32_t gb = gbase | ((uint32_t)gi << 4);
-                    acc ^= cc_lds(cc_prmt(v, gb | jj[0], 0x7604u)) ^
-                           cc_lds(cc_prmt(v, gb | jj[1], 0x7614u)) ^
-                           cc_lds(cc_prmt(v, gb | jj[2], 0x7624u)) ^
-                           cc_lds(cc_prmt(v, gb | jj[3], 0x7634u));
-                }
-                S = cc_mul_nib(acc, rowsh);  // row `lane` -> the segment's last row
-            }
+            for (int c = 0; c < C; ++c)
+                wv[c] = __ldg(cf.wtab + (int64_t)(cf.nseg - 1 - ((p.s * C + c) * g.nrb + rb)) * 32 +
+                              lane);
+            cc_wait(&pfull[st], ph);
+            uint32_t S[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                S[c] = lane < g.R ? part[st * part_words + (c * g.R + lane) * runs + run] : 0u;
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);  // the stage is no longer read
+            if (lane == 0) mbar_arrive(&empty[st]);  // the run buffer is read
             if (++st == NST) st = 0, ph ^= 1;
 #pragma unroll
-            for (int k2 = 16; k2 >= 1; k2 >>= 1) S ^= __shfl_xor_sync(0xFFFFFFFFu, S, k2);
-            // the run's column -> the segment's end, then the segment -> the slot's end
-            uint32_t t2 = ((S >> lane) & 1u) ? wrun : 0u;
+            for (int c = 0; c < C; ++c) {
+                uint32_t x = lane < g.R ? cc_mul_nib(S[c], rowsh) : 0u;  // row -> segment's last row
 #pragma unroll
-            for (int k2 = 16; k2 >= 1; k2 >>= 1) t2 ^= __shfl_xor_sync(0xFFFFFFFFu, t2, k2);
-            wacc ^= ((t2 >> lane) & 1u) ? wv : 0u;
+                for (int k2 = 16; k2 >= 1; k2 >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, k2);
+                // the run's column -> the row's end, then the segment -> the slot's end
+                uint32_t t2 = ((x >> lane) & 1u) ? wrun : 0u;
+#pragma unroll
+                for (int k2 = 16; k2 >= 1; k2 >>= 1) t2 ^= __shfl_xor_sync(0xFFFFFFFFu, t2, k2);
+                wacc ^= ((t2 >> lane) & 1u) ? wv[c] : 0u;
+            }
         }
 #pragma unroll
         for (int k2 = 16; k2 >= 1; k2 >>= 1) wacc ^= __shfl_xor_sync(0xFFFFFFFFu, wacc, k2);
         if (lane == 0 && wacc) atomicXor(cf.acc, wacc);
     }
-    // the completing CTA finishes the checksum (and, fused, publishes the slot)
-    asm volatile("bar.sync 1, %0;" ::"r"(NT + 32 * ncrc) : "memory");
+    // the completing CTA finishes the checksum, then publishes the slot
+    asm volatile("bar.sync 1, %0;" ::"r"(NT + 32 * runs) : "memory");
     if (tid == 0) {
         __threadfence();
         const unsigned int prev = atomicAdd(cf.count, 1u);
@@ -413,12 +474,11 @@ __global__ void __launch_bounds__(1024, 1)
             const uint32_t v = atomicExch(cf.acc, 0u);
             *cf.out = v ^ cf.init;
             __threadfence_system();
-            if (EMIT)
-                for (int d = 0; d < ep.n; ++d)
-                    if (ep.ready[d])
-                        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready[d]),
-                                     "l"(ep.seq)
-                                     : "memory");
+            for (int d = 0; d < ep.n; ++d)
+                if (ep.ready[d])
+                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready[d]),
+                                 "l"(ep.seq)
+                                 : "memory");
         }
     }
 }
@@ -573,33 +633,40 @@ int cc_plan(const CcKey &key, cudaStream_t s, const CcPlan **out) {
     return TSB_OK;
 }
 
-// TSB_CRC_FUSED: 2 (default) the fused emit + checksum kernel, 1 the checksum
-// kernel after the collate, 0 the output-side CRC (tsb_crc32) after it.
+// TSB_CRC_FUSED: 1 (default) the fused kernel, 0 the output-side CRC
+// (tsb_crc32) after the collate (A/B).
 int cc_mode_knob() {
-    static const int v = getenv("TSB_CRC_FUSED") ? atoi(getenv("TSB_CRC_FUSED")) : 2;
+    static const int v = getenv("TSB_CRC_FUSED") ? atoi(getenv("TSB_CRC_FUSED")) : 1;
     return v;
 }
 
-// Can this batch take the source-side checksum?  (else: collate, then tsb_crc32)
-bool cc_fusable(const CaGeom &g, int c, const Dsts &dsts, const Epi &ep) {
+// Can this batch take the fused kernel?  Returns its emit thread count
+// (groups x dr, a whole number of warps, dr dividing the item's rows) or 0:
+// collate, then tsb_crc32.
+int cc_fusable(const CaGeom &g, int c, int out_kind, const Dsts &dsts, const Epi &ep) {
     if (!cc_mode_knob() || !ep.counter || dsts.n != 1 || c > CC_MAX_C || !g.use_tma ||
         g.use_direct)
-        return false;
-    if (g.w % 32 || g.R > 32 || g.h % g.R || g.nrb * g.R != g.h) return false;
-    const int ncrc = c * (g.w / 32);
-    if (ncrc > (cc_mode_knob() == 2 ? 32 - 1 - CC_EMIT / 32 : 31)) return false;
+        return 0;
+    const int P = out_kind == TSB_OUT_U8 ? 16 : out_kind == TSB_OUT_F32 ? 4 : 8;
+    if (g.w % 32 || g.w / 32 > CC_MAX_RUNS || g.R > 32 || g.h % g.R || g.nrb * g.R != g.h) return 0;
+    const int groups = g.w / P;
+    int ne = 0;
+    for (int dr = g.R; dr >= 1 && !ne; --dr)
+        if (g.R % dr == 0 && groups * dr <= CC_EMIT && (groups * dr) % 32 == 0) ne = groups * dr;
+    if (!ne) return 0;
     // the layout must fit for the dynamic shared base the runtime may pick
     CcLayout L;
+    const uint32_t part = 4u * (uint32_t)(c * g.R * (g.w / 32));
     for (uint32_t sb : {0u, 1024u, 2048u})
-        if (!cc_layout(sb, (uint32_t)(g.R * g.rs), (uint32_t)g.rs, CC_STAGES, L)) return false;
-    return true;
+        if (!cc_layout(sb, (uint32_t)(g.R * g.rs), (uint32_t)g.rs, part, CC_STAGES, L)) return 0;
+    return ne;
 }
 
-template <int K, int C, bool EMIT>
+template <int K, int C>
 int launch_cc(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64_t aug_mixed,
               uint64_t epoch, const Norm &norm, const int32_t *params, const Dsts &dsts,
-              cudaStream_t s, const Epi &ep, const CrcFuse &cf, int pdl) {
-    auto kern = collate_crc_kernel<K, C, EMIT>;
+              cudaStream_t s, const Epi &ep, const CrcFuse &cf) {
+    auto kern = collate_crc_kernel<K, C>;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -611,38 +678,37 @@ int launch_cc(const uint8_t *src, const int64_t *idx, CaGeom g, int flip, uint64
     const int grid = g.items < sm_count() ? g.items : sm_count();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3((EMIT ? CC_EMIT : 0) + 32 + 32 * cf.ncrc);
+    cfg.blockDim = dim3(cf.ne + 32 + 32 * (g.w / 32));
     cfg.dynamicSmemBytes = CC_SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = ep.pdl ? 1 : 0;
     TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts,
                                 ep, cf));
     return TSB_OK;
 }
 
-template <int K, bool EMIT>
+template <int K>
 int launch_cc_c(int c, const uint8_t *src, const int64_t *idx, const CaGeom &g, int flip,
                 uint64_t aug_mixed, uint64_t epoch, const Norm &norm, const int32_t *params,
-                const Dsts &dsts, cudaStream_t s, const Epi &ep, const CrcFuse &cf, int pdl) {
+                const Dsts &dsts, cudaStream_t s, const Epi &ep, const CrcFuse &cf) {
     switch (c) {
-        case 1: return launch_cc<K, 1, EMIT>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf, pdl);
-        case 2: return launch_cc<K, 2, EMIT>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf, pdl);
-        default: return launch_cc<K, 3, EMIT>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf, pdl);
+        case 1: return launch_cc<K, 1>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
+        case 2: return launch_cc<K, 2>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
+        default: return launch_cc<K, 3>(src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
     }
 }
 
-// The batch checksum from the staged source rows (the caller checked
-// cc_fusable).  emit: the fused kernel also writes and publishes the batch;
-// else the checksum kernel alone, PDL-chained after the collate that did.
-// crc_out receives the zlib CRC-32 of input + target.
+// Fused collate + batch checksum into a ring slot (the caller checked
+// cc_fusable).  crc_out receives the zlib CRC-32 of input + target before
+// the slot is published.
 int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, int flip,
                        uint64_t aug_mixed, uint64_t epoch, const Norm &norm, int out_kind,
                        const int32_t *params, const Dsts &dsts, cudaStream_t s, const Epi &ep,
-                       uint32_t *crc_out, bool emit, int pdl) {
+                       uint32_t *crc_out, int ne) {
     int dev = 0;
     TSB_CUDA(cudaGetDevice(&dev));
     CcKey key{};
@@ -683,28 +749,21 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     cf.tab_c = key.out_kind == TSB_OUT_U8;
     cf.acc = acc_base[dev] + slot;
     cf.count = cnt_base[dev] + slot;
-    cf.ncrc = c * (g.w / 32);
     cf.out = crc_out;
+    cf.ne = ne;
     g.nstage = CC_STAGES;  // (the kernel uses the compile-time count)
-    const auto *s8 = src;
-#define TSB_CC_KIND(KK)                                                                            \
-    return emit ? launch_cc_c<KK, true>(c, s8, idx, g, flip, aug_mixed, epoch, norm, params, dsts, \
-                                        s, ep, cf, pdl)                                            \
-                : launch_cc_c<KK, false>(c, s8, idx, g, flip, aug_mixed, epoch, norm, params,      \
-                                         dsts, s, ep, cf, pdl)
-    if (out_kind == TSB_OUT_U8) TSB_CC_KIND(TSB_OUT_U8);
-    if (out_kind == TSB_OUT_F32) TSB_CC_KIND(TSB_OUT_F32);
-    if (out_kind == OUT_BF16_FMA) TSB_CC_KIND(OUT_BF16_FMA);
-    TSB_CC_KIND(TSB_OUT_BF16);
-#undef TSB_CC_KIND
+    if (out_kind == TSB_OUT_U8)
+        return launch_cc_c<TSB_OUT_U8>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
+    if (out_kind == TSB_OUT_F32)
+        return launch_cc_c<TSB_OUT_F32>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
+    if (out_kind == OUT_BF16_FMA)
+        return launch_cc_c<OUT_BF16_FMA>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
+    return launch_cc_c<TSB_OUT_BF16>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
 }
 
 template <int K>
 void preload_cc() {
-    touch_kernel(collate_crc_kernel<K, 1, true>);
-    touch_kernel(collate_crc_kernel<K, 2, true>);
-    touch_kernel(collate_crc_kernel<K, 3, true>);
-    touch_kernel(collate_crc_kernel<K, 1, false>);
-    touch_kernel(collate_crc_kernel<K, 2, false>);
-    touch_kernel(collate_crc_kernel<K, 3, false>);
+    touch_kernel(collate_crc_kernel<K, 1>);
+    touch_kernel(collate_crc_kernel<K, 2>);
+    touch_kernel(collate_crc_kernel<K, 3>);
 }
