@@ -986,7 +986,8 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
                               (g.sample_bytes % 16 == 0);
     const CaKnobs &kn = ca_knobs();
     const bool src_dev = is_device_memory(src);
-    g.use_tma = aligned_rows && src_dev && !kn.notma;
+    static const bool tma_host = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "direct");
+    g.use_tma = aligned_rows && (src_dev || tma_host) && !kn.notma;
     g.vec_ldg = aligned_rows && (g.io % 4 == 0);
     {
         static int knobs = -1;  // A/B knobs, read once per process

@@ -153,6 +153,30 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         nbytes += sizeof(int32_t) * 3 * (size_t)b;
     }
     const int row_bytes = crop ? crop->row_bytes : 0;
+    // A/B (TSB_INGEST=memcpy): one copy-engine operation per sample instead
+    static const bool per_sample = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "memcpy");
+    if (per_sample) {
+        for (int64_t i = 0; i < b; ++i) {
+            size_t off = 0, len = sb;
+            if (crop) {
+                const int oy = hp[3 * i];
+                const int lo = oy - crop->pad > 0 ? oy - crop->pad : 0;
+                const int hi = crop->h + oy - crop->pad < crop->h ? crop->h + oy - crop->pad : crop->h;
+                off = (size_t)lo * (size_t)row_bytes;
+                len = hi > lo ? (size_t)(hi - lo) * (size_t)row_bytes : 0;
+            }
+            if (len)
+                TSB_CUDA(cudaMemcpyAsync(out + (size_t)i * sb + off,
+                                         static_cast<const uint8_t *>(host_store) +
+                                             (size_t)h_idx[i] * sb + off,
+                                         len, cudaMemcpyHostToDevice, g->stream));
+        }
+        g->bytes += nbytes;
+        TSB_CUDA(cudaEventRecord(g->done[k], g->stream));
+        TSB_CUDA(cudaStreamWaitEvent(as_stream(stream), g->done[k], 0));
+        *k_out = k;
+        return TSB_OK;
+    }
     const bool vec = ((uintptr_t)host_store & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
                      sb % 16 == 0 && (!crop || row_bytes % 16 == 0);
     dim3 grid((unsigned)((sb + IG_CHUNK - 1) / IG_CHUNK), (unsigned)b);

@@ -85,7 +85,11 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         TSB_CHECK(!no_fused && ring_writers(r) == 1,
                   "the JPEG source needs the fused single-writer path");
     }
-    const bool staged = !jpeg && a->ingest && a->h_order && !ev;
+    // TSB_INGEST=direct (A/B): the collate's TMA reads the pinned store's rows
+    // itself, no staging copy
+    static const bool direct_ingest =
+        getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "direct");
+    const bool staged = !jpeg && a->ingest && a->h_order && !ev && !direct_ingest;
     if (a->persistent) {  // one cooperative launch for the whole range, gated on the device
         TSB_CHECK(ring_has_host_control(r) && ring_writers(r) == 1 && !staged && !jpeg &&
                       !a->d_crc && !ev,
