@@ -78,8 +78,11 @@ __global__ void __launch_bounds__(RB_THREADS)
 // producer whose slots hold `per_slot` samples laid out [inputs][targets]
 // (the pair layout of sl/abi.py:27-31).  slots[k] = base of the k-th
 // producer slot the window touches (first / per_slot is slot 0).  Output:
-// [count inputs][count targets].  One CTA row per window sample, 16 B
-// vectors when aligned.
+// [count inputs][count targets].  One CTA row per window sample; each part
+// moves in 16 B vectors when its offsets allow (vec bit 0: inputs, bit 1:
+// targets, bit 2: aligned 8-byte int64 targets; the int64 target alone used
+// to force the byte loop on the inputs too -- 241 us for a 115 MB window,
+// profiles/r2/ncu_full_rebatch_v1.txt).
 constexpr int RW_MAX_SLOTS = 32;
 struct SlotList {
     const uint8_t *p[RW_MAX_SLOTS];
@@ -100,9 +103,24 @@ __global__ void __launch_bounds__(RB_THREADS)
         uint8_t *o = part ? out + count * in_sb + j * tg_sb : out + j * in_sb;
         const int64_t b0 = (int64_t)blockIdx.x * RB_BYTES_PER_CTA;
         const int64_t b1 = min(b0 + RB_BYTES_PER_CTA, sb);
-        if (vec) {
-            for (int64_t q = b0 + 16 * threadIdx.x; q < b1; q += 16 * RB_THREADS)
-                st_v4(o + q, ld_nc_v4(in + q));
+        if ((vec >> part) & 1) {  // 4 independent 16 B loads in flight per thread
+            constexpr int U = 4;
+            for (int64_t q = b0 + 16 * threadIdx.x; q < b1; q += 16 * RB_THREADS * U) {
+                uint4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t qq = q + (int64_t)u * 16 * RB_THREADS;
+                    if (qq < b1) v[u] = ld_nc_v4(in + qq);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t qq = q + (int64_t)u * 16 * RB_THREADS;
+                    if (qq < b1) st_v4(o + qq, v[u]);
+                }
+            }
+        } else if (part && sb == 8 && (vec & 4)) {  // one aligned int64 target per sample
+            if (blockIdx.x == 0 && threadIdx.x == 0)
+                *reinterpret_cast<int64_t *>(o) = *reinterpret_cast<const int64_t *>(in);
         } else {
             for (int64_t q = b0 + threadIdx.x; q < b1; q += RB_THREADS) o[q] = in[q];
         }
@@ -125,13 +143,20 @@ int tsb_rebatch_window(const void *const *slots, int n_slots, int64_t first, int
     TSB_CHECK(n_slots >= need && n_slots <= RW_MAX_SLOTS, "window needs %lld slots, got %d (max %d)",
               (long long)need, n_slots, RW_MAX_SLOTS);
     SlotList sl{};
-    bool vec = (in_sample_bytes % 16 == 0) && (tgt_sample_bytes % 16 == 0) &&
-               (((uintptr_t)out & 15) == 0) && ((per_slot * in_sample_bytes) % 16 == 0);
+    bool aligned = ((uintptr_t)out & 15) == 0;
     for (int k = 0; k < n_slots; ++k) {
         TSB_CHECK(slots[k], "null slot %d", k);
         sl.p[k] = static_cast<const uint8_t *>(slots[k]);
-        vec = vec && (((uintptr_t)slots[k] & 15) == 0);
+        aligned = aligned && (((uintptr_t)slots[k] & 15) == 0);
     }
+    // inputs: every sample offset 16-byte aligned; targets: their region's
+    // start in the slot and in the output too
+    const bool vec_in = aligned && in_sample_bytes % 16 == 0;
+    const bool vec_tg = aligned && tgt_sample_bytes % 16 == 0 &&
+                        (per_slot * in_sample_bytes) % 16 == 0 && (count * in_sample_bytes) % 16 == 0;
+    const bool tg8 = tgt_sample_bytes == 8 && (per_slot * in_sample_bytes) % 8 == 0 &&
+                     (((uintptr_t)out + (uintptr_t)(count * in_sample_bytes)) & 7) == 0 && aligned;
+    const int vec = (vec_in ? 1 : 0) | (vec_tg ? 2 : 0) | (tg8 ? 4 : 0);
     const int64_t mx = in_sample_bytes > tgt_sample_bytes ? in_sample_bytes : tgt_sample_bytes;
     dim3 grid((unsigned)((mx + RB_BYTES_PER_CTA - 1) / RB_BYTES_PER_CTA), (unsigned)count);
     rebatch_window_kernel<<<grid, RB_THREADS, 0, as_stream(stream)>>>(
