@@ -287,6 +287,14 @@ typedef struct {
     tsb_jpeg *jpeg;          /* non-null (with h_order): samples are JPEG files,
                                 decoded per batch into HBM staging (augment) or
                                 straight into the slot (gather); src unused */
+    uint32_t *h_crc;         /* optional host-mapped (pinned) uint32[slots]: where
+                                the batch CRC-32 is computed inside the collate
+                                kernel, it is also stored here before the slot's
+                                ready word, so a host that sees ready[slot] == q
+                                reads it with no copy */
+    int *crc_fused;          /* optional out: 1 if every batch of the call got its
+                                CRC inside the collate kernel (d_crc / h_crc hold
+                                it when the slot is published), else 0 */
 } tsb_produce_args;
 #define TSB_GATE_DEVICE 0
 #define TSB_GATE_HOST 1

@@ -130,6 +130,7 @@ class ProduceArgs(ctypes.Structure):
         ("ingest", ctypes.c_void_p), ("h_order", ctypes.c_void_p), ("persistent", ctypes.c_int),
         ("chain", ctypes.c_int),
         ("jpeg", ctypes.c_void_p),
+        ("h_crc", ctypes.c_void_p), ("crc_fused", ctypes.c_void_p),
     ]
 
 

@@ -953,7 +953,8 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
                    int pad, int flip, uint64_t aug_seed, uint64_t epoch, const float *scale,
                    const float *bias, int out_kind, const int32_t *d_params, const Dsts &dsts,
                    void *stream, const Epi &ep = Epi{}, uint32_t *crc_out = nullptr,
-                   int *crc_done = nullptr, const CcRange *range = nullptr) {
+                   int *crc_done = nullptr, const CcRange *range = nullptr,
+                   uint32_t *crc_host = nullptr) {
     TSB_CHECK(src && d_indices, "null src/indices");
     TSB_CHECK(b >= 0 && h > 0 && w > 0 && c > 0 && c <= 4, "bad shape b=%lld h=%d w=%d c=%d",
               (long long)b, h, w, c);
@@ -1081,7 +1082,7 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     if (cc_ne) {  // collate + batch CRC, one kernel
         const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
         const int rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
-                                          d_params, dsts, s, ep, crc_out, cc_ne);
+                                          d_params, dsts, s, ep, crc_out, cc_ne, crc_host);
         if (rc != TSB_ERR_STALE) {
             if (!rc && crc_done) *crc_done = 1;
             return rc;
@@ -1364,7 +1365,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
                             int pdl, void *stream, const int32_t *d_params,
                             const int64_t *tgt_idx, uint64_t *release, uint32_t *crc_out,
-                            int *crc_done) {
+                            int *crc_done, uint32_t *crc_host) {
     Dsts d{};
     d.p[0] = out;
     d.n = 1;
@@ -1383,7 +1384,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     ep.fence_all = fence_all_knob();
     ep.early_pdl = ca_early_knob();
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
-                          out_kind, d_params, d, stream, ep, crc_out, crc_done);
+                          out_kind, d_params, d, stream, ep, crc_out, crc_done, nullptr, crc_host);
 }
 
 // n batches of the augment mode into a host-control single-writer ring in one

@@ -66,6 +66,7 @@ struct CrcFuse {
     uint32_t *acc;          // this launch's accumulator (the completing CTA resets it)
     unsigned int *count;    // this launch's CTA completion counter (same)
     uint32_t *out;          // the slot's CRC-32
+    uint32_t *out_host;     // optional host-mapped copy (written before the ready word)
     int ne;                 // emit threads: groups x dr (dr rows apart, dr divides R)
 };
 
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
             __threadfence();
             const uint32_t v = atomicExch(cf.acc, 0u);
             *cf.out = v ^ cf.init;
+            if (cf.out_host) *cf.out_host = v ^ cf.init;
             __threadfence_system();
             for (int d = 0; d < ep.n; ++d)
                 if (ep.ready[d])
@@ -1059,7 +1061,7 @@ int launch_cc_c(int c, const uint8_t *src, const int64_t *idx, const CaGeom &g, 
 int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, int flip,
                        uint64_t aug_mixed, uint64_t epoch, const Norm &norm, int out_kind,
                        const int32_t *params, const Dsts &dsts, cudaStream_t s, const Epi &ep,
-                       uint32_t *crc_out, int ne) {
+                       uint32_t *crc_out, int ne, uint32_t *crc_host) {
     int dev = 0;
     TSB_CUDA(cudaGetDevice(&dev));
     CcKey key{};
@@ -1102,6 +1104,7 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     cf.acc = acc_base[dev] + slot;
     cf.count = cnt_base[dev] + slot;
     cf.out = crc_out;
+    cf.out_host = crc_host;
     cf.ne = ne;
     g.nstage = CC_STAGES;  // (the kernel uses the compile-time count)
     if (out_kind == TSB_OUT_U8)

@@ -9,9 +9,14 @@
 //   tsb_facade_produce:  the reference's flow gate on received wire Acks
 //                        (hub acked seqs >= q - buffer_depth), then the fused
 //                        producer launch with its slot-reuse gate on the
-//                        release cursors (tsb_produce_range), then, with a
-//                        checksum, the CRC's 4-byte read-back + an event;
-//   tsb_facade_announce: wait for that batch's CRC (if any), patch the 80-byte
+//                        release cursors (tsb_produce_range).  With a checksum
+//                        the collate kernel stores the batch CRC in host-mapped
+//                        memory before it publishes the slot (no copy, and the
+//                        next launch still chains); where the kernel cannot
+//                        (unfused geometries), the CRC's 4-byte read-back + an
+//                        event follow the launch;
+//   tsb_facade_announce: wait for that batch's CRC (if any: its ready word, or
+//                        the event), patch the 80-byte
 //                        segment header (epoch, crc, batch_index), base64 it
 //                        into the slot name, encode the Announce frame with
 //                        the native codec and write it to every consumer
@@ -43,6 +48,8 @@ struct tsb_facade {
     uint32_t *d_crc = nullptr;
     uint32_t *h_crc = nullptr;
     std::vector<cudaEvent_t> events;
+    std::vector<uint8_t> fused;  // per slot: the CRC came from the kernel (host-mapped)
+    bool tail_kernel = false;    // the stream's last operation is a fused produce kernel
     std::vector<uint64_t> ack_ids;
     std::vector<int> live;
     std::vector<int> fds;
@@ -106,6 +113,9 @@ int tsb_facade_set_batch(tsb_facade *f, tsb_hub *hub, tsb_ring *ring, const tsb_
         for (int i = 0; i < slots; ++i) f->events[i] = static_cast<cudaEvent_t>(events[i]);
     }
     f->args.d_crc = d_crc;
+    f->args.h_crc = d_crc ? h_crc : nullptr;  // pinned: device-accessible under UVA
+    f->fused.assign(slots, 0);
+    f->tail_kernel = false;
     return TSB_OK;
 }
 
@@ -125,12 +135,18 @@ int tsb_facade_produce(tsb_facade *f, uint64_t seq, int64_t index, int chain, in
                                           seq - (uint64_t)f->depth, timeout_us);
         if (rc) return rc;  // TSB_ERR_STALE: timed out (the caller re-checks for shutdown)
     }
-    f->args.chain = chain;
+    int fused = 0;
+    f->args.chain = chain && f->tail_kernel;
+    f->args.crc_fused = &fused;
     int rc = tsb_produce_range(f->ring, &f->args, seq, index, 1, f->live.data(),
                                (int)f->live.size(), nullptr, f->stream);
+    f->args.crc_fused = nullptr;
     if (rc) return rc;
+    f->tail_kernel = !f->d_crc || fused;
     if (f->d_crc) {
         const int slot = (int)((seq - 1) % (uint64_t)f->slots);
+        f->fused[slot] = (uint8_t)fused;
+        if (fused) return TSB_OK;  // the CRC is in h_crc[slot] when the slot is published
         auto s = static_cast<cudaStream_t>(f->stream);
         cudaError_t e = cudaMemcpyAsync(f->h_crc + slot, f->d_crc + slot, 4,
                                         cudaMemcpyDeviceToHost, s);
@@ -149,12 +165,17 @@ int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t in
     const int slot = (int)((seq - 1) % (uint64_t)f->slots);
     uint32_t crc = 0;
     if (with_crc && f->d_crc) {
-        const cudaError_t e = cudaEventSynchronize(f->events[slot]);
-        if (e != cudaSuccess) {
-            tsb::set_error("facade: checksum wait: %s", cudaGetErrorString(e));
-            return TSB_ERR_CUDA;
+        if (f->fused[slot]) {  // the kernel stored the CRC before the slot's ready word
+            if (int rc = tsb_ring_host_wait_ready(f->ring, slot, seq, 60 * 1000000ll)) return rc;
+            crc = reinterpret_cast<volatile uint32_t *>(f->h_crc)[slot];
+        } else {
+            const cudaError_t e = cudaEventSynchronize(f->events[slot]);
+            if (e != cudaSuccess) {
+                tsb::set_error("facade: checksum wait: %s", cudaGetErrorString(e));
+                return TSB_ERR_CUDA;
+            }
+            crc = f->h_crc[slot];
         }
-        crc = f->h_crc[slot];
     }
     // the segment header (payload.py:220-233): epoch u32 @8, crc u32 @12, index u64 @16
     uint8_t hdr[80];

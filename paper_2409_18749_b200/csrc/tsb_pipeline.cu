@@ -37,7 +37,8 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
                             int64_t *tgt, uint64_t *ready, uint64_t seq, unsigned int *counter,
                             int pdl, void *stream, const int32_t *d_params,
                             const int64_t *tgt_idx, uint64_t *release = nullptr,
-                            uint32_t *crc_out = nullptr, int *crc_done = nullptr);
+                            uint32_t *crc_out = nullptr, int *crc_done = nullptr,
+                            uint32_t *crc_host = nullptr);
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
                  void *dst, void *stream, int *k_out, bool after_stream,
                  const IngestCrop *crop = nullptr);
@@ -129,6 +130,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         TSB_CHECK(ingest_sample_bytes(a->ingest) == a->sample_bytes,
                   "ingest staging is for %lld-byte samples, not %lld",
                   (long long)ingest_sample_bytes(a->ingest), (long long)a->sample_bytes);
+    bool all_fused = a->d_crc != nullptr;  // every batch's CRC came from the collate kernel
+    if (a->crc_fused) *a->crc_fused = 0;
     for (int i = 0; i < n; ++i) {
         const uint64_t q = seq0 + (uint64_t)i;
         const int slot = (int)((q - 1) % (uint64_t)slots);
@@ -157,6 +160,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         // per-batch CRC fused into the collate when the geometry allows (the
         // kernel's completing CTA writes d_crc[slot] before the ready word)
         uint32_t *crc_out = a->d_crc ? a->d_crc + slot : nullptr;
+        uint32_t *crc_host = a->d_crc && a->h_crc ? a->h_crc + slot : nullptr;
         int crc_done = 0;
         switch (a->mode) {
             case TSB_SRC_AUGMENT:
@@ -183,7 +187,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                      a->epoch, a->scale, a->bias, a->out_kind, out,
                                                      tgt, ready, q, counter, 0, stream, params,
                                                      jpeg_indices(a->jpeg), nullptr, crc_out,
-                                                     &crc_done);
+                                                     &crc_done, crc_host);
                         published = true;
                         break;
                     }
@@ -203,7 +207,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                      a->scale, a->bias, a->out_kind, out, tgt,
                                                      ready, q, counter, 0, stream, params,
                                                      ingest_indices(a->ingest, k), nullptr,
-                                                     crc_out, &crc_done);
+                                                     crc_out, &crc_done, crc_host);
                         if (!rc) rc = ingest_release(a->ingest, k, stream);
                         published = true;
                         break;
@@ -212,7 +216,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                                                  a->flip, a->seed, a->epoch, a->scale, a->bias,
                                                  a->out_kind, out, tgt, ready, q, counter, pdl,
                                                  stream, nullptr, nullptr, nullptr, crc_out,
-                                                 &crc_done);
+                                                 &crc_done, crc_host);
                     published = true;
                     break;
                 }
@@ -285,6 +289,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         // (and nothing rewrites it before every consumer released it).  The
         // CRC launches sit between two collates, so that pair is not PDL-chained.
         prev_fused = published && (!a->d_crc || crc_done);
+        all_fused = all_fused && crc_done;
         if (ev) TSB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[2 * i + 1]), s));
         if (published) {
             if (a->d_crc && !crc_done)
@@ -298,6 +303,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
             if (int rc2 = tsb_crc32(out, nbytes, a->d_crc + slot, nullptr, stream)) return rc2;
         if (int rc3 = tsb_ring_publish(r, slot, q, stream)) return rc3;
     }
+    if (a->crc_fused) *a->crc_fused = all_fused && n > 0 ? 1 : 0;
     return TSB_OK;
 }
 
