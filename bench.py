@@ -663,7 +663,7 @@ def bf16_line(dev, store, ds, K: int, Wm: int) -> dict:
 
 def run_e2e(args, ctx, dev, rank, world):
     """e2e through the public API.  N = 1: TensorProducer over a pinned-host
-    store (copy-engine ingest) and 4 SharedLoader processes.  N > 1: rank 0
+    store (gather-kernel ingest) and 4 SharedLoader processes.  N > 1: rank 0
     runs ONE TensorProducer(devices=[every rank's GPU]) -- each GPU ingests
     its 1/N rows of every batch over its own PCIe link and the collate kernel
     stores them into every GPU's ring (fused all-gather) -- and every rank
@@ -719,7 +719,7 @@ def run_e2e(args, ctx, dev, rank, world):
         producer.join(drain_timeout_s=60)
     h2d = B * SAMPLE_BYTES  # every sample row (sharded multi-GPU ingest)
     if producer is not None and world == 1 and loader._ingest is not None and produced:
-        # copy-engine ingest counts what it enqueued: the rows the crop reads,
+        # the ingest counts what it enqueued: the rows the crop reads,
         # plus the index and parameter uploads
         h2d = int(round(loader._ingest.bytes_enqueued() / produced))
     rates, stamps = {}, {}

@@ -306,7 +306,7 @@ class CollateLoader:
         self.with_target = with_target
         self.device = torch.cuda.current_device() if device is None else device
         self._order = _EpochOrder()
-        self._ingest = None  # staged copy-engine ingest (pinned-host stores)
+        self._ingest = None  # staged PCIe ingest (pinned-host stores)
         self.epoch = 0  # the epoch __iter__ produces next
         src = dataset.source
         if augment is not None:

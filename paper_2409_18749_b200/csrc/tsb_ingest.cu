@@ -33,7 +33,7 @@ struct tsb_ingest {
     int64_t *h_idx;       // [depth][max_batch] pinned upload buffer
     int32_t *h_params;    // [depth][max_batch][3] pinned upload buffer (crop-aware batches)
     uint64_t bytes;       // H2D bytes enqueued (tsb_ingest_bytes)
-    cudaStream_t stream;  // copy-engine stream
+    cudaStream_t stream;  // ingest stream (beside the producer stream)
     std::vector<cudaEvent_t> done, freed;
     std::vector<int> used;
     int next;

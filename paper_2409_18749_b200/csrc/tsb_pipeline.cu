@@ -191,7 +191,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                         published = true;
                         break;
                     }
-                    if (staged) {  // copy-engine ingest into HBM staging, then collate it
+                    if (staged) {  // PCIe ingest into HBM staging, then collate it
                         // crop-aware: only the rows the crop reads cross PCIe, and the
                         // param table is derived on the host and uploaded with the indices
                         const IngestCrop crop{mix64(a->seed ^ AUG_DOMAIN), a->epoch, a->h, a->w,
@@ -237,7 +237,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
                     }
                     break;
                 }
-                if (staged) {  // copy engine straight into the slot (no kernel)
+                if (staged) {  // the ingest gather straight into the slot
                     int k = 0;
                     if ((rc = ingest_batch(a->ingest, a->src, a->h_order + bi * b, b, out, stream,
                                            &k, !host_gate)))

@@ -202,7 +202,7 @@ class TensorProducer:
         self._hdr_key = None
         self._hdr_reserved = b""
         # checksum=True: a batch is announced once its CRC-32 reached the host,
-        # which is after the NEXT batch was enqueued (the copy engine / collate
+        # which is after the NEXT batch was enqueued (the ingest / collate
         # of batch q+1 never waits for batch q's checksum)
         self._pending_ann = None
         # the fast path with a checksum announces ANN_LAG batches behind the
