@@ -46,7 +46,7 @@ constexpr int CC_EMIT = 448;       // 14 emit warps (8 / 16 / 32 rows apart for 
 constexpr int CC_MAX_RUNS = 9;     // combiner warps: 32-element column runs per row (w <= 288)
 constexpr int CC_MAX_C = 3;
 constexpr int CC_SMEM = 232448;    // the 227 KB opt-in maximum
-constexpr int CC_STAGES = 3;
+constexpr int CC_MAX_STAGES = 8;  // item stages: as many as fit next to the tables (3 at 32 rows of 224x3)
 constexpr uint32_t CC_IMG_WORDS = 2 * 256 * 64;  // the two table regions (128 KB)
 constexpr int CC_ACC_POOL = 1024;
 constexpr int CC_MAX_PLANS = 64;   // table sets per process (never freed: kernels may be in flight)
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
     constexpr int NS = P / 4;
     const int NT = cf.ne;
     const int NCW = NT >> 5;             // emit warps; warp NCW = producer; then the combiners
-    constexpr int NST = CC_STAGES;
+    const int NST = g.nstage;
     const int runs = g.w >> 5;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
     constexpr int P = T::P;
     constexpr int E = T::ELEM;
     constexpr int NS = P / 4;
-    constexpr int NST = CC_STAGES;
+    const int NST = g.nstage;
     const int NT = cf.ne;
     const int NCW = NT >> 5;
     const int runs = g.w >> 5;
@@ -993,6 +993,21 @@ int cc_mode_knob() {
     return v;
 }
 
+// Item stages that fit next to the tables for any dynamic shared base the
+// runtime may pick (TSB_CC_STAGES caps it, A/B); < 2: the kernel does not fit.
+int cc_stages(const CaGeom &g, int c) {
+    static const int cap = getenv("TSB_CC_STAGES") ? atoi(getenv("TSB_CC_STAGES")) : CC_MAX_STAGES;
+    const uint32_t part = 4u * (uint32_t)(c * g.R * (g.w / 32));
+    for (int n = cap < CC_MAX_STAGES ? cap : CC_MAX_STAGES; n >= 2; --n) {
+        bool ok = true;
+        CcLayout L;
+        for (uint32_t sb : {0u, 1024u, 2048u})
+            ok = ok && cc_layout(sb, (uint32_t)(g.R * g.rs), (uint32_t)g.rs, part, n, L);
+        if (ok) return n;
+    }
+    return 0;
+}
+
 // Can this batch take the fused kernel?  Returns its emit thread count
 // (groups x dr, a whole number of warps, dr dividing the item's rows) or 0:
 // collate, then tsb_crc32.
@@ -1007,11 +1022,7 @@ int cc_fusable(const CaGeom &g, int c, int out_kind, const Dsts &dsts, bool publ
     for (int dr = g.R; dr >= 1 && !ne; --dr)
         if (g.R % dr == 0 && groups * dr <= CC_EMIT && (groups * dr) % 32 == 0) ne = groups * dr;
     if (!ne) return 0;
-    // the layout must fit for the dynamic shared base the runtime may pick
-    CcLayout L;
-    const uint32_t part = 4u * (uint32_t)(c * g.R * (g.w / 32));
-    for (uint32_t sb : {0u, 1024u, 2048u})
-        if (!cc_layout(sb, (uint32_t)(g.R * g.rs), (uint32_t)g.rs, part, CC_STAGES, L)) return 0;
+    if (cc_stages(g, c) < 2) return 0;
     return ne;
 }
 
@@ -1106,7 +1117,7 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     cf.out = crc_out;
     cf.out_host = crc_host;
     cf.ne = ne;
-    g.nstage = CC_STAGES;  // (the kernel uses the compile-time count)
+    g.nstage = cc_stages(g, c);
     if (out_kind == TSB_OUT_U8)
         return launch_cc_c<TSB_OUT_U8>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
     if (out_kind == TSB_OUT_F32)
@@ -1192,7 +1203,7 @@ int launch_collate_crc_range(const uint8_t *src, const int64_t *order0, CaGeom g
     rg.acc_base = acc_next.fetch_add((unsigned)rg.n, std::memory_order_relaxed) % CC_ACC_POOL;
     rg.gate = gate_words[dev];
     TSB_CUDA(cudaMemsetAsync(rg.gate, 0, sizeof(unsigned long long), s));
-    g.nstage = CC_STAGES;
+    g.nstage = cc_stages(g, c);
 #define TSB_CCR(KK)                                                                            \
     switch (c) {                                                                               \
         case 1: return launch_ccr<KK, 1>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \

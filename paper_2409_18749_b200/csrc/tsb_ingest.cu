@@ -51,11 +51,11 @@ __global__ void iota_kernel(int64_t *p, int64_t n) {
 // the crop reads (rows [max(0, oy-pad), min(h, h+oy-pad))); else the sample.
 // 16-byte vectors when every offset is 16-byte aligned, else bytes.
 constexpr int IG_THREADS = 256;
-constexpr int IG_CHUNK = 16384;  // bytes per CTA and sample
+constexpr int IG_U = 4;            // 16-byte loads in flight per thread
 __global__ void __launch_bounds__(IG_THREADS)
     ingest_gather_kernel(const uint8_t *__restrict__ host, const int64_t *__restrict__ idx,
                          const int32_t *__restrict__ params, int64_t sb, int row_bytes, int h,
-                         int pad, int vec, uint8_t *__restrict__ out) {
+                         int pad, int vec, int64_t chunk, uint8_t *__restrict__ out) {
     const int s = blockIdx.y;
     int64_t begin = 0, end = sb;
     if (params) {
@@ -64,23 +64,24 @@ __global__ void __launch_bounds__(IG_THREADS)
         begin = (int64_t)lo * row_bytes;
         end = hi > lo ? (int64_t)hi * row_bytes : begin;
     }
-    const int64_t c0 = begin + (int64_t)blockIdx.x * IG_CHUNK;
-    const int64_t c1 = min(c0 + IG_CHUNK, end);
+    const int64_t c0 = begin + (int64_t)blockIdx.x * chunk;
+    const int64_t c1 = min(c0 + chunk, end);
     if (c0 >= c1) return;
     const uint8_t *src = host + idx[s] * sb;
     uint8_t *dst = out + (int64_t)s * sb;
     if (vec) {
-        constexpr int U = IG_CHUNK / 16 / IG_THREADS;
-        uint4 v[U];
+        for (int64_t o0 = c0 + 16 * (int64_t)threadIdx.x; o0 < c1; o0 += 16 * IG_THREADS * IG_U) {
+            uint4 v[IG_U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t o = c0 + 16 * (int64_t)(threadIdx.x + u * IG_THREADS);
-            if (o < c1) v[u] = ld_nc_v4(src + o);
-        }
+            for (int u = 0; u < IG_U; ++u) {
+                const int64_t o = o0 + 16 * (int64_t)(u * IG_THREADS);
+                if (o < c1) v[u] = ld_nc_v4(src + o);
+            }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t o = c0 + 16 * (int64_t)(threadIdx.x + u * IG_THREADS);
-            if (o < c1) *reinterpret_cast<uint4 *>(dst + o) = v[u];
+            for (int u = 0; u < IG_U; ++u) {
+                const int64_t o = o0 + 16 * (int64_t)(u * IG_THREADS);
+                if (o < c1) *reinterpret_cast<uint4 *>(dst + o) = v[u];
+            }
         }
     } else {
         for (int64_t o = c0 + threadIdx.x; o < c1; o += IG_THREADS) dst[o] = src[o];
@@ -179,11 +180,14 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     }
     const bool vec = ((uintptr_t)host_store & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
                      sb % 16 == 0 && (!crop || row_bytes % 16 == 0);
-    dim3 grid((unsigned)((sb + IG_CHUNK - 1) / IG_CHUNK), (unsigned)b);
+    // bytes per CTA and sample (TSB_IG_CHUNK A/B; 16 KB default)
+    static const int64_t chunk =
+        getenv("TSB_IG_CHUNK") ? (int64_t)atoll(getenv("TSB_IG_CHUNK")) : 16384;
+    dim3 grid((unsigned)((sb + chunk - 1) / chunk), (unsigned)b);
     TSB_CHECK(b <= 65535, "batch %lld exceeds the gather grid", (long long)b);
     ingest_gather_kernel<<<grid, IG_THREADS, 0, g->stream>>>(
         static_cast<const uint8_t *>(host_store), dk, crop ? pk : nullptr, (int64_t)sb, row_bytes,
-        crop ? crop->h : 0, crop ? crop->pad : 0, vec ? 1 : 0, out);
+        crop ? crop->h : 0, crop ? crop->pad : 0, vec ? 1 : 0, chunk, out);
     TSB_LAUNCH_CHECK();
     g->bytes += nbytes;
     TSB_CUDA(cudaEventRecord(g->done[k], g->stream));
