@@ -32,7 +32,8 @@
 // lane-replicated nibble tables), the warp XOR-reduces the rows, and the run
 // offset and the segment's place in the slot are applied by bit expansion
 // (W[m][i] = x^(8 (SEGB m + tail)) * e_i: bit i of the value selects lane i's
-// word), accumulated per lane -- no per-segment reduction.  Block 0's first
+// word; one table per column run folds in the run's offset), accumulated per
+// lane -- no per-segment reduction.  Block 0's first
 // combiner also folds in the int64 target that follows the input.  At the
 // end each combiner reduces its accumulator into one device word
 // (atomicXor), and the CTA that completes the batch turns it into the zlib
@@ -56,8 +57,7 @@ __device__ unsigned int g_cc_cnt[CC_ACC_POOL]; // per-launch CTA completion coun
 struct CrcFuse {
     const uint32_t *img;    // CC_IMG_WORDS: the shared image of the two table regions
     const uint32_t *slice;  // zlib slice-by-4 tables T0..T3 (target checksum)
-    const uint32_t *wtab;   // [nseg][32]
-    const uint32_t *wrun;   // [runs][32]: x^(8*32E*(runs-1-run)) * e_i
+    const uint32_t *wtab;   // [runs][nseg][32]: run -> row end, segment -> slot end
     uint32_t tgt_k[5];      // x^(8 * 8 nl 2^k): the target lanes' tree
     uint32_t init;          // x^(8 total) * ~0 ^ ~0: the init/xorout term of the slot
     int nseg;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
         // ------- combiner warps: one column run, lane = row of the item ---------------
         const int run = warp - NCW - 1;
         const uint32_t rowsh = L.r2 + 128u + 4u * (uint32_t)lane + (128u << 8);  // x^(8 wE (R-1-lane))
-        const uint32_t wrun = __ldg(cf.wrun + run * 32 + lane);  // x^(8*32E*(runs-1-run)) * e_lane
+        const uint32_t *wrun_tab = cf.wtab + (int64_t)run * cf.nseg * 32 + lane;
         uint32_t wacc = 0;
         if (blockIdx.x == 0 && run == 0 && cf.with_tgt) {
             // raw CRC of the int64 target (b entries after the input): lane l takes
@@ -440,8 +440,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
             uint32_t wv[C];
 #pragma unroll
             for (int c = 0; c < C; ++c)
-                wv[c] = __ldg(cf.wtab + (int64_t)(cf.nseg - 1 - ((p.s * C + c) * g.nrb + rb)) * 32 +
-                              lane);
+                wv[c] = __ldg(wrun_tab + (int64_t)(cf.nseg - 1 - ((p.s * C + c) * g.nrb + rb)) * 32);
             cc_wait(&pfull[st], ph);
             uint32_t S[C];
 #pragma unroll
@@ -455,11 +454,8 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
                 uint32_t x = lane < g.R ? cc_mul_nib(S[c], rowsh) : 0u;  // row -> segment's last row
 #pragma unroll
                 for (int k2 = 16; k2 >= 1; k2 >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, k2);
-                // the run's column -> the row's end, then the segment -> the slot's end
-                uint32_t t2 = ((x >> lane) & 1u) ? wrun : 0u;
-#pragma unroll
-                for (int k2 = 16; k2 >= 1; k2 >>= 1) t2 ^= __shfl_xor_sync(0xFFFFFFFFu, t2, k2);
-                wacc ^= ((t2 >> lane) & 1u) ? wv[c] : 0u;
+                // the run's column -> the row's end and the segment -> the slot's end
+                wacc ^= ((x >> lane) & 1u) ? wv[c] : 0u;
             }
         }
 #pragma unroll
@@ -772,7 +768,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
         // ------- combiner warps: one column run, lane = row of the item ---------------
         const int run = warp - NCW - 1;
         const uint32_t rowsh = L.r2 + 128u + 4u * (uint32_t)lane + (128u << 8);
-        const uint32_t wrun = __ldg(cf.wrun + run * 32 + lane);
+        const uint32_t *wrun_tab = cf.wtab + (int64_t)run * cf.nseg * 32 + lane;
         uint32_t wacc = 0;
         cc_wait(tab_bar, 0);
         for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
@@ -782,7 +778,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
             uint32_t wv[C];
 #pragma unroll
             for (int c = 0; c < C; ++c)
-                wv[c] = __ldg(cf.wtab + (int64_t)(cf.nseg - 1 - ((s_ * C + c) * g.nrb + rb)) * 32 + lane);
+                wv[c] = __ldg(wrun_tab + (int64_t)(cf.nseg - 1 - ((s_ * C + c) * g.nrb + rb)) * 32);
             if (j == 0 && run == 0 && cf.with_tgt) {  // raw CRC of the batch's int64 target
                 const int64_t *idx = order0 + (int64_t)bi * g.b;
                 const int nl = (g.b + 31) >> 5, z = 32 * nl - g.b;
@@ -816,10 +812,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
                 uint32_t x = lane < g.R ? cc_mul_nib(S[c], rowsh) : 0u;
 #pragma unroll
                 for (int k2 = 16; k2 >= 1; k2 >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, k2);
-                uint32_t t2 = ((x >> lane) & 1u) ? wrun : 0u;
-#pragma unroll
-                for (int k2 = 16; k2 >= 1; k2 >>= 1) t2 ^= __shfl_xor_sync(0xFFFFFFFFu, t2, k2);
-                wacc ^= ((t2 >> lane) & 1u) ? wv[c] : 0u;
+                wacc ^= ((x >> lane) & 1u) ? wv[c] : 0u;
             }
             if (batch_ends(k, bi)) {  // flush this batch's share of the checksum
 #pragma unroll
@@ -893,7 +886,7 @@ struct CcKey {
 };
 struct CcPlan {
     CcKey key;
-    uint32_t *d_img = nullptr, *d_slice = nullptr, *d_w = nullptr, *d_wrun = nullptr;
+    uint32_t *d_img = nullptr, *d_slice = nullptr, *d_w = nullptr;
     uint32_t tgt_k[5];
     uint32_t init;
     int nseg;
@@ -941,28 +934,26 @@ int cc_plan(const CcKey &key, cudaStream_t s, const CcPlan **out) {
                 img[(size_t)(256 + 128 + j * 16 + q) * 64 + 32 + l] =
                     l < key.R ? cc_h_multmodp(kr, q << (4 * j)) : 0u;
     }
-    // the column run -> the row's end: x^(8*32E*(runs-1-run)) * e_i
     const int runs = key.w / 32;
-    std::vector<uint32_t> wr((size_t)runs * 32);
-    for (int r = 0; r < runs; ++r) {
-        const uint32_t kr = cc_h_x8n((uint64_t)32 * E * (runs - 1 - r));
-        for (int i = 0; i < 32; ++i) wr[(size_t)r * 32 + i] = cc_h_multmodp(kr, 1u << i);
-    }
     const int nrb = key.h / key.R;
     const int64_t nseg = (int64_t)key.b * key.c * nrb;
     const uint64_t segb = (uint64_t)key.R * key.w * E;
     const uint64_t tail = key.with_tgt ? 8ull * (uint64_t)key.b : 0ull;
-    std::vector<uint32_t> wt((size_t)nseg * 32);
+    // W[run][m][i] = x^(8 (SEGB m + tail + 32E (runs-1-run))) * e_i: the column
+    // run's value -> the end of its row, and segment m -> the slot's end.  Bit i
+    // is x^(31-i), so W[..][31] = K and each step down multiplies by x.
+    std::vector<uint32_t> wt((size_t)runs * nseg * 32);
     const uint32_t k_seg = cc_h_x8n(segb);
-    uint32_t km = cc_h_x8n(tail);
-    for (int64_t m = 0; m < nseg; ++m) {
-        // W[m][i] = K_m * e_i: bit i is x^(31-i), so W[m][31] = K_m and each step down is *x
-        uint32_t v = km;
-        for (int i = 31; i >= 0; --i) {
-            wt[(size_t)m * 32 + i] = v;
-            v = (v & 1) ? (v >> 1) ^ CC_POLY : v >> 1;
+    for (int r = 0; r < runs; ++r) {
+        uint32_t km = cc_h_multmodp(cc_h_x8n(tail), cc_h_x8n((uint64_t)32 * E * (runs - 1 - r)));
+        for (int64_t m = 0; m < nseg; ++m) {
+            uint32_t v = km;
+            for (int i = 31; i >= 0; --i) {
+                wt[((size_t)r * nseg + m) * 32 + i] = v;
+                v = (v & 1) ? (v >> 1) ^ CC_POLY : v >> 1;
+            }
+            km = cc_h_multmodp(k_seg, km);
         }
-        km = cc_h_multmodp(k_seg, km);
     }
     CcPlan &pl = plans[n_plans];
     pl.key = key;
@@ -973,13 +964,11 @@ int cc_plan(const CcKey &key, cudaStream_t s, const CcPlan **out) {
     TSB_CUDA(cudaMalloc(&pl.d_img, img.size() * 4));
     TSB_CUDA(cudaMalloc(&pl.d_slice, slice.size() * 4));
     TSB_CUDA(cudaMalloc(&pl.d_w, wt.size() * 4));
-    TSB_CUDA(cudaMalloc(&pl.d_wrun, wr.size() * 4));
     // stream-ordered before the launch; synchronous on the host side so the
     // staging vectors may go (pageable sources are staged before return)
     TSB_CUDA(cudaMemcpyAsync(pl.d_img, img.data(), img.size() * 4, cudaMemcpyHostToDevice, s));
     TSB_CUDA(cudaMemcpyAsync(pl.d_slice, slice.data(), slice.size() * 4, cudaMemcpyHostToDevice, s));
     TSB_CUDA(cudaMemcpyAsync(pl.d_w, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice, s));
-    TSB_CUDA(cudaMemcpyAsync(pl.d_wrun, wr.data(), wr.size() * 4, cudaMemcpyHostToDevice, s));
     TSB_CUDA(cudaStreamSynchronize(s));
     ++n_plans;
     *out = &pl;
@@ -1106,7 +1095,6 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     cf.img = pl->d_img;
     cf.slice = pl->d_slice;
     cf.wtab = pl->d_w;
-    cf.wrun = pl->d_wrun;
     memcpy(cf.tgt_k, pl->tgt_k, sizeof(cf.tgt_k));
     cf.init = pl->init;
     cf.nseg = pl->nseg;
@@ -1192,7 +1180,6 @@ int launch_collate_crc_range(const uint8_t *src, const int64_t *order0, CaGeom g
     cf.img = pl->d_img;
     cf.slice = pl->d_slice;
     cf.wtab = pl->d_w;
-    cf.wrun = pl->d_wrun;
     memcpy(cf.tgt_k, pl->tgt_k, sizeof(cf.tgt_k));
     cf.init = pl->init;
     cf.nseg = pl->nseg;

@@ -816,7 +816,8 @@ class TensorProducer:
         # the native path knows whether its stream ends in a fused kernel (a
         # checksum read-back copy breaks the chain only for unfused geometries)
         self._chain_ok = True
-        self._sample_live(q, {0: self._fast_live})
+        if ann is not None:  # live = announced and not yet released
+            self._sample_live(ann[0], {0: self._fast_live})
         if self._checksum:
             if ann is not None:
                 self._pend_fast.popleft()
