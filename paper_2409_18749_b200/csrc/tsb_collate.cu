@@ -256,6 +256,7 @@ __device__ __forceinline__ void publish_epilogue(const Epi &ep, int tid, int nth
         else
             __threadfence();
     }
+    __syncwarp();  // reconverge: a named barrier counts whole warps
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
     if (tid == 0) {
         if (ep.sys_fence)
@@ -953,8 +954,7 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
                    int pad, int flip, uint64_t aug_seed, uint64_t epoch, const float *scale,
                    const float *bias, int out_kind, const int32_t *d_params, const Dsts &dsts,
                    void *stream, const Epi &ep = Epi{}, uint32_t *crc_out = nullptr,
-                   int *crc_done = nullptr, const CcRange *range = nullptr,
-                   uint32_t *crc_host = nullptr) {
+                   int *crc_done = nullptr, uint32_t *crc_host = nullptr) {
     TSB_CHECK(src && d_indices, "null src/indices");
     TSB_CHECK(b >= 0 && h > 0 && w > 0 && c > 0 && c <= 4, "bad shape b=%lld h=%d w=%d c=%d",
               (long long)b, h, w, c);
@@ -1071,13 +1071,6 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     const auto *s8 = static_cast<const uint8_t *>(src);
     auto s = as_stream(stream);
     if (crc_done) *crc_done = 0;
-    if (range) {  // n batches, one persistent launch (TSB_ERR_STALE: not this geometry)
-        const int ne = cc_fusable(g, c, out_kind, dsts, true);
-        if (!ne) return TSB_ERR_STALE;
-        const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
-        return launch_collate_crc_range(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k, s,
-                                        *range, ne);
-    }
     const int cc_ne = crc_out ? cc_fusable(g, c, out_kind, dsts, ep.counter != nullptr) : 0;
     if (cc_ne) {  // collate + batch CRC, one kernel
         const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
@@ -1384,40 +1377,7 @@ int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b
     ep.fence_all = fence_all_knob();
     ep.early_pdl = ca_early_knob();
     return launch_collate(src, d_indices, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
-                          out_kind, d_params, d, stream, ep, crc_out, crc_done, nullptr, crc_host);
-}
-
-// n batches of the augment mode into a host-control single-writer ring in one
-// persistent launch, the batch CRC-32 fused, the slot gate on the device.
-// TSB_ERR_STALE: the geometry does not take the fused kernel (per-batch path).
-int collate_crc_range(const void *src, const int64_t *order0, int64_t b, int h, int w, int c,
-                      int pad, int flip, uint64_t aug_seed, uint64_t epoch, const float *scale,
-                      const float *bias, int out_kind, uint8_t *ring_base, int64_t slot_stride,
-                      int slots, uint64_t *ready, const uint64_t *cursors, unsigned int *counters,
-                      const int *live, int n_live, int64_t input_bytes, int with_target,
-                      uint64_t seq0, int n, uint32_t *d_crc, void *stream) {
-    TSB_CHECK(n_live <= CC_MAX_LIVE, "at most %d live consumers", CC_MAX_LIVE);
-    TSB_CHECK(d_crc && ring_base && ready && counters, "null argument");
-    if (n <= 0) return TSB_OK;
-    CcRange rg{};
-    rg.ring_base = ring_base;
-    rg.slot_stride = slot_stride;
-    rg.slots = slots;
-    rg.ready = ready;
-    rg.cursors = cursors;
-    rg.counters = counters;
-    for (int j = 0; j < n_live; ++j) rg.live[j] = live[j];
-    rg.n_live = n_live;
-    rg.seq0 = seq0;
-    rg.n = n;
-    rg.input_bytes = input_bytes;
-    rg.with_target = with_target;
-    rg.d_crc = d_crc;
-    Dsts d{};
-    d.p[0] = ring_base;  // (alignment check only; the kernel addresses slots itself)
-    d.n = 1;
-    return launch_collate(src, order0, b, h, w, c, pad, flip, aug_seed, epoch, scale, bias,
-                          out_kind, nullptr, d, stream, Epi{}, nullptr, nullptr, &rg);
+                          out_kind, d_params, d, stream, ep, crc_out, crc_done, crc_host);
 }
 
 // One batch shard into n destinations (fan-out), fused target copy + publish:

@@ -154,7 +154,7 @@ __device__ __forceinline__ uint32_t cc_gather4(const uint32_t *wv) {
 struct CcLayout {
     uint32_t r1, r2;        // shared addresses of the two table regions
     uint32_t lo_stage, n_lo, hi_stage;  // stages: n_lo at lo_stage, the rest at hi_stage
-    uint32_t zero, bars, par, part, meta;  // offsets
+    uint32_t zero, bars, par, part;     // offsets
 };
 __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, uint32_t rs,
                                           uint32_t part_bytes, int nstage, CcLayout &L) {
@@ -172,7 +172,7 @@ __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, 
     };
     bool ok = take((3 * nstage + 1) * 8, 8, L.bars) &&
               take(META_CAP * (uint32_t)sizeof(ItemPar), 16, L.par) && take(rs, 128, L.zero) &&
-              take(part_bytes * nstage, 16, L.part) && take(32u * nstage, 16, L.meta);
+              take(part_bytes * nstage, 16, L.part);
     // stages: as many as fit below region 1, the rest above region 2
     L.lo_stage = (lo + 127) & ~127u;
     const uint32_t below = lo_end > L.lo_stage ? (lo_end - L.lo_stage) / stage_bytes : 0;
@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
         for (int k2 = 16; k2 >= 1; k2 >>= 1) wacc ^= __shfl_xor_sync(0xFFFFFFFFu, wacc, k2);
         if (lane == 0 && wacc) atomicXor(cf.acc, wacc);
     }
-    // the completing CTA finishes the checksum, then publishes the slot
+    // the completing CTA finishes the checksum, then publishes the slot (each
+    // warp reconverges first: a named barrier counts whole warps)
+    __syncwarp();
     asm volatile("bar.sync 1, %0;" ::"r"(NT + 32 * runs) : "memory");
     if (tid == 0) {
         __threadfence();
@@ -479,349 +481,6 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
                     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ep.ready[d]),
                                  "l"(ep.seq)
                                  : "memory");
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent range variant: ONE launch produces n consecutive batches of a
-// range (tsb_produce_range with persistent=1), one CTA per SM for the whole
-// range.  The per-batch kernel pays, per batch and SM, the CTA launch, the
-// 128 KB table load, the stage zeroing and the pipeline fill and drain --
-// 6 us of a 36 us f32 batch (per-batch time vs B: 21.6 / 36.3 / 66.5 us at
-// B = 128 / 256 / 512).  Here the work items of all n batches form one
-// stream (CTA b takes items b, b + grid, ...), so a CTA's pipeline runs
-// across batch boundaries.  The slot gate moves to the device: before the
-// first item of batch q the producer warp waits until every live consumer
-// released q - slots (CTA 0 reads the host-shared cursors and raises a gate
-// word the other CTAs poll in L2; bs/producer.py:230-238 is the reference's
-// gate).  When a CTA has done its last item of a batch, its consumer warps
-// meet on a named barrier, the combiners having flushed the batch's partial
-// checksum, and one thread counts the CTA's items into the slot's counter;
-// the CTA that completes the batch writes its CRC-32 and publishes the slot.
-constexpr int CC_MAX_LIVE = 16;
-struct CcRange {
-    uint8_t *ring_base;
-    int64_t slot_stride;
-    int slots;
-    uint64_t *ready;             // [slots] (single writer)
-    const uint64_t *cursors;     // release cursors (host-shared, device-mapped)
-    unsigned int *counters;      // [slots] completion counters (zero at rest)
-    unsigned long long *gate;    // device word: every live cursor has released this much
-    int live[CC_MAX_LIVE];
-    int n_live;
-    uint64_t seq0;
-    int n;
-    int64_t input_bytes;
-    int with_target;
-    uint32_t *d_crc;             // [slots]: each batch's CRC-32, written before its publish
-    uint32_t *acc_pool;          // g_cc_acc
-    unsigned acc_base;           // batch i accumulates into acc_pool[(acc_base + i) % POOL]
-};
-struct CcItem {                  // per stage: the staged item (written by the producer)
-    ItemPar p;
-    int batch, j;
-};
-
-__device__ __forceinline__ uint64_t cc_ld_acquire_sys(const uint64_t *p) {
-    uint64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// min over the live release cursors (host-shared, PCIe reads), wrap-around order
-__device__ __forceinline__ uint64_t cc_min_live(const CcRange &rg, uint64_t need) {
-    uint64_t lo = need + (1ull << 61);
-    for (int j = 0; j < rg.n_live; ++j) {
-        const uint64_t c = cc_ld_acquire_sys(rg.cursors + rg.live[j]);
-        if ((int64_t)(c - lo) < 0) lo = c;
-    }
-    return lo;
-}
-
-template <int OUT_KIND, int C>
-__global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
-    collate_crc_range_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ order0,
-                             CaGeom g, int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
-                             CrcFuse cf, CcRange rg) {
-    using T = OutTraits<OUT_KIND>;
-    constexpr int P = T::P;
-    constexpr int E = T::ELEM;
-    constexpr int NS = P / 4;
-    const int NST = g.nstage;
-    const int NT = cf.ne;
-    const int NCW = NT >> 5;
-    const int runs = g.w >> 5;
-    extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t stage_bytes = (uint32_t)(g.R * g.rs);
-    const int part_words = C * g.R * runs;
-    CcLayout L;
-    if (!cc_layout(sbase, stage_bytes, (uint32_t)g.rs, 4u * part_words, NST, L)) __trap();
-    auto soff = [&](int st) -> uint32_t {
-        return (uint32_t)st < L.n_lo ? L.lo_stage + (uint32_t)st * stage_bytes
-                                      : L.hi_stage + ((uint32_t)st - L.n_lo) * stage_bytes;
-    };
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
-    uint64_t *empty = full + NST;
-    uint64_t *pfull = empty + NST;
-    uint64_t *tab_bar = pfull + NST;
-    uint32_t *part = reinterpret_cast<uint32_t *>(smem + L.part);
-    CcItem *meta = reinterpret_cast<CcItem *>(smem + L.meta);
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int items = g.items;  // per batch
-    const int64_t total = (int64_t)items * rg.n;
-    const int grid = (int)gridDim.x;
-    // the item sequence of this CTA: k -> item b + k * grid of the range
-    const int nk = (int)((total - (int64_t)blockIdx.x + grid - 1) / grid);
-
-    for (int st = 0; st < NST; ++st) {
-        uint4 *z = reinterpret_cast<uint4 *>(smem + soff(st));
-        for (int i = tid; i < (int)(stage_bytes >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    }
-    {
-        uint4 *z = reinterpret_cast<uint4 *>(smem + L.zero);
-        for (int i = tid; i < (g.rs >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    }
-    if (tid == 0) {
-        for (int i = 0; i < NST; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NCW + runs);
-            mbar_init(&pfull[i], NT);
-        }
-        mbar_init(tab_bar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    auto item_of = [&](int k, int &bi, int &j) {
-        const int64_t gi = (int64_t)blockIdx.x + (int64_t)k * grid;
-        bi = (int)(gi / items);
-        j = (int)(gi - (int64_t)bi * items);
-    };
-    // is item k this CTA's last of its batch?
-    auto batch_ends = [&](int k, int bi) {
-        if (k + 1 >= nk) return true;
-        int b2, j2;
-        item_of(k + 1, b2, j2);
-        return b2 != bi;
-    };
-
-    if (warp == NCW) {
-        // ---------------- producer warp: tables, the device slot gate, the items ----
-        if (lane == 0) {
-            fence_proxy_async();
-            mbar_arrive_expect_tx(tab_bar, CC_IMG_WORDS * 4u);
-            tma_load_1d(smem + (L.r1 - sbase), cf.img, 65536u, tab_bar);
-            tma_load_1d(smem + (L.r2 - sbase), cf.img + CC_IMG_WORDS / 2, 65536u, tab_bar);
-        }
-        uint64_t known = 0;  // lane 0: every live cursor is known to have released this level
-        int gated = -1;
-        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
-            int bi, j;
-            item_of(k, bi, j);
-            if (k >= NST) cc_wait(&empty[st], ph ^ 1);
-            const uint64_t q = rg.seq0 + (uint64_t)bi;
-            if (bi != gated) {  // first item of a batch: its slot must be free
-                gated = bi;
-                if (lane == 0 && q > (uint64_t)rg.slots) {
-                    const uint64_t need = q - (uint64_t)rg.slots;
-                    while ((int64_t)(known - need) < 0) {
-                        uint64_t gw;
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw) : "l"(rg.gate)
-                                     : "memory");
-                        if ((int64_t)(gw - known) > 0) known = gw;
-                        if ((int64_t)(known - need) >= 0) break;
-                        if (blockIdx.x == 0) {  // CTA 0 alone reads the host-shared cursors
-                            const uint64_t lo = cc_min_live(rg, need);
-                            if ((int64_t)(lo - known) > 0) {
-                                known = lo;
-                                atomicMax(rg.gate, (unsigned long long)lo);
-                            }
-                        }
-                        if ((int64_t)(known - need) < 0) __nanosleep(blockIdx.x == 0 ? 200 : 100);
-                    }
-                }
-                __syncwarp();
-            }
-            const int64_t *idx = order0 + (int64_t)bi * g.b;
-            ItemPar p;
-            p.s = j / g.nrb;
-            p.src_off = idx[p.s] * g.sample_bytes;
-            derive_aug(aug_mixed, epoch, idx[p.s], g.pad, flip_en, p.oy, p.ox, p.fl);
-            const int y0 = (j - p.s * g.nrb) * g.R;
-            const int sy_first = y0 + p.oy - g.pad;
-            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
-            const uint8_t *sample = src + p.src_off;
-            uint8_t *dst = smem + soff(st) + g.io;
-            if (lane == 0) {
-                meta[st].p = p;
-                meta[st].batch = bi;
-                meta[st].j = j;
-                fence_proxy_async();
-                mbar_arrive_expect_tx(&full[st], (uint32_t)max(0, hi - lo) * (uint32_t)g.row_bytes);
-            }
-            __syncwarp();
-            const uint64_t pol = l2_evict_first_policy();
-            for (int r = lo + lane; r < hi; r += 32)
-                tma_load_1d_hint(dst + (r - sy_first) * g.rs, sample + (int64_t)r * g.row_bytes,
-                                 (uint32_t)g.row_bytes, &full[st], pol);
-            if (++st == NST) st = 0, ph ^= 1;
-        }
-        // CTA 0 keeps the gate level moving until the range's last batch is out:
-        // other CTAs may still wait on it after CTA 0 ran out of items
-        if (blockIdx.x == 0 && lane == 0 && rg.n > 0) {
-            const uint64_t q_last = rg.seq0 + (uint64_t)rg.n - 1;
-            const int last_slot = (int)((q_last - 1) % (uint64_t)rg.slots);
-            while (cc_ld_acquire_sys(rg.ready + last_slot) != q_last) {
-                const uint64_t need = q_last > (uint64_t)rg.slots ? q_last - (uint64_t)rg.slots : 0;
-                const uint64_t lo = cc_min_live(rg, need);
-                if ((int64_t)(lo - known) > 0) {
-                    known = lo;
-                    atomicMax(rg.gate, (unsigned long long)lo);
-                }
-                __nanosleep(500);
-            }
-        }
-        return;
-    }
-
-    // the consumer warps' batch boundary: the CTA's items of batch bi are done
-    unsigned int cnt = 0;  // items of the current batch (thread 0)
-    auto finish_batch = [&](int bi) {
-        asm volatile("bar.sync 1, %0;" ::"r"(NT + 32 * runs) : "memory");
-        if (tid == 0) {
-            const uint64_t q = rg.seq0 + (uint64_t)bi;
-            const int slot = (int)((q - 1) % (uint64_t)rg.slots);
-            __threadfence();
-            const unsigned int prev = atomicAdd(rg.counters + slot, cnt);
-            if (prev + cnt == (unsigned int)items) {  // the batch is complete
-                rg.counters[slot] = 0u;
-                __threadfence();
-                uint32_t *acc = rg.acc_pool + (rg.acc_base + (unsigned)bi) % CC_ACC_POOL;
-                const uint32_t v = atomicExch(acc, 0u);
-                rg.d_crc[slot] = v ^ cf.init;
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(rg.ready + slot), "l"(q)
-                             : "memory");
-            }
-        }
-        cnt = 0;
-    };
-
-    if (warp < NCW) {
-        // ------- emit warps: normalised NCHW + per-element checksum lookups -----------
-        const uint32_t *smem_words = reinterpret_cast<const uint32_t *>(smem);
-        const int64_t plane_bytes = g.plane * E;
-        const int xg = tid % g.groups, r_first = tid / g.groups, dr = NT / g.groups;
-        const int x0 = xg * P, run = x0 >> 5;
-        const int ridx = lane / (32 / P), ra = ridx >> 2, rb = ridx & 3;
-        uint32_t A[NS], B[4];
-#pragma unroll
-        for (int s2 = 0; s2 < NS; ++s2)
-            A[s2] = L.r1 | ((uint32_t)((x0 & 31) + 4 * ((s2 + ra) % NS)) << 2);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) B[t] = (uint32_t)((t + rb) & 3) << 2;
-        const int n_iter = g.R / dr;
-        cc_wait(tab_bar, 0);
-        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
-            cc_wait(&full[st], ph);
-            const CcItem it = meta[st];
-            const ItemPar p = it.p;
-            const uint64_t q = rg.seq0 + (uint64_t)it.batch;
-            uint8_t *slot_base = rg.ring_base + (int64_t)((q - 1) % (uint64_t)rg.slots) * rg.slot_stride;
-            if (it.j == 0 && rg.with_target) {  // the batch's target: its sample indices
-                const int64_t *idx = order0 + (int64_t)it.batch * g.b;
-                int64_t *tgt = reinterpret_cast<int64_t *>(slot_base + rg.input_bytes);
-                for (int t = tid; t < g.b; t += NT) tgt[t] = idx[t];
-            }
-            const int y0 = (it.j - p.s * g.nrb) * g.R;
-            const int sy_first = y0 + p.oy - g.pad;
-            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
-            uint8_t *out_item = slot_base + ((int64_t)p.s * C * g.plane + (int64_t)y0 * g.w + x0) * E;
-            const uint32_t so = soff(st);
-            uint32_t *pst = part + st * part_words + run;
-#pragma unroll 1
-            for (int jj = 0; jj < n_iter; ++jj) {
-                const int r = r_first + jj * dr;
-                const int sy = sy_first + r;
-                const uint32_t row_off = (sy >= lo && sy < hi) ? so + (uint32_t)(r * g.rs) : L.zero;
-                uint8_t *o = out_item + (int64_t)r * g.w * E;
-                uint32_t *pr = pst + r * runs;
-                if (!p.fl)
-                    cc_emit_slot<OUT_KIND, C, false>(smem_words, row_off + g.rdoff + (x0 + p.ox) * C,
-                                                     norm, o, plane_bytes, lane, A, B, ra, rb, pr,
-                                                     g.R * runs, std::make_integer_sequence<int, C>{});
-                else
-                    cc_emit_slot<OUT_KIND, C, true>(smem_words,
-                                                    row_off + g.rdoff + (g.w - P - x0 + p.ox) * C,
-                                                    norm, o, plane_bytes, lane, A, B, ra, rb, pr,
-                                                    g.R * runs, std::make_integer_sequence<int, C>{});
-            }
-            mbar_arrive(&pfull[st]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == NST) st = 0, ph ^= 1;
-            ++cnt;
-            if (batch_ends(k, it.batch)) finish_batch(it.batch);
-        }
-    } else {
-        // ------- combiner warps: one column run, lane = row of the item ---------------
-        const int run = warp - NCW - 1;
-        const uint32_t rowsh = L.r2 + 128u + 4u * (uint32_t)lane + (128u << 8);
-        const uint32_t *wrun_tab = cf.wtab + (int64_t)run * cf.nseg * 32 + lane;
-        uint32_t wacc = 0;
-        cc_wait(tab_bar, 0);
-        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
-            int bi, j;
-            item_of(k, bi, j);
-            const int s_ = j / g.nrb, rb = j - s_ * g.nrb;
-            uint32_t wv[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c)
-                wv[c] = __ldg(wrun_tab + (int64_t)(cf.nseg - 1 - ((s_ * C + c) * g.nrb + rb)) * 32);
-            if (j == 0 && run == 0 && cf.with_tgt) {  // raw CRC of the batch's int64 target
-                const int64_t *idx = order0 + (int64_t)bi * g.b;
-                const int nl = (g.b + 31) >> 5, z = 32 * nl - g.b;
-                uint32_t cr = 0;
-                for (int e = 0; e < nl; ++e) {
-                    const int v = lane * nl + e - z;
-                    if (v >= 0) {
-                        const uint64_t x = (uint64_t)idx[v];
-                        cr = cc_crc_word(cf.slice, cr, (uint32_t)x);
-                        cr = cc_crc_word(cf.slice, cr, (uint32_t)(x >> 32));
-                    }
-                }
-#pragma unroll
-                for (int k2 = 0; k2 < 5; ++k2) {
-                    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, cr, 1 << k2);
-                    cr = (lane & (1 << k2)) ? cc_multmodp(cf.tgt_k[k2], other) ^ cr
-                                            : cc_multmodp(cf.tgt_k[k2], cr) ^ other;
-                }
-                if (lane == 0) wacc ^= cr;
-            }
-            cc_wait(&pfull[st], ph);
-            uint32_t S[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c)
-                S[c] = lane < g.R ? part[st * part_words + (c * g.R + lane) * runs + run] : 0u;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == NST) st = 0, ph ^= 1;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                uint32_t x = lane < g.R ? cc_mul_nib(S[c], rowsh) : 0u;
-#pragma unroll
-                for (int k2 = 16; k2 >= 1; k2 >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, k2);
-                wacc ^= ((x >> lane) & 1u) ? wv[c] : 0u;
-            }
-            if (batch_ends(k, bi)) {  // flush this batch's share of the checksum
-#pragma unroll
-                for (int k2 = 16; k2 >= 1; k2 >>= 1) wacc ^= __shfl_xor_sync(0xFFFFFFFFu, wacc, k2);
-                if (lane == 0 && wacc)
-                    atomicXor(rg.acc_pool + (rg.acc_base + (unsigned)bi) % CC_ACC_POOL, wacc);
-                wacc = 0;
-                finish_batch(bi);
-            }
         }
     }
 }
@@ -1115,101 +774,9 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     return launch_cc_c<TSB_OUT_BF16>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
 }
 
-template <int K, int C>
-int launch_ccr(const uint8_t *src, const int64_t *order0, const CaGeom &g, int flip,
-               uint64_t aug_mixed, uint64_t epoch, const Norm &norm, cudaStream_t s,
-               const CrcFuse &cf, const CcRange &rg) {
-    auto kern = collate_crc_range_kernel<K, C>;
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 64) dev = 63;
-    if (!attr_set[dev]) {
-        TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CC_SMEM));
-        attr_set[dev] = true;
-    }
-    const int64_t total = (int64_t)g.items * rg.n;
-    const int grid = (int)(total < sm_count() ? total : sm_count());
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(cf.ne + 32 + 32 * (g.w / 32));
-    cfg.dynamicSmemBytes = CC_SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: CTAs gate independently
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, src, order0, g, flip, aug_mixed, epoch, norm, cf, rg));
-    return TSB_OK;
-}
-
-// n batches of the fused collate + checksum in one persistent launch (the
-// caller checked cc_fusable); TSB_ERR_STALE: take the per-batch path.
-int launch_collate_crc_range(const uint8_t *src, const int64_t *order0, CaGeom g, int c, int flip,
-                             uint64_t aug_mixed, uint64_t epoch, const Norm &norm, int out_kind,
-                             cudaStream_t s, CcRange rg, int ne) {
-    int dev = 0;
-    TSB_CUDA(cudaGetDevice(&dev));
-    CcKey key{};
-    key.dev = dev;
-    key.out_kind = out_kind == OUT_BF16_FMA ? TSB_OUT_BF16 : out_kind;
-    key.c = c;
-    key.w = g.w;
-    key.h = g.h;
-    key.R = g.R;
-    key.b = g.b;
-    key.with_tgt = rg.with_target;
-    if (key.out_kind != TSB_OUT_U8) {
-        memcpy(key.scale, norm.scale, sizeof(key.scale));
-        memcpy(key.bias, norm.bias, sizeof(key.bias));
-    }
-    const CcPlan *pl = nullptr;
-    if (int rc = cc_plan(key, s, &pl)) return rc;
-    if (!pl) return TSB_ERR_STALE;
-    static uint32_t *acc_base[64] = {nullptr};
-    static unsigned long long *gate_words[64] = {nullptr};
-    static std::atomic<unsigned> acc_next{0};
-    if (!acc_base[dev]) {
-        void *p = nullptr;
-        TSB_CUDA(cudaGetSymbolAddress(&p, g_cc_acc));
-        acc_base[dev] = static_cast<uint32_t *>(p);
-        TSB_CUDA(cudaMalloc(&gate_words[dev], 256));
-    }
-    CrcFuse cf{};
-    cf.img = pl->d_img;
-    cf.slice = pl->d_slice;
-    cf.wtab = pl->d_w;
-    memcpy(cf.tgt_k, pl->tgt_k, sizeof(cf.tgt_k));
-    cf.init = pl->init;
-    cf.nseg = pl->nseg;
-    cf.with_tgt = key.with_tgt;
-    cf.tab_c = key.out_kind == TSB_OUT_U8;
-    cf.ne = ne;
-    rg.acc_pool = acc_base[dev];
-    rg.acc_base = acc_next.fetch_add((unsigned)rg.n, std::memory_order_relaxed) % CC_ACC_POOL;
-    rg.gate = gate_words[dev];
-    TSB_CUDA(cudaMemsetAsync(rg.gate, 0, sizeof(unsigned long long), s));
-    g.nstage = cc_stages(g, c);
-#define TSB_CCR(KK)                                                                            \
-    switch (c) {                                                                               \
-        case 1: return launch_ccr<KK, 1>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \
-        case 2: return launch_ccr<KK, 2>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \
-        default: return launch_ccr<KK, 3>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \
-    }
-    if (out_kind == TSB_OUT_U8) TSB_CCR(TSB_OUT_U8)
-    if (out_kind == TSB_OUT_F32) TSB_CCR(TSB_OUT_F32)
-    if (out_kind == OUT_BF16_FMA) TSB_CCR(OUT_BF16_FMA)
-    TSB_CCR(TSB_OUT_BF16)
-#undef TSB_CCR
-}
-
 template <int K>
 void preload_cc() {
     touch_kernel(collate_crc_kernel<K, 1>);
     touch_kernel(collate_crc_kernel<K, 2>);
     touch_kernel(collate_crc_kernel<K, 3>);
-    touch_kernel(collate_crc_range_kernel<K, 1>);
-    touch_kernel(collate_crc_range_kernel<K, 2>);
-    touch_kernel(collate_crc_range_kernel<K, 3>);
 }

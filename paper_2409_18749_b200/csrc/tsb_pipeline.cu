@@ -24,12 +24,6 @@ int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int 
                   int64_t *const *tgts, uint64_t *const *readys, int n, unsigned int *counter,
                   uint64_t seq, int pdl, int sys_fence, void *stream);
 bool ring_has_host_control(const tsb_ring *r);
-int collate_crc_range(const void *src, const int64_t *order0, int64_t b, int h, int w, int c,
-                      int pad, int flip, uint64_t aug_seed, uint64_t epoch, const float *scale,
-                      const float *bias, int out_kind, uint8_t *ring_base, int64_t slot_stride,
-                      int slots, uint64_t *ready, const uint64_t *cursors, unsigned int *counters,
-                      const int *live, int n_live, int64_t input_bytes, int with_target,
-                      uint64_t seq0, int n, uint32_t *d_crc, void *stream);
 int ring_host_gate(tsb_ring *r, const int *live, int n_live, uint64_t need);
 int collate_augment_publish(const void *src, const int64_t *d_indices, int64_t b, int h, int w,
                             int c, int pad, int flip, uint64_t aug_seed, uint64_t epoch,
@@ -97,21 +91,7 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     static const bool direct_ingest =
         getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "direct");
     const bool staged = !jpeg && a->ingest && a->h_order && !ev && !direct_ingest;
-    if (a->persistent && a->mode == TSB_SRC_AUGMENT && a->d_crc && ring_has_host_control(r) &&
-        ring_writers(r) == 1 && !staged && !jpeg && !ev && a->out_kind >= 0) {
-        // the fused collate + batch CRC over the whole range, one persistent launch
-        uint8_t *base = nullptr;
-        int64_t sstride = 0;
-        uint64_t *ready = nullptr, *cursors = nullptr;
-        unsigned int *counters = nullptr;
-        ring_internals(r, &base, &sstride, &ready, &cursors, &counters);
-        const int rc = collate_crc_range(a->src, a->d_order + batch0 * b, b, a->h, a->w, a->c,
-                                         a->pad, a->flip, a->seed, a->epoch, a->scale, a->bias,
-                                         a->out_kind, base, sstride, slots, ready, cursors,
-                                         counters, live, n_live, a->input_bytes, a->with_target,
-                                         seq0, n, a->d_crc, stream);
-        if (rc != TSB_ERR_STALE) return rc;  // else: the per-batch path below
-    } else if (a->persistent) {  // one cooperative launch for the whole range, gated on the device
+    if (a->persistent) {  // one cooperative launch for the whole range, gated on the device
         TSB_CHECK(ring_has_host_control(r) && ring_writers(r) == 1 && !staged && !jpeg &&
                       !a->d_crc && !ev,
                   "the persistent producer needs a host-control single-writer ring, a "

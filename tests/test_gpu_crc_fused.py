@@ -22,14 +22,14 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 from paper_2409_18749_b200 import AugmentSpec, CollateLoader, DatasetSpec, StoreSource  # noqa: E402
-from paper_2409_18749_b200._lib import GATE_HOST, ProduceArgs  # noqa: E402
+from paper_2409_18749_b200._lib import GATE_HOST  # noqa: E402
 from paper_2409_18749_b200.ring import DeviceRing, produce_range  # noqa: E402
 
 KIND = {"float32": 1, "bfloat16": 2, "uint8": 0}
 
 
 def _run(oracle, h, w, c, B, N, pad, out_dtype, n, with_target=True, seed=3, aug_seed=5,
-         crc_at_ready=True, persistent=False, slots=3):
+         crc_at_ready=True, slots=3):
     """n batches through the native producer loop with a per-batch CRC.  The
     fused kernel's CRC is in d_crc[slot] when the slot is published, and the
     consumer reads it then (crc_at_ready); the separate CRC kernel runs after
@@ -67,9 +67,8 @@ def _run(oracle, h, w, c, B, N, pad, out_dtype, n, with_target=True, seed=3, aug
     while q <= n:
         epoch, bi = divmod(q - 1, L)
         m = min(n - q + 1, L - bi)
-        a = ProduceArgs.from_buffer_copy(ld.produce_args(epoch, with_crc=d_crc))
+        a = ld.produce_args(epoch, with_crc=d_crc)
         a.gate = GATE_HOST
-        a.persistent = int(persistent)  # one launch per range, slot gate on the device
         produce_range(ring, a, q, bi, m, [0], stream=ps)
         q += m
     ps.synchronize()
@@ -146,44 +145,4 @@ def test_fused_kernel_is_the_one_that_runs():
     names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
     assert any("collate_crc_kernel" in n for n in names), names
     assert not any("crc_tile_kernel" in n or "crc_kernel" == n for n in names), names
-    ring.close()
-
-
-@pytest.mark.parametrize("out_dtype,c,B", [("float32", 3, 8), ("bfloat16", 3, 37), ("uint8", 3, 8),
-                                           ("float32", 1, 33)])
-def test_persistent_range_crc(oracle, out_dtype, c, B):
-    """persistent=1: all batches of a range in ONE launch (one CTA per SM for the
-    whole range), the slot gate on the device (3 ring slots, 11 batches in one
-    launch, so batches wait for the consumer's releases; then ranges cut at
-    epoch boundaries) and each batch's CRC written before its publish."""
-    _run(oracle, 64, 96, c, B, 20 * B + 5, 6, out_dtype, 11, persistent=True)
-    _run(oracle, 64, 96, c, B, 3 * B + 5, 6, out_dtype, 8, persistent=True)  # epoch boundaries
-
-
-def test_persistent_range_full_c2(oracle):
-    """C2 at size through the persistent range: B=256 f32, 10 batches on 4 slots."""
-    _run(oracle, 224, 224, 3, 256, 1024, 16, "float32", 10, persistent=True, slots=4)
-
-
-def test_persistent_range_is_one_launch():
-    """The range runs as one collate_crc_range_kernel launch."""
-    from torch.profiler import ProfilerActivity, profile
-
-    h = w = 64
-    B, N = 8, 64
-    ld = CollateLoader(DatasetSpec(StoreSource.synthetic(1, N, (h, w, 3)), N, B),
-                       AugmentSpec(pad=4, flip=True, out_dtype="float32"))
-    ring = DeviceRing(8, ld.batch_nbytes, 1, control="host")
-    d_crc = torch.zeros(8, dtype=torch.int32, device="cuda")
-    a = ProduceArgs.from_buffer_copy(ld.produce_args(0, with_crc=d_crc))
-    a.gate = GATE_HOST
-    a.persistent = 1
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        produce_range(ring, a, 1, 0, 6, [])
-        torch.cuda.synchronize()
-    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
-    assert sum("collate_crc_range_kernel" in n for n in names) == 1, names
-    assert not any("collate_augment_kernel" in n for n in names), names
-    for q in range(1, 7):
-        assert ring.read_ready(ring.slot_of(q)) == q
     ring.close()

@@ -16,7 +16,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2409_18749_b200 import AugmentSpec, CollateLoader, DatasetSpec, StoreSource  # noqa: E402
 from paper_2409_18749_b200 import dataplane as dp  # noqa: E402
-from paper_2409_18749_b200._lib import GATE_HOST, ProduceArgs  # noqa: E402
+from paper_2409_18749_b200._lib import GATE_HOST  # noqa: E402
 from paper_2409_18749_b200.ring import DeviceRing, produce_range  # noqa: E402
 
 kinds = (sys.argv[1] if len(sys.argv) > 1 else "f32,bf16,u8").split(",")
@@ -24,7 +24,6 @@ K = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 H = W = 224
 C, N, SLOTS = 3, 16384, 8
 B = int(os.environ.get("TIMING_B", "256"))
-PERSIST = int(os.environ.get("TIMING_PERSISTENT", "0"))  # one launch per range (checksum on)
 torch.cuda.set_device(0)
 store = StoreSource.synthetic(0, N, (H, W, C), location="hbm")
 E = {"f32": 4, "bf16": 2, "u8": 1}
@@ -43,9 +42,8 @@ for kind in kinds:
                 q = q0 + done
                 epoch, bi = divmod(q - 1, L)
                 m = min(n - done, L - bi)
-                a = ProduceArgs.from_buffer_copy(ld.produce_args(epoch, with_crc=d_crc))
+                a = ld.produce_args(epoch, with_crc=d_crc)
                 a.gate = GATE_HOST
-                a.persistent = PERSIST if crc else 0
                 produce_range(ring, a, q, bi, m, [], stream=s)
                 done += m
 
@@ -58,7 +56,7 @@ for kind in kinds:
         s.synchronize()
         ms = e0.elapsed_ms(e1) / K
         alg = B * (H * W * C + C * H * W * E[kind])
-        print(json.dumps({"kind": kind, "b": B, "persistent": PERSIST, "checksum": crc, "us_per_batch": round(ms * 1e3, 2),
+        print(json.dumps({"kind": kind, "b": B, "checksum": crc, "us_per_batch": round(ms * 1e3, 2),
                           "alg_gbs": round(alg / (ms / 1e3) / 1e9, 1)}),
               flush=True)
     ring.close()
