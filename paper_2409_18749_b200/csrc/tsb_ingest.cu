@@ -34,6 +34,8 @@ struct tsb_ingest {
     int32_t *h_params;    // [depth][max_batch][3] pinned upload buffer (crop-aware batches)
     uint64_t bytes;       // H2D bytes enqueued (tsb_ingest_bytes)
     cudaStream_t stream;  // ingest stream (beside the producer stream)
+    cudaStream_t ce_stream;  // copy-engine share of a batch (TSB_INGEST_CE samples)
+    cudaEvent_t ce_done;
     std::vector<cudaEvent_t> done, freed;
     std::vector<int> used;
     int next;
@@ -178,17 +180,44 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         *k_out = k;
         return TSB_OK;
     }
+    // TSB_INGEST_CE=n: the batch's last n samples go by the copy engine (one
+    // copy per sample on a second stream, issued from this thread) beside the
+    // gather kernel's SM loads of the others -- both share the PCIe link
+    static const int64_t n_ce_knob =
+        getenv("TSB_INGEST_CE") ? (int64_t)atoll(getenv("TSB_INGEST_CE")) : 0;
+    const int64_t n_ce = n_ce_knob < b ? n_ce_knob : b - 1;
+    if (n_ce > 0) {
+        TSB_CUDA(cudaStreamWaitEvent(g->ce_stream, g->freed[k], 0));
+        for (int64_t i = b - n_ce; i < b; ++i) {
+            size_t off = 0, len = sb;
+            if (crop) {
+                const int oy = hp[3 * i];
+                const int lo = oy - crop->pad > 0 ? oy - crop->pad : 0;
+                const int hi = crop->h + oy - crop->pad < crop->h ? crop->h + oy - crop->pad : crop->h;
+                off = (size_t)lo * (size_t)row_bytes;
+                len = hi > lo ? (size_t)(hi - lo) * (size_t)row_bytes : 0;
+            }
+            if (len)
+                TSB_CUDA(cudaMemcpyAsync(out + (size_t)i * sb + off,
+                                         static_cast<const uint8_t *>(host_store) +
+                                             (size_t)h_idx[i] * sb + off,
+                                         len, cudaMemcpyHostToDevice, g->ce_stream));
+        }
+        TSB_CUDA(cudaEventRecord(g->ce_done, g->ce_stream));
+    }
+    const int64_t b_sm = b - (n_ce > 0 ? n_ce : 0);
     const bool vec = ((uintptr_t)host_store & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
                      sb % 16 == 0 && (!crop || row_bytes % 16 == 0);
     // bytes per CTA and sample (TSB_IG_CHUNK A/B; 16 KB default)
     static const int64_t chunk =
         getenv("TSB_IG_CHUNK") ? (int64_t)atoll(getenv("TSB_IG_CHUNK")) : 16384;
-    dim3 grid((unsigned)((sb + chunk - 1) / chunk), (unsigned)b);
+    dim3 grid((unsigned)((sb + chunk - 1) / chunk), (unsigned)b_sm);
     TSB_CHECK(b <= 65535, "batch %lld exceeds the gather grid", (long long)b);
     ingest_gather_kernel<<<grid, IG_THREADS, 0, g->stream>>>(
         static_cast<const uint8_t *>(host_store), dk, crop ? pk : nullptr, (int64_t)sb, row_bytes,
         crop ? crop->h : 0, crop ? crop->pad : 0, vec ? 1 : 0, chunk, out);
     TSB_LAUNCH_CHECK();
+    if (n_ce > 0) TSB_CUDA(cudaStreamWaitEvent(g->stream, g->ce_done, 0));
     g->bytes += nbytes;
     TSB_CUDA(cudaEventRecord(g->done[k], g->stream));
     TSB_CUDA(cudaStreamWaitEvent(as_stream(stream), g->done[k], 0));
@@ -233,6 +262,8 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
     if (e == cudaSuccess)
         e = cudaHostAlloc(&g->h_params, sizeof(int32_t) * 3 * max_batch * depth, 0);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->ce_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ce_done, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         set_error("ingest allocation: %s", cudaGetErrorString(e));
         tsb_ingest_destroy(g);
@@ -259,6 +290,9 @@ int tsb_ingest_destroy(tsb_ingest *g) {
     for (auto ev : g->done) cudaEventDestroy(ev);
     for (auto ev : g->freed) cudaEventDestroy(ev);
     if (g->stream) cudaStreamDestroy(g->stream);
+    if (g->ce_stream) cudaStreamSynchronize(g->ce_stream);
+    if (g->ce_stream) cudaStreamDestroy(g->ce_stream);
+    if (g->ce_done) cudaEventDestroy(g->ce_done);
     cudaFree(g->staging);
     cudaFree(g->d_idx);
     cudaFree(g->d_params);

@@ -1,4 +1,4 @@
 #!/bin/bash
-out=gpurun_out/${1:-ingp}; mkdir -p $out
-for c in 8192 16384 32768 65536 150528; do TSB_IG_CHUNK=$c timeout 300 python tools/ingest_probe.py 96 >> $out/probe.jsonl 2>> $out/probe.err; done
-timeout 300 python tools/h2d_probe.py > $out/h2d.json 2>> $out/probe.err
+out=gpurun_out/${1:-ingp}; mkdir -p $out; shift
+for n in ${@:-0 16 32 48 64}; do TSB_INGEST_CE=$n timeout 300 python tools/ingest_probe.py 96 | sed "s/^{/{\"ce_samples\": $n, /" >> $out/probe.jsonl 2>> $out/probe.err; done
+timeout 300 python -m pytest tests/test_gpu_pipeline.py -q -x -k staged > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log
