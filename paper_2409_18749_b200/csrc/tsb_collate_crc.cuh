@@ -234,9 +234,8 @@ __device__ __forceinline__ void cc_emit_channel(const uint32_t *wv, const Norm &
 #pragma unroll
         for (int t = 0; t < 4; ++t)
             acc ^= cc_lds_off<COFF>(cc_prmt(R[s], A[s] | B[t], 0x7604u | (t << 4)));
-#pragma unroll
-    for (int k = 1; k < LPR; k <<= 1) acc ^= __shfl_xor_sync(0xFFFFFFFFu, acc, k);
-    if ((lane & (LPR - 1)) == 0) *part_c = acc;
+    // the run's lanes fold their lookups into its word (zeroed by the combiner)
+    atomicXor(part_c, acc);
 }
 
 template <int OUT_KIND, int C, bool FLIP, int... CHs>
@@ -306,6 +305,7 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
         uint4 *z = reinterpret_cast<uint4 *>(smem + L.zero);
         for (int i = tid; i < (g.rs >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     }
+    for (int i = tid; i < NST * part_words; i += blockDim.x) part[i] = 0u;
     for (int k = tid; k < min(nk, META_CAP); k += blockDim.x)
         par[k] = item_par(g, i0 + k * istep, idx, kidx, params, aug_mixed, epoch, flip_en);
     if (tid == 0) {
@@ -445,7 +445,11 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
             uint32_t S[C];
 #pragma unroll
             for (int c = 0; c < C; ++c)
-                S[c] = lane < g.R ? part[st * part_words + (c * g.R + lane) * runs + run] : 0u;
+            {
+                uint32_t *w = part + st * part_words + (c * g.R + lane) * runs + run;
+                S[c] = lane < g.R ? *w : 0u;
+                if (lane < g.R) *w = 0u;  // ready for the stage's next item
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);  // the run buffer is read
             if (++st == NST) st = 0, ph ^= 1;
