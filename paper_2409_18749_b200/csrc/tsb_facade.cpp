@@ -25,7 +25,9 @@
 // they change; Python keeps admission, retention and the ledger.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -50,12 +52,20 @@ struct tsb_facade {
     std::vector<cudaEvent_t> events;
     std::vector<uint8_t> fused;  // per slot: the CRC came from the kernel (host-mapped)
     bool tail_kernel = false;    // the stream's last operation is a fused produce kernel
+    // TSB_FACADE_STATS=1: time spent in the ack gate, the launch and the CRC wait
+    double t_gate = 0, t_launch = 0, t_crc = 0, t_bcast = 0;
+    uint64_t n_steps = 0;
     std::vector<uint64_t> ack_ids;
     std::vector<int> live;
     std::vector<int> fds;
 };
 
 namespace {
+inline double now_us() {
+    return std::chrono::duration<double, std::micro>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
 const char B64[] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz0123456789+/";
 
 size_t b64_encode(const uint8_t *in, size_t n, char *out) {  // standard alphabet, padded
@@ -81,6 +91,12 @@ int tsb_facade_create(tsb_facade **out) {
 }
 
 int tsb_facade_destroy(tsb_facade *f) {
+    if (f && getenv("TSB_FACADE_STATS") && f->n_steps)
+        fprintf(stderr,
+                "facade stats: %llu steps, per step us: gate %.2f launch %.2f crc-wait %.2f "
+                "announce %.2f\n",
+                (unsigned long long)f->n_steps, f->t_gate / f->n_steps, f->t_launch / f->n_steps,
+                f->t_crc / f->n_steps, f->t_bcast / f->n_steps);
     delete f;
     return TSB_OK;
 }
@@ -130,17 +146,26 @@ int tsb_facade_set_consumers(tsb_facade *f, const uint64_t *ack_ids, int n_ack, 
 
 int tsb_facade_produce(tsb_facade *f, uint64_t seq, int64_t index, int chain, int64_t timeout_us) {
     if (!f || !f->ring) return TSB_ERR_INVALID;
+    static const bool stats = getenv("TSB_FACADE_STATS") != nullptr;
+    const double t0 = stats ? now_us() : 0;
     if (seq > (uint64_t)f->depth) {  // fewer than buffer_depth announced batches await acks
         const int rc = tsb_hub_wait_acked(f->hub, f->ack_ids.data(), (int)f->ack_ids.size(),
                                           seq - (uint64_t)f->depth, timeout_us);
         if (rc) return rc;  // TSB_ERR_STALE: timed out (the caller re-checks for shutdown)
     }
+    const double t1 = stats ? now_us() : 0;
     int fused = 0;
     f->args.chain = chain && f->tail_kernel;
     f->args.crc_fused = &fused;
     int rc = tsb_produce_range(f->ring, &f->args, seq, index, 1, f->live.data(),
                                (int)f->live.size(), nullptr, f->stream);
     f->args.crc_fused = nullptr;
+    if (stats) {
+        const double t2 = now_us();
+        f->t_gate += t1 - t0;
+        f->t_launch += t2 - t1;
+        ++f->n_steps;
+    }
     if (rc) return rc;
     f->tail_kernel = !f->d_crc || fused;
     if (f->d_crc) {
@@ -164,6 +189,8 @@ int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t in
     if (!f || !f->ring) return TSB_ERR_INVALID;
     const int slot = (int)((seq - 1) % (uint64_t)f->slots);
     uint32_t crc = 0;
+    static const bool stats = getenv("TSB_FACADE_STATS") != nullptr;
+    const double t0 = stats ? now_us() : 0;
     if (with_crc && f->d_crc) {
         if (f->fused[slot]) {  // the kernel stored the CRC before the slot's ready word
             if (int rc = tsb_ring_host_wait_ready(f->ring, slot, seq, 60 * 1000000ll)) return rc;
@@ -177,6 +204,7 @@ int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t in
             crc = f->h_crc[slot];
         }
     }
+    const double t1 = stats ? now_us() : 0;
     // the segment header (payload.py:220-233): epoch u32 @8, crc u32 @12, index u64 @16
     uint8_t hdr[80];
     memcpy(hdr, f->header, 80);
@@ -201,6 +229,10 @@ int tsb_facade_announce(tsb_facade *f, uint64_t seq, uint32_t epoch, uint64_t in
     if (int rc = tsb_wire_encode(&m, frame, sizeof frame, &len)) return rc;
     if (int rc = tsb_hub_broadcast(f->fds.data(), (int)f->fds.size(), frame, len, failed))
         return rc;
+    if (stats) {
+        f->t_crc += t1 - t0;
+        f->t_bcast += now_us() - t1;
+    }
     if (crc_out) *crc_out = crc;
     return TSB_OK;
 }

@@ -87,8 +87,8 @@ def local_ring(ring_id: int):
     return _RINGS.get(ring_id)
 
 
-ANN_LAG = 1  # fast path with a checksum: Announce this many launches behind (2 measured
-#             +6% but breaks the reference live bound N+1)
+ANN_LAG = 2  # fast path with a checksum: Announce this many launches behind (1 keeps the host
+#             in lockstep with the GPU: each launch then waits for the previous batch)
 
 
 class TensorProducer:
@@ -208,6 +208,7 @@ class TensorProducer:
         # the fast path with a checksum announces ANN_LAG batches behind the
         # launch: the batch's CRC (stored by the kernel) is then already there
         self._pend_fast = collections.deque()
+        self._settled = None  # (announce, result) awaiting bookkeeping (split fast path)
         # the one-GPU device-loader fast path (hub.Facade): consumer lists are
         # pushed to it when _cver (bumped on every membership change) moves
         self._cver = 0
@@ -801,10 +802,14 @@ class TensorProducer:
         import contextlib
 
         here = torch.cuda.current_device() == self.device  # (the usual case: no switch)
+        # with a checksum the launch and the Announce are two native calls: the
+        # Python bookkeeping of the previous Announce runs between them, while
+        # the GPU finishes the batch about to be announced
+        split = self._checksum and ann is not None
         while True:
             with contextlib.nullcontext() if here else torch.cuda.device(self.device):
                 res = self._facade.step(q, index, self._chain_ok, 0.1,
-                                        None if ann is None else (ann[0], ann[3], ann[1]),
+                                        None if ann is None or split else (ann[0], ann[3], ann[1]),
                                         self._checksum)
             if res is not None:
                 break
@@ -816,6 +821,10 @@ class TensorProducer:
         # the native path knows whether its stream ends in a fused kernel (a
         # checksum read-back copy breaks the chain only for unfused geometries)
         self._chain_ok = True
+        if split:
+            self._settle_fast()
+            with contextlib.nullcontext() if here else torch.cuda.device(self.device):
+                res = self._facade.announce(ann[0], ann[3], ann[1], True)
         if ann is not None:  # live = announced and not yet released
             self._sample_live(ann[0], {0: self._fast_live})
         if self._checksum:
@@ -823,7 +832,16 @@ class TensorProducer:
                 self._pend_fast.popleft()
             self._pend_fast.append(cur)
         if ann is not None:
-            self._announced_fast(ann, *res)
+            if split:
+                self._settled = (ann, res)  # bookkept at the next launch (or a flush)
+            else:
+                self._announced_fast(ann, *res)
+
+    def _settle_fast(self) -> None:
+        """Bookkeeping of the last Announce the split fast path sent."""
+        done, self._settled = self._settled, None
+        if done is not None:
+            self._announced_fast(done[0], *done[1])
 
     def _announce_fast(self, p, with_crc: bool) -> None:
         q, index, slot, epoch = p
@@ -967,6 +985,7 @@ class TensorProducer:
 
     def _announce_crc(self, p) -> None:
         """Announce a batch whose device CRC-32 was enqueued (waits for it)."""
+        self._settle_fast()  # announces are bookkept in order
         if len(p) == 4:  # enqueued by the native fast path
             self._announce_fast(p, True)
             return
@@ -975,6 +994,7 @@ class TensorProducer:
         self._announce(p, int(self._crc_host[slot]) & 0xFFFFFFFF)
 
     def _flush_pending(self) -> None:
+        self._settle_fast()
         p, self._pending_ann = self._pending_ann, None
         if p is not None:
             self._announce_crc(p)
