@@ -209,6 +209,7 @@ class TensorProducer:
         # launch: the batch's CRC (stored by the kernel) is then already there
         self._pend_fast = collections.deque()
         self._settled = None  # (announce, result) awaiting bookkeeping (split fast path)
+        self._live_lists = None  # the host gate's live cursors (live-slot sampling)
         # the one-GPU device-loader fast path (hub.Facade): consumer lists are
         # pushed to it when _cver (bumped on every membership change) moves
         self._cver = 0
@@ -924,7 +925,7 @@ class TensorProducer:
             # never park on a device wait, so no stream of this process
             # (in-process consumers included) can be blocked behind one
             self._host_gate(q, live_by_ring)
-            self._sample_live(q, live_by_ring)
+            self._live_lists = live_by_ring  # sampled when a batch is announced
         if self._two_stage and not self._checksum:
             self._publish_two_stage(q, index)
         elif self._multi and self._device_loader and not self._checksum:
@@ -1018,6 +1019,8 @@ class TensorProducer:
             self.batches.append((epoch, index, crc))
             self._announced_in_epoch = index + 1
             self.stats["announced"] += 1
+            if self._live_lists is not None:  # live = announced, not released
+                self._sample_live(q, self._live_lists)
             window = retention_window(self._fraction, L)
             if self._retention_active:
                 self._retained[q] = anns
