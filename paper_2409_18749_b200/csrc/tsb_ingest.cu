@@ -14,7 +14,11 @@
 // link (profiles/r1/h2d_probe.json).  The collate kernel then reads HBM
 // through its TMA path.  Passthrough batches are gathered straight into the
 // ring slot.
+#include <atomic>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "tsb_common.cuh"
@@ -39,6 +43,24 @@ struct tsb_ingest {
     std::vector<cudaEvent_t> done, freed;
     std::vector<int> used;
     int next;
+    // TSB_INGEST=hostpack: host threads gather the batch's sample rows into a
+    // pinned buffer, then ONE contiguous copy-engine transfer per batch
+    uint8_t *h_pack = nullptr;  // [depth][max_batch * sample_bytes] pinned
+    std::vector<std::thread> workers;
+    std::mutex mu;
+    std::condition_variable cv, cv_done;
+    uint64_t gen = 0;      // job generation (workers wake on a change)
+    int busy = 0;          // workers still on the current job
+    bool stop = false;
+    struct Job {
+        const uint8_t *src;
+        const int64_t *idx;
+        const int32_t *params;  // crop params (null: whole samples)
+        int64_t b, sb;
+        int row_bytes, h, pad;
+        uint8_t *dst;
+    } job{};
+    std::atomic<int64_t> next_sample{0};
 };
 
 namespace {
@@ -107,6 +129,61 @@ void preload_ingest() { touch_kernel(iota_kernel); }
 // kernel loads exactly those rows of a staged sample, never the others.
 // (Columns too would save another 3.7%, but 2D copies -- one op per sample --
 // ran ~10x slower: e2e 154 k vs 1.49 M samples/s; profiles/r1/ingest_2d_ab.txt.)
+// one sample's rows (all, or the crop's) into the pinned pack buffer
+static void pack_sample(const tsb_ingest::Job &j, int64_t i) {
+    size_t off = 0, len = (size_t)j.sb;
+    if (j.params) {
+        const int oy = j.params[3 * i];
+        const int lo = oy - j.pad > 0 ? oy - j.pad : 0;
+        const int hi = j.h + oy - j.pad < j.h ? j.h + oy - j.pad : j.h;
+        off = (size_t)lo * (size_t)j.row_bytes;
+        len = hi > lo ? (size_t)(hi - lo) * (size_t)j.row_bytes : 0;
+    }
+    if (len) memcpy(j.dst + (size_t)i * (size_t)j.sb + off, j.src + (size_t)j.idx[i] * (size_t)j.sb + off, len);
+}
+static void pack_work(tsb_ingest *g) {
+    const tsb_ingest::Job j = g->job;
+    for (;;) {
+        const int64_t i = g->next_sample.fetch_add(1, std::memory_order_relaxed);
+        if (i >= j.b) break;
+        pack_sample(j, i);
+    }
+}
+static void pack_worker(tsb_ingest *g) {
+    uint64_t seen = 0;
+    for (;;) {
+        {
+            std::unique_lock<std::mutex> lk(g->mu);
+            g->cv.wait(lk, [&] { return g->stop || g->gen != seen; });
+            if (g->stop) return;
+            seen = g->gen;
+        }
+        pack_work(g);
+        std::lock_guard<std::mutex> lk(g->mu);
+        if (--g->busy == 0) g->cv_done.notify_all();
+    }
+}
+// the calling thread and the workers pack the batch; returns when done
+static void pack_batch(tsb_ingest *g, const tsb_ingest::Job &j) {
+    if (g->workers.empty()) {
+        static const int want = getenv("TSB_INGEST_THREADS")
+                                    ? atoi(getenv("TSB_INGEST_THREADS"))
+                                    : (int)std::min(7u, std::max(1u, std::thread::hardware_concurrency() / 2));
+        for (int t = 0; t < want; ++t) g->workers.emplace_back(pack_worker, g);
+    }
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->job = j;
+        g->next_sample.store(0, std::memory_order_relaxed);
+        g->busy = (int)g->workers.size();
+        ++g->gen;
+    }
+    g->cv.notify_all();
+    pack_work(g);
+    std::unique_lock<std::mutex> lk(g->mu);
+    g->cv_done.wait(lk, [&] { return g->busy == 0; });
+}
+
 int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, int64_t b,
                  void *dst, void *stream, int *k_out, bool after_stream, const IngestCrop *crop) {
     TSB_CHECK(g && host_store && h_idx && k_out, "null argument");
@@ -156,6 +233,22 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         nbytes += sizeof(int32_t) * 3 * (size_t)b;
     }
     const int row_bytes = crop ? crop->row_bytes : 0;
+    static const bool host_pack = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "hostpack");
+    if (host_pack) {
+        if (!g->h_pack)
+            TSB_CUDA(cudaHostAlloc(&g->h_pack, (size_t)g->depth * (size_t)g->max_batch * sb, 0));
+        uint8_t *hb = g->h_pack + (size_t)k * (size_t)g->max_batch * sb;  // free: done[k] synced
+        tsb_ingest::Job j{static_cast<const uint8_t *>(host_store), h_idx, crop ? hp : nullptr, b,
+                          (int64_t)sb, row_bytes, crop ? crop->h : 0, crop ? crop->pad : 0, hb};
+        pack_batch(g, j);
+        TSB_CUDA(cudaMemcpyAsync(out, hb, (size_t)b * sb, cudaMemcpyHostToDevice, g->stream));
+        g->bytes += (size_t)b * sb + sizeof(int64_t) * (size_t)b +
+                    (crop ? sizeof(int32_t) * 3 * (size_t)b : 0);
+        TSB_CUDA(cudaEventRecord(g->done[k], g->stream));
+        TSB_CUDA(cudaStreamWaitEvent(as_stream(stream), g->done[k], 0));
+        *k_out = k;
+        return TSB_OK;
+    }
     // A/B (TSB_INGEST=memcpy): one copy-engine operation per sample instead
     static const bool per_sample = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "memcpy");
     if (per_sample) {
@@ -286,6 +379,16 @@ int tsb_ingest_create(int dev, int64_t max_batch, int64_t sample_bytes, int dept
 
 int tsb_ingest_destroy(tsb_ingest *g) {
     if (!g) return TSB_OK;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->stop = true;
+    }
+    g->cv.notify_all();
+    for (auto &t : g->workers) t.join();
+    if (g->h_pack) {
+        if (g->stream) cudaStreamSynchronize(g->stream);
+        cudaFreeHost(g->h_pack);
+    }
     if (g->stream) cudaStreamSynchronize(g->stream);
     for (auto ev : g->done) cudaEventDestroy(ev);
     for (auto ev : g->freed) cudaEventDestroy(ev);
