@@ -444,6 +444,9 @@ class CollateLoader:
         d, src = self.dataset, self.dataset.source
         a = _lib.ProduceArgs()
         a.d_order = dorder.data_ptr()
+        # the order buffers stay allocated for the launches that read them
+        # (ring.hold_for_stream records them on the launching stream)
+        a._keep = (dorder, self._order.host)
         a.batch_size = d.batch_size
         a.sample_bytes = src.sample_nbytes
         a.epoch = epoch

@@ -200,6 +200,7 @@ struct Epi {
     const int64_t *tgt_idx;  // sample indices written as the target (nullptr = the gather indices)
     int fence_all;           // A/B (TSB_FENCE_ALL=1): every thread fences before the CTA barrier
     int early_pdl;           // passthrough: let the next batch launch at this kernel's start
+    const struct CcRange *range;  // fused collate + CRC over a range of batches (persistent)
 };
 
 // Publish ordering knob, read once per process.
@@ -1072,6 +1073,12 @@ int launch_collate(const void *src, const int64_t *d_indices, int64_t b, int h, 
     auto s = as_stream(stream);
     if (crc_done) *crc_done = 0;
     const int cc_ne = crc_out ? cc_fusable(g, c, out_kind, dsts, ep.counter != nullptr) : 0;
+    if (ep.range) {  // persistent range: the fused kernel or nothing (the caller falls back)
+        if (!cc_ne || d_params) return TSB_ERR_STALE;
+        const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
+        return launch_collate_crc_range(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k, s,
+                                        *ep.range, cc_ne);
+    }
     if (cc_ne) {  // collate + batch CRC, one kernel
         const int k = out_kind == TSB_OUT_BF16 && bf16_fma_exact(norm, c) ? OUT_BF16_FMA : out_kind;
         const int rc = launch_collate_crc(s8, d_indices, g, c, flip, aug_mixed, epoch, norm, k,
@@ -1439,6 +1446,46 @@ int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int 
     return launch_maybe_pdl(passthrough_multi_kernel<false, true>, grid, PT_THREADS, 0, s, pdl, s8,
                             idx, sample_bytes, bb, seed, epoch, d, ep);
 }
+// n batches of the augment mode with the per-batch CRC-32 in one cooperative
+// persistent launch of the fused kernel (collate_crc_range_kernel);
+// TSB_ERR_STALE when the geometry is not fusable (the caller runs per batch).
+int produce_persistent_crc(const void *src, const int64_t *order, int64_t b, int h, int w, int c,
+                           int pad, int flip, uint64_t aug_seed, uint64_t epoch,
+                           const float *scale, const float *bias, int out_kind,
+                           uint8_t *ring_base, int64_t slot_stride, int slots, uint64_t *ready,
+                           const uint64_t *cursors, unsigned int *counters, const int *live,
+                           int n_live, int64_t input_bytes, int with_target, uint64_t seq0,
+                           int64_t batch0, int n, uint32_t *d_crc, uint32_t *h_crc,
+                           void *stream) {
+    if (n <= 0) return TSB_OK;
+    if (n_live > CC_MAX_LIVE) return TSB_ERR_STALE;
+    TSB_CHECK(slot_stride % 16 == 0 && ((uintptr_t)ring_base & 15) == 0,
+              "slots must be 16-byte aligned");
+    CcRange rg{};
+    rg.ring_base = ring_base;
+    rg.slot_stride = slot_stride;
+    rg.slots = slots;
+    rg.ready = ready;
+    rg.cursors = cursors;
+    rg.counters = counters;
+    for (int j = 0; j < n_live; ++j) rg.live[j] = live[j];
+    rg.n_live = n_live;
+    rg.seq0 = seq0;
+    rg.n = n;
+    rg.input_bytes = input_bytes;
+    rg.with_target = with_target;
+    rg.d_crc = d_crc;
+    rg.h_crc = h_crc;
+    Dsts d{};
+    d.p[0] = ring_base;
+    d.n = 1;
+    Epi ep{};
+    ep.counter = counters;
+    ep.range = &rg;
+    return launch_collate(src, order + batch0 * b, b, h, w, c, pad, flip, aug_seed, epoch, scale,
+                          bias, out_kind, nullptr, d, stream, ep, d_crc, nullptr, h_crc);
+}
+
 // n batches of a passthrough source in one cooperative persistent launch
 int produce_persistent(int mode, const void *src, const int64_t *order, int64_t b,
                        int64_t sample_bytes, uint64_t seed, uint64_t epoch, uint8_t *ring_base,

@@ -48,6 +48,8 @@ constexpr int CC_MAX_RUNS = 9;     // combiner warps: 32-element column runs per
 constexpr int CC_MAX_C = 3;
 constexpr int CC_SMEM = 232448;    // the 227 KB opt-in maximum
 constexpr int CC_MAX_STAGES = 8;  // item stages: as many as fit next to the tables (3 at 32 rows of 224x3)
+constexpr uint32_t CC_META_STRIDE = 48;  // range kernel: per-stage item record
+constexpr int CC_BCNT = 16;       // range kernel: per-batch completion counters (ring > stages)
 constexpr uint32_t CC_IMG_WORDS = 2 * 256 * 64;  // the two table regions (128 KB)
 constexpr int CC_ACC_POOL = 1024;
 constexpr int CC_MAX_PLANS = 64;   // table sets per process (never freed: kernels may be in flight)
@@ -154,7 +156,7 @@ __device__ __forceinline__ uint32_t cc_gather4(const uint32_t *wv) {
 struct CcLayout {
     uint32_t r1, r2;        // shared addresses of the two table regions
     uint32_t lo_stage, n_lo, hi_stage;  // stages: n_lo at lo_stage, the rest at hi_stage
-    uint32_t zero, bars, par, part;     // offsets
+    uint32_t zero, bars, par, part, meta;  // offsets
 };
 __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, uint32_t rs,
                                           uint32_t part_bytes, int nstage, CcLayout &L) {
@@ -172,7 +174,8 @@ __host__ __device__ inline bool cc_layout(uint32_t sbase, uint32_t stage_bytes, 
     };
     bool ok = take((3 * nstage + 1) * 8, 8, L.bars) &&
               take(META_CAP * (uint32_t)sizeof(ItemPar), 16, L.par) && take(rs, 128, L.zero) &&
-              take(part_bytes * nstage, 16, L.part);
+              take(part_bytes * nstage, 16, L.part) &&
+              take(CC_META_STRIDE * nstage + 4u * CC_BCNT, 16, L.meta);
     // stages: as many as fit below region 1, the rest above region 2
     L.lo_stage = (lo + 127) & ~127u;
     const uint32_t below = lo_end > L.lo_stage ? (lo_end - L.lo_stage) / stage_bytes : 0;
@@ -489,6 +492,408 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent range kernel (tsb_produce_range with persistent=1 and a CRC):
+// ONE cooperative launch produces n consecutive batches, one CTA per SM for
+// the whole range.  The per-batch kernel pays, per batch and SM, the CTA
+// start, the 128 KB table load, the stage zeroing and the pipeline fill --
+// the 6 us intercept of per-batch time against B (21.6 / 36.3 / 66.5 us at
+// B = 128 / 256 / 512, profiles/r2/crc_fused_bscaling.jsonl).  Here the work
+// items of all n batches form one stream (CTA b takes b, b + grid, ...), so a
+// CTA's stages run across batch boundaries.
+//   * the slot gate moves to the device: before the first item of batch q the
+//     producer warp waits until every live consumer released q - slots (CTA 0
+//     reads the host-shared cursors and raises a gate word the others poll in
+//     L2; the reference's gate is bs/producer.py:230-238);
+//   * the producer derives the next item's crop before it waits for a stage,
+//     and writes each staged item's params into the stage record;
+//   * completion without a CTA-wide barrier and off the emit path: each
+//     consumer warp, after its last item of a batch, counts itself in a
+//     per-CTA shared counter (CTA-scope release); a publisher warp waits for
+//     the CTA's count, fences at GPU scope (cumulative over what it observed,
+//     the cooperative-groups grid-barrier pattern) and counts the CTA into the
+//     slot's global counter; the CTA that completes the batch writes its
+//     CRC-32 and publishes the slot.  The emit warps never wait on a fence.
+constexpr int CC_MAX_LIVE = 16;
+struct CcRange {
+    uint8_t *ring_base;
+    int64_t slot_stride;
+    int slots;
+    uint64_t *ready;             // [slots] (single writer)
+    const uint64_t *cursors;     // release cursors (host-shared, device-mapped)
+    unsigned int *counters;      // [slots] completion counters (zero at rest)
+    unsigned long long *gate;    // device word: every live cursor has released this much
+    int live[CC_MAX_LIVE];
+    int n_live;
+    uint64_t seq0;
+    int n;
+    int64_t input_bytes;
+    int with_target;
+    uint32_t *d_crc;             // [slots]: each batch's CRC-32, written before its publish
+    uint32_t *h_crc;             // optional host-mapped [slots] copy
+    uint32_t *acc_pool;          // g_cc_acc
+    unsigned acc_base;           // batch i accumulates into acc_pool[(acc_base + i) % POOL]
+};
+struct CcItem {                  // per stage: the staged item (written by the producer)
+    ItemPar p;
+    int batch, j, slot, last;    // last: the CTA's last item of this batch
+};
+static_assert(sizeof(CcItem) <= CC_META_STRIDE, "stage record");
+
+__device__ __forceinline__ uint64_t cc_ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// min over the live release cursors (host-shared, PCIe reads), wrap-around order
+__device__ __forceinline__ uint64_t cc_min_live(const CcRange &rg, uint64_t need) {
+    uint64_t lo = need + (1ull << 61);
+    for (int j = 0; j < rg.n_live; ++j) {
+        const uint64_t c = cc_ld_acquire_sys(rg.cursors + rg.live[j]);
+        if ((int64_t)(c - lo) < 0) lo = c;
+    }
+    return lo;
+}
+
+template <int OUT_KIND, int C>
+__global__ void __launch_bounds__(CC_EMIT + 64 + 32 * CC_MAX_RUNS, 1)
+    collate_crc_range_kernel(const uint8_t *__restrict__ src, const int64_t *__restrict__ order0,
+                             CaGeom g, int flip_en, uint64_t aug_mixed, uint64_t epoch, Norm norm,
+                             CrcFuse cf, CcRange rg) {
+    using T = OutTraits<OUT_KIND>;
+    constexpr int P = T::P;
+    constexpr int E = T::ELEM;
+    constexpr int NS = P / 4;
+    const int NT = cf.ne;
+    const int NCW = NT >> 5;
+    const int NST = g.nstage;
+    const int runs = g.w >> 5;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t stage_bytes = (uint32_t)(g.R * g.rs);
+    const int part_words = C * g.R * runs;
+    CcLayout L;
+    if (!cc_layout(sbase, stage_bytes, (uint32_t)g.rs, 4u * part_words, NST, L)) __trap();
+    auto soff = [&](int st) -> uint32_t {
+        return (uint32_t)st < L.n_lo ? L.lo_stage + (uint32_t)st * stage_bytes
+                                      : L.hi_stage + ((uint32_t)st - L.n_lo) * stage_bytes;
+    };
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + L.bars);
+    uint64_t *empty = full + NST;
+    uint64_t *pfull = empty + NST;
+    uint64_t *tab_bar = pfull + NST;
+    uint32_t *part = reinterpret_cast<uint32_t *>(smem + L.part);
+    CcItem *meta = reinterpret_cast<CcItem *>(smem + L.meta);
+    unsigned int *bcnt =
+        reinterpret_cast<unsigned int *>(smem + L.meta + CC_META_STRIDE * NST);  // [CC_BCNT]
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int items = g.items;  // per batch
+    const int64_t total = (int64_t)items * rg.n;
+    const int grid = (int)gridDim.x;
+    const int nk = (int)((total - (int64_t)blockIdx.x + grid - 1) / grid);
+    // CTAs that take part in each batch (a window of `items` consecutive items)
+    const unsigned int ctas_per_batch = (unsigned int)(items < grid ? items : grid);
+
+    for (int st = 0; st < NST; ++st) {
+        uint4 *z = reinterpret_cast<uint4 *>(smem + soff(st));
+        for (int i = tid; i < (int)(stage_bytes >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(smem + L.zero);
+        for (int i = tid; i < (g.rs >> 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    for (int i = tid; i < NST * part_words; i += blockDim.x) part[i] = 0u;
+    if (tid < CC_BCNT) bcnt[tid] = 0u;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCW + runs);
+            mbar_init(&pfull[i], NT);
+        }
+        mbar_init(tab_bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // this CTA's items b, b + grid, ... as (batch, item-in-batch), stepped
+    // without divisions; is_last: the CTA's last item of that batch
+    const int bi0 = (int)blockIdx.x / items, j0 = (int)blockIdx.x - bi0 * items;
+    auto step = [&](int &bi, int &j) {
+        j += grid;
+        while (j >= items) j -= items, ++bi;
+    };
+    auto is_last = [&](int k, int j) { return k + 1 >= nk || j + grid >= items; };
+    const int slot0 = (int)((rg.seq0 - 1) % (uint64_t)rg.slots);
+    // a consumer warp is done with batch bi (its stores and checksum share
+    // issued): count it for the publisher warp, CTA-scope release
+    auto warp_done = [&](int bi) {
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            atomicAdd(bcnt + (bi & (CC_BCNT - 1)), 1u);
+        }
+    };
+
+    if (warp == NCW + 1 + runs) {
+        // ---------------- publisher warp: the CTA's share of each batch -------------
+        // Consumer warps stay within NST items of each other (they share the
+        // stages), so a ring of CC_BCNT > NST monotonic counters cannot alias.
+        if (lane == 0) {
+            unsigned int want[CC_BCNT];
+            for (int x = 0; x < CC_BCNT; ++x) want[x] = 0u;
+            const unsigned int W = (unsigned int)(NCW + runs);
+            for (int k = 0, bi = bi0, j = j0; k < nk; ++k, step(bi, j)) {
+                if (!is_last(k, j)) continue;
+                const int x = bi & (CC_BCNT - 1);
+                want[x] += W;
+                while ((int)(*(volatile unsigned int *)(bcnt + x) - want[x]) < 0) __nanosleep(64);
+                __threadfence();  // the consumers' stores and checksum shares, GPU-wide
+                const uint64_t q = rg.seq0 + (uint64_t)bi;
+                const int slot = (slot0 + bi) % rg.slots;
+                const unsigned int gp = atomicAdd(rg.counters + slot, 1u);
+                if (gp == ctas_per_batch - 1u) {  // the batch is complete
+                    rg.counters[slot] = 0u;
+                    __threadfence();
+                    uint32_t *acc = rg.acc_pool + (rg.acc_base + (unsigned)bi) % CC_ACC_POOL;
+                    const uint32_t v = atomicExch(acc, 0u) ^ cf.init;
+                    rg.d_crc[slot] = v;
+                    if (rg.h_crc) rg.h_crc[slot] = v;
+                    __threadfence_system();
+                    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(rg.ready + slot),
+                                 "l"(q)
+                                 : "memory");
+                }
+            }
+        }
+        return;
+    }
+
+    if (warp == NCW) {
+        // ---------------- producer warp: tables, the device slot gate, the items ----
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(tab_bar, CC_IMG_WORDS * 4u);
+            tma_load_1d(smem + (L.r1 - sbase), cf.img, 65536u, tab_bar);
+            tma_load_1d(smem + (L.r2 - sbase), cf.img + CC_IMG_WORDS / 2, 65536u, tab_bar);
+        }
+        // item params (sample, crop, flip) one 32-item chunk ahead, one item
+        // per lane, into a 64-entry ring: the dependent order/sample loads stay
+        // off the per-item path (the per-batch kernel caches them in its prologue)
+        ItemPar *par = reinterpret_cast<ItemPar *>(smem + L.par);
+        auto fill = [&](int k0) {  // items k0 .. k0 + 31
+            const int k = k0 + lane;
+            if (k < nk) {
+                const int64_t gi = (int64_t)blockIdx.x + (int64_t)k * grid;
+                const int bi = (int)(gi / items), j = (int)(gi - (int64_t)bi * items);
+                ItemPar p;
+                p.s = j / g.nrb;
+                const int64_t sample = order0[(int64_t)bi * g.b + p.s];
+                p.src_off = sample * g.sample_bytes;
+                derive_aug(aug_mixed, epoch, sample, g.pad, flip_en, p.oy, p.ox, p.fl);
+                par[k & 63] = p;
+            }
+        };
+        fill(0);
+        fill(32);
+        __syncwarp();
+        uint64_t known = 0;  // lane 0: every live cursor is known to have released this level
+        int gated = -1;
+        for (int k = 0, st = 0, ph = 0, bi = bi0, j = j0; k < nk; ++k, step(bi, j)) {
+            if ((k & 31) == 0 && k >= 32) {  // items k .. k+31 were filled; fill k+32 ..
+                fill(k + 32);
+                __syncwarp();
+            }
+            const ItemPar p = par[k & 63];
+            if (k >= NST) cc_wait(&empty[st], ph ^ 1);
+            const uint64_t q = rg.seq0 + (uint64_t)bi;
+            if (bi != gated) {  // first item of a batch: its slot must be free
+                gated = bi;
+                if (lane == 0 && q > (uint64_t)rg.slots) {
+                    const uint64_t need = q - (uint64_t)rg.slots;
+                    // the slot's previous batch is published: its completion counter
+                    // is free again (without live consumers nothing else orders it)
+                    const uint64_t *rw = rg.ready + (slot0 + bi) % rg.slots;
+                    uint64_t pub;
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(pub) : "l"(rw)
+                                     : "memory");
+                        if ((int64_t)(pub - need) >= 0) break;
+                        __nanosleep(64);
+                    }
+                    while ((int64_t)(known - need) < 0) {
+                        uint64_t gw;
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw) : "l"(rg.gate)
+                                     : "memory");
+                        if ((int64_t)(gw - known) > 0) known = gw;
+                        if ((int64_t)(known - need) >= 0) break;
+                        if (blockIdx.x == 0) {  // CTA 0 alone reads the host-shared cursors
+                            const uint64_t lo = cc_min_live(rg, need);
+                            if ((int64_t)(lo - known) > 0) {
+                                known = lo;
+                                atomicMax(rg.gate, (unsigned long long)lo);
+                            }
+                        }
+                        if ((int64_t)(known - need) < 0) __nanosleep(blockIdx.x == 0 ? 200 : 100);
+                    }
+                }
+                __syncwarp();
+            }
+            const int y0 = (j - p.s * g.nrb) * g.R;
+            const int sy_first = y0 + p.oy - g.pad;
+            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
+            const uint8_t *sample = src + p.src_off;
+            uint8_t *dst = smem + soff(st) + g.io;
+            if (lane == 0) {
+                meta[st].p = p;
+                meta[st].batch = bi;
+                meta[st].j = j;
+                meta[st].slot = (slot0 + bi) % rg.slots;
+                meta[st].last = is_last(k, j);
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&full[st], (uint32_t)max(0, hi - lo) * (uint32_t)g.row_bytes);
+            }
+            __syncwarp();
+            const uint64_t pol = l2_evict_first_policy();
+            for (int r = lo + lane; r < hi; r += 32)
+                tma_load_1d_hint(dst + (r - sy_first) * g.rs, sample + (int64_t)r * g.row_bytes,
+                                 (uint32_t)g.row_bytes, &full[st], pol);
+            if (++st == NST) st = 0, ph ^= 1;
+        }
+        // CTA 0 keeps the gate level moving until the range's last batch is out:
+        // other CTAs may still wait on it after CTA 0 ran out of items
+        if (blockIdx.x == 0 && lane == 0 && rg.n > 0) {
+            const uint64_t q_last = rg.seq0 + (uint64_t)rg.n - 1;
+            const int last_slot = (int)((q_last - 1) % (uint64_t)rg.slots);
+            while (cc_ld_acquire_sys(rg.ready + last_slot) != q_last) {
+                const uint64_t need = q_last > (uint64_t)rg.slots ? q_last - (uint64_t)rg.slots : 0;
+                const uint64_t lo = cc_min_live(rg, need);
+                if ((int64_t)(lo - known) > 0) {
+                    known = lo;
+                    atomicMax(rg.gate, (unsigned long long)lo);
+                }
+                __nanosleep(500);
+            }
+        }
+        return;
+    }
+
+    if (warp < NCW) {
+        // ------- emit warps: normalised NCHW + per-element checksum lookups -----------
+        const uint32_t *smem_words = reinterpret_cast<const uint32_t *>(smem);
+        const int64_t plane_bytes = g.plane * E;
+        const int xg = tid % g.groups, r_first = tid / g.groups, dr = NT / g.groups;
+        const int x0 = xg * P, run = x0 >> 5;
+        const int ridx = lane / (32 / P), ra = ridx >> 2, rb = ridx & 3;
+        uint32_t A[NS], B[4];
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2)
+            A[s2] = L.r1 | ((uint32_t)((x0 & 31) + 4 * ((s2 + ra) % NS)) << 2);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) B[t] = (uint32_t)((t + rb) & 3) << 2;
+        const int n_iter = g.R / dr;
+        cc_wait(tab_bar, 0);
+        for (int k = 0, st = 0, ph = 0; k < nk; ++k) {
+            cc_wait(&full[st], ph);
+            const CcItem it = meta[st];
+            const ItemPar p = it.p;
+            uint8_t *slot_base = rg.ring_base + (int64_t)it.slot * rg.slot_stride;
+            if (it.j == 0 && rg.with_target) {  // the batch's target: its sample indices
+                const int64_t *idx = order0 + (int64_t)it.batch * g.b;
+                int64_t *tgt = reinterpret_cast<int64_t *>(slot_base + rg.input_bytes);
+                for (int t = tid; t < g.b; t += NT) tgt[t] = idx[t];
+            }
+            const int y0 = (it.j - p.s * g.nrb) * g.R;
+            const int sy_first = y0 + p.oy - g.pad;
+            const int lo = max(sy_first, 0), hi = min(sy_first + g.R, g.h);
+            uint8_t *out_item = slot_base + ((int64_t)p.s * C * g.plane + (int64_t)y0 * g.w + x0) * E;
+            const uint32_t so = soff(st);
+            uint32_t *pst = part + st * part_words + run;
+#pragma unroll 1
+            for (int jj = 0; jj < n_iter; ++jj) {
+                const int r = r_first + jj * dr;
+                const int sy = sy_first + r;
+                const uint32_t row_off = (sy >= lo && sy < hi) ? so + (uint32_t)(r * g.rs) : L.zero;
+                uint8_t *o = out_item + (int64_t)r * g.w * E;
+                uint32_t *pr = pst + r * runs;
+                if (!p.fl)
+                    cc_emit_slot<OUT_KIND, C, false>(smem_words, row_off + g.rdoff + (x0 + p.ox) * C,
+                                                     norm, o, plane_bytes, lane, A, B, ra, rb, pr,
+                                                     g.R * runs, std::make_integer_sequence<int, C>{});
+                else
+                    cc_emit_slot<OUT_KIND, C, true>(smem_words,
+                                                    row_off + g.rdoff + (g.w - P - x0 + p.ox) * C,
+                                                    norm, o, plane_bytes, lane, A, B, ra, rb, pr,
+                                                    g.R * runs, std::make_integer_sequence<int, C>{});
+            }
+            mbar_arrive(&pfull[st]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == NST) st = 0, ph ^= 1;
+            if (it.last) warp_done(it.batch);
+        }
+    } else {
+        // ------- combiner warps: one column run, lane = row of the item ---------------
+        const int run = warp - NCW - 1;
+        const uint32_t rowsh = L.r2 + 128u + 4u * (uint32_t)lane + (128u << 8);
+        const uint32_t *wrun_tab = cf.wtab + (int64_t)run * cf.nseg * 32 + lane;
+        uint32_t wacc = 0;
+        cc_wait(tab_bar, 0);
+        for (int k = 0, st = 0, ph = 0, bi = bi0, j = j0; k < nk; ++k, step(bi, j)) {
+            const int s_ = j / g.nrb, rb = j - s_ * g.nrb;
+            uint32_t wv[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                wv[c] = __ldg(wrun_tab + (int64_t)(cf.nseg - 1 - ((s_ * C + c) * g.nrb + rb)) * 32);
+            if (j == 0 && run == 0 && cf.with_tgt) {  // raw CRC of the batch's int64 target
+                const int64_t *idx = order0 + (int64_t)bi * g.b;
+                const int nl = (g.b + 31) >> 5, z = 32 * nl - g.b;
+                uint32_t cr = 0;
+                for (int e = 0; e < nl; ++e) {
+                    const int v = lane * nl + e - z;
+                    if (v >= 0) {
+                        const uint64_t x = (uint64_t)idx[v];
+                        cr = cc_crc_word(cf.slice, cr, (uint32_t)x);
+                        cr = cc_crc_word(cf.slice, cr, (uint32_t)(x >> 32));
+                    }
+                }
+#pragma unroll
+                for (int k2 = 0; k2 < 5; ++k2) {
+                    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, cr, 1 << k2);
+                    cr = (lane & (1 << k2)) ? cc_multmodp(cf.tgt_k[k2], other) ^ cr
+                                            : cc_multmodp(cf.tgt_k[k2], cr) ^ other;
+                }
+                if (lane == 0) wacc ^= cr;
+            }
+            cc_wait(&pfull[st], ph);
+            uint32_t S[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                uint32_t *w = part + st * part_words + (c * g.R + lane) * runs + run;
+                S[c] = lane < g.R ? *w : 0u;
+                if (lane < g.R) *w = 0u;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == NST) st = 0, ph ^= 1;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                uint32_t x = lane < g.R ? cc_mul_nib(S[c], rowsh) : 0u;
+#pragma unroll
+                for (int k2 = 16; k2 >= 1; k2 >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, k2);
+                wacc ^= ((x >> lane) & 1u) ? wv[c] : 0u;
+            }
+            if (is_last(k, j)) {  // this warp's share of the batch's checksum
+#pragma unroll
+                for (int k2 = 16; k2 >= 1; k2 >>= 1) wacc ^= __shfl_xor_sync(0xFFFFFFFFu, wacc, k2);
+                if (lane == 0 && wacc)
+                    atomicXor(rg.acc_pool + (rg.acc_base + (unsigned)bi) % CC_ACC_POOL, wacc);
+                wacc = 0;
+                warp_done(bi);
+            }
+        }
+    }
+}
+
 // ---- host: tables (cached per configuration) and the launch ---------------
 constexpr uint32_t CC_POLY = 0xEDB88320u;
 inline uint32_t cc_h_multmodp(uint32_t a, uint32_t b) {
@@ -778,9 +1183,101 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     return launch_cc_c<TSB_OUT_BF16>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
 }
 
+template <int K, int C>
+int launch_ccr(const uint8_t *src, const int64_t *order0, const CaGeom &g, int flip,
+               uint64_t aug_mixed, uint64_t epoch, const Norm &norm, cudaStream_t s,
+               const CrcFuse &cf, const CcRange &rg) {
+    auto kern = collate_crc_range_kernel<K, C>;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64) dev = 63;
+    if (!attr_set[dev]) {
+        TSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CC_SMEM));
+        attr_set[dev] = true;
+    }
+    const int64_t total = (int64_t)g.items * rg.n;
+    const int grid = (int)(total < sm_count() ? total : sm_count());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(cf.ne + 64 + 32 * (g.w / 32));  // emit, producer, combiners, publisher
+    cfg.dynamicSmemBytes = CC_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: CTAs gate independently
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, src, order0, g, flip, aug_mixed, epoch, norm, cf, rg));
+    return TSB_OK;
+}
+
+// n batches of the fused collate + checksum in one persistent launch (the
+// caller checked cc_fusable); TSB_ERR_STALE: take the per-batch path.
+int launch_collate_crc_range(const uint8_t *src, const int64_t *order0, CaGeom g, int c, int flip,
+                             uint64_t aug_mixed, uint64_t epoch, const Norm &norm, int out_kind,
+                             cudaStream_t s, CcRange rg, int ne) {
+    int dev = 0;
+    TSB_CUDA(cudaGetDevice(&dev));
+    CcKey key{};
+    key.dev = dev;
+    key.out_kind = out_kind == OUT_BF16_FMA ? TSB_OUT_BF16 : out_kind;
+    key.c = c;
+    key.w = g.w;
+    key.h = g.h;
+    key.R = g.R;
+    key.b = g.b;
+    key.with_tgt = rg.with_target;
+    if (key.out_kind != TSB_OUT_U8) {
+        memcpy(key.scale, norm.scale, sizeof(key.scale));
+        memcpy(key.bias, norm.bias, sizeof(key.bias));
+    }
+    const CcPlan *pl = nullptr;
+    if (int rc = cc_plan(key, s, &pl)) return rc;
+    if (!pl) return TSB_ERR_STALE;
+    static uint32_t *acc_base[64] = {nullptr};
+    static unsigned long long *gate_words[64] = {nullptr};
+    static std::atomic<unsigned> acc_next{0};
+    if (!acc_base[dev]) {
+        void *p = nullptr;
+        TSB_CUDA(cudaGetSymbolAddress(&p, g_cc_acc));
+        acc_base[dev] = static_cast<uint32_t *>(p);
+        TSB_CUDA(cudaMalloc(&gate_words[dev], 256));
+    }
+    CrcFuse cf{};
+    cf.img = pl->d_img;
+    cf.slice = pl->d_slice;
+    cf.wtab = pl->d_w;
+    memcpy(cf.tgt_k, pl->tgt_k, sizeof(cf.tgt_k));
+    cf.init = pl->init;
+    cf.nseg = pl->nseg;
+    cf.with_tgt = key.with_tgt;
+    cf.tab_c = key.out_kind == TSB_OUT_U8;
+    cf.ne = ne;
+    rg.acc_pool = acc_base[dev];
+    rg.acc_base = acc_next.fetch_add((unsigned)rg.n, std::memory_order_relaxed) % CC_ACC_POOL;
+    rg.gate = gate_words[dev];
+    TSB_CUDA(cudaMemsetAsync(rg.gate, 0, sizeof(unsigned long long), s));
+    g.nstage = cc_stages(g, c);
+#define TSB_CCR(KK)                                                                                \
+    switch (c) {                                                                                   \
+        case 1: return launch_ccr<KK, 1>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \
+        case 2: return launch_ccr<KK, 2>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \
+        default: return launch_ccr<KK, 3>(src, order0, g, flip, aug_mixed, epoch, norm, s, cf, rg); \
+    }
+    if (out_kind == TSB_OUT_U8) TSB_CCR(TSB_OUT_U8)
+    if (out_kind == TSB_OUT_F32) TSB_CCR(TSB_OUT_F32)
+    if (out_kind == OUT_BF16_FMA) TSB_CCR(OUT_BF16_FMA)
+    TSB_CCR(TSB_OUT_BF16)
+#undef TSB_CCR
+}
+
 template <int K>
 void preload_cc() {
     touch_kernel(collate_crc_kernel<K, 1>);
     touch_kernel(collate_crc_kernel<K, 2>);
     touch_kernel(collate_crc_kernel<K, 3>);
+    touch_kernel(collate_crc_range_kernel<K, 1>);
+    touch_kernel(collate_crc_range_kernel<K, 2>);
+    touch_kernel(collate_crc_range_kernel<K, 3>);
 }

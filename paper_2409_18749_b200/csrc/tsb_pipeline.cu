@@ -13,6 +13,14 @@ int ring_writers(const tsb_ring *r);
 int ring_phys_device(const tsb_ring *r);
 void ring_internals(tsb_ring *r, uint8_t **base, int64_t *stride, uint64_t **ready,
                     uint64_t **cursors, unsigned int **counters);
+int produce_persistent_crc(const void *src, const int64_t *order, int64_t b, int h, int w, int c,
+                           int pad, int flip, uint64_t aug_seed, uint64_t epoch,
+                           const float *scale, const float *bias, int out_kind,
+                           uint8_t *ring_base, int64_t slot_stride, int slots, uint64_t *ready,
+                           const uint64_t *cursors, unsigned int *counters, const int *live,
+                           int n_live, int64_t input_bytes, int with_target, uint64_t seq0,
+                           int64_t batch0, int n, uint32_t *d_crc, uint32_t *h_crc,
+                           void *stream);
 int produce_persistent(int mode, const void *src, const int64_t *order, int64_t b,
                        int64_t sample_bytes, uint64_t seed, uint64_t epoch, uint8_t *ring_base,
                        int64_t slot_stride, int slots, uint64_t *ready, const uint64_t *cursors,
@@ -91,7 +99,25 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     static const bool direct_ingest =
         getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "direct");
     const bool staged = !jpeg && a->ingest && a->h_order && !ev && !direct_ingest;
-    if (a->persistent) {  // one cooperative launch for the whole range, gated on the device
+    if (a->persistent && a->d_crc && a->mode == TSB_SRC_AUGMENT && !staged && !jpeg && !ev &&
+        !no_fused && ring_has_host_control(r) && ring_writers(r) == 1) {
+        // fused collate + CRC, one cooperative launch for the whole range
+        uint8_t *base = nullptr;
+        int64_t sstride = 0;
+        uint64_t *ready = nullptr, *cursors = nullptr;
+        unsigned int *counters = nullptr;
+        ring_internals(r, &base, &sstride, &ready, &cursors, &counters);
+        const int rc = produce_persistent_crc(
+            a->src, a->d_order, b, a->h, a->w, a->c, a->pad, a->flip, a->seed, a->epoch, a->scale,
+            a->bias, a->out_kind, base, sstride, slots, ready, cursors, counters, live, n_live,
+            a->input_bytes, a->with_target, seq0, batch0, n, a->d_crc, a->h_crc, stream);
+        if (rc != TSB_ERR_STALE) {
+            if (a->crc_fused) *a->crc_fused = rc == TSB_OK && n > 0 ? 1 : 0;
+            return rc;
+        }
+    }
+    if (a->persistent && !(a->d_crc && a->mode == TSB_SRC_AUGMENT)) {
+        // one cooperative launch for the whole range, gated on the device
         TSB_CHECK(ring_has_host_control(r) && ring_writers(r) == 1 && !staged && !jpeg &&
                       !a->d_crc && !ev,
                   "the persistent producer needs a host-control single-writer ring, a "

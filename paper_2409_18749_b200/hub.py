@@ -121,9 +121,12 @@ class Facade:
 
     def set_batch(self, hub: Hub, ring, args, stream, depth: int, ring_id: int, header: bytes,
                   nbytes: int, d_crc=None, h_crc=None, events=None) -> None:
+        from .ring import hold_for_stream
+
         evs = None
         if d_crc is not None:
             evs = (ctypes.c_void_p * ring.slots)(*[int(e.cuda_event) for e in events])
+        hold_for_stream(args, stream)
         self._keep = [args, evs, header]
         _lib.call("tsb_facade_set_batch", self._h, hub._h, ring._h, ctypes.byref(args),
                   _lib.stream_handle(stream), depth, ring_id, header, nbytes,

@@ -1100,7 +1100,9 @@ class TensorProducer:
             args = []
             for k in writers:
                 a = ProduceArgs.from_buffer_copy(base)
-                a.d_order = self._order_on(self._devices[k], self._epoch).data_ptr()
+                o = self._order_on(self._devices[k], self._epoch)
+                a.d_order = o.data_ptr()
+                a._keep = (o,)
                 a.gate = GATE_HOST
                 args.append(a)
             self._group_cache = (key, args)
@@ -1131,10 +1133,13 @@ class TensorProducer:
             gargs, aargs = [], []
             for k in range(G):
                 a = ProduceArgs.from_buffer_copy(gbase)
-                a.d_order = self._order_on(self._devices[k], self._epoch).data_ptr()
+                o = self._order_on(self._devices[k], self._epoch)
+                a.d_order = o.data_ptr()
+                a._keep = (o,)
                 a.gate = GATE_HOST
                 gargs.append(a)
                 a2 = ProduceArgs.from_buffer_copy(abase)
+                a2._keep = getattr(abase, "_keep", None)
                 a2.ingest = self._tables[k].handle
                 a2.gate = GATE_HOST
                 aargs.append(a2)

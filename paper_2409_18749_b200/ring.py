@@ -302,6 +302,33 @@ def _stream(stream):
     return _lib.stream_handle(stream)
 
 
+def hold_for_stream(args, stream) -> None:
+    """Keep the device buffers ``args`` points at (``args._keep``: the epoch
+    order) allocated for the work enqueued on ``stream``.  The loader drops an
+    epoch's order when the next epoch starts while launches that read it may
+    still be queued on the producer stream (a persistent range launch, or the
+    last batches of the epoch behind the slot gate); without this the caching
+    allocator hands the block to the next epoch's order and those launches
+    gather the wrong samples.  Recorded once per (buffer, stream)."""
+    keep = getattr(args, "_keep", None)
+    if not keep:
+        return
+    import torch
+
+    if stream is None:
+        s = torch.cuda.current_stream()
+    elif isinstance(stream, torch.cuda.Stream):
+        s = stream
+    else:
+        h = getattr(stream, "cuda_stream", stream)
+        s = torch.cuda.ExternalStream(int(h.value if hasattr(h, "value") else h))
+    held = args.__dict__.setdefault("_held", set())
+    for t in keep:
+        if isinstance(t, torch.Tensor) and t.is_cuda and (id(t), s.cuda_stream) not in held:
+            t.record_stream(s)
+            held.add((id(t), s.cuda_stream))
+
+
 def _ev_array(events):
     if events is None:
         return None
@@ -314,6 +341,7 @@ def produce_range(ring: DeviceRing, args, seq0: int, batch0: int, n: int, live, 
     """Native producer loop: n batches of one epoch into the ring (tsb_produce_range)."""
     live = list(live)
     arr = (ctypes.c_int * max(1, len(live)))(*live)
+    hold_for_stream(args, stream)
     call("tsb_produce_range", ring._h, ctypes.byref(args), seq0, batch0, n, arr, len(live),
          _ev_array(events), _stream(stream))
 
@@ -338,6 +366,7 @@ def produce_group(rings, local: int, args, shard: int, n_shards: int, seq0: int,
     counts = (ctypes.c_int * len(rings))(*[len(lv) for lv in live_per_ring])
     if len(live_per_ring) != len(rings):
         raise ValueError("one live list per ring")
+    hold_for_stream(args, stream)
     call("tsb_produce_group", ptrs, len(rings), local, ctypes.byref(args), shard, n_shards, seq0,
          batch0, n, live, counts, _stream(stream))
 
@@ -357,6 +386,8 @@ def produce_group_multi(rings, args_list, locals_, devices, streams, seq0: int, 
     flat = [c for lv in live_per_ring for c in lv]
     live = (ctypes.c_int * max(1, len(flat)))(*flat)
     counts = (ctypes.c_int * len(rings))(*[len(lv) for lv in live_per_ring])
+    for a, s in zip(args_list, streams):
+        hold_for_stream(a, s)
     call("tsb_produce_group_multi", ptrs, len(rings), arr, loc, devs, sts, W, seq0, batch0, n,
          live, counts)
 
@@ -366,5 +397,6 @@ def restage_collate(in_ring: DeviceRing, in_consumer: int, out_ring: DeviceRing,
     """Stage 2 of two-stage multi-GPU production (tsb_restage_collate)."""
     live = list(live)
     arr = (ctypes.c_int * max(1, len(live)))(*live)
+    hold_for_stream(args, stream)
     call("tsb_restage_collate", in_ring._h, in_consumer, out_ring._h, ctypes.byref(args), seq0, n,
          arr, len(live), _stream(stream))

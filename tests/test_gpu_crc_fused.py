@@ -11,6 +11,7 @@ entirely), flips, batch sizes that leave the target lanes ragged, a full C2
 batch, and geometries the fused kernel does not take (separate CRC kernel)."""
 
 import threading
+import time
 import zlib
 
 import numpy as np
@@ -29,7 +30,7 @@ KIND = {"float32": 1, "bfloat16": 2, "uint8": 0}
 
 
 def _run(oracle, h, w, c, B, N, pad, out_dtype, n, with_target=True, seed=3, aug_seed=5,
-         crc_at_ready=True, slots=3):
+         crc_at_ready=True, slots=3, persistent=False, consumer_delay=0.0):
     """n batches through the native producer loop with a per-batch CRC.  The
     fused kernel's CRC is in d_crc[slot] when the slot is published, and the
     consumer reads it then (crc_at_ready); the separate CRC kernel runs after
@@ -51,6 +52,8 @@ def _run(oracle, h, w, c, B, N, pad, out_dtype, n, with_target=True, seed=3, aug
             for q in range(1, n + 1):
                 slot = ring.slot_of(q)
                 ring.host_wait_ready(slot, q, timeout_s=120)
+                if consumer_delay:
+                    time.sleep(consumer_delay)
                 with torch.cuda.stream(cs):
                     raw = ring.view(slot, (ld.batch_nbytes,), torch.uint8).cpu().numpy().copy()
                     crc = int(d_crc[slot].item()) & 0xFFFFFFFF if crc_at_ready else None
@@ -69,6 +72,7 @@ def _run(oracle, h, w, c, B, N, pad, out_dtype, n, with_target=True, seed=3, aug
         m = min(n - q + 1, L - bi)
         a = ld.produce_args(epoch, with_crc=d_crc)
         a.gate = GATE_HOST
+        a.persistent = int(persistent)
         produce_range(ring, a, q, bi, m, [0], stream=ps)
         q += m
     ps.synchronize()
@@ -146,3 +150,36 @@ def test_fused_kernel_is_the_one_that_runs():
     assert any("collate_crc_kernel" in n for n in names), names
     assert not any("crc_tile_kernel" in n or "crc_kernel" == n for n in names), names
     ring.close()
+
+
+@pytest.mark.parametrize("out_dtype,c,B,n,slots", [
+    ("float32", 3, 8, 9, 3), ("bfloat16", 3, 5, 12, 2), ("uint8", 1, 33, 7, 4),
+    ("float32", 3, 1, 16, 3),
+])
+def test_persistent_range_crc(oracle, out_dtype, c, B, n, slots):
+    """One cooperative launch for the range (collate_crc_range_kernel): the
+    slot gate runs on the device against the consumer's acks, batches cross
+    CTA boundaries mid-stage, every slot's CRC is in place at its publish.
+    B=1: a batch of 2 items (fewer items than CTAs)."""
+    _run(oracle, 64, 64, c, B, 60, 6, out_dtype, n, slots=slots, persistent=True)
+
+
+def test_persistent_range_crc_full_c2(oracle):
+    """C2 geometry, 6 batches through a 2-slot ring in one launch."""
+    _run(oracle, 224, 224, 3, 256, 1024, 16, "float32", 6, slots=2, persistent=True)
+
+
+def test_persistent_range_crc_epoch_boundary(oracle):
+    """A range that crosses the epoch (the loop splits it: one launch per epoch chunk)."""
+    _run(oracle, 32, 64, 3, 4, 12, 4, "float32", 7, persistent=True)
+
+
+@pytest.mark.parametrize("persistent", [False, True])
+def test_epoch_orders_outlive_queued_launches(oracle, persistent):
+    """One batch per epoch and a slow consumer: the producer enqueues launches
+    for later epochs while earlier ones still wait on the slot gate, and each
+    epoch switch drops the previous epoch's device order.  The order buffers
+    must stay allocated for the queued launches (ring.hold_for_stream), or the
+    next epoch's order lands in the same block and they gather wrong samples."""
+    _run(oracle, 32, 64, 3, 33, 60, 4, "float32", 10, slots=2, persistent=persistent,
+         consumer_delay=0.05)

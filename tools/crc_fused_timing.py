@@ -24,6 +24,7 @@ K = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 H = W = 224
 C, N, SLOTS = 3, 16384, 8
 B = int(os.environ.get("TIMING_B", "256"))
+PERSIST = int(os.environ.get("TIMING_PERSIST", "0"))  # 1: one persistent launch per range
 torch.cuda.set_device(0)
 store = StoreSource.synthetic(0, N, (H, W, C), location="hbm")
 E = {"f32": 4, "bf16": 2, "u8": 1}
@@ -44,7 +45,12 @@ for kind in kinds:
                 m = min(n - done, L - bi)
                 a = ld.produce_args(epoch, with_crc=d_crc)
                 a.gate = GATE_HOST
+                a.persistent = PERSIST if crc else 0
                 produce_range(ring, a, q, bi, m, [], stream=s)
+                if os.environ.get("TIMING_SYNC"):
+                    print("range", q, bi, m, flush=True)
+                    s.synchronize()
+                    print("  done", flush=True)
                 done += m
 
         run(1, 8)
@@ -56,7 +62,7 @@ for kind in kinds:
         s.synchronize()
         ms = e0.elapsed_ms(e1) / K
         alg = B * (H * W * C + C * H * W * E[kind])
-        print(json.dumps({"kind": kind, "b": B, "checksum": crc, "us_per_batch": round(ms * 1e3, 2),
+        print(json.dumps({"kind": kind, "b": B, "checksum": crc, "persistent": PERSIST, "us_per_batch": round(ms * 1e3, 2),
                           "alg_gbs": round(alg / (ms / 1e3) / 1e9, 1)}),
               flush=True)
     ring.close()
