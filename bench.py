@@ -193,13 +193,17 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the collate kernel from the committed ncu capture."""
+def ncu_traffic(per_batch=True):
+    """DRAM bytes per batch of the collate kernel from the committed ncu capture
+    (persistent range launch / its batches; per_batch=False: the per-batch
+    launch's figure)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get("collate_f32_b256_bytes_per_launch")
+        if per_batch:
+            return d.get("collate_f32_b256_bytes_per_batch")
+        return d.get("per_launch_kernel", {}).get("collate_f32_b256_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
@@ -472,7 +476,9 @@ def run_ours(args):
     if world == 1:
         achieved = B * ALG_BYTES_PER_SAMPLE / (avg_launch_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
+                    "frac": round(achieved / peak, 4),
+                    "traffic": ncu_traffic(persistent) if d_crc is not None else None,
+                    "traffic_per": "batch (ncu dram read + write of one launch / its batches)",
                     # the measured peak is a best-of-10 torch copy; the HGX spec figure
                     # (B200_PROFILING.md) for comparison
                     "spec_peak_gbs": 7700.0, "frac_of_spec": round(achieved / 7700.0, 4),
