@@ -276,11 +276,15 @@ typedef struct {
                                 engine into HBM staging first (augment), or
                                 straight into the slot (gather) */
     const int64_t *h_order;  /* host copy of d_order (row addresses for ingest) */
-    int persistent;          /* 1 (passthrough modes, host-control ring): the whole
+    int persistent;          /* 1 (host-control single-writer ring): the whole
                                 range is ONE cooperative persistent launch whose
                                 CTAs gate on the release cursors themselves -- no
-                                host launch per batch.  Consumers must not need
-                                this process's SMs to release slots. */
+                                host launch per batch.  Passthrough modes; and the
+                                augment mode with d_crc when the fused collate +
+                                CRC kernel takes the geometry (each slot's CRC is
+                                in d_crc / h_crc before its ready word; other
+                                augment geometries run per batch).  Consumers must
+                                not need this process's SMs to release slots. */
     int chain;               /* 1: the previous operation on `stream` was a fused
                                 produce kernel (so the call's first batch may chain
                                 with programmatic dependent launch too) */
