@@ -1197,7 +1197,17 @@ int launch_ccr(const uint8_t *src, const int64_t *order0, const CaGeom &g, int f
         attr_set[dev] = true;
     }
     const int64_t total = (int64_t)g.items * rg.n;
-    const int grid = (int)(total < sm_count() ? total : sm_count());
+    // SMs the range leaves free for other kernels (TSB_CC_RANGE_FREE_SMS,
+    // default 0): the launch holds one CTA per SM for the whole range.  Alone,
+    // f32 runs faster on 136 SMs (31.0 vs 32.4 us per C2 batch), but inside the
+    // bench with its consumers and the device gate all 148 are best (32.2 vs
+    // 33.4 us); bf16/u8 lose 9% with 12 free (profiles/r2/range/
+    // range_free_sms.jsonl, bench_free_sms.txt)
+    static const int free_sms = getenv("TSB_CC_RANGE_FREE_SMS")
+                                    ? atoi(getenv("TSB_CC_RANGE_FREE_SMS")) : 0;
+    int sms = sm_count() - (free_sms > 0 ? free_sms : 0);
+    if (sms < 1) sms = 1;
+    const int grid = (int)(total < sms ? total : sms);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(cf.ne + 64 + 32 * (g.w / 32));  // emit, producer, combiners, publisher
