@@ -87,8 +87,10 @@ def local_ring(ring_id: int):
     return _RINGS.get(ring_id)
 
 
-ANN_LAG = 2  # fast path with a checksum: Announce this many launches behind (1 keeps the host
-#             in lockstep with the GPU: each launch then waits for the previous batch)
+ANN_LAG = int(os.environ.get("TSB_ANN_LAG", "2"))
+# fast path with a checksum: Announce this many launches behind (1 keeps the host
+# in lockstep with the GPU: each launch then waits for the previous batch); the
+# ack gate bounds it by buffer_depth
 
 
 class TensorProducer:
