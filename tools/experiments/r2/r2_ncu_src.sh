@@ -1,6 +1,6 @@
 #!/bin/bash
 # one ncu --set full capture with the per-instruction source page kept (CSV)
-# usage: bash tools/r2_ncu_src.sh <outdir> <target> <kernel-regex> [env...]
+# usage: bash tools/experiments/r2/r2_ncu_src.sh <outdir> <target> <kernel-regex> [env...]
 out=gpurun_out/$1; mkdir -p $out; t=$2; k=$3; shift 3
 env "$@" timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
     -o /tmp/src_$t -f python tools/profile_r2.py $t 6 > $out/$t.log 2>&1
