@@ -371,8 +371,10 @@ def run_ours(args):
     # the reference checksums every segment it creates (bs/payload.py:218): the
     # per-batch CRC-32 (input + target) is fused into the collate kernel and
     # lands in d_crc[slot] before the slot is published
+    # (N > 1: the two-stage path's local collate computes it too; the fused
+    # output all-gather, fanout "outputs", runs without it)
     d_crc = (torch.zeros(RING_SLOTS, dtype=torch.int32, device=f"cuda:{dev}")
-             if CHECKSUM and world == 1 else None)
+             if CHECKSUM and (world == 1 or fanout == "inputs") else None)
 
     def chunks(seq0, n):
         done = 0
@@ -400,7 +402,7 @@ def run_ours(args):
             a.gate = GATE_HOST  # gate on the host-shared cursors; PDL-chained kernels
             # persistent: the fused collate + CRC runs the whole chunk in one
             # cooperative launch, the slot gate on the device
-            a.persistent = int(PERSIST and d_crc is not None)
+            a.persistent = int(PERSIST and d_crc is not None and world == 1)
             if world == 1:
                 produce_range(ring, a, q0, bi, m, live, stream=stream)
             elif fanout == "outputs":
@@ -451,7 +453,7 @@ def run_ours(args):
     # publish fused into the kernel, consecutive launches PDL-chained), so the
     # kernel's average launch duration is the timed region / K
     avg_launch_ms = ms / K
-    persistent = bool(PERSIST and d_crc is not None)
+    persistent = bool(PERSIST and d_crc is not None and world == 1)
     launches = sum(1 for _ in chunks(Wm + 1, K)) if persistent else K
     if world > 1:
         ms_max = reduce_over_ranks(ms, "max", backend)
@@ -536,7 +538,7 @@ def run_ours(args):
                              "against the host-shared release cursors (CTA 0 polls them and "
                              "raises a gate word) and the slot's previous publish; fused publish "
                              "(release store from the batch's completing CTA)"
-                             if PERSIST and d_crc is not None else
+                             if persistent else
                              "slot-reuse gate on the host-shared release cursors (producer "
                              "thread blocks, never the stream); fused publish (release store "
                              "from the kernel's last CTA); consecutive batches chained with "

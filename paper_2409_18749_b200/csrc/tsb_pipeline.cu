@@ -492,12 +492,20 @@ int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
         // params itself, no table kernel); the last CTA publishes the output slot
         // and releases the input slot (its cursor := q) once every CTA has read
         // its rows -- so the stream carries only these kernels, PDL-chained
-        if (int rc = collate_augment_publish(in, ingest_identity(a->ingest), b, a->h, a->w, a->c,
-                                             a->pad, a->flip, a->seed, a->epoch, a->scale, a->bias,
-                                             a->out_kind, out, tgt, ready, q, counter,
-                                             (i > 0 || a->chain) ? 1 : 0, stream, nullptr, ridx,
-                                             in_cursors + in_consumer))
+        // with a->d_crc the batch CRC-32 comes from the collate kernel too (in
+        // d_crc[oslot], and h_crc[oslot] if given, before the publish); where the
+        // fused kernel does not take the geometry the CRC kernel follows the
+        // publish, in stream order
+        int crc_done = 0;
+        if (int rc = collate_augment_publish(
+                in, ingest_identity(a->ingest), b, a->h, a->w, a->c, a->pad, a->flip, a->seed,
+                a->epoch, a->scale, a->bias, a->out_kind, out, tgt, ready, q, counter,
+                (i > 0 || a->chain) ? 1 : 0, stream, nullptr, ridx, in_cursors + in_consumer,
+                a->d_crc ? a->d_crc + oslot : nullptr, &crc_done,
+                a->d_crc && a->h_crc ? a->h_crc + oslot : nullptr))
             return rc;
+        if (a->d_crc && !crc_done)
+            if (int rc = tsb_crc32(out, out_bytes, a->d_crc + oslot, nullptr, stream)) return rc;
     }
     return TSB_OK;
 }

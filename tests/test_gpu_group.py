@@ -233,8 +233,10 @@ def test_group_cross_process_ipc():
     assert results == {r: "ok" for r in range(world)}, results
 
 
-@pytest.mark.parametrize("out_dtype,kind", [("float32", 1), ("bfloat16", 2)])
-def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind):
+@pytest.mark.parametrize("out_dtype,kind,checksum", [("float32", 1, False),
+                                                    ("bfloat16", 2, False),
+                                                    ("float32", 1, True)])
+def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind, checksum):
     """Two-stage multi-GPU production: stage 1 all-gathers the compact u8 rows
     into every GPU's input ring (passthrough group, G writers); stage 2 on
     each GPU collates the staged rows into its own output ring
@@ -256,6 +258,11 @@ def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind):
     tables = [_Ingest(0, B, h * w * c) for _ in range(G)]
     L = len(aug_ld)
     errors, got = [], {g: {} for g in range(G)}
+    # checksum: stage 2's collate kernel also writes each output slot's CRC-32
+    # (read by the consumer when the slot is published)
+    d_crc = [torch.zeros(3, dtype=torch.int32, device="cuda") if checksum else None
+             for _ in range(G)]
+    crcs = {g: {} for g in range(G)}
 
     def stage1(g):
         try:
@@ -280,7 +287,9 @@ def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind):
                 m = min(n - q + 1, L - bi)
                 from paper_2409_18749_b200._lib import ProduceArgs
 
-                a = ProduceArgs.from_buffer_copy(aug_ld.produce_args(e))
+                base = aug_ld.produce_args(e, with_crc=d_crc[g])
+                a = ProduceArgs.from_buffer_copy(base)
+                a._keep = base._keep
                 a.ingest = tables[g].handle
                 a.gate = GATE_HOST
                 restage_collate(in_rings[g], 0, out_rings[g], a, q, m, [0], stream=s)
@@ -294,6 +303,8 @@ def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind):
         for q in range(1, n + 1):
             r.host_wait_ready(r.slot_of(q), q, timeout_s=60)
             got[g][q] = r.view(r.slot_of(q), (aug_ld.batch_nbytes,), torch.uint8).cpu().numpy()
+            if checksum:
+                crcs[g][q] = int(d_crc[g][r.slot_of(q)].item()) & 0xFFFFFFFF
             r.host_ack(0, q)
 
     ts = [threading.Thread(target=f, args=(g,)) for f in (stage1, stage2, consumer)
@@ -313,5 +324,7 @@ def test_two_stage_input_allgather_then_local_collate(oracle, out_dtype, kind):
         want = np.concatenate([x.reshape(-1).view(np.uint8), idx.astype("<i8").view(np.uint8)])
         for g in range(G):
             assert got[g][q].tobytes() == want.tobytes(), (g, q)
+            if checksum:
+                assert crcs[g][q] == zlib.crc32(want.tobytes()), (g, q)
     for r in in_rings + out_rings:
         r.close()
