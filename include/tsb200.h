@@ -342,7 +342,9 @@ int tsb_produce_group(tsb_ring *const *rings, int n_rings, int local, const tsb_
  * publishes the output slot and releases the input slot (in_ring cursor
  * in_consumer := q).  a: augment geometry of the OUTPUT, a->ingest for the
  * identity table, a->chain = the stream's previous op was this call's
- * kernel. */
+ * kernel; a->d_crc (optional, [out slots]): the output slot's CRC-32, from
+ * the same kernel when it takes the geometry (also into a->h_crc if set),
+ * else from a CRC kernel after the publish. */
 int tsb_restage_collate(tsb_ring *in_ring, int in_consumer, tsb_ring *out_ring,
                         const tsb_produce_args *a, uint64_t seq0, int n, const int *live,
                         int n_live, void *stream);
