@@ -73,9 +73,12 @@ __global__ void iota_kernel(int64_t *p, int64_t n) {
 // Sample s of the batch: bytes [lo*row_bytes, hi*row_bytes) of store row
 // idx[s] -> out + s*sb (+ the same offset).  With crop params only the rows
 // the crop reads (rows [max(0, oy-pad), min(h, h+oy-pad))); else the sample.
-// 16-byte vectors when every offset is 16-byte aligned, else bytes.
+// 16-byte vectors when every offset is 16-byte aligned (vec & 1), else bytes;
+// vec & 2: the crop's row span widened to whole 128-byte lines (the extra
+// bytes belong to rows the collate does not read).
 constexpr int IG_THREADS = 256;
 constexpr int IG_U = 4;            // 16-byte loads in flight per thread
+constexpr int IG_LINE = 128;       // the crop's row span is widened to whole lines
 __global__ void __launch_bounds__(IG_THREADS)
     ingest_gather_kernel(const uint8_t *__restrict__ host, const int64_t *__restrict__ idx,
                          const int32_t *__restrict__ params, int64_t sb, int row_bytes, int h,
@@ -87,6 +90,10 @@ __global__ void __launch_bounds__(IG_THREADS)
         const int lo = max(oy - pad, 0), hi = min(h + oy - pad, h);
         begin = (int64_t)lo * row_bytes;
         end = hi > lo ? (int64_t)hi * row_bytes : begin;
+        if ((vec & 2) && end > begin) {  // whole 128-byte lines: no split PCIe read requests
+            begin &= ~(int64_t)(IG_LINE - 1);
+            end = min((end + IG_LINE - 1) & ~(int64_t)(IG_LINE - 1), sb);
+        }
     }
     const int64_t c0 = begin + (int64_t)blockIdx.x * chunk;
     const int64_t c1 = min(c0 + chunk, end);
@@ -207,6 +214,12 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     const size_t sb = (size_t)g->sample_bytes;
     int32_t *hp = g->h_params + (size_t)k * g->max_batch * 3;
     size_t nbytes = 0;
+    static const bool host_pack = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "hostpack");
+    static const bool per_sample = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "memcpy");
+    // TSB_IG_ALIGN=0 (A/B): the crop's exact row span, not widened to whole lines
+    static const bool align = !getenv("TSB_IG_ALIGN") || atoi(getenv("TSB_IG_ALIGN")) != 0;
+    const bool vec = ((uintptr_t)host_store & 15) == 0 && sb % 16 == 0 &&
+                     (!crop || crop->row_bytes % 16 == 0);
     for (int64_t i = 0; i < b; ++i) {
         size_t len = sb;
         if (crop) {
@@ -219,6 +232,12 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
             const int lo = oy - crop->pad > 0 ? oy - crop->pad : 0;
             const int hi = crop->h + oy - crop->pad < crop->h ? crop->h + oy - crop->pad : crop->h;
             len = hi > lo ? (size_t)(hi - lo) * (size_t)crop->row_bytes : 0;
+            if (vec && align && len && !host_pack && !per_sample) {  // the gather kernel reads whole lines
+                const size_t b0 = ((size_t)lo * (size_t)crop->row_bytes) & ~(size_t)(IG_LINE - 1);
+                size_t b1 = ((size_t)hi * (size_t)crop->row_bytes + IG_LINE - 1) & ~(size_t)(IG_LINE - 1);
+                if (b1 > sb) b1 = sb;
+                len = b1 - b0;
+            }
         }
         nbytes += len;
     }
@@ -233,7 +252,6 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         nbytes += sizeof(int32_t) * 3 * (size_t)b;
     }
     const int row_bytes = crop ? crop->row_bytes : 0;
-    static const bool host_pack = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "hostpack");
     if (host_pack) {
         if (!g->h_pack)
             TSB_CUDA(cudaHostAlloc(&g->h_pack, (size_t)g->depth * (size_t)g->max_batch * sb, 0));
@@ -250,7 +268,6 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         return TSB_OK;
     }
     // A/B (TSB_INGEST=memcpy): one copy-engine operation per sample instead
-    static const bool per_sample = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "memcpy");
     if (per_sample) {
         for (int64_t i = 0; i < b; ++i) {
             size_t off = 0, len = sb;
@@ -299,8 +316,7 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
         TSB_CUDA(cudaEventRecord(g->ce_done, g->ce_stream));
     }
     const int64_t b_sm = b - (n_ce > 0 ? n_ce : 0);
-    const bool vec = ((uintptr_t)host_store & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
-                     sb % 16 == 0 && (!crop || row_bytes % 16 == 0);
+    const bool vec_k = vec && ((uintptr_t)out & 15) == 0;
     // bytes per CTA and sample (TSB_IG_CHUNK A/B; 16 KB default)
     static const int64_t chunk =
         getenv("TSB_IG_CHUNK") ? (int64_t)atoll(getenv("TSB_IG_CHUNK")) : 16384;
@@ -308,7 +324,7 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     TSB_CHECK(b <= 65535, "batch %lld exceeds the gather grid", (long long)b);
     ingest_gather_kernel<<<grid, IG_THREADS, 0, g->stream>>>(
         static_cast<const uint8_t *>(host_store), dk, crop ? pk : nullptr, (int64_t)sb, row_bytes,
-        crop ? crop->h : 0, crop ? crop->pad : 0, vec ? 1 : 0, chunk, out);
+        crop ? crop->h : 0, crop ? crop->pad : 0, vec_k ? (align ? 3 : 1) : 0, chunk, out);
     TSB_LAUNCH_CHECK();
     if (n_ce > 0) TSB_CUDA(cudaStreamWaitEvent(g->stream, g->ce_done, 0));
     g->bytes += nbytes;
