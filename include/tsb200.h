@@ -299,6 +299,14 @@ typedef struct {
     int *crc_fused;          /* optional out: 1 if every batch of the call got its
                                 CRC inside the collate kernel (d_crc / h_crc hold
                                 it when the slot is published), else 0 */
+    int64_t order_epochs;    /* persistent passthrough only (<= 1 elsewhere): d_order
+                                holds this many consecutive epochs' orders
+                                (epoch, epoch + 1, ...), order_stride entries
+                                apart, and the range may run past the epoch's
+                                epoch_len batches into the following epochs --
+                                ONE launch across epoch boundaries */
+    int64_t epoch_len;       /* batches per epoch (order_epochs > 1)         */
+    int64_t order_stride;    /* int64 entries per epoch order (order_epochs > 1) */
 } tsb_produce_args;
 #define TSB_GATE_DEVICE 0
 #define TSB_GATE_HOST 1

@@ -131,6 +131,8 @@ class ProduceArgs(ctypes.Structure):
         ("chain", ctypes.c_int),
         ("jpeg", ctypes.c_void_p),
         ("h_crc", ctypes.c_void_p), ("crc_fused", ctypes.c_void_p),
+        ("order_epochs", ctypes.c_int64), ("epoch_len", ctypes.c_int64),
+        ("order_stride", ctypes.c_int64),
     ]
 
 

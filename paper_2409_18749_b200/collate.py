@@ -306,6 +306,7 @@ class CollateLoader:
         self.with_target = with_target
         self.device = torch.cuda.current_device() if device is None else device
         self._order = _EpochOrder()
+        self._next_order = None  # (epoch, thread, [host order]) computed ahead
         self._ingest = None  # staged PCIe ingest (pinned-host stores)
         self.epoch = 0  # the epoch __iter__ produces next
         src = dataset.source
@@ -365,11 +366,43 @@ class CollateLoader:
 
         if self._order.epoch != epoch:
             d = self.dataset
-            host = dp.epoch_order(d.samples_per_epoch, d.shuffle_seed, epoch,
-                                  d.reshuffle_each_epoch)
-            dev = torch.from_numpy(host).to(f"cuda:{self.device}", non_blocking=False)
+            if not d.reshuffle_each_epoch and self._order.host is not None:
+                host, dev = self._order.host, self._order.dev  # every epoch's order is the same
+            else:
+                host = self._take_next_order(epoch)
+                if host is None:
+                    host = dp.epoch_order(d.samples_per_epoch, d.shuffle_seed, epoch,
+                                          d.reshuffle_each_epoch)
+                dev = torch.from_numpy(host).to(f"cuda:{self.device}", non_blocking=False)
             self._order = _EpochOrder(epoch, host, dev)
+            if d.reshuffle_each_epoch:
+                self._start_next_order(epoch + 1)
         return self._order.host, self._order.dev
+
+    def _start_next_order(self, epoch: int) -> None:
+        """Compute the next epoch's order on a helper thread while this epoch's
+        batches run: the host Fisher-Yates (~0.2 ms at 16k samples, ~15 ms at
+        1.28M) would otherwise stall the launches at every epoch boundary (the
+        native call releases the GIL)."""
+        import threading
+
+        d = self.dataset
+        out: list = []
+
+        def work():
+            out.append(dp.epoch_order(d.samples_per_epoch, d.shuffle_seed, epoch,
+                                      d.reshuffle_each_epoch))
+
+        t = threading.Thread(target=work, name="tsb-next-order", daemon=True)
+        t.start()
+        self._next_order = (epoch, t, out)
+
+    def _take_next_order(self, epoch: int):
+        nxt, self._next_order = self._next_order, None
+        if nxt is None or nxt[0] != epoch:
+            return None
+        nxt[1].join()
+        return nxt[2][0] if nxt[2] else None
 
     def indices(self, epoch: int, batch_index: int) -> np.ndarray:
         host, _ = self.order(epoch)
@@ -435,6 +468,29 @@ class CollateLoader:
             return cached[1]
         a = self._build_args(epoch, with_crc)
         self._args_cache = (key, a)
+        return a
+
+    def produce_args_epochs(self, epoch: int, k: int):
+        """tsb_produce_args whose order covers epochs epoch..epoch+k-1 (the
+        device orders concatenated), for ONE persistent passthrough launch that
+        runs across epoch boundaries (batch0 + n <= k * len(self)): the launch
+        per epoch and its host work would otherwise set the per-batch floor of
+        small batches (C5 LLM: 64 batches of 2 MB per epoch)."""
+        import torch
+
+        from . import _lib
+
+        if k <= 1:
+            return self.produce_args(epoch)
+        base = self.produce_args(epoch)
+        a = _lib.ProduceArgs.from_buffer_copy(base)
+        host = np.concatenate([self.order(epoch + j)[0] for j in range(k)])
+        cat = torch.from_numpy(host).to(f"cuda:{self.device}", non_blocking=False)
+        a.d_order = cat.data_ptr()
+        a.order_epochs = k
+        a.epoch_len = len(self)
+        a.order_stride = self.dataset.samples_per_epoch
+        a._keep = (cat,)
         return a
 
     def _build_args(self, epoch: int, with_crc=None):

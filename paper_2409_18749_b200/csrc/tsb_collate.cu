@@ -1205,7 +1205,18 @@ struct PersistArgs {
     uint64_t seq0;
     int64_t batch0;
     int n;
+    int64_t ep_len, ep_stride;  // batches per epoch, order entries per epoch (multi-epoch ranges)
+    unsigned long long *trace;  // TSB_PT_TRACE: [2 CTAs][PT_TRACE_ITEMS][4] globaltimer stamps
+    int fence_mode;  // 0: fence.sc.gpu per count (__threadfence); 1: fence.acq_rel.gpu
+    int defer;       // items whose completion is counted under ONE fence (1..PT_DEFER_MAX)
 };
+constexpr int PT_DEFER_MAX = 8;
+constexpr int PT_TRACE_ITEMS = 320;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t *p) {
     uint64_t v;
@@ -1214,6 +1225,9 @@ __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t *p) {
 }
 
 // min over the live release cursors (host-shared, PCIe reads), wrap-around order
+// (one acquire load per cursor: a batched variant -- relaxed loads, then one
+// fence.acq_rel.sys -- measured slower, the system-scope fence costs more
+// than the serial loads; profiles/r2/passthrough/README.md)
 __device__ __forceinline__ uint64_t min_live_cursor(const PersistArgs &a, uint64_t need) {
     uint64_t lo = need + (1ull << 61);
     for (int j = 0; j < a.n_live; ++j) {
@@ -1243,18 +1257,84 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
     const int64_t nvec = a.sb >> 4;
     constexpr int U = PT_CHUNK / 16 / PT_THREADS;
     __shared__ uint64_t s_known;  // every live cursor is known to have released this level
-    if (tid == 0) s_known = 0;
+    // items copied but not yet counted (their batch's sequence number), counted
+    // in groups of `defer` under one fence; only the item's counting thread
+    // touches the list, and the per-item barrier orders the turns
+    __shared__ uint64_t s_pend[PT_DEFER_MAX];
+    __shared__ int s_pend_slot[PT_DEFER_MAX];
+    __shared__ int s_npend;
+    if (tid == 0) {
+        s_known = 0;
+        s_npend = 0;
+    }
     __syncthreads();
+    const int defer = a.defer < 1 ? 1 : (a.defer > PT_DEFER_MAX ? PT_DEFER_MAX : a.defer);
+    // one fence covers every item in the list (cumulative over the barrier-ordered
+    // stores of the CTA), then one atomic per batch run; the item that completes a
+    // batch publishes the slot (st.release.sys of the ready word)
+    auto flush = [&]() {
+        const int np = s_npend;
+        if (np == 0) return;
+        if (a.fence_mode == 1)
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        else
+            __threadfence();
+        int k = 0;
+        while (k < np) {
+            const uint64_t qq = s_pend[k];
+            int m = 1;
+            while (k + m < np && s_pend[k + m] == qq) ++m;
+            const int sl = s_pend_slot[k];
+            const unsigned int prev = atomicAdd(a.counters + sl, (unsigned int)m);
+            if (prev + (unsigned int)m == (unsigned int)ipb) {  // the batch's last items
+                a.counters[sl] = 0u;
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.ready + sl), "l"(qq)
+                             : "memory");
+            }
+            k += m;
+        }
+        s_npend = 0;
+    };
     int turn = 0;
+    const int trow = !a.trace ? -1 : blockIdx.x == 0 ? 0 : blockIdx.x == gridDim.x / 2 ? 1 : -1;
+    unsigned long long *tr = trow >= 0 && tid == 0 ? a.trace + (size_t)trow * PT_TRACE_ITEMS * 4
+                                                   : nullptr;
+    // (batch i, item it, slot) of work item g, stepped by the grid without a
+    // 64-bit division per item (one costs a CTA ~0.25 us of latency)
+    const int gstep_i = (int)(gridDim.x / (unsigned)ipb), gstep_it = (int)(gridDim.x % (unsigned)ipb);
+    const int gstep_slot = gstep_i % a.slots;
+    int i = (int)(blockIdx.x / (unsigned)ipb), it = (int)(blockIdx.x % (unsigned)ipb);
+    int slot = (int)((a.seq0 - 1 + (uint64_t)i) % (uint64_t)a.slots);
+    // the range may cross epochs: (epoch offset e, batch bi within it) of batch i
+    int64_t e = (a.batch0 + i) / a.ep_len, bi = (a.batch0 + i) - e * a.ep_len;
     for (int64_t g = blockIdx.x; g < total; g += gridDim.x, ++turn) {
-        const int i = (int)(g / ipb);
-        const int it = (int)(g - (int64_t)i * ipb);
+        if (g != (int64_t)blockIdx.x) {
+            int di = gstep_i;
+            it += gstep_it;
+            slot += gstep_slot;
+            if (it >= ipb) {
+                it -= ipb;
+                ++di;
+                ++slot;
+            }
+            if (slot >= a.slots) slot -= a.slots;
+            i += di;
+            bi += di;
+            while (bi >= a.ep_len) {
+                bi -= a.ep_len;
+                ++e;
+            }
+        }
         const uint64_t q = a.seq0 + (uint64_t)i;
-        const int slot = (int)((q - 1) % (uint64_t)a.slots);
+        if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn] = gtimer();
         if (q > (uint64_t)a.slots && (int64_t)(s_known - (q - (uint64_t)a.slots)) < 0) {
             // (uniform: s_known only changes between these two barriers)
             __syncthreads();
             if (tid == 0) {
+                // count what this CTA holds first: the consumers may need those
+                // batches published to release the slot this gate waits for
+                flush();
                 const uint64_t need = q - (uint64_t)a.slots;
                 uint64_t known = s_known;
                 while ((int64_t)(known - need) < 0) {
@@ -1276,16 +1356,18 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
             }
             __syncthreads();
         }
-        const int64_t *idx = a.order + (a.batch0 + i) * a.b;
+        const int64_t *idx = a.order + e * a.ep_stride + bi * a.b;
         uint8_t *out = a.ring_base + (int64_t)slot * a.slot_stride;
         if (it == 0 && a.with_target) {
             int64_t *tgt = reinterpret_cast<int64_t *>(out + a.input_bytes);
             for (int k = tid; k < a.b; k += PT_THREADS) tgt[k] = idx[k];
         }
+        if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 1] = gtimer();
         const int sidx = it / chunks, c = it - sidx * chunks;
         const int64_t v0 = (int64_t)c * (PT_CHUNK / 16);
         const int64_t v1 = min(v0 + PT_CHUNK / 16, nvec);
-        const uint64_t key = SYNTH ? derive_key(a.seed, a.epoch, (uint64_t)idx[sidx]) : 0;
+        const uint64_t key =
+            SYNTH ? derive_key(a.seed, a.epoch + (uint64_t)e, (uint64_t)idx[sidx]) : 0;
         const uint8_t *in = SYNTH ? nullptr : a.src + idx[sidx] * a.sb;
         uint8_t *o = out + (int64_t)sidx * a.sb;
         uint4 v[U];
@@ -1308,18 +1390,18 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
             const int64_t k = v0 + tid + u * PT_THREADS;
             if (k < v1) st_v4(o + 16 * k, v[u]);
         }
+        if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 2] = gtimer();
         __syncthreads();  // this item's stores are issued by every thread
+        if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 3] = gtimer();
         if (tid == 32 * (turn % (PT_THREADS / 32))) {
-            __threadfence();
-            const unsigned int prev = atomicAdd(a.counters + slot, 1u);
-            if (prev == (unsigned int)ipb - 1) {  // the batch's last item: publish the slot
-                a.counters[slot] = 0u;
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.ready + slot), "l"(q)
-                             : "memory");
-            }
+            s_pend_slot[s_npend] = slot;
+            s_pend[s_npend++] = q;
+            if (s_npend >= defer || g + gridDim.x >= total) flush();
         }
     }
+    __syncthreads();
+    if (tid == 0) flush();  // (the list is empty here: the last item flushed it)
+    if (tr) tr[4 * (PT_TRACE_ITEMS - 1)] = gtimer();  // loop exit
     // CTA 0 keeps the gate level moving until the range's last batch is out:
     // other CTAs may still wait on it after CTA 0 ran out of items
     if (blockIdx.x == 0 && tid == 0 && a.n > 0) {
@@ -1491,7 +1573,8 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
                        int64_t sample_bytes, uint64_t seed, uint64_t epoch, uint8_t *ring_base,
                        int64_t slot_stride, int slots, uint64_t *ready, const uint64_t *cursors,
                        unsigned int *counters, const int *live, int n_live, int64_t input_bytes,
-                       int with_target, uint64_t seq0, int64_t batch0, int n, void *stream) {
+                       int with_target, uint64_t seq0, int64_t batch0, int n, void *stream,
+                       int64_t ep_len, int64_t ep_stride) {
     TSB_CHECK(mode == TSB_SRC_GATHER || mode == TSB_SRC_SYNTHETIC,
               "the persistent producer serves the passthrough modes");
     TSB_CHECK(sample_bytes % 16 == 0 && ((uintptr_t)ring_base & 15) == 0 &&
@@ -1529,13 +1612,36 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     a.seq0 = seq0;
     a.batch0 = batch0;
     a.n = n;
+    a.ep_len = ep_len > 0 ? ep_len : batch0 + n;  // single epoch: never wraps
+    a.ep_stride = ep_stride;
+    // A/B knobs: TSB_PT_FENCE (0 = fence.sc.gpu, 1 = fence.acq_rel.gpu),
+    // TSB_PT_DEFER (items counted under one fence)
+    static int fence_mode = -1, defer = -1;
+    if (fence_mode < 0) fence_mode = getenv("TSB_PT_FENCE") ? atoi(getenv("TSB_PT_FENCE")) : 0;
+    if (defer < 0) defer = getenv("TSB_PT_DEFER") ? atoi(getenv("TSB_PT_DEFER")) : 1;
+    a.fence_mode = fence_mode;
+    a.defer = defer;
+    // TSB_PT_TRACE=k (diagnostics): the first k launches record per-item
+    // globaltimer stamps of two CTAs and print them (synchronises the stream)
+    static int trace_left = -1;
+    static unsigned long long *d_trace = nullptr;
+    if (trace_left < 0) trace_left = getenv("TSB_PT_TRACE") ? atoi(getenv("TSB_PT_TRACE")) : 0;
+    if (trace_left > 0) {
+        if (!d_trace) TSB_CUDA(cudaMalloc(&d_trace, 2 * PT_TRACE_ITEMS * 4 * 8));
+        TSB_CUDA(cudaMemsetAsync(d_trace, 0, 2 * PT_TRACE_ITEMS * 4 * 8, as_stream(stream)));
+        a.trace = d_trace;
+    }
     const bool synth = mode == TSB_SRC_SYNTHETIC;
     auto kern = synth ? persistent_passthrough_kernel<true> : persistent_passthrough_kernel<false>;
     int occ = 0;
     TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT_THREADS, 0));
-    const int64_t items = b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK);
-    static int per_sm = -1;  // CTAs per SM: fewer CTAs = fewer same-address completion atomics
-    if (per_sm < 0) per_sm = getenv("TSB_PT_PER_SM") ? atoi(getenv("TSB_PT_PER_SM")) : 2;
+    // the grid may exceed a batch's items: a CTA's items are then batches apart
+    const int64_t items = b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK) * (int64_t)n;
+    // CTAs per SM: each CTA runs one item at a time with a ~2 us per-item latency
+    // (index load, copy, barrier, count), so more CTAs per SM keep more items in
+    // flight: C5 LLM 5.4 / 3.1 / 2.9 us per batch at 2 / 4 / 8 (profiles/r2/passthrough/README.md)
+    static int per_sm = -1;
+    if (per_sm < 0) per_sm = getenv("TSB_PT_PER_SM") ? atoi(getenv("TSB_PT_PER_SM")) : 8;
     int64_t cap = (int64_t)sm_count() * (occ > 0 ? occ : 1);
     if (per_sm > 0 && (int64_t)sm_count() * per_sm < cap) cap = (int64_t)sm_count() * per_sm;
     const int grid = (int)(items < cap ? items : cap);
@@ -1549,6 +1655,33 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     TSB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    if (a.trace) {
+        --trace_left;
+        static unsigned long long h[2 * PT_TRACE_ITEMS * 4];
+        TSB_CUDA(cudaStreamSynchronize(as_stream(stream)));
+        TSB_CUDA(cudaMemcpy(h, d_trace, sizeof(h), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "pt-trace grid=%d ipb=%lld n=%d (ns from item start: gate, loaded, synced; "
+                        "item period; periods > 4 us listed)\n", grid, (long long)(items), n);
+        for (int r = 0; r < 2; ++r) {
+            const unsigned long long *row = h + (size_t)r * PT_TRACE_ITEMS * 4;
+            int k = 0;
+            unsigned long long sum_gate = 0, sum_work = 0, sum_tail = 0;
+            for (; k + 2 < PT_TRACE_ITEMS && row[(k + 1) * 4]; ++k) {
+                const unsigned long long *e = row + k * 4;
+                sum_gate += e[1] - e[0];
+                sum_work += e[3] - e[1];
+                sum_tail += e[4] - e[3];
+                if (e[4] - e[0] > 4000)
+                    fprintf(stderr, "  cta%d item%03d gate %6llu loaded %6llu synced %6llu period %6llu\n",
+                            r, k, e[1] - e[0], e[2] - e[0], e[3] - e[0], e[4] - e[0]);
+            }
+            const unsigned long long exit_t = row[4 * (PT_TRACE_ITEMS - 1)];
+            fprintf(stderr, "  cta%d: %d items, span %llu ns (gate %llu, work %llu, after-sync %llu), "
+                            "last item end -> loop exit %lld ns\n",
+                    r, k, row[k * 4] - row[0], sum_gate, sum_work, sum_tail,
+                    exit_t ? (long long)(exit_t - row[k * 4]) : -1ll);
+        }
+    }
     return TSB_OK;
 }
 }  // namespace tsb

@@ -73,16 +73,16 @@ __global__ void iota_kernel(int64_t *p, int64_t n) {
 // Sample s of the batch: bytes [lo*row_bytes, hi*row_bytes) of store row
 // idx[s] -> out + s*sb (+ the same offset).  With crop params only the rows
 // the crop reads (rows [max(0, oy-pad), min(h, h+oy-pad))); else the sample.
-// 16-byte vectors when every offset is 16-byte aligned (vec & 1), else bytes;
-// vec & 2: the crop's row span widened to whole 128-byte lines (the extra
-// bytes belong to rows the collate does not read).
+// 16-byte vectors when every offset is 16-byte aligned, else bytes.  `line`
+// (vector path): the crop's row span widened to whole lines of that many bytes
+// (the extra bytes belong to rows the collate does not read).
 constexpr int IG_THREADS = 256;
 constexpr int IG_U = 4;            // 16-byte loads in flight per thread
-constexpr int IG_LINE = 128;       // the crop's row span is widened to whole lines
+constexpr int IG_LINE = 128;       // default line the crop's row span is widened to
 __global__ void __launch_bounds__(IG_THREADS)
     ingest_gather_kernel(const uint8_t *__restrict__ host, const int64_t *__restrict__ idx,
                          const int32_t *__restrict__ params, int64_t sb, int row_bytes, int h,
-                         int pad, int vec, int64_t chunk, uint8_t *__restrict__ out) {
+                         int pad, int vec, int line, int64_t chunk, uint8_t *__restrict__ out) {
     const int s = blockIdx.y;
     int64_t begin = 0, end = sb;
     if (params) {
@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(IG_THREADS)
         const int lo = max(oy - pad, 0), hi = min(h + oy - pad, h);
         begin = (int64_t)lo * row_bytes;
         end = hi > lo ? (int64_t)hi * row_bytes : begin;
-        if ((vec & 2) && end > begin) {  // whole 128-byte lines: no split PCIe read requests
-            begin &= ~(int64_t)(IG_LINE - 1);
-            end = min((end + IG_LINE - 1) & ~(int64_t)(IG_LINE - 1), sb);
+        if (line && end > begin) {  // whole lines: no split PCIe read requests
+            begin &= ~(int64_t)(line - 1);
+            end = min((end + line - 1) & ~(int64_t)(line - 1), sb);
         }
     }
     const int64_t c0 = begin + (int64_t)blockIdx.x * chunk;
@@ -216,8 +216,9 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     size_t nbytes = 0;
     static const bool host_pack = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "hostpack");
     static const bool per_sample = getenv("TSB_INGEST") && !strcmp(getenv("TSB_INGEST"), "memcpy");
-    // TSB_IG_ALIGN=0 (A/B): the crop's exact row span, not widened to whole lines
-    static const bool align = !getenv("TSB_IG_ALIGN") || atoi(getenv("TSB_IG_ALIGN")) != 0;
+    // TSB_IG_ALIGN=bytes (A/B; a power of two, 0 = the crop's exact row span)
+    static const int line = getenv("TSB_IG_ALIGN") ? atoi(getenv("TSB_IG_ALIGN")) : IG_LINE;
+    static const bool align = line >= 16 && (line & (line - 1)) == 0;
     const bool vec = ((uintptr_t)host_store & 15) == 0 && sb % 16 == 0 &&
                      (!crop || crop->row_bytes % 16 == 0);
     for (int64_t i = 0; i < b; ++i) {
@@ -233,8 +234,8 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
             const int hi = crop->h + oy - crop->pad < crop->h ? crop->h + oy - crop->pad : crop->h;
             len = hi > lo ? (size_t)(hi - lo) * (size_t)crop->row_bytes : 0;
             if (vec && align && len && !host_pack && !per_sample) {  // the gather kernel reads whole lines
-                const size_t b0 = ((size_t)lo * (size_t)crop->row_bytes) & ~(size_t)(IG_LINE - 1);
-                size_t b1 = ((size_t)hi * (size_t)crop->row_bytes + IG_LINE - 1) & ~(size_t)(IG_LINE - 1);
+                const size_t b0 = ((size_t)lo * (size_t)crop->row_bytes) & ~(size_t)(line - 1);
+                size_t b1 = ((size_t)hi * (size_t)crop->row_bytes + line - 1) & ~(size_t)(line - 1);
                 if (b1 > sb) b1 = sb;
                 len = b1 - b0;
             }
@@ -324,7 +325,7 @@ int ingest_batch(tsb_ingest *g, const void *host_store, const int64_t *h_idx, in
     TSB_CHECK(b <= 65535, "batch %lld exceeds the gather grid", (long long)b);
     ingest_gather_kernel<<<grid, IG_THREADS, 0, g->stream>>>(
         static_cast<const uint8_t *>(host_store), dk, crop ? pk : nullptr, (int64_t)sb, row_bytes,
-        crop ? crop->h : 0, crop ? crop->pad : 0, vec_k ? (align ? 3 : 1) : 0, chunk, out);
+        crop ? crop->h : 0, crop ? crop->pad : 0, vec_k ? 1 : 0, vec_k && align ? line : 0, chunk, out);
     TSB_LAUNCH_CHECK();
     if (n_ce > 0) TSB_CUDA(cudaStreamWaitEvent(g->stream, g->ce_done, 0));
     g->bytes += nbytes;

@@ -25,7 +25,8 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
                        int64_t sample_bytes, uint64_t seed, uint64_t epoch, uint8_t *ring_base,
                        int64_t slot_stride, int slots, uint64_t *ready, const uint64_t *cursors,
                        unsigned int *counters, const int *live, int n_live, int64_t input_bytes,
-                       int with_target, uint64_t seq0, int64_t batch0, int n, void *stream);
+                       int with_target, uint64_t seq0, int64_t batch0, int n, void *stream,
+                       int64_t ep_len, int64_t ep_stride);
 int produce_multi(int mode, const void *src, const int64_t *idx, int64_t b, int h, int w, int c,
                   int pad, int flip, uint64_t seed, uint64_t epoch, const float *scale,
                   const float *bias, int out_kind, int64_t sample_bytes, void *const *outs,
@@ -81,6 +82,8 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
     TSB_CHECK(a->gate == TSB_GATE_DEVICE || ring_has_host_control(r),
               "TSB_GATE_HOST needs a ring with a host control block");
     const bool host_gate = a->gate == TSB_GATE_HOST;
+    TSB_CHECK(a->order_epochs <= 1 || (a->persistent && a->mode != TSB_SRC_AUGMENT),
+              "a multi-epoch order (order_epochs > 1) is for the persistent passthrough producer");
     static const bool no_pdl = getenv("TSB_NO_PDL") && atoi(getenv("TSB_NO_PDL"));      // A/B knobs
     static const bool no_fused = getenv("TSB_NO_FUSED") && atoi(getenv("TSB_NO_FUSED"));
     bool prev_fused = a->chain != 0;
@@ -127,11 +130,22 @@ int tsb_produce_range(tsb_ring *r, const tsb_produce_args *a, uint64_t seq0, int
         uint64_t *ready = nullptr, *cursors = nullptr;
         unsigned int *counters = nullptr;
         ring_internals(r, &base, &sstride, &ready, &cursors, &counters);
+        int64_t ep_len = 0, ep_stride = 0;
+        if (a->order_epochs > 1) {  // one launch across epoch boundaries
+            TSB_CHECK(a->epoch_len >= 1 && a->order_stride >= a->epoch_len * b &&
+                          batch0 + n <= a->order_epochs * a->epoch_len,
+                      "multi-epoch range: batches %lld..%lld exceed %lld epochs of %lld",
+                      (long long)batch0, (long long)(batch0 + n), (long long)a->order_epochs,
+                      (long long)a->epoch_len);
+            ep_len = a->epoch_len;
+            ep_stride = a->order_stride;
+        }
         return produce_persistent(a->mode, a->src, a->d_order, a->batch_size, a->sample_bytes,
                                   a->seed, a->epoch, base, sstride, slots, ready, cursors,
                                   counters, live, n_live, a->input_bytes, a->with_target, seq0,
-                                  batch0, n, stream);
+                                  batch0, n, stream, ep_len, ep_stride);
     }
+
     if (staged)
         TSB_CHECK(ingest_sample_bytes(a->ingest) == a->sample_bytes,
                   "ingest staging is for %lld-byte samples, not %lld",

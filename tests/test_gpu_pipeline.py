@@ -242,13 +242,17 @@ def test_staged_copy_engine_ingest_from_pinned_store(oracle, mode, h, pad):
     sent = ld._ingest.bytes_enqueued() - 8 * B * n  # less the index uploads
     if kind is None:
         assert sent == n * B * h * w * c
-    else:  # the rows the crop reads, plus the 12-byte param rows
-        rows = 0
+    else:  # the rows the crop reads widened to whole 128-byte lines, plus the param rows
+        rows, line, sb, rb = 0, 128, h * w * c, w * c
         for q in range(1, n + 1):
             epoch, bi = divmod(q - 1, L)
             idx = oracle.epoch_order(N, 1, epoch)[bi * B:(bi + 1) * B]
-            d = h - np.abs(oracle.aug_params(2, epoch, idx, pad)[:, 0].astype(np.int64) - pad)
-            rows += int(np.where(d > 0, d * w * c, 0).sum())  # cropped-out sample: no bytes
+            for oy in oracle.aug_params(2, epoch, idx, pad)[:, 0].astype(np.int64):
+                lo, hi = max(oy - pad, 0), min(h + oy - pad, h)
+                if hi > lo:  # cropped-out sample: no bytes
+                    b0 = (lo * rb) // line * line
+                    b1 = min(-(-(hi * rb) // line) * line, sb)
+                    rows += b1 - b0
         assert sent == rows + 12 * B * n
     ring.close()
 
@@ -361,4 +365,78 @@ def test_persistent_producer_pipelines_small_batches(oracle):
         np.testing.assert_array_equal(got[q][1], idx)
         assert got[q][0] == oracle.crc32(oracle.prepare_synthetic(3, 1, idx, 2048 * 4)), q
     a.persistent = 0
+    ring.close()
+
+
+@pytest.mark.parametrize("mode", ["synthetic", "gather"])
+def test_persistent_producer_runs_across_epochs(oracle, mode):
+    """One persistent launch across epoch boundaries (order_epochs > 1): a
+    range that starts mid-epoch and runs through three short epochs of a
+    ragged dataset (N % B != 0: each epoch drops its tail, bs/pipeline.py:77-79),
+    through a 3-slot ring gated on a host consumer.  Every batch equals the
+    oracle's batch of ITS epoch (synthetic: the epoch keys the sample bytes,
+    bs/pipeline.py:186; gather: the epoch's own order)."""
+    import threading
+    import zlib
+
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    N, B, sb = 1000, 96, 2048  # 10 batches per epoch, 40 samples dropped
+    if mode == "synthetic":
+        src = SyntheticSource(5, (sb // 4,), DType.I32)
+    else:
+        src = StoreSource.synthetic(5, N, (sb,))
+    ld = CollateLoader(DatasetSpec(src, N, B, shuffle_seed=6))
+    L = len(ld)
+    assert L == N // B
+    ring = DeviceRing(3, ld.batch_nbytes, 1, control="host")
+    ring.set_cursor(0, 0)
+    e0, b0, n = 2, 7, 2 * L + 5  # epoch 2 batch 7 .. epoch 5 batch 1
+    got = {}
+
+    def consumer():
+        for q in range(1, n + 1):
+            s = ring.slot_of(q)
+            ring.host_wait_ready(s, q, timeout_s=60)
+            v = ring.view(s, (ld.batch_nbytes,), torch.uint8).cpu().numpy()
+            got[q] = (zlib.crc32(v[:ld.input_nbytes].tobytes()),
+                      v[ld.input_nbytes:].view(np.int64).copy())
+            ring.host_ack(0, q)
+
+    t = threading.Thread(target=consumer)
+    t.start()
+    k = -(-(b0 + n) // L)
+    a = ld.produce_args_epochs(e0, k)
+    assert a.order_epochs == k == 4
+    a.gate = GATE_HOST
+    a.persistent = 1
+    ps = torch.cuda.Stream()
+    produce_range(ring, a, 1, b0, n, [0], stream=ps)
+    ps.synchronize()
+    t.join(60)
+    assert not t.is_alive() and len(got) == n
+    store = None if mode == "synthetic" else oracle.make_store(5, N, sb)
+    for q in range(1, n + 1):
+        e, bi = divmod(b0 + q - 1, L)
+        idx = oracle.epoch_order(N, 6, e0 + e)[bi * B:(bi + 1) * B]
+        np.testing.assert_array_equal(got[q][1], idx)
+        want = (oracle.prepare_synthetic(5, e0 + e, idx, sb) if mode == "synthetic"
+                else oracle.gather(store, idx, sb))
+        assert got[q][0] == oracle.crc32(want), q
+    ring.close()
+
+
+def test_multi_epoch_order_is_refused_outside_the_persistent_passthrough():
+    """order_epochs > 1 is a persistent-passthrough contract; the per-batch
+    producer refuses it loudly instead of reading past the epoch's order."""
+    from paper_2409_18749_b200._lib import GATE_HOST
+
+    src = SyntheticSource(5, (512,), DType.I32)
+    ld = CollateLoader(DatasetSpec(src, 1000, 96, shuffle_seed=6))
+    ring = DeviceRing(3, ld.batch_nbytes, 1, control="host")
+    a = ld.produce_args_epochs(0, 2)
+    a.gate = GATE_HOST
+    a.persistent = 0
+    with pytest.raises(Exception, match="multi-epoch"):
+        produce_range(ring, a, 1, 0, 12, [0], stream=torch.cuda.Stream())
     ring.close()

@@ -29,6 +29,8 @@ from bench import host_consumer  # noqa: E402
 REF = {"c1": 19050.7, "c2_shape_u8": 35139.1, "c5_llm_k8": 938897.3, "c5_video_k8": 18014.0}
 REF_SOURCE = "profiles/r1/ref_cpu_gpu_host.jsonl (unmodified reference, 16 host cores)"
 L2_BYTES = 126 * 2**20
+# persistent passthrough: epochs per launch (TSB_EPOCHS_PER_LAUNCH; 1 = a launch per epoch)
+EPOCHS_PER_LAUNCH = int(os.environ.get("TSB_EPOCHS_PER_LAUNCH", "1"))
 
 
 def hbm_line(r: dict, sample_bytes: int, slots: int, slot_bytes: int, rw: int = 2) -> dict:
@@ -72,13 +74,22 @@ def device_run(loader, n_consumers, steps, warmup, slots=8, persistent=False):
     L = len(loader)
     s = torch.cuda.Stream()
 
+    # persistent passthrough: one launch may span several epochs (short epochs,
+    # e.g. C5 LLM's 64 batches, would otherwise pay a launch + host round each)
+    multi = persistent and loader.augment is None and EPOCHS_PER_LAUNCH > 1
+
     def produce(seq0, n):
         done = 0
         while done < n:
             q0 = seq0 + done
             ep, bi = divmod(q0 - 1, L)
-            m = min(n - done, L - bi)
-            a = loader.produce_args(ep)
+            if multi:
+                k = min(EPOCHS_PER_LAUNCH, -(-(bi + n - done) // L))
+                m = min(n - done, k * L - bi)
+                a = loader.produce_args_epochs(ep, k)
+            else:
+                m = min(n - done, L - bi)
+                a = loader.produce_args(ep)
             a.gate = GATE_HOST
             a.persistent = int(persistent)
             produce_range(ring, a, q0, bi, m, list(range(n_consumers)), stream=s)
