@@ -7,11 +7,15 @@ what: f32 | bf16 | u8            C2 collate (B=256 224x224x3) through produce_ra
       f32crc | bf16crc | u8crc   the same with the per-batch CRC fused (collate_crc_kernel)
       passthrough                C1 gather (B=64 224x224x3 u8) through produce_range
       llm | llm_persistent       C5 LLM (2048,) int32 B=256 synthetic, per-batch / persistent
+                                 (llm_persistent under ncu --set full: the replayed cooperative
+                                 launch did not finish in 20 min; use TSB_PT_TRACE instead)
       video                      C5 video (16,3,112,112) u8 B=16 synthetic
       rebatch                    C4 window b=384 straddling two B=512 bf16 slots
       fanout                     one 77 MB slot copied to 2 destinations (same GPU)
       twostage                   stage-1 row gather into 2 input rings + stage-2 restage collate
       crc                        tile CRC-32 of a 154 MB f32 batch
+      ingest                     C2 f32 from a PINNED host store: the PCIe gather
+                                 (ingest_gather_kernel) + collate, per batch
 """
 import sys
 import threading
@@ -126,6 +130,9 @@ elif what == "crc":
     for _ in range(n):
         dp.crc32(data, nbytes, out)
     torch.cuda.synchronize()
+elif what == "ingest":
+    store = StoreSource.synthetic(0, 4096, (H, W, C), location="pinned")
+    run_range(CollateLoader(DatasetSpec(store, 4096, 256), AugmentSpec(out_dtype="float32")))
 else:
     raise SystemExit(f"unknown target {what}")
 print("done", what)
