@@ -24,6 +24,7 @@ into a ring slot with one kernel launch + one tiny D2D copy.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -280,6 +281,12 @@ class AugmentSpec:
         return {"float32": DType.F32, "bfloat16": DType.BF16, "uint8": DType.U8}[self.out_dtype]
 
 
+# TSB_ORDER_PREFETCH=1: the next epoch's order computed ahead on a helper thread
+# (A/B: no gain on the bench or on C5 LLM's 64-batch epochs, so off by default;
+# profiles/r2/passthrough/prefetch_ab.jsonl)
+_PREFETCH_ORDER = os.environ.get("TSB_ORDER_PREFETCH", "0") == "1"
+
+
 @dataclass
 class _EpochOrder:
     epoch: int = -1
@@ -375,15 +382,14 @@ class CollateLoader:
                                           d.reshuffle_each_epoch)
                 dev = torch.from_numpy(host).to(f"cuda:{self.device}", non_blocking=False)
             self._order = _EpochOrder(epoch, host, dev)
-            if d.reshuffle_each_epoch:
+            if d.reshuffle_each_epoch and _PREFETCH_ORDER:
                 self._start_next_order(epoch + 1)
         return self._order.host, self._order.dev
 
     def _start_next_order(self, epoch: int) -> None:
         """Compute the next epoch's order on a helper thread while this epoch's
-        batches run: the host Fisher-Yates (~0.2 ms at 16k samples, ~15 ms at
-        1.28M) would otherwise stall the launches at every epoch boundary (the
-        native call releases the GIL)."""
+        batches run (the native call releases the GIL): the host Fisher-Yates
+        costs ~0.2 ms at 16k samples, ~15 ms at 1.28M, per epoch."""
         import threading
 
         d = self.dataset
