@@ -1331,28 +1331,44 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
         if (q > (uint64_t)a.slots && (int64_t)(s_known - (q - (uint64_t)a.slots)) < 0) {
             // (uniform: s_known only changes between these two barriers)
             __syncthreads();
-            if (tid == 0) {
+            if (tid < 32) {  // warp 0 gates the CTA
                 // count what this CTA holds first: the consumers may need those
                 // batches published to release the slot this gate waits for
-                flush();
+                if (tid == 0) flush();
+                __syncwarp();
                 const uint64_t need = q - (uint64_t)a.slots;
                 uint64_t known = s_known;
                 while ((int64_t)(known - need) < 0) {
-                    uint64_t gw;  // the level CTA 0 verified (an L2 read)
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw) : "l"(a.gate)
-                                 : "memory");
+                    uint64_t gw = 0;  // the level CTA 0 verified (an L2 read)
+                    if (tid == 0)
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw)
+                                     : "l"(a.gate) : "memory");
+                    gw = __shfl_sync(0xffffffffu, gw, 0);
                     if ((int64_t)(gw - known) > 0) known = gw;
                     if ((int64_t)(known - need) >= 0) break;
-                    if (blockIdx.x == 0) {  // CTA 0 alone reads the host-shared cursors (PCIe)
-                        const uint64_t lo = min_live_cursor(a, need);
+                    if (blockIdx.x == 0) {
+                        // CTA 0 alone reads the host-shared cursors (PCIe), one
+                        // lane per consumer: the acquire loads are in flight
+                        // together (serially, 8 consumers cost ~10 us per poll)
+                        uint64_t lo = need + (1ull << 61);
+                        for (int j = tid; j < a.n_live; j += 32) {
+                            const uint64_t c = ld_acquire_sys_u64(a.cursors + a.live[j]);
+                            if ((int64_t)(c - lo) < 0) lo = c;
+                        }
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) {
+                            const uint64_t other = __shfl_xor_sync(0xffffffffu, lo, o);
+                            if ((int64_t)(other - lo) < 0) lo = other;
+                        }
+                        __syncwarp();  // every lane's acquire before lane 0 raises the gate
                         if ((int64_t)(lo - known) > 0) {
                             known = lo;
-                            atomicMax(a.gate, (unsigned long long)lo);
+                            if (tid == 0) atomicMax(a.gate, (unsigned long long)lo);
                         }
                     }
                     if ((int64_t)(known - need) < 0) __nanosleep(blockIdx.x == 0 ? 200 : 100);
                 }
-                s_known = known;
+                if (tid == 0) s_known = known;
             }
             __syncthreads();
         }
