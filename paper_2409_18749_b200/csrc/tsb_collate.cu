@@ -1207,6 +1207,7 @@ struct PersistArgs {
     int n;
     int64_t ep_len, ep_stride;  // batches per epoch, order entries per epoch (multi-epoch ranges)
     unsigned long long *trace;  // TSB_PT_TRACE: [2 CTAs][PT_TRACE_ITEMS][4] globaltimer stamps
+    int poller;      // 1: a 9th warp in CTA 0 polls the cursors and raises the gate word
     int fence_mode;  // 0: fence.sc.gpu per count (__threadfence); 1: fence.acq_rel.gpu
     int defer;       // items whose completion is counted under ONE fence (1..PT_DEFER_MAX)
 };
@@ -1237,6 +1238,43 @@ __device__ __forceinline__ uint64_t min_live_cursor(const PersistArgs &a, uint64
     return lo;
 }
 
+// The gate poller (a.poller): one extra warp of CTA 0 polls the live release
+// cursors (one lane per consumer, the acquire loads in flight together) and
+// raises the device gate word (release) until the range's last batch is
+// published.  Without it, CTA 0 polled only when CTA 0 itself reached a gated
+// batch, so CTAs ahead of it waited for CTA 0 to catch up: 40% of CTA 0's
+// span in a C1 range was gate wait, ~12% with the poller -- yet the rate did
+// not move, so it is opt-in (TSB_PT_POLLER=1; profiles/r2/passthrough/README.md).
+__device__ __forceinline__ void pt_gate_poller(const PersistArgs &a) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t q_last = a.seq0 + (uint64_t)a.n - 1;
+    const int last_slot = (int)((q_last - 1) % (uint64_t)a.slots);
+    uint64_t last = 0;
+    for (;;) {
+        uint64_t lo = q_last + (1ull << 61);  // no live consumer: open
+        for (int j = lane; j < a.n_live; j += 32) {
+            const uint64_t c = ld_acquire_sys_u64(a.cursors + a.live[j]);
+            if ((int64_t)(c - lo) < 0) lo = c;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, lo, o);
+            if ((int64_t)(other - lo) < 0) lo = other;
+        }
+        __syncwarp();  // every lane's acquire before lane 0's release of the level
+        if ((int64_t)(lo - last) > 0) {
+            last = lo;
+            if (lane == 0)
+                asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(a.gate), "l"(lo)
+                             : "memory");
+        }
+        uint64_t r = 0;
+        if (lane == 0) r = ld_acquire_sys_u64(a.ready + last_slot);
+        if (__shfl_sync(0xffffffffu, r, 0) == q_last) break;
+        __nanosleep(200);
+    }
+}
+
 // The range is one stream of work items (batch i, 16 KB chunk c), i-major,
 // strided over the grid: CTAs do not wait for each other at batch boundaries,
 // so small batches (C5 LLM: 128 items of 2 MB per batch on 296 CTAs) from
@@ -1249,7 +1287,7 @@ __device__ __forceinline__ uint64_t min_live_cursor(const PersistArgs &a, uint64
 // slot (st.release.sys of the ready word).  The next item's copy overlaps
 // that fence + atomic.
 template <bool SYNTH>
-__global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(PersistArgs a) {
+__global__ void __launch_bounds__(PT_THREADS + 32, 4) persistent_passthrough_kernel(PersistArgs a) {
     const int tid = threadIdx.x;
     const int chunks = (int)((a.sb + PT_CHUNK - 1) / PT_CHUNK);
     const int ipb = (int)a.b * chunks;  // items per batch
@@ -1268,6 +1306,12 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
         s_npend = 0;
     }
     __syncthreads();
+    if (tid >= PT_THREADS) {  // the poller warp (a.poller: blockDim = PT_THREADS + 32)
+        if (blockIdx.x == 0) pt_gate_poller(a);
+        return;
+    }
+    // the copy threads synchronise on named barrier 1 (the poller warp never joins)
+    auto cta_sync = []() { asm volatile("bar.sync 1, %0;" ::"r"(PT_THREADS) : "memory"); };
     const int defer = a.defer < 1 ? 1 : (a.defer > PT_DEFER_MAX ? PT_DEFER_MAX : a.defer);
     // one fence covers every item in the list (cumulative over the barrier-ordered
     // stores of the CTA), then one atomic per batch run; the item that completes a
@@ -1330,7 +1374,7 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn] = gtimer();
         if (q > (uint64_t)a.slots && (int64_t)(s_known - (q - (uint64_t)a.slots)) < 0) {
             // (uniform: s_known only changes between these two barriers)
-            __syncthreads();
+            cta_sync();
             if (tid < 32) {  // warp 0 gates the CTA
                 // count what this CTA holds first: the consumers may need those
                 // batches published to release the slot this gate waits for
@@ -1346,7 +1390,7 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
                     gw = __shfl_sync(0xffffffffu, gw, 0);
                     if ((int64_t)(gw - known) > 0) known = gw;
                     if ((int64_t)(known - need) >= 0) break;
-                    if (blockIdx.x == 0) {
+                    if (blockIdx.x == 0 && !a.poller) {
                         // CTA 0 alone reads the host-shared cursors (PCIe), one
                         // lane per consumer: the acquire loads are in flight
                         // together (serially, 8 consumers cost ~10 us per poll)
@@ -1370,7 +1414,7 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
                 }
                 if (tid == 0) s_known = known;
             }
-            __syncthreads();
+            cta_sync();
         }
         const int64_t *idx = a.order + e * a.ep_stride + bi * a.b;
         uint8_t *out = a.ring_base + (int64_t)slot * a.slot_stride;
@@ -1407,7 +1451,7 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
             if (k < v1) st_v4(o + 16 * k, v[u]);
         }
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 2] = gtimer();
-        __syncthreads();  // this item's stores are issued by every thread
+        cta_sync();  // this item's stores are issued by every thread
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 3] = gtimer();
         if (tid == 32 * (turn % (PT_THREADS / 32))) {
             s_pend_slot[s_npend] = slot;
@@ -1415,12 +1459,12 @@ __global__ void __launch_bounds__(PT_THREADS) persistent_passthrough_kernel(Pers
             if (s_npend >= defer || g + gridDim.x >= total) flush();
         }
     }
-    __syncthreads();
+    cta_sync();
     if (tid == 0) flush();  // (the list is empty here: the last item flushed it)
     if (tr) tr[4 * (PT_TRACE_ITEMS - 1)] = gtimer();  // loop exit
     // CTA 0 keeps the gate level moving until the range's last batch is out:
     // other CTAs may still wait on it after CTA 0 ran out of items
-    if (blockIdx.x == 0 && tid == 0 && a.n > 0) {
+    if (blockIdx.x == 0 && tid == 0 && a.n > 0 && !a.poller) {
         const uint64_t q_last = a.seq0 + (uint64_t)a.n - 1;
         const int last_slot = (int)((q_last - 1) % (uint64_t)a.slots);
         uint64_t known = s_known;
@@ -1637,6 +1681,10 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     if (defer < 0) defer = getenv("TSB_PT_DEFER") ? atoi(getenv("TSB_PT_DEFER")) : 1;
     a.fence_mode = fence_mode;
     a.defer = defer;
+    static int poller = -1;  // TSB_PT_POLLER=1 (A/B): the poller warp (neutral: off by default)
+    if (poller < 0) poller = getenv("TSB_PT_POLLER") ? atoi(getenv("TSB_PT_POLLER")) : 0;
+    a.poller = poller;
+    const int block = PT_THREADS + (poller ? 32 : 0);
     // TSB_PT_TRACE=k (diagnostics): the first k launches record per-item
     // globaltimer stamps of two CTAs and print them (synchronises the stream)
     static int trace_left = -1;
@@ -1650,7 +1698,7 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     const bool synth = mode == TSB_SRC_SYNTHETIC;
     auto kern = synth ? persistent_passthrough_kernel<true> : persistent_passthrough_kernel<false>;
     int occ = 0;
-    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT_THREADS, 0));
+    TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, 0));
     // the grid may exceed a batch's items: a CTA's items are then batches apart
     const int64_t items = b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK) * (int64_t)n;
     // CTAs per SM: each CTA runs one item at a time with a ~2 us per-item latency
@@ -1663,7 +1711,7 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     const int grid = (int)(items < cap ? items : cap);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(PT_THREADS);
+    cfg.blockDim = dim3(block);
     cfg.stream = as_stream(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: CTAs gate independently
