@@ -51,7 +51,7 @@ SAMPLE_BYTES = H * W * C           # 150,528 B u8 HWC
 B = 256
 N_SAMPLES = 16384                  # samples_per_epoch
 N_CONSUMERS = 4
-RING_SLOTS = 8
+RING_SLOTS = int(os.environ.get("TSB_BENCH_SLOTS", "8"))  # A/B knob
 PAD = 16
 OUT_BYTES = C * H * W * 4          # f32 NCHW per sample
 ALG_BYTES_PER_SAMPLE = SAMPLE_BYTES + OUT_BYTES  # 752,640 B read + write (collate)

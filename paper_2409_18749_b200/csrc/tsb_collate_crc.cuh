@@ -70,7 +70,24 @@ struct CrcFuse {
     uint32_t *out;          // the slot's CRC-32
     uint32_t *out_host;     // optional host-mapped copy (written before the ready word)
     int ne;                 // emit threads: groups x dr (dr rows apart, dr divides R)
+    int fold;               // shuffle levels before the run's atomic XOR fold (TSB_CC_FOLD)
 };
+
+// Shuffle levels before the atomic fold: the 32/P lanes of a column run XOR
+// k shuffle levels first, so 32/P >> k of them (not all) fold into the run's
+// word -- fewer same-address shared atomics, each an N-way bank conflict
+// (118 M of the 123 M excess shared wavefronts of an f32 range).  Measured per
+// output kind (range kernel, us per B=256 batch, k = 0/1/2/3):
+// f32 32.5 / 30.65 / 33.5 / 35.9, bf16 24.0 / 25.5 / 26.5 / 26.5, u8 30.8 /
+// 32.0 / 31.7 / 31.8 (profiles/r2/range/fold_ab.jsonl, no consumers): one
+// level for f32 (8 lanes per run), none for bf16 / u8.  Inside bench.py (4
+// consumers, 8-slot gate) f32 runs 31.9-32.3 us either way (fold_bench_ab.jsonl):
+// the kernel is then held elsewhere.  TSB_CC_FOLD=k overrides (A/B).
+inline int cc_fold_knob(int out_kind) {
+    static const int k = getenv("TSB_CC_FOLD") ? atoi(getenv("TSB_CC_FOLD")) : -1;
+    if (k >= 0) return k;
+    return out_kind == TSB_OUT_F32 ? 1 : 0;
+}
 
 __device__ __forceinline__ uint32_t cc_lds(uint32_t a) {
     uint32_t v;
@@ -193,7 +210,7 @@ template <int OUT_KIND, int C, bool FLIP, int CH>
 __device__ __forceinline__ void cc_emit_channel(const uint32_t *wv, const Norm &norm, uint8_t *out,
                                                 int64_t plane_bytes, int lane,
                                                 const uint32_t *A, const uint32_t *B, int ra,
-                                                int rb, uint32_t *part_c) {
+                                                int rb, uint32_t *part_c, int fold) {
     using T = OutTraits<OUT_KIND>;
     constexpr int P = T::P;
     constexpr int NS = P / 4;          // 4-element sub-words per lane
@@ -237,8 +254,17 @@ __device__ __forceinline__ void cc_emit_channel(const uint32_t *wv, const Norm &
 #pragma unroll
         for (int t = 0; t < 4; ++t)
             acc ^= cc_lds_off<COFF>(cc_prmt(R[s], A[s] | B[t], 0x7604u | (t << 4)));
-    // the run's lanes fold their lookups into its word (zeroed by the combiner)
-    atomicXor(part_c, acc);
+    // the run's lanes fold their lookups into its word (zeroed by the combiner);
+    // the run's lanes are the aligned group of LPR consecutive lanes
+    int writers = LPR;
+#pragma unroll
+    for (int d = LPR / 2; d >= 1; d >>= 1) {
+        if (fold <= 0) break;
+        acc ^= __shfl_xor_sync(0xffffffffu, acc, d);
+        writers = d;
+        --fold;
+    }
+    if ((lane & (LPR - 1)) < writers) atomicXor(part_c, acc);
 }
 
 template <int OUT_KIND, int C, bool FLIP, int... CHs>
@@ -246,7 +272,8 @@ __device__ __forceinline__ void cc_emit_slot(const uint32_t *smem_words, uint32_
                                              const Norm &norm, uint8_t *out, int64_t plane_bytes,
                                              int lane, const uint32_t *A,
                                              const uint32_t *B, int ra, int rb, uint32_t *part,
-                                             int part_cstride, std::integer_sequence<int, CHs...>) {
+                                             int part_cstride, int fold,
+                                             std::integer_sequence<int, CHs...>) {
     constexpr int P = OutTraits<OUT_KIND>::P;
     constexpr int NB = P * C;
     constexpr int NW = (NB + 3) / 4 + 1;
@@ -259,7 +286,7 @@ __device__ __forceinline__ void cc_emit_slot(const uint32_t *smem_words, uint32_
 #pragma unroll
     for (int i = 0; i < NW - 1; ++i) wv[i] = __funnelshift_r(raw[i], raw[i + 1], shift);
     (cc_emit_channel<OUT_KIND, C, FLIP, CHs>(wv, norm, out, plane_bytes, lane, A, B, ra, rb,
-                                             part + CHs * part_cstride),
+                                             part + CHs * part_cstride, fold),
      ...);
 }
 
@@ -396,12 +423,12 @@ __global__ void __launch_bounds__(CC_EMIT + 32 + 32 * CC_MAX_RUNS, 1)
                 if (!p.fl)
                     cc_emit_slot<OUT_KIND, C, false>(smem_words, row_off + g.rdoff + (x0 + p.ox) * C,
                                                      norm, o, plane_bytes, lane, A, B, ra, rb,
-                                                     pr, g.R * runs, std::make_integer_sequence<int, C>{});
+                                                     pr, g.R * runs, cf.fold, std::make_integer_sequence<int, C>{});
                 else
                     cc_emit_slot<OUT_KIND, C, true>(smem_words,
                                                     row_off + g.rdoff + (g.w - P - x0 + p.ox) * C,
                                                     norm, o, plane_bytes, lane, A, B, ra, rb,
-                                                    pr, g.R * runs, std::make_integer_sequence<int, C>{});
+                                                    pr, g.R * runs, cf.fold, std::make_integer_sequence<int, C>{});
             }
             mbar_arrive(&pfull[st]);  // this thread's run values are in the buffer
             __syncwarp();
@@ -696,7 +723,7 @@ __global__ void __launch_bounds__(CC_EMIT + 64 + 32 * CC_MAX_RUNS, 1)
         fill(0);
         fill(32);
         __syncwarp();
-        uint64_t known = 0;  // lane 0: every live cursor is known to have released this level
+        uint64_t known = 0;  // (every lane) every live cursor is known to have released this level
         int gated = -1;
         for (int k = 0, st = 0, ph = 0, bi = bi0, j = j0; k < nk; ++k, step(bi, j)) {
             if ((k & 31) == 0 && k >= 32) {  // items k .. k+31 were filled; fill k+32 ..
@@ -708,29 +735,46 @@ __global__ void __launch_bounds__(CC_EMIT + 64 + 32 * CC_MAX_RUNS, 1)
             const uint64_t q = rg.seq0 + (uint64_t)bi;
             if (bi != gated) {  // first item of a batch: its slot must be free
                 gated = bi;
-                if (lane == 0 && q > (uint64_t)rg.slots) {
+                if (q > (uint64_t)rg.slots) {  // (warp-uniform: every lane steps bi alike)
                     const uint64_t need = q - (uint64_t)rg.slots;
-                    // the slot's previous batch is published: its completion counter
-                    // is free again (without live consumers nothing else orders it)
-                    const uint64_t *rw = rg.ready + (slot0 + bi) % rg.slots;
-                    uint64_t pub;
-                    for (;;) {
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(pub) : "l"(rw)
-                                     : "memory");
-                        if ((int64_t)(pub - need) >= 0) break;
-                        __nanosleep(64);
+                    if (lane == 0) {
+                        // the slot's previous batch is published: its completion counter
+                        // is free again (without live consumers nothing else orders it)
+                        const uint64_t *rw = rg.ready + (slot0 + bi) % rg.slots;
+                        uint64_t pub;
+                        for (;;) {
+                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(pub)
+                                         : "l"(rw) : "memory");
+                            if ((int64_t)(pub - need) >= 0) break;
+                            __nanosleep(64);
+                        }
                     }
-                    while ((int64_t)(known - need) < 0) {
-                        uint64_t gw;
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw) : "l"(rg.gate)
-                                     : "memory");
+                    __syncwarp();
+                    while ((int64_t)(known - need) < 0) {  // `known` is warp-uniform
+                        uint64_t gw = 0;
+                        if (lane == 0)
+                            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(gw)
+                                         : "l"(rg.gate) : "memory");
+                        gw = __shfl_sync(0xffffffffu, gw, 0);
                         if ((int64_t)(gw - known) > 0) known = gw;
                         if ((int64_t)(known - need) >= 0) break;
-                        if (blockIdx.x == 0) {  // CTA 0 alone reads the host-shared cursors
-                            const uint64_t lo = cc_min_live(rg, need);
+                        if (blockIdx.x == 0) {
+                            // CTA 0 alone reads the host-shared cursors, one lane per
+                            // consumer: the PCIe acquire loads are in flight together
+                            uint64_t lo = need + (1ull << 61);
+                            for (int jl = lane; jl < rg.n_live; jl += 32) {
+                                const uint64_t cv = cc_ld_acquire_sys(rg.cursors + rg.live[jl]);
+                                if ((int64_t)(cv - lo) < 0) lo = cv;
+                            }
+#pragma unroll
+                            for (int o = 16; o; o >>= 1) {
+                                const uint64_t other = __shfl_xor_sync(0xffffffffu, lo, o);
+                                if ((int64_t)(other - lo) < 0) lo = other;
+                            }
+                            __syncwarp();  // every lane's acquire before lane 0 raises the gate
                             if ((int64_t)(lo - known) > 0) {
                                 known = lo;
-                                atomicMax(rg.gate, (unsigned long long)lo);
+                                if (lane == 0) atomicMax(rg.gate, (unsigned long long)lo);
                             }
                         }
                         if ((int64_t)(known - need) < 0) __nanosleep(blockIdx.x == 0 ? 200 : 100);
@@ -818,12 +862,12 @@ __global__ void __launch_bounds__(CC_EMIT + 64 + 32 * CC_MAX_RUNS, 1)
                 if (!p.fl)
                     cc_emit_slot<OUT_KIND, C, false>(smem_words, row_off + g.rdoff + (x0 + p.ox) * C,
                                                      norm, o, plane_bytes, lane, A, B, ra, rb, pr,
-                                                     g.R * runs, std::make_integer_sequence<int, C>{});
+                                                     g.R * runs, cf.fold, std::make_integer_sequence<int, C>{});
                 else
                     cc_emit_slot<OUT_KIND, C, true>(smem_words,
                                                     row_off + g.rdoff + (g.w - P - x0 + p.ox) * C,
                                                     norm, o, plane_bytes, lane, A, B, ra, rb, pr,
-                                                    g.R * runs, std::make_integer_sequence<int, C>{});
+                                                    g.R * runs, cf.fold, std::make_integer_sequence<int, C>{});
             }
             mbar_arrive(&pfull[st]);
             __syncwarp();
@@ -1173,6 +1217,7 @@ int launch_collate_crc(const uint8_t *src, const int64_t *idx, CaGeom g, int c, 
     cf.out = crc_out;
     cf.out_host = crc_host;
     cf.ne = ne;
+    cf.fold = cc_fold_knob(key.out_kind);
     g.nstage = cc_stages(g, c);
     if (out_kind == TSB_OUT_U8)
         return launch_cc_c<TSB_OUT_U8>(c, src, idx, g, flip, aug_mixed, epoch, norm, params, dsts, s, ep, cf);
@@ -1264,6 +1309,7 @@ int launch_collate_crc_range(const uint8_t *src, const int64_t *order0, CaGeom g
     cf.with_tgt = key.with_tgt;
     cf.tab_c = key.out_kind == TSB_OUT_U8;
     cf.ne = ne;
+    cf.fold = cc_fold_knob(key.out_kind);
     rg.acc_pool = acc_base[dev];
     rg.acc_base = acc_next.fetch_add((unsigned)rg.n, std::memory_order_relaxed) % CC_ACC_POOL;
     rg.gate = gate_words[dev];
