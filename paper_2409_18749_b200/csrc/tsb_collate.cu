@@ -1208,6 +1208,7 @@ struct PersistArgs {
     int64_t ep_len, ep_stride;  // batches per epoch, order entries per epoch (multi-epoch ranges)
     unsigned long long *trace;  // TSB_PT_TRACE: [2 CTAs][PT_TRACE_ITEMS][4] globaltimer stamps
     int poller;      // 1: a 9th warp in CTA 0 polls the cursors and raises the gate word
+    int *work;       // non-null: CTAs claim work items from this counter (dynamic)
     int fence_mode;  // 0: fence.sc.gpu per count (__threadfence); 1: fence.acq_rel.gpu
     int defer;       // items whose completion is counted under ONE fence (1..PT_DEFER_MAX)
 };
@@ -1352,8 +1353,28 @@ __global__ void __launch_bounds__(PT_THREADS + 32, 4) persistent_passthrough_ker
     int slot = (int)((a.seq0 - 1 + (uint64_t)i) % (uint64_t)a.slots);
     // the range may cross epochs: (epoch offset e, batch bi within it) of batch i
     int64_t e = (a.batch0 + i) / a.ep_len, bi = (a.batch0 + i) - e * a.ep_len;
-    for (int64_t g = blockIdx.x; g < total; g += gridDim.x, ++turn) {
-        if (g != (int64_t)blockIdx.x) {
+    // a.work (TSB_PT_DYNAMIC=1): items are claimed from a global counter instead
+    // of the static grid stride, so faster CTAs take more; thread 0 claims the
+    // next item during the current one (double-buffered in shared memory)
+    __shared__ int s_claim[2];
+    const bool dyn = a.work != nullptr;
+    int claim_next = 0;
+    const int slot0 = (int)((a.seq0 - 1) % (uint64_t)a.slots);
+    if (dyn) {
+        if (tid == 0) s_claim[0] = atomicAdd(a.work, 1);
+        cta_sync();
+    }
+    for (int64_t g = dyn ? (int64_t)s_claim[0] : (int64_t)blockIdx.x; g < total; ++turn) {
+        if (dyn) {
+            const int gi = (int)g;
+            i = gi / ipb;
+            it = gi - i * ipb;
+            slot = (slot0 + i) % a.slots;
+            const int64_t gb = a.batch0 + i;
+            e = gb >= a.ep_len ? gb / a.ep_len : 0;
+            bi = gb - e * a.ep_len;
+            if (tid == 0) claim_next = atomicAdd(a.work, 1);  // stored before the item's barrier
+        } else if (g != (int64_t)blockIdx.x) {
             int di = gstep_i;
             it += gstep_it;
             slot += gstep_slot;
@@ -1451,13 +1472,15 @@ __global__ void __launch_bounds__(PT_THREADS + 32, 4) persistent_passthrough_ker
             if (k < v1) st_v4(o + 16 * k, v[u]);
         }
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 2] = gtimer();
+        if (dyn && tid == 0) s_claim[(turn + 1) & 1] = claim_next;
         cta_sync();  // this item's stores are issued by every thread
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 3] = gtimer();
         if (tid == 32 * (turn % (PT_THREADS / 32))) {
             s_pend_slot[s_npend] = slot;
             s_pend[s_npend++] = q;
-            if (s_npend >= defer || g + gridDim.x >= total) flush();
+            if (s_npend >= defer || (!dyn && g + gridDim.x >= total)) flush();
         }
+        g = dyn ? (int64_t)s_claim[(turn + 1) & 1] : g + gridDim.x;
     }
     cta_sync();
     if (tid == 0) flush();  // (the list is empty here: the last item flushed it)
@@ -1664,7 +1687,14 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     TSB_CHECK(dev < 64, "device index");
     if (!gate_words[dev]) TSB_CUDA(cudaMalloc(&gate_words[dev], 256));
     a.gate = gate_words[dev];
-    TSB_CUDA(cudaMemsetAsync(a.gate, 0, sizeof(unsigned long long), as_stream(stream)));
+    TSB_CUDA(cudaMemsetAsync(a.gate, 0, 16, as_stream(stream)));  // gate word + work counter
+    // TSB_PT_DYNAMIC=0 (A/B): the static grid stride.  Claiming from a counter:
+    // C1 6.9 -> 4.3, C5 video 7.0 -> 4.3, C5 LLM 3.1 -> 2.0 us per batch
+    // (profiles/r2/passthrough/dynamic_ab.jsonl): the static stride left the range
+    // to the slowest CTAs (launches 1.59 ms vs 0.9-1.16 ms of CTA 0 items)
+    static int dynamic = -1;
+    if (dynamic < 0) dynamic = getenv("TSB_PT_DYNAMIC") ? atoi(getenv("TSB_PT_DYNAMIC")) : 1;
+    a.work = dynamic ? reinterpret_cast<int *>(reinterpret_cast<uint8_t *>(a.gate) + 8) : nullptr;
     for (int j = 0; j < n_live; ++j) a.live[j] = live[j];
     a.n_live = n_live;
     a.input_bytes = input_bytes;
@@ -1701,6 +1731,7 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, 0));
     // the grid may exceed a batch's items: a CTA's items are then batches apart
     const int64_t items = b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK) * (int64_t)n;
+    if (items >= (1ll << 31) - (1ll << 20)) a.work = nullptr;  // claims are 32-bit
     // CTAs per SM: each CTA runs one item at a time with a ~2 us per-item latency
     // (index load, copy, barrier, count), so more CTAs per SM keep more items in
     // flight: C5 LLM 5.4 / 3.1 / 2.9 us per batch at 2 / 4 / 8 (profiles/r2/passthrough/README.md)
