@@ -1209,6 +1209,7 @@ struct PersistArgs {
     unsigned long long *trace;  // TSB_PT_TRACE: [2 CTAs][PT_TRACE_ITEMS][4] globaltimer stamps
     int poller;      // 1: a 9th warp in CTA 0 polls the cursors and raises the gate word
     int *work;       // non-null: CTAs claim work items from this counter (dynamic)
+    int spi;         // samples per work item (> 1: samples below PT_CHUNK packed)
     int fence_mode;  // 0: fence.sc.gpu per count (__threadfence); 1: fence.acq_rel.gpu
     int defer;       // items whose completion is counted under ONE fence (1..PT_DEFER_MAX)
 };
@@ -1291,7 +1292,8 @@ template <bool SYNTH>
 __global__ void __launch_bounds__(PT_THREADS + 32, 4) persistent_passthrough_kernel(PersistArgs a) {
     const int tid = threadIdx.x;
     const int chunks = (int)((a.sb + PT_CHUNK - 1) / PT_CHUNK);
-    const int ipb = (int)a.b * chunks;  // items per batch
+    const int spi = a.spi > 1 ? a.spi : 1;  // (chunks == 1 when spi > 1)
+    const int ipb = spi > 1 ? (int)((a.b + spi - 1) / spi) : (int)a.b * chunks;  // items per batch
     const int64_t total = (int64_t)ipb * a.n;
     const int64_t nvec = a.sb >> 4;
     constexpr int U = PT_CHUNK / 16 / PT_THREADS;
@@ -1444,6 +1446,38 @@ __global__ void __launch_bounds__(PT_THREADS + 32, 4) persistent_passthrough_ker
             for (int k = tid; k < a.b; k += PT_THREADS) tgt[k] = idx[k];
         }
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 1] = gtimer();
+        if (spi > 1) {
+            // spi whole samples per item (samples below PT_CHUNK): vector kk of
+            // the item is vector kk % nvec of sample s0 + kk / nvec; the item's
+            // output is one contiguous range of the slot
+            const int s0 = it * spi;
+            const int ns = min(spi, (int)a.b - s0);
+            const int nv = (int)nvec, vend = ns * nv;
+            uint8_t *o = out + (int64_t)s0 * a.sb;
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int kk = tid + u * PT_THREADS;
+                if (kk < vend) {
+                    const int sl = kk / nv, k = kk - sl * nv;
+                    const int64_t sample = idx[s0 + sl];
+                    if constexpr (SYNTH) {
+                        const uint64_t key = derive_key(a.seed, a.epoch + (uint64_t)e, (uint64_t)sample);
+                        const uint64_t w0 = mix64(key + (uint64_t)(2 * k + 1) * GAMMA);
+                        const uint64_t w1 = mix64(key + (uint64_t)(2 * k + 2) * GAMMA);
+                        v[u] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1,
+                                          (uint32_t)(w1 >> 32));
+                    } else {
+                        v[u] = ld_nc_v4(a.src + sample * a.sb + 16 * (int64_t)k);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int kk = tid + u * PT_THREADS;
+                if (kk < vend) st_v4(o + 16 * (int64_t)kk, v[u]);
+            }
+        } else {
         const int sidx = it / chunks, c = it - sidx * chunks;
         const int64_t v0 = (int64_t)c * (PT_CHUNK / 16);
         const int64_t v1 = min(v0 + PT_CHUNK / 16, nvec);
@@ -1470,6 +1504,7 @@ __global__ void __launch_bounds__(PT_THREADS + 32, 4) persistent_passthrough_ker
         for (int u = 0; u < U; ++u) {
             const int64_t k = v0 + tid + u * PT_THREADS;
             if (k < v1) st_v4(o + 16 * k, v[u]);
+        }
         }
         if (tr && turn < PT_TRACE_ITEMS) tr[4 * turn + 2] = gtimer();
         if (dyn && tid == 0) s_claim[(turn + 1) & 1] = claim_next;
@@ -1730,7 +1765,15 @@ int produce_persistent(int mode, const void *src, const int64_t *order, int64_t 
     int occ = 0;
     TSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, 0));
     // the grid may exceed a batch's items: a CTA's items are then batches apart
-    const int64_t items = b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK) * (int64_t)n;
+    // TSB_PT_PACK=1 (A/B): samples below PT_CHUNK packed, PT_CHUNK / sample_bytes
+    // per work item; C5 LLM 2.0-2.2 us per batch either way (neutral with the
+    // dynamic claims, profiles/r2/passthrough/pack_ab.jsonl), so off by default
+    static int pack = -1;
+    if (pack < 0) pack = getenv("TSB_PT_PACK") ? atoi(getenv("TSB_PT_PACK")) : 0;
+    a.spi = pack && sample_bytes < PT_CHUNK ? (int)(PT_CHUNK / sample_bytes) : 1;
+    const int64_t ipb_h = a.spi > 1 ? (b + a.spi - 1) / a.spi
+                                    : b * ((sample_bytes + PT_CHUNK - 1) / PT_CHUNK);
+    const int64_t items = ipb_h * (int64_t)n;
     if (items >= (1ll << 31) - (1ll << 20)) a.work = nullptr;  // claims are 32-bit
     // CTAs per SM: each CTA runs one item at a time with a ~2 us per-item latency
     // (index load, copy, barrier, count), so more CTAs per SM keep more items in
