@@ -1335,8 +1335,9 @@ int launch_collate_crc_range(const uint8_t *src, const int64_t *order0, CaGeom g
     rg.acc_pool = acc_base[dev];
     rg.acc_base = acc_next.fetch_add((unsigned)rg.n, std::memory_order_relaxed) % CC_ACC_POOL;
     rg.gate = gate_words[dev];
-    // bench A/B (profiles/r2/range/refresh_ab.jsonl): 0 -> 32.4-32.5 us per f32
-    // batch, 4 -> 31.9-32.1, 6 -> 32.5
+    // bench A/B (profiles/r2/range/refresh_ab.jsonl, refresh_sweep.jsonl): 0 ->
+    // 32.4-32.5 us per f32 batch, 2 -> 32.1-35.3, 3 -> 32.6, 4 -> 31.9-32.1,
+    // 5 -> 32.1, 6 -> 32.5
     static const int refresh = getenv("TSB_CC_REFRESH") ? atoi(getenv("TSB_CC_REFRESH")) : 4;
     rg.refresh = refresh;
     TSB_CUDA(cudaMemsetAsync(rg.gate, 0, sizeof(unsigned long long), s));
